@@ -1,0 +1,402 @@
+/*
+ * oracle.c -- plain single-threaded CPU oracle for Pipette (arXiv 2405.18093).
+ *
+ * TEST INFRASTRUCTURE ONLY (see oracle.h).  Nothing here is blocked, fused or
+ * incremental: every proposal of the simulated annealing is re-evaluated from the
+ * definition.  Citations: "P:n" = /root/reference/PAPER.md line n; "Rk" = reading k
+ * in DESIGN.md section 2 (where the paper is silent, ambiguous or garbled).
+ *
+ * Build: gcc -O2 -std=c99 -ffp-contract=off -fno-fast-math -fPIC -shared
+ * (binary64 on SSE2, no FMA contraction, so every operation below is one IEEE op).
+ *
+ * Parity status: every function is pinned by a -m "not gpu" test in
+ * tests/test_oracle_*.py (worked examples, closed forms, DES, brute force, KATs);
+ * see DESIGN.md section 5 for the pin of each function.
+ */
+#include "oracle.h"
+#include <math.h>
+#include <stdlib.h>
+#include <string.h>
+
+/* ------------------------------------------------------------------------- */
+/* Enumeration: Alg.1 lines 3-5.  R1: tp | gpus_per_node (TP groups  */
+/* stay inside a server); R2: pp <= n_layers; dp must divide bs_global     */
+/* (bs_mini = bs_global/dp, l.4); mb ranges over all divisors of bs_mini (l.5).   */
+/* Canonical order: pp ascending, tp ascending, mb ascending.                      */
+/* ------------------------------------------------------------------------- */
+int32_t or_feasible(uint64_t mem, uint64_t cap, int32_t margin_permille) {
+  /* Alg.1 l.7 "MemEstimator(Conf, bs_micro) > M_limit then continue"
+     with the soft margin of P:370 (R12): runnable iff mem <= floor(cap*(1000-m)/1000). */
+  uint64_t limit = cap / 1000u * (uint64_t)(1000 - margin_permille)
+                 + (cap % 1000u) * (uint64_t)(1000 - margin_permille) / 1000u;
+  return mem <= limit;
+}
+
+static int32_t has_profile(const or_profile* prof, int32_t n_prof, int32_t tp, int32_t mb) {
+  for (int32_t i = 0; i < n_prof; ++i)
+    if (prof[i].tp == tp && prof[i].mb == mb) return 1;
+  return 0;
+}
+
+int32_t or_enumerate(const or_cluster* cl, const or_model* m, int64_t bs_global,
+                     const or_profile* prof, int32_t n_prof, or_config* out, int32_t cap) {
+  int64_t G = (int64_t)cl->n_nodes * cl->gpus_per_node;
+  int32_t E = 0;
+  for (int64_t pp = 1; pp <= G; ++pp) {
+    if (G % pp != 0 || pp > m->n_layers) continue;
+    for (int64_t tp = 1; tp <= cl->gpus_per_node; ++tp) {
+      if (cl->gpus_per_node % tp != 0) continue;
+      if (G % (pp * tp) != 0) continue;
+      int64_t dp = G / (pp * tp);
+      if (bs_global % dp != 0) continue;
+      int64_t bs_mini = bs_global / dp;
+      for (int64_t mb = 1; mb <= bs_mini; ++mb) {
+        if (bs_mini % mb != 0) continue;
+        if (out && E < cap) {
+          or_config* c = &out[E];
+          c->pp = (int32_t)pp; c->tp = (int32_t)tp; c->dp = (int32_t)dp; c->mb = (int32_t)mb;
+          c->n_mb = (int32_t)(bs_mini / mb);
+          c->e = E;
+          c->mem_bytes = or_memory(m, c->pp, c->tp, c->mb, c->n_mb);
+          c->feasible = or_feasible(c->mem_bytes, cl->mem_capacity_bytes, cl->mem_margin_permille);
+          c->has_profile = has_profile(prof, n_prof, c->tp, c->mb);
+        }
+        ++E;
+      }
+    }
+  }
+  return E;
+}
+
+/* ------------------------------------------------------------------------- */
+/* Analytic memory estimator (R11; north_star "parameters, optimizer state, and   */
+/* 1F1B in-flight activations per stage"; the paper's heuristic family).   */
+/* Stage s is 1-based.  All integers, exact.                                      */
+/* ------------------------------------------------------------------------- */
+static uint64_t ceil_div(uint64_t a, uint64_t b) { return (a + b - 1) / b; }
+
+uint64_t or_stage_memory(const or_model* m, int32_t pp, int32_t tp, int32_t mb, int32_t n_mb, int32_t s) {
+  uint64_t L = (uint64_t)m->n_layers, h = (uint64_t)m->hidden, a = (uint64_t)m->heads;
+  uint64_t seq = (uint64_t)m->seq_len, V = (uint64_t)m->vocab;
+  uint64_t Lps = ceil_div(L, (uint64_t)pp);                       /* layers per stage */
+  uint64_t P = Lps * (12u * h * h + 13u * h);                     /* transformer layers */
+  if (s == 1) P += V * h + seq * h;                               /* word + position embeddings */
+  if (s == pp && pp > 1) P += V * h;                              /* tied LM head copy on last stage */
+  uint64_t W = (uint64_t)m->bytes_per_param_state * ceil_div(P, (uint64_t)tp); /* params+grads+Adam */
+  /* Korthikanti et al. per-layer activations, TP without SP, no recompute:        */
+  /* seq*mb*h*(10 + 24/tp) + 5*a*seq^2*mb/tp bytes.                                  */
+  uint64_t act_num = seq * (uint64_t)mb * h * (10u * (uint64_t)tp + 24u)
+                   + 5u * a * seq * seq * (uint64_t)mb;
+  uint64_t act = ceil_div(act_num, (uint64_t)tp);
+  int64_t inflight = (int64_t)pp - s + 1;                         /* 1F1B bound */
+  if (inflight > n_mb) inflight = n_mb;
+  uint64_t A = (uint64_t)inflight * Lps * act;
+  return W + A + m->overhead_bytes;
+}
+
+uint64_t or_memory(const or_model* m, int32_t pp, int32_t tp, int32_t mb, int32_t n_mb) {
+  uint64_t best = 0;
+  for (int32_t s = 1; s <= pp; ++s) {                            /* max over every stage */
+    uint64_t v = or_stage_memory(m, pp, tp, mb, n_mb, s);
+    if (v > best) best = v;
+  }
+  return best;
+}
+
+/* ------------------------------------------------------------------------- */
+/* Per-config constants.  C = per-stage fwd+bwd compute for one   */
+/* microbatch = Lps * c_layer (R3); T_TP likewise.                  */
+/* msg_PP = mb*seq*h*bpe, msg_DP = floor(n_params/(pp*tp))*bpe (R4).              */
+/* ------------------------------------------------------------------------- */
+int32_t or_constants(const or_cluster* cl, const or_model* m, const or_config* c,
+                     const or_profile* prof, int32_t n_prof, or_consts* K) {
+  const or_profile* pe = NULL;
+  for (int32_t i = 0; i < n_prof; ++i)
+    if (prof[i].tp == c->tp && prof[i].mb == c->mb) { pe = &prof[i]; break; }
+  if (!pe) return 3;
+  uint64_t L = (uint64_t)m->n_layers, h = (uint64_t)m->hidden;
+  uint64_t Lps = ceil_div(L, (uint64_t)c->pp);
+  uint64_t msg_pp = (uint64_t)c->mb * (uint64_t)m->seq_len * h * (uint64_t)m->bytes_per_elem;
+  uint64_t n_params = 12u * L * h * h + (uint64_t)m->vocab * h;
+  uint64_t msg_dp = n_params / ((uint64_t)c->pp * (uint64_t)c->tp) * (uint64_t)m->bytes_per_elem;
+  double Lf = (double)Lps;
+  K->pp = c->pp; K->dp = c->dp; K->spn = cl->gpus_per_node / c->tp;
+  K->N = c->pp * c->dp; K->n_nodes = cl->n_nodes; K->n_mb = c->n_mb;
+  K->S  = (Lf * pe->c_layer_s) + (Lf * pe->tp_layer_s);         /* C + T_TP */
+  K->m2 = 2.0 * (double)msg_pp;                                  /* Eq.5 "2*msg_PP" */
+  K->md = (double)msg_dp;
+  K->r  = (double)c->n_mb / (double)c->pp;                       /* n_mb/pp, real (R7) */
+  K->Sb = (double)c->pp * K->S;                                  /* pp*(C+T_TP), Eq.4 */
+  K->Ss = (double)(c->pp - 1) * K->S;                            /* (pp-1)*(C+T_TP), Eq.4 */
+  return 0;
+}
+
+/* Eq.6 intra-node factor 4(|W|-1)msg/|W| and inter-node factor 2(|W|-1)msg/|W|. */
+double or_qi(const or_consts* K, int32_t c) { return ((4.0 * (double)(c - 1)) * K->md) / (double)c; }
+double or_qe(const or_consts* K, int32_t k) { return ((2.0 * (double)(k - 1)) * K->md) / (double)k; }
+
+/* R = 1/B elementwise (R5: node-granular directed matrix, diagonal = intra-node). */
+void or_inverse_bandwidth(const double* B, int32_t n, double* R) {
+  for (int32_t i = 0; i < n * n; ++i) R[i] = 1.0 / B[i];
+}
+
+int32_t or_is_permutation(const uint16_t* perm, int32_t N) {
+  char* seen = (char*)calloc((size_t)N + 1, 1);
+  int32_t ok = 1;
+  for (int32_t w = 0; w < N; ++w) {
+    if (perm[w] >= N || seen[perm[w]]) { ok = 0; break; }
+    seen[perm[w]] = 1;
+  }
+  free(seen);
+  return ok;
+}
+
+/* ------------------------------------------------------------------------- */
+/* Latency of a mapping, Eq.3-6, from the definition.                 */
+/* Worker position w = z*pp + x (R9: pipeline-major string); slot perm[w] is a    */
+/* TP block of tp GPUs inside node perm[w]/spn (R8, Eq.2).              */
+/*   T_PP = max_z sum_{x<pp-1} m2 * R[node(z,x)][node(z,x+1)]       Eq.5  */
+/*   T_DP = max_n qi(c_n) R[n][n] + qe(k) max_{a!=b in N1} R[a][b]  Eq.6  */
+/*   T    = (pp*S + T_PP) * n_mb/pp + (pp-1)*S + T_DP               Eq.3-4, R6    */
+/* ------------------------------------------------------------------------- */
+double or_latency(const or_consts* K, const double* R, const uint16_t* perm, or_breakdown* bd) {
+  const int32_t pp = K->pp, dp = K->dp, n = K->n_nodes, spn = K->spn;
+  /* Eq.5: sum along each pipeline in stage order, then the slowest pipeline. */
+  double t_pp = 0.0;
+  for (int32_t z = 0; z < dp; ++z) {
+    double Pz = 0.0;
+    for (int32_t x = 0; x + 1 < pp; ++x) {
+      int32_t a = perm[z * pp + x] / spn;
+      int32_t b = perm[z * pp + x + 1] / spn;
+      Pz = Pz + K->m2 * R[a * n + b];
+    }
+    if (Pz > t_pp) t_pp = Pz;
+  }
+  /* Eq.6, stage 1 only: occupancy of each node by stage-1 DP members. */
+  int32_t* cnt = (int32_t*)calloc((size_t)n, sizeof(int32_t));
+  for (int32_t z = 0; z < dp; ++z) cnt[perm[z * pp] / spn] += 1;
+  int32_t k = 0;
+  double t_in = 0.0;
+  for (int32_t a = 0; a < n; ++a) {
+    if (cnt[a] > 0) ++k;
+    if (cnt[a] >= 2) {                                  /* R10: per-node intra ring */
+      double v = or_qi(K, cnt[a]) * R[a * n + a];
+      if (v > t_in) t_in = v;
+    }
+  }
+  double t_ex = 0.0;
+  if (k >= 2) {                                         /* slowest link over all pairs (R10) */
+    double maxR = 0.0;
+    for (int32_t a = 0; a < n; ++a)
+      for (int32_t b = 0; b < n; ++b)
+        if (a != b && cnt[a] > 0 && cnt[b] > 0 && R[a * n + b] > maxR) maxR = R[a * n + b];
+    t_ex = or_qe(K, k) * maxR;
+  }
+  free(cnt);
+  double t_dp = t_in + t_ex;
+  double T = (((K->Sb + t_pp) * K->r) + K->Ss) + t_dp;
+  if (bd) {
+    bd->T = T; bd->t_pp = t_pp; bd->t_in = t_in; bd->t_ex = t_ex; bd->t_dp = t_dp;
+    bd->t_bubble = K->Sb + t_pp; bd->t_straggler = K->Ss; bd->k = k;
+  }
+  return T;
+}
+
+/* ------------------------------------------------------------------------- */
+/* Philox4x32-10 (Salmon et al. SC'11), R14: counter (step, chain, cfg, 0),       */
+/* key (seed lo32, seed hi32).  Round = Random123 / cuRAND definition.            */
+/* ------------------------------------------------------------------------- */
+void or_philox4x32_10(const uint32_t ctr[4], const uint32_t key[2], uint32_t out[4]) {
+  uint32_t c0 = ctr[0], c1 = ctr[1], c2 = ctr[2], c3 = ctr[3];
+  uint32_t k0 = key[0], k1 = key[1];
+  for (int r = 0; r < 10; ++r) {
+    if (r > 0) { k0 += 0x9E3779B9u; k1 += 0xBB67AE85u; }
+    uint64_t p0 = (uint64_t)0xD2511F53u * (uint64_t)c0;
+    uint64_t p1 = (uint64_t)0xCD9E8D57u * (uint64_t)c2;
+    uint32_t hi0 = (uint32_t)(p0 >> 32), lo0 = (uint32_t)p0;
+    uint32_t hi1 = (uint32_t)(p1 >> 32), lo1 = (uint32_t)p1;
+    uint32_t n0 = hi1 ^ c1 ^ k0, n1 = lo1, n2 = hi0 ^ c3 ^ k1, n3 = lo0;
+    c0 = n0; c1 = n1; c2 = n2; c3 = n3;
+  }
+  out[0] = c0; out[1] = c1; out[2] = c2; out[3] = c3;
+}
+
+/* One SA proposal's randomness (R14): positions p != q in [0,N) by 64-bit          */
+/* multiply-high, and a 53-bit uniform u in [0,1).                                   */
+void or_draw(uint32_t i, uint32_t c, uint32_t e, uint64_t seed, int32_t N,
+             uint32_t* p, uint32_t* q, double* u) {
+  uint32_t ctr[4] = {i, c, e, 0u};
+  uint32_t key[2] = {(uint32_t)seed, (uint32_t)(seed >> 32)};
+  uint32_t w[4];
+  or_philox4x32_10(ctr, key, w);
+  uint32_t pp_ = (uint32_t)(((uint64_t)w[0] * (uint64_t)N) >> 32);
+  uint32_t off = (uint32_t)(((uint64_t)w[1] * (uint64_t)(N - 1)) >> 32);
+  *p = pp_;
+  *q = (pp_ + 1u + off) % (uint32_t)N;
+  uint64_t bits = ((uint64_t)(w[2] >> 5) << 26) | (uint64_t)(w[3] >> 6);
+  *u = (double)bits * 0x1p-53;
+}
+
+/* ------------------------------------------------------------------------- */
+/* exp(x) for x <= 0 with only IEEE + - * and floor (R15), so that the Metropolis  */
+/* decision is reproducible on any IEEE machine.  Cody-Waite reduction by ln 2,    */
+/* degree-13 Taylor polynomial of e^r on |r| <= ln2/2, exact scaling by 2^k.       */
+/* ------------------------------------------------------------------------- */
+double or_exp_det(double x) {
+  if (x < -708.0) return 0.0;
+  double k = floor(x * 1.4426950408889634 + 0.5);
+  double r = (x - k * 6.93147180369123816490e-01) - k * 1.90821492927058770002e-10;
+  double fact = 1.0;
+  double coef[14];
+  for (int n = 0; n <= 13; ++n) {               /* coef[n] = fl(1/n!) ; n! exact for n<=13 */
+    if (n > 0) fact = fact * (double)n;
+    coef[n] = 1.0 / fact;
+  }
+  double poly = coef[13];
+  for (int n = 12; n >= 0; --n) poly = poly * r + coef[n];
+  int64_t ki = (int64_t)k;                      /* k in [-1022, 0] */
+  uint64_t bits = (uint64_t)(ki + 1023) << 52;
+  double scale;
+  memcpy(&scale, &bits, sizeof scale);
+  return poly * scale;
+}
+
+/* ------------------------------------------------------------------------- */
+/* One simulated-annealing chain of worker dedication (Alg.1 l.9-15).  */
+/* Swap move only (north_star); Metropolis acceptance (R13); beta <- beta/alpha    */
+/* every iteration (R13); pi0 = identity "alphabetical" (R16); best updated */
+/* on strict < (R17).  Every proposal is re-evaluated from the definition.         */
+/* ------------------------------------------------------------------------- */
+void or_sa_chain(const or_consts* K, const double* R, int32_t iterations, uint64_t seed,
+                 uint32_t chain, uint32_t e, double alpha, double tau, double t0,
+                 or_chain_result* res, uint16_t* best_perm,
+                 or_trace_record* trace, int32_t trace_cap) {
+  const int32_t N = K->N;
+  uint16_t* perm = (uint16_t*)malloc(sizeof(uint16_t) * (size_t)N);
+  for (int32_t w = 0; w < N; ++w) perm[w] = (uint16_t)w;
+  or_breakdown bd;
+  double L0 = or_latency(K, R, perm, &bd);
+  double cur = L0, best = L0;
+  double best_tpp = bd.t_pp, best_tdp = bd.t_dp;
+  int32_t best_step = -1;
+  uint32_t accepted = 0;
+  if (best_perm) memcpy(best_perm, perm, sizeof(uint16_t) * (size_t)N);
+  double beta = (t0 > 0.0) ? 1.0 / t0 : 1.0 / (tau * L0);
+  double ia = 1.0 / alpha;
+  if (N >= 2) {
+    for (int32_t i = 0; i < iterations; ++i) {
+      uint32_t p, q; double u;
+      or_draw((uint32_t)i, chain, e, seed, N, &p, &q, &u);
+      uint16_t t = perm[p]; perm[p] = perm[q]; perm[q] = t;          /* swap move */
+      double Lp = or_latency(K, R, perm, &bd);
+      double d = Lp - cur;
+      int acc = (d <= 0.0) || (u < or_exp_det(-(d * beta)));        /* Metropolis */
+      if (acc) {
+        cur = Lp; ++accepted;
+        if (Lp < best) {
+          best = Lp; best_step = i; best_tpp = bd.t_pp; best_tdp = bd.t_dp;
+          if (best_perm) memcpy(best_perm, perm, sizeof(uint16_t) * (size_t)N);
+        }
+      } else {
+        t = perm[p]; perm[p] = perm[q]; perm[q] = t;                  /* undo */
+      }
+      beta = beta * ia;
+      if (trace && i < trace_cap) {
+        trace[i].i = (uint32_t)i; trace[i].p = (uint16_t)p; trace[i].q = (uint16_t)q;
+        trace[i].accept = (uint32_t)acc; trace[i].L = Lp;
+      }
+    }
+  }
+  res->best = best; res->best_t_pp = best_tpp; res->best_t_dp = best_tdp; res->L0 = L0;
+  res->best_step = best_step; res->accepted = accepted;
+  free(perm);
+}
+
+/* ------------------------------------------------------------------------- */
+/* Alg.1: every feasible (Conf, bs_micro) runs `chains` SA chains;     */
+/* winner = lexicographic min of (latency, config index e, chain c) (R17).         */
+/* `world` simulates the W-rank sharding: item j = f*chains + c belongs to rank    */
+/* j mod W; each rank takes its local argmin; the ranks are combined by a min over */
+/* the latency bits, then a min over the item ids that attain it (R18).           */
+/* ------------------------------------------------------------------------- */
+int32_t or_search(const or_cluster* cl, const double* B, const or_profile* prof, int32_t n_prof,
+                  const or_model* m, int64_t bs_global, int32_t chains, int32_t iterations,
+                  uint64_t seed, double alpha, double tau, double t0, int32_t world,
+                  or_plan* plan, uint16_t* perm_out, int32_t perm_cap,
+                  double* per_config_best, int32_t* per_config_chain) {
+  memset(plan, 0, sizeof *plan);
+  int32_t n = cl->n_nodes;
+  int32_t E = or_enumerate(cl, m, bs_global, prof, n_prof, NULL, 0);
+  or_config* cfgs = (or_config*)calloc((size_t)E + 1, sizeof(or_config));
+  or_enumerate(cl, m, bs_global, prof, n_prof, cfgs, E);
+  double* R = (double*)malloc(sizeof(double) * (size_t)n * (size_t)n);
+  or_inverse_bandwidth(B, n, R);
+  int32_t F = 0;
+  for (int32_t i = 0; i < E; ++i) {
+    if (!cfgs[i].feasible) continue;
+    if (!cfgs[i].has_profile) { plan->status = 3; plan->E = E; free(cfgs); free(R); return 3; }
+    ++F;
+  }
+  plan->E = E; plan->F = F;
+  if (F == 0) { plan->status = 1; free(cfgs); free(R); return 1; }
+
+  /* per-rank local winners */
+  double* rank_best = (double*)malloc(sizeof(double) * (size_t)world);
+  int64_t* rank_item = (int64_t*)malloc(sizeof(int64_t) * (size_t)world);
+  for (int32_t r = 0; r < world; ++r) { rank_best[r] = INFINITY; rank_item[r] = INT64_MAX; }
+  int32_t maxN = 0;
+  for (int32_t i = 0; i < E; ++i) if (cfgs[i].feasible && cfgs[i].pp * cfgs[i].dp > maxN) maxN = cfgs[i].pp * cfgs[i].dp;
+  uint16_t* bp = (uint16_t*)malloc(sizeof(uint16_t) * (size_t)maxN);
+  uint64_t steps = 0, acc = 0;
+  int32_t f = 0;
+  for (int32_t i = 0; i < E; ++i) {
+    if (!cfgs[i].feasible) continue;
+    or_consts K;
+    or_constants(cl, m, &cfgs[i], prof, n_prof, &K);
+    if (per_config_best) per_config_best[f] = INFINITY;
+    if (per_config_chain) per_config_chain[f] = -1;
+    for (int32_t c = 0; c < chains; ++c) {
+      or_chain_result res;
+      or_sa_chain(&K, R, iterations, seed, (uint32_t)c, (uint32_t)cfgs[i].e, alpha, tau, t0, &res, NULL, NULL, 0);
+      if (K.N >= 2) steps += (uint64_t)iterations;
+      acc += res.accepted;
+      int64_t j = (int64_t)f * chains + c;
+      int32_t r = (int32_t)(j % world);
+      if (res.best < rank_best[r] || (res.best == rank_best[r] && j < rank_item[r])) {
+        rank_best[r] = res.best; rank_item[r] = j;
+      }
+      if (per_config_best && (res.best < per_config_best[f])) {
+        per_config_best[f] = res.best;
+        if (per_config_chain) per_config_chain[f] = c;
+      }
+    }
+    ++f;
+  }
+  /* combine: min over latency, then min item id among ranks attaining it */
+  double gbest = INFINITY;
+  for (int32_t r = 0; r < world; ++r) if (rank_best[r] < gbest) gbest = rank_best[r];
+  int64_t gitem = INT64_MAX;
+  for (int32_t r = 0; r < world; ++r) if (rank_best[r] == gbest && rank_item[r] < gitem) gitem = rank_item[r];
+  int32_t wf = (int32_t)(gitem / chains), wc = (int32_t)(gitem % chains);
+  /* re-run the winning chain to recover its best mapping and breakdown */
+  f = 0;
+  for (int32_t i = 0; i < E; ++i) {
+    if (!cfgs[i].feasible) continue;
+    if (f == wf) {
+      or_consts K;
+      or_constants(cl, m, &cfgs[i], prof, n_prof, &K);
+      or_chain_result res;
+      or_sa_chain(&K, R, iterations, seed, (uint32_t)wc, (uint32_t)cfgs[i].e, alpha, tau, t0, &res, bp, NULL, 0);
+      plan->cfg = cfgs[i];
+      or_latency(&K, R, bp, &plan->bd);
+      plan->cfg_index = cfgs[i].e; plan->chain = wc; plan->best_step = res.best_step;
+      plan->n_slots = K.N;
+      if (perm_out && perm_cap >= K.N) memcpy(perm_out, bp, sizeof(uint16_t) * (size_t)K.N);
+      break;
+    }
+    ++f;
+  }
+  plan->sa_steps = steps; plan->sa_accepted = acc; plan->status = 0;
+  free(bp); free(rank_best); free(rank_item); free(cfgs); free(R);
+  return 0;
+}
