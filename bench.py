@@ -1,0 +1,344 @@
+#!/usr/bin/env python
+"""Benchmark of the Pipette hot path on B200 (contract: DESIGN.md section 8).
+
+A step = one pipette_search (Alg.1: K1 enumerate + memory filter, K3 SA chains, K4
+argmin, NCCL combine) on BASELINE config C2 (64 GPUs, GPT-3
+2.7B, bs 512, 1024 SA chains x 10k swaps per feasible config) -- rows a10 (the eval
+stream) is measured beside it in the same run ("eval_stream").  Multi-GPU (torchrun):
+weak scaling, every rank runs 1024 chains per config (chains_per_config = 1024 * N),
+winners combined with NCCL.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import workloads as W  # noqa: E402
+
+PEAKS = os.path.join(ROOT, "MEASURED_PEAKS.json")
+FP64_LANES_PER_SM = 64          # B200 (sm_100) FP64 units per SM per clock
+N_SMS = 148
+
+
+def peaks():
+    try:
+        return json.load(open(PEAKS))
+    except Exception:
+        return {"hbm_gbs": 6650.0, "sm_max_mhz": 1965.0, "fallback": True}
+
+
+# --------------------------------------------------------------------------- clocks
+class ClockSampler:
+    """nvidia-smi-equivalent sampling (NVML) of SM clock and throttle reasons during the
+    timed region."""
+
+    REASONS = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap", 0x8: "hw_slowdown",
+               0x20: "sw_thermal_slowdown", 0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown",
+               0x100: "display_clock_setting"}
+
+    def __init__(self, device: int):
+        self.samples, self.reasons, self._stop = [], 0, threading.Event()
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(device)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+        except Exception:
+            self.nv = None
+            self.max_mhz = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+                fn = getattr(self.nv, "nvmlDeviceGetCurrentClocksEventReasons", None) or \
+                    self.nv.nvmlDeviceGetCurrentClocksThrottleReasons
+                self.reasons |= fn(self.h)
+            except Exception:
+                pass
+            time.sleep(0.02)
+
+    def __enter__(self):
+        if self.nv:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self.nv:
+            self.t.join()
+
+    def summary(self):
+        if not self.nv or not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": ["unavailable"]}
+        rs = [name for bit, name in self.REASONS.items() if self.reasons & bit and name != "gpu_idle"]
+        return {"sm_mhz": statistics.median(self.samples), "sm_max_mhz": self.max_mhz, "reasons": rs,
+                "samples": len(self.samples)}
+
+
+# --------------------------------------------------------------------------- helpers
+def fp64_ops_per_step(pp: int, dp: int) -> int:
+    """Algorithmic FP64 operations of one SA proposal: re-sum of the two
+    touched pipelines (pp-1 hops x (mul + add) each), Eq.3-4 composition (5), the
+    Metropolis difference (1) and the temperature update (1)."""
+    return (4 * (pp - 1) if pp >= 2 and dp >= 2 else 2 * (pp - 1)) + 7
+
+
+def setup(name: str):
+    w = W.WORKLOADS[name]
+    B, prof = W.workload_inputs(w)
+    return w, B, prof
+
+
+def _oracle_sample(w, B, prof, seconds: float):
+    """The CPU oracle (single thread, as it stands) on a bounded sample of workload w:
+    round-robin over the feasible configs, one full-length chain each, until `seconds`."""
+    import oracle as O
+    m = w.model
+    cl = O.make_cluster(w.n_nodes, w.gpus_per_node, w.cap_bytes, w.margin_permille)
+    mo = O.make_model(m.n_layers, m.hidden, m.heads, m.seq_len, m.vocab)
+    P = O.make_profile(prof)
+    R = O.inverse_bandwidth(B)
+    feas = [c for c in O.enumerate_configs(cl, mo, w.bs_global, P) if c.feasible]
+    Ks = [(c, O.constants(cl, mo, c, P)) for c in feas]
+    steps, chains = 0, 0
+    t0 = time.perf_counter()
+    i = 0
+    while time.perf_counter() - t0 < seconds:
+        c, K = Ks[i % len(Ks)]
+        O.sa_chain(K, R, w.iterations, w.seed, i // len(Ks), c.e)
+        steps += w.iterations if K.N >= 2 else 0
+        chains += 1
+        i += 1
+    dt = time.perf_counter() - t0
+    return steps / dt, dt, chains
+
+
+def run_reference(args):
+    """--impl reference: the CPU oracle on the host cores (rank 0 only)."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    w, B, prof = setup(args.workload)
+    for _ in range(args.warmup):
+        _oracle_sample(w, B, prof, 0.5)
+    vals, secs, nch = [], 0.0, 0
+    for _ in range(args.steps):
+        v, dt, c = _oracle_sample(w, B, prof, args.ref_seconds)
+        vals.append(v); secs += dt; nch += c
+    value = float(np.mean(vals))
+    line = {"metric": "plan evaluations/sec", "value": value, "unit": "evals/s", "impl": "reference",
+            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": 1000.0 * secs / args.steps, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": f"{w.name}: {w.n_nodes * w.gpus_per_node} GPUs, {w.model.name}, bs {w.bs_global}, "
+                                   f"{w.chains} chains x {w.iterations} swaps per config",
+                       "l2": "n/a (host)"},
+            "cpu_baseline": {"value": value, "unit": "evals/s", "cores": 1, "kind": "oracle",
+                             "sample": f"{nch} full-length SA chains round-robin over the feasible configs, "
+                                       f"{args.ref_seconds:.0f} s per step"},
+            "e2e": {"value": value, "unit": "evals/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line))
+
+
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    from paper_2405_18093_b200 import Model, Pipette
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    w, B, prof = setup(args.workload)
+    m = w.model
+    model = Model(m.n_layers, m.hidden, m.heads, m.seq_len, m.vocab)
+    kw = dict(mem_capacity_bytes=w.cap_bytes, mem_margin_permille=w.margin_permille)
+    pip = (Pipette.from_torch_distributed(w.n_nodes, w.gpus_per_node, B, prof, device=local, **kw) if world > 1
+           else Pipette(w.n_nodes, w.gpus_per_node, B, prof, device=local, **kw))
+    chains = w.chains * world if args.weak else w.chains
+    stream = torch.cuda.current_stream()
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")    # > 126 MB L2
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    res = None
+    for _ in range(args.warmup):
+        res = pip.search(model, w.bs_global, chains, w.iterations, w.seed)
+    plan = res["plan"] if res else None
+
+    # ---------------- timed region: K steps, per-step CUDA events, L2 flushed between steps
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    sa_ms, launches = [], 0
+    barrier()
+    with ClockSampler(local) as clk:
+        for k in range(args.steps):
+            flush.fill_(k & 0xFF)
+            evs[k][0].record(stream)
+            res = pip.search(model, w.bs_global, chains, w.iterations, w.seed)
+            evs[k][1].record(stream)
+            sa_ms.append(res["plan"].timings_ms["sa"])
+            launches += pip.last_launch_count
+        barrier()
+    step_ms = [a.elapsed_time(b) for a, b in evs]
+    t_local = sum(step_ms)
+    t = torch.tensor([t_local, sum(sa_ms)], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    t_max, sa_max = float(t[0]), float(t[1])
+    plan = res["plan"]
+    evals_per_step = plan.sa_steps                    # global SA proposals (all ranks)
+    value = evals_per_step * args.steps / (t_max / 1000.0)
+
+    # ---------------- roofline of the dominant kernel (k_sa_chains), achieved = algorithmic
+    cfgs, nmb, mem, feas = pip.enumerate(model, w.bs_global)
+    ops = 0
+    for (pp, tp, dp, mb), f in zip(cfgs.tolist(), feas.tolist()):
+        if f and pp * dp >= 2:
+            ops += fp64_ops_per_step(pp, dp) * chains * w.iterations
+    ops_local = ops / world
+    sa_avg_s = (sa_max / args.steps) / 1000.0
+    pk = peaks()
+    clocks = clk.summary()
+    fp64_peak = N_SMS * FP64_LANES_PER_SM * (pk.get("sm_max_mhz", 1965.0) * 1e6) / 1e12
+    achieved = ops_local / sa_avg_s / 1e12
+    roofline = {"kernel": "k_sa_chains", "bound": "alu", "achieved": achieved, "peak": fp64_peak,
+                "unit": "TFLOP/s (fp64 DADD/DMUL ops)", "frac": achieved / fp64_peak, "traffic": None,
+                "peak_source": "148 SMs x 64 FP64 lanes x sm_max_mhz (MEASURED_PEAKS.json), DESIGN.md 8",
+                "sa_kernel_ms": sa_avg_s * 1000.0, "sa_share_of_step": (sa_max / t_max) if t_max else None}
+
+    # ---------------- e2e through the public API: host bandwidth matrix in, plan out
+    e2e = None
+    if not args.no_e2e:
+        Bh = np.ascontiguousarray(B)
+        barrier()
+        ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        ev0.record(stream)
+        for k in range(args.steps):
+            pip.set_bandwidth(Bh)                     # H2D of the profiled matrix (Alg.1 l.1 output)
+            r2 = pip.search(model, w.bs_global, chains, w.iterations, w.seed)   # D2H of the plan
+        ev1.record(stream)
+        barrier()
+        te = torch.tensor([ev0.elapsed_time(ev1)], dtype=torch.float64, device="cuda")
+        if world > 1:
+            dist.all_reduce(te, op=dist.ReduceOp.MAX)
+        F = int(feas.sum())
+        row_words = 4 + (max(int(c[0] * c[2]) for c in cfgs[feas]) + 3) // 4
+        e2e = {"value": evals_per_step * args.steps / (float(te[0]) / 1000.0), "unit": "evals/s",
+               "h2d_bytes_per_step": int(Bh.nbytes), "d2h_bytes_per_step": int(8 * F * (row_words + 2) + 8)}
+
+    # ---------------- eval stream (row a10), HBM-bound, measured beside the step
+    eval_stream = None
+    if not args.no_eval and rank == 0:
+        eval_stream = bench_eval(pip, model, w, cfgs, feas, pk)
+
+    # ---------------- CPU baseline: the oracle on this host, rank 0 at N=1 only
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        v, dt, nch = _oracle_sample(w, B, prof, args.cpu_seconds)
+        cpu = {"value": v, "unit": "evals/s", "cores": 1, "kind": "oracle",
+               "sample": f"{nch} full-length ({w.iterations}-swap) chains round-robin over the "
+                         f"{int(feas.sum())} feasible configs of {w.name}, {dt:.1f} s single thread"}
+
+    if rank == 0:
+        line = {"metric": "plan evaluations/sec", "value": value, "unit": "evals/s", "n_gpus": world,
+                "steps": args.steps, "warmup": args.warmup, "ms_per_step": t_max / args.steps,
+                "time_to_best_plan_ms": t_max / args.steps,
+                "higher_is_better": True, "scaling": "weak" if args.weak else "strong", "vs_baseline": None,
+                "dtype": "f64", "data": "synthetic (workloads/: B with per-link variance, Megatron-flop profile)",
+                "config": {"workload": f"{w.name}: {w.n_nodes * w.gpus_per_node} GPUs ({w.n_nodes} nodes x "
+                                       f"{w.gpus_per_node}), {m.name}, bs_global {w.bs_global}, "
+                                       f"{w.chains} SA chains/config/GPU x {w.iterations} swaps",
+                           "chains_per_config": chains, "feasible_configs": int(feas.sum()),
+                           "enumerated_configs": int(len(feas)), "sa_proposals_per_step": evals_per_step,
+                           "l2": "flushed between timed steps (256 MiB write)", "parallelism": f"chains sharded x{world}"},
+                "plan": {"cfg": list(plan.cfg), "latency_s": plan.latency_s, "cfg_index": plan.cfg_index,
+                         "chain": plan.chain, "best_step": plan.best_step},
+                "phase_ms": plan.timings_ms,
+                "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
+                "clocks": clocks, "eval_stream": eval_stream}
+        print(json.dumps(line))
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def bench_eval(pip, model, w, cfgs, feas, pk, n=1 << 22, reps=5):
+    """pipette_eval on a homogeneous batch of 2^22 random mappings of the feasible config
+    with the largest N; HBM roofline with 25 + 2N algorithmic bytes."""
+    import torch
+    idx = max((i for i in range(len(feas)) if feas[i]), key=lambda i: (cfgs[i][0] * cfgs[i][2], -i))
+    pp, tp, dp, mb = (int(x) for x in cfgs[idx])
+    N = pp * dp
+    stride = ((N + 7) // 8) * 8
+    g = torch.Generator(device="cuda").manual_seed(5)
+    keys = torch.rand((n, N), device="cuda", generator=g)
+    perm = torch.zeros((n, stride), dtype=torch.int16, device="cuda")
+    perm[:, :N] = torch.argsort(keys, dim=1).to(torch.int16)
+    del keys
+    cfg = torch.tensor([pp, tp, dp, mb], dtype=torch.int16, device="cuda").repeat(n, 1).contiguous()
+    out = (torch.empty(n, dtype=torch.float64, device="cuda"), torch.empty(n, dtype=torch.int64, device="cuda"),
+           torch.empty(n, dtype=torch.uint8, device="cuda"))
+    for _ in range(3):
+        pip.eval(model, w.bs_global, cfg, perm, out=out)
+    torch.cuda.synchronize()
+    ts = []
+    for _ in range(reps):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        pip.eval(model, w.bs_global, cfg, perm, out=out)
+        b.record()
+        torch.cuda.synchronize()
+        ts.append(a.elapsed_time(b) / 1000.0)
+    t = statistics.median(ts)
+    alg = 8 + 2 * N + 17                      # config + mapping in, latency + mem + status out
+    gbs = alg * n / t / 1e9
+    return {"value": n / t, "unit": "candidates/s", "config": [pp, tp, dp, mb], "N": N, "batch": n,
+            "stride": stride, "roofline": {"kernel": "k_eval_stream", "bound": "hbm", "achieved": gbs,
+                                             "peak": pk.get("hbm_gbs"), "unit": "GB/s",
+                                             "frac": gbs / pk.get("hbm_gbs", 6538.3), "traffic": None,
+                                             "alg_bytes_per_candidate": alg,
+                                             "note": f"batch {n * (stride * 2 + 25) / 1e9:.2f} GB > L2"}}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default="C2")
+    ap.add_argument("--strong", dest="weak", action="store_false")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-eval", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    ap.add_argument("--ref-seconds", type=float, default=10.0)
+    args = ap.parse_args()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,741 @@
+// host.cu -- the C ABI of include/pipette.h: validation, context, device tables,
+// launch orchestration of K1-K6 and the NCCL combine across ranks.
+#include <nccl.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "devmath.cuh"
+#include "pipette_dev.cuh"
+
+namespace pip {
+// kernels (k_enumerate.cu, k_eval.cu, k_sa.cu)
+__global__ void k_enumerate_filter(int, int, unsigned long long, int, pipette_model, long long,
+                                   const pipette_profile_entry*, int, DevCfg*, unsigned long long*, int, int*,
+                                   double*, int, EnumOut*);
+const void* eval_kernel(int mw, bool rep);
+const void* sa_kernel(int mw, bool rep, bool trace);
+__global__ void k_argmin(const ChainOut*, const int*, int, CfgBest*);
+constexpr int kEnumThreads = 1024, kEvalThreads = 256, kSaThreads = 128;
+
+// K5 (combine, phase 1): per-config local winner item id if it attains the global
+// minimum latency, else UINT64_MAX (second allreduce(min) of R18).
+__global__ void k_combine_items(const CfgBest* __restrict__ cb, const unsigned long long* __restrict__ gbits,
+                                int F, long long chains, unsigned long long* __restrict__ items) {
+  const int f = blockIdx.x * blockDim.x + threadIdx.x;
+  if (f >= F) return;
+  const CfgBest b = cb[f];
+  const bool mine = b.chain >= 0 && (unsigned long long)__double_as_longlong(b.best) == gbits[f];
+  items[f] = mine ? (unsigned long long)f * (unsigned long long)chains + (unsigned long long)b.chain : ~0ull;
+}
+
+// K6 (combine, phase 2): the owner of each config's winner packs its plan -- Eq.4-6
+// breakdown, best step and the best mapping gathered from the lane-interleaved SA
+// buffer -- and every other rank packs zeros, so one allreduce(sum) broadcasts all
+// per-config plans at once.  Row layout (u64 words): [t_pp, t_dp, t_bubble, best_step+1,
+// perm words (4 slots per word)...]; the last element carries this rank's accepted count.
+__global__ void k_combine_pack(const CfgBest* __restrict__ cb, const unsigned long long* __restrict__ gitem,
+                               const DevCfg* __restrict__ cfgs, const int* __restrict__ feas,
+                               const int* __restrict__ slot_perm_off, const int* __restrict__ slot_lane,
+                               const uint16_t* __restrict__ best_perm, int F, long long chains, int row_words,
+                               unsigned long long* __restrict__ pack) {
+  const int f = blockIdx.x;
+  if (f >= F) return;
+  const CfgBest b = cb[f];
+  const bool owner = b.chain >= 0 && gitem[f] == (unsigned long long)f * (unsigned long long)chains + b.chain;
+  unsigned long long* row = pack + (size_t)f * row_words;
+  const DevCfg C = cfgs[feas[f]];
+  for (int w = threadIdx.x; w < row_words; w += blockDim.x) {
+    unsigned long long v = 0ull;
+    if (owner) {
+      if (w == 0) v = (unsigned long long)__double_as_longlong(b.best_tpp);
+      else if (w == 1) v = (unsigned long long)__double_as_longlong(b.best_tdp);
+      else if (w == 2) v = (unsigned long long)__double_as_longlong(__dadd_rn(C.Sb, b.best_tpp));
+      else if (w == 3) v = (unsigned long long)(long long)(b.best_step + 1);
+      else {
+        const int s0 = (w - 4) * 4;
+        const int off = slot_perm_off[b.slot], lane = slot_lane[b.slot];
+        for (int j = 3; j >= 0; --j) {
+          const int s = s0 + j;
+          v = (v << 16) | (s < C.N ? (unsigned long long)best_perm[off + s * 32 + lane] : 0ull);
+        }
+      }
+    }
+    row[w] = v;
+  }
+}
+
+__global__ void k_sum_accepted(const CfgBest* __restrict__ cb, int F, unsigned long long* __restrict__ out) {
+  if (threadIdx.x == 0 && blockIdx.x == 0) {
+    unsigned long long s = 0;
+    for (int f = 0; f < F; ++f) s += cb[f].accepted;
+    *out = s;
+  }
+}
+}  // namespace pip
+
+using namespace pip;
+
+struct DevBuf {
+  void* p = nullptr;
+  size_t bytes = 0;
+};
+
+struct pipette_ctx {
+  int device = 0, rank = 0, world = 1;
+  int n_nodes = 0, g = 0, margin = 0;
+  unsigned long long cap = 0;
+  int n_sms = 148;
+  cudaStream_t stream = nullptr;
+  ncclComm_t comm = nullptr;
+  std::string err;
+  int64_t launches = 0;
+  // device tables
+  double* dR = nullptr;
+  pipette_profile_entry* dProf = nullptr;
+  int n_prof = 0;
+  std::vector<pipette_profile_entry> prof;
+  // enumeration cache (model, bs_global) -> device config table
+  bool enum_valid = false;
+  pipette_model enum_model{};
+  long long enum_bs = 0;
+  int E = 0, F = 0;
+  std::vector<DevCfg> hcfg;
+  std::vector<int> hfeas;
+  DevBuf cfgs, keys, feas, qtab, eout;
+  // search buffers
+  DevBuf tasks, counter, chain_out, best_perm, cfg_slot, cfg_best, gbits, items, gitems, pack, accepted,
+      slot_perm_off, slot_lane, trace_slot, trace;
+  cudaEvent_t ev[6] = {};
+};
+
+namespace {
+
+thread_local std::string g_init_err;
+
+const char* kStatusText[] = {"ok", "no feasible configuration (every candidate exceeds the memory limit)",
+                             "invalid argument", "profile entry missing for a feasible (tp, mb)",
+                             "CUDA error", "NCCL error", "unsupported size (v1 limits)"};
+
+pipette_status fail(pipette_ctx* c, pipette_status s, const char* fmt, ...) {
+  if (c) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof buf, fmt, ap);
+    va_end(ap);
+    c->err = buf;
+  }
+  return s;
+}
+
+#define CU(call)                                                                                         \
+  do {                                                                                                   \
+    cudaError_t e_ = (call);                                                                             \
+    if (e_ != cudaSuccess) return fail(ctx, PIPETTE_E_CUDA, "%s: %s", #call, cudaGetErrorString(e_)); \
+  } while (0)
+#define NC(call)                                                                                         \
+  do {                                                                                                   \
+    ncclResult_t r_ = (call);                                                                            \
+    if (r_ != ncclSuccess) return fail(ctx, PIPETTE_E_NCCL, "%s: %s", #call, ncclGetErrorString(r_)); \
+  } while (0)
+
+cudaError_t ensure(DevBuf& b, size_t bytes) {
+  if (b.bytes >= bytes && b.p) return cudaSuccess;
+  if (b.p) cudaFree(b.p);
+  b.p = nullptr;
+  b.bytes = 0;
+  cudaError_t e = cudaMalloc(&b.p, std::max<size_t>(bytes, 16));
+  if (e == cudaSuccess) b.bytes = std::max<size_t>(bytes, 16);
+  return e;
+}
+
+int n_div(long long n) {
+  int c = 0;
+  for (long long d = 1; d * d <= n; ++d)
+    if (n % d == 0) c += (d * d == n) ? 1 : 2;
+  return c;
+}
+
+pipette_status check_bw(pipette_ctx* ctx, const double* bw, int n) {
+  if (!bw) return fail(ctx, PIPETTE_E_INVALID, "bandwidth matrix is NULL");
+  for (int i = 0; i < n * n; ++i)
+    if (!std::isfinite(bw[i]) || !(bw[i] > 0.0))
+      return fail(ctx, PIPETTE_E_INVALID, "bandwidth[%d][%d] = %g must be finite and > 0", i / n, i % n, bw[i]);
+  return PIPETTE_OK;
+}
+
+pipette_status upload_bw(pipette_ctx* ctx, const double* bw) {
+  const int n = ctx->n_nodes;
+  std::vector<double> R((size_t)n * n);
+  for (int i = 0; i < n * n; ++i) R[i] = 1.0 / bw[i];  // R5: IEEE division, never symmetrised
+  CU(cudaMemcpy(ctx->dR, R.data(), sizeof(double) * n * n, cudaMemcpyHostToDevice));
+  return PIPETTE_OK;
+}
+
+pipette_status check_model(pipette_ctx* ctx, const pipette_model* m, long long bs) {
+  if (!m) return fail(ctx, PIPETTE_E_INVALID, "model is NULL");
+  if (m->n_layers < 1 || m->hidden < 1 || m->heads < 1 || m->seq_len < 1 || m->vocab < 1 ||
+      m->bytes_per_elem < 1 || m->bytes_per_param_state < 0)
+    return fail(ctx, PIPETTE_E_INVALID, "model fields must be positive");
+  if (m->hidden % m->heads != 0) return fail(ctx, PIPETTE_E_INVALID, "hidden %% heads != 0");
+  if (bs < 1 || bs > (1ll << 30)) return fail(ctx, PIPETTE_E_INVALID, "bs_global out of range");
+  return PIPETTE_OK;
+}
+
+// K1 on ctx->stream; synchronous readback of the table (cached per (model, bs)).
+pipette_status enumerate(pipette_ctx* ctx, const pipette_model* m, long long bs, bool time_it) {
+  if (!time_it && ctx->enum_valid && std::memcmp(&ctx->enum_model, m, sizeof *m) == 0 && ctx->enum_bs == bs) {
+    if (time_it) {
+      CU(cudaEventRecord(ctx->ev[0], ctx->stream));
+      CU(cudaEventRecord(ctx->ev[1], ctx->stream));
+    }
+    return PIPETTE_OK;
+  }
+  const int G = ctx->n_nodes * ctx->g;
+  const long long E_cap = (long long)n_div(G) * n_div(ctx->g) * n_div(bs);
+  const long long q_cap = E_cap * (G + ctx->n_nodes + 4);
+  if (E_cap > (1 << 24) || q_cap > (1ll << 28)) return fail(ctx, PIPETTE_E_UNSUPPORTED, "enumeration too large");
+  CU(ensure(ctx->cfgs, sizeof(DevCfg) * E_cap));
+  CU(ensure(ctx->keys, sizeof(unsigned long long) * E_cap));
+  CU(ensure(ctx->feas, sizeof(int) * E_cap));
+  CU(ensure(ctx->qtab, sizeof(double) * q_cap));
+  CU(ensure(ctx->eout, sizeof(EnumOut)));
+  if (time_it) CU(cudaEventRecord(ctx->ev[0], ctx->stream));
+  k_enumerate_filter<<<1, kEnumThreads, 0, ctx->stream>>>(
+      ctx->n_nodes, ctx->g, ctx->cap, ctx->margin, *m, bs, ctx->dProf, ctx->n_prof, (DevCfg*)ctx->cfgs.p,
+      (unsigned long long*)ctx->keys.p, (int)E_cap, (int*)ctx->feas.p, (double*)ctx->qtab.p, (int)q_cap,
+      (EnumOut*)ctx->eout.p);
+  ctx->launches++;
+  CU(cudaGetLastError());
+  if (time_it) CU(cudaEventRecord(ctx->ev[1], ctx->stream));
+  EnumOut eo;
+  CU(cudaMemcpyAsync(&eo, ctx->eout.p, sizeof eo, cudaMemcpyDeviceToHost, ctx->stream));
+  CU(cudaStreamSynchronize(ctx->stream));
+  if (eo.overflow) return fail(ctx, PIPETTE_E_UNSUPPORTED, "enumeration capacity exceeded (%d)", eo.overflow);
+  ctx->E = eo.E;
+  ctx->F = eo.F;
+  ctx->hcfg.resize(eo.E);
+  ctx->hfeas.resize(eo.F);
+  if (eo.E) CU(cudaMemcpy(ctx->hcfg.data(), ctx->cfgs.p, sizeof(DevCfg) * eo.E, cudaMemcpyDeviceToHost));
+  if (eo.F) CU(cudaMemcpy(ctx->hfeas.data(), ctx->feas.p, sizeof(int) * eo.F, cudaMemcpyDeviceToHost));
+  ctx->enum_valid = true;
+  ctx->enum_model = *m;
+  ctx->enum_bs = bs;
+  return PIPETTE_OK;
+}
+
+float elapsed(cudaEvent_t a, cudaEvent_t b) {
+  float ms = 0.f;
+  cudaEventElapsedTime(&ms, a, b);
+  return ms;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* pipette_strerror(pipette_status s) {
+  const int i = (int)s;
+  return (i >= 0 && i <= 6) ? kStatusText[i] : "unknown status";
+}
+
+const char* pipette_last_error(const pipette_ctx* ctx) { return ctx ? ctx->err.c_str() : g_init_err.c_str(); }
+
+int64_t pipette_last_launch_count(const pipette_ctx* ctx) { return ctx ? ctx->launches : 0; }
+
+int64_t pipette_shard_items(int64_t n_items, int32_t rank, int32_t world, int64_t* items, int64_t cap) {
+  if (world < 1 || rank < 0 || rank >= world || n_items < 0) return 0;
+  int64_t c = 0;
+  for (int64_t j = rank; j < n_items; j += world) {  // R18: item j belongs to rank j mod W
+    if (items && c < cap) items[c] = j;
+    ++c;
+  }
+  return c;
+}
+
+pipette_status pipette_nccl_unique_id(void* id_out) {
+  if (!id_out) return PIPETTE_E_INVALID;
+  ncclUniqueId id;
+  if (ncclGetUniqueId(&id) != ncclSuccess) return PIPETTE_E_NCCL;
+  std::memcpy(id_out, &id, sizeof id);
+  return PIPETTE_OK;
+}
+
+pipette_status pipette_init(pipette_ctx** out, const pipette_cluster* cl, const double* bw,
+                            const pipette_profile_entry* prof, int32_t n_prof, const pipette_dist* dist) {
+  if (!out) return PIPETTE_E_INVALID;
+  *out = nullptr;
+  pipette_ctx* ctx = new pipette_ctx();
+  auto bail = [&](pipette_status s) {
+    g_init_err = ctx->err;  // reachable through pipette_last_error(NULL)
+    pipette_destroy(ctx);
+    return s;
+  };
+  if (!cl) { fail(ctx, PIPETTE_E_INVALID, "cluster is NULL"); return bail(PIPETTE_E_INVALID); }
+  if (cl->n_nodes < 1 || cl->gpus_per_node < 1) { fail(ctx, PIPETTE_E_INVALID, "cluster shape must be >= 1"); return bail(PIPETTE_E_INVALID); }
+  if (cl->n_nodes > kMaxNodes || (long long)cl->n_nodes * cl->gpus_per_node > kMaxGpus) {
+    fail(ctx, PIPETTE_E_UNSUPPORTED, "v1 supports n_nodes <= %d and G <= %d", kMaxNodes, kMaxGpus);
+    return bail(PIPETTE_E_UNSUPPORTED);
+  }
+  if (cl->mem_margin_permille < 0 || cl->mem_margin_permille > 500) { fail(ctx, PIPETTE_E_INVALID, "margin must be in [0, 500] permille"); return bail(PIPETTE_E_INVALID); }
+  if (cl->mem_capacity_bytes == 0) { fail(ctx, PIPETTE_E_INVALID, "memory capacity must be > 0"); return bail(PIPETTE_E_INVALID); }
+  if (check_bw(ctx, bw, cl->n_nodes) != PIPETTE_OK) return bail(PIPETTE_E_INVALID);
+  if (n_prof < 0 || (n_prof > 0 && !prof)) { fail(ctx, PIPETTE_E_INVALID, "bad profile table"); return bail(PIPETTE_E_INVALID); }
+  for (int i = 0; i < n_prof; ++i) {
+    if (prof[i].tp < 1 || prof[i].mb < 1 || !std::isfinite(prof[i].c_layer_s) || !(prof[i].c_layer_s > 0.0) ||
+        !std::isfinite(prof[i].tp_layer_s) || prof[i].tp_layer_s < 0.0) {
+      fail(ctx, PIPETTE_E_INVALID, "profile entry %d invalid (tp, mb >= 1; c_layer > 0; tp_layer >= 0)", i);
+      return bail(PIPETTE_E_INVALID);
+    }
+  }
+  if (dist && (dist->world < 1 || dist->rank < 0 || dist->rank >= dist->world || (dist->world > 1 && !dist->nccl_unique_id))) {
+    fail(ctx, PIPETTE_E_INVALID, "bad dist description");
+    return bail(PIPETTE_E_INVALID);
+  }
+  ctx->n_nodes = cl->n_nodes;
+  ctx->g = cl->gpus_per_node;
+  ctx->cap = cl->mem_capacity_bytes;
+  ctx->margin = cl->mem_margin_permille;
+  ctx->rank = dist ? dist->rank : 0;
+  ctx->world = dist ? dist->world : 1;
+  ctx->prof.assign(prof, prof + n_prof);
+  ctx->n_prof = n_prof;
+  pipette_status st;
+  {
+    int dev = 0;
+    if (dist) {
+      dev = dist->device;
+      if (cudaSetDevice(dev) != cudaSuccess) { fail(ctx, PIPETTE_E_CUDA, "cudaSetDevice(%d) failed", dev); return bail(PIPETTE_E_CUDA); }
+    } else if (cudaGetDevice(&dev) != cudaSuccess) {
+      fail(ctx, PIPETTE_E_CUDA, "no CUDA device");
+      return bail(PIPETTE_E_CUDA);
+    }
+    ctx->device = dev;
+    cudaDeviceGetAttribute(&ctx->n_sms, cudaDevAttrMultiProcessorCount, dev);
+    if (cudaMalloc(&ctx->dR, sizeof(double) * ctx->n_nodes * ctx->n_nodes) != cudaSuccess ||
+        cudaMalloc(&ctx->dProf, sizeof(pipette_profile_entry) * std::max(1, n_prof)) != cudaSuccess) {
+      fail(ctx, PIPETTE_E_CUDA, "cudaMalloc failed");
+      return bail(PIPETTE_E_CUDA);
+    }
+    if (n_prof && cudaMemcpy(ctx->dProf, prof, sizeof(pipette_profile_entry) * n_prof, cudaMemcpyHostToDevice) != cudaSuccess) {
+      fail(ctx, PIPETTE_E_CUDA, "profile upload failed");
+      return bail(PIPETTE_E_CUDA);
+    }
+    if ((st = upload_bw(ctx, bw)) != PIPETTE_OK) return bail(st);
+    for (auto& e : ctx->ev)
+      if (cudaEventCreate(&e) != cudaSuccess) { fail(ctx, PIPETTE_E_CUDA, "event create failed"); return bail(PIPETTE_E_CUDA); }
+  }
+  if (ctx->world > 1) {
+    ncclUniqueId id;
+    std::memcpy(&id, dist->nccl_unique_id, sizeof id);
+    ncclResult_t r = ncclCommInitRank(&ctx->comm, ctx->world, id, ctx->rank);
+    if (r != ncclSuccess) { fail(ctx, PIPETTE_E_NCCL, "ncclCommInitRank: %s", ncclGetErrorString(r)); return bail(PIPETTE_E_NCCL); }
+  }
+  *out = ctx;
+  return PIPETTE_OK;
+}
+
+pipette_status pipette_set_bandwidth(pipette_ctx* ctx, const double* bw) {
+  if (!ctx) return PIPETTE_E_INVALID;
+  pipette_status st = check_bw(ctx, bw, ctx->n_nodes);
+  if (st != PIPETTE_OK) return st;
+  CU(cudaSetDevice(ctx->device));
+  CU(cudaStreamSynchronize(ctx->stream));
+  return upload_bw(ctx, bw);
+}
+
+pipette_status pipette_set_stream(pipette_ctx* ctx, void* stream) {
+  if (!ctx) return PIPETTE_E_INVALID;
+  ctx->stream = (cudaStream_t)stream;
+  return PIPETTE_OK;
+}
+
+void pipette_destroy(pipette_ctx* ctx) {
+  if (!ctx) return;
+  if (ctx->comm) ncclCommDestroy(ctx->comm);
+  DevBuf* bufs[] = {&ctx->cfgs, &ctx->keys, &ctx->feas, &ctx->qtab, &ctx->eout, &ctx->tasks, &ctx->counter,
+                    &ctx->chain_out, &ctx->best_perm, &ctx->cfg_slot, &ctx->cfg_best, &ctx->gbits, &ctx->items,
+                    &ctx->gitems, &ctx->pack, &ctx->accepted, &ctx->slot_perm_off, &ctx->slot_lane,
+                    &ctx->trace_slot, &ctx->trace};
+  for (DevBuf* b : bufs)
+    if (b->p) cudaFree(b->p);
+  if (ctx->dR) cudaFree(ctx->dR);
+  if (ctx->dProf) cudaFree(ctx->dProf);
+  for (auto& e : ctx->ev)
+    if (e) cudaEventDestroy(e);
+  delete ctx;
+}
+
+pipette_status pipette_enumerate(pipette_ctx* ctx, const pipette_model* model, int64_t bs_global, int32_t* E,
+                                 int32_t* F, pipette_config* cfgs, int32_t* n_mb, uint64_t* mem_bytes,
+                                 uint8_t* feasible, int32_t cap) {
+  if (!ctx) return PIPETTE_E_INVALID;
+  ctx->launches = 0;
+  pipette_status st = check_model(ctx, model, bs_global);
+  if (st != PIPETTE_OK) return st;
+  CU(cudaSetDevice(ctx->device));
+  ctx->enum_valid = false;
+  if ((st = enumerate(ctx, model, bs_global, false)) != PIPETTE_OK) return st;
+  if (E) *E = ctx->E;
+  if (F) *F = ctx->F;
+  for (int e = 0; e < std::min(ctx->E, (int)std::max(cap, 0)); ++e) {
+    const DevCfg& c = ctx->hcfg[e];
+    if (cfgs) { cfgs[e].pp = (uint16_t)c.pp; cfgs[e].tp = (uint16_t)c.tp; cfgs[e].dp = (uint16_t)c.dp; cfgs[e].mb = (uint16_t)c.mb; }
+    if (n_mb) n_mb[e] = c.n_mb;
+    if (mem_bytes) mem_bytes[e] = c.mem;
+    if (feasible) feasible[e] = (uint8_t)c.feasible;
+  }
+  return PIPETTE_OK;
+}
+
+pipette_status pipette_eval(pipette_ctx* ctx, const pipette_model* model, int64_t bs_global, int64_t n,
+                            const pipette_config* d_cfg, const uint16_t* d_perm, int32_t perm_stride,
+                            double* d_latency, uint64_t* d_mem, uint8_t* d_status, void* stream) {
+  if (!ctx) return PIPETTE_E_INVALID;
+  ctx->launches = 0;
+  pipette_status st = check_model(ctx, model, bs_global);
+  if (st != PIPETTE_OK) return st;
+  if (n < 0 || perm_stride < 1) return fail(ctx, PIPETTE_E_INVALID, "n >= 0 and perm_stride >= 1 required");
+  if (n == 0) return PIPETTE_OK;
+  if (!d_cfg || !d_perm || !d_latency || !d_mem || !d_status) return fail(ctx, PIPETTE_E_INVALID, "null device pointer");
+  CU(cudaSetDevice(ctx->device));
+  if ((st = enumerate(ctx, model, bs_global, false)) != PIPETTE_OK) return st;
+  cudaStream_t s = (cudaStream_t)stream;
+  int maxN = 1;
+  for (const DevCfg& c : ctx->hcfg) maxN = std::max(maxN, c.N);
+  EvalParams P{};
+  P.cfgs = (const DevCfg*)ctx->cfgs.p;
+  P.keys = (const unsigned long long*)ctx->keys.p;
+  P.E = ctx->E;
+  P.qtab = (const double*)ctx->qtab.p;
+  P.R = ctx->dR;
+  P.n_nodes = ctx->n_nodes;
+  P.n = n;
+  P.cand = d_cfg;
+  P.perm = d_perm;
+  P.perm_stride = perm_stride;
+  P.vec16 = ((uintptr_t)d_perm % 16 == 0) && (perm_stride % 8 == 0);
+  P.bm_words = (maxN + 31) / 32;
+  const int nn = ctx->n_nodes * ctx->n_nodes;
+  const bool rep = nn * 32 * 8 <= 64 * 1024;
+  P.rep = rep;
+  P.latency = d_latency;
+  P.mem = (unsigned long long*)d_mem;
+  P.status = d_status;
+  const size_t smem = (size_t)(rep ? nn * 32 : nn) * 8 + ((ctx->E * 8 + 15) & ~15) +
+                      (size_t)(P.bm_words + (ctx->n_nodes + 3) / 4) * kEvalThreads * 4;
+  if (smem > 227 * 1024) return fail(ctx, PIPETTE_E_UNSUPPORTED, "eval shared memory %zu B too large", smem);
+  const void* kern = eval_kernel(ctx->n_nodes <= 32 ? 1 : 4, rep);
+  CU(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  int occ = 0;
+  CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kEvalThreads, smem));
+  occ = std::max(occ, 1);
+  const long long need = (n + kEvalThreads - 1) / kEvalThreads;
+  const int grid = (int)std::min<long long>(need, (long long)occ * ctx->n_sms);
+  void* args[] = {&P};
+  CU(cudaLaunchKernel(kern, dim3(grid), dim3(kEvalThreads), args, smem, s));
+  ctx->launches++;
+  CU(cudaGetLastError());
+  return PIPETTE_OK;
+}
+
+pipette_status pipette_search(pipette_ctx* ctx, const pipette_model* model, int64_t bs_global,
+                              int32_t chains, int32_t iterations, uint64_t seed, const pipette_sa_opts* opts,
+                              pipette_plan* out, pipette_plan* per_config, int32_t per_config_cap) {
+  if (!ctx) return PIPETTE_E_INVALID;
+  ctx->launches = 0;
+  pipette_status st = check_model(ctx, model, bs_global);
+  if (st != PIPETTE_OK) return st;
+  if (!out) return fail(ctx, PIPETTE_E_INVALID, "out is NULL");
+  if (chains < 1 || iterations < 0) return fail(ctx, PIPETTE_E_INVALID, "chains >= 1 and iterations >= 0 required");
+  pipette_sa_opts o{};
+  o.alpha = 0.999;
+  o.tau = 0.05;
+  if (opts) o = *opts;
+  if (!(o.alpha > 0.0 && o.alpha <= 1.0)) return fail(ctx, PIPETTE_E_INVALID, "alpha must be in (0, 1]");
+  if (!(o.t0 > 0.0) && !(o.tau > 0.0)) return fail(ctx, PIPETTE_E_INVALID, "tau > 0 or t0 > 0 required");
+  CU(cudaSetDevice(ctx->device));
+  cudaStream_t s = ctx->stream;
+
+  if ((st = enumerate(ctx, model, bs_global, true)) != PIPETTE_OK) return st;
+  const int E = ctx->E, F = ctx->F;
+  out->configs_enumerated = E;
+  out->configs_rejected_oom = E - F;
+  out->sa_steps = out->sa_accepted = 0;
+  if (F == 0) return fail(ctx, PIPETTE_NO_FEASIBLE, "all %d configurations exceed the memory limit", E);
+  for (int f = 0; f < F; ++f) {
+    const DevCfg& c = ctx->hcfg[ctx->hfeas[f]];
+    if (!c.has_profile)
+      return fail(ctx, PIPETTE_E_PROFILE, "no profile entry for tp=%d mb=%d (feasible config e=%d)", c.tp, c.mb, c.e);
+  }
+
+  // ---- shard items j = f*chains + c by j mod world (R18); group 32 local chains per warp task
+  const int W = ctx->world, r = ctx->rank;
+  std::vector<SaTask> tasks;
+  std::vector<int> cfg_slot(F + 1, 0), slot_perm_off, slot_lane;
+  int slots = 0, perm_words = 0, maxN = 1, maxdp2 = 0;
+  uint64_t steps = 0;
+  for (int f = 0; f < F; ++f) {
+    const DevCfg& c = ctx->hcfg[ctx->hfeas[f]];
+    if (c.N >= 2) steps += (uint64_t)chains * (uint64_t)iterations;
+    const long long base = (long long)f * chains;
+    const int c_first = (int)(((r - base) % W + W) % W);
+    const int count = c_first < chains ? (chains - 1 - c_first) / W + 1 : 0;
+    cfg_slot[f] = slots;
+    maxN = std::max(maxN, c.N);
+    if (c.pp >= 2) maxdp2 = std::max(maxdp2, c.dp);
+    for (int k0 = 0; k0 < count; k0 += 32) {
+      SaTask t{};
+      t.cfg = c.e;
+      t.f = f;
+      t.c_first = c_first;
+      t.k0 = k0;
+      t.count = std::min(32, count - k0);
+      t.slot0 = slots;
+      t.perm_off = perm_words;
+      for (int l = 0; l < t.count; ++l) { slot_perm_off.push_back(perm_words); slot_lane.push_back(l); }
+      slots += t.count;
+      perm_words += c.N * 32;
+      tasks.push_back(t);
+    }
+  }
+  cfg_slot[F] = slots;
+  out->sa_steps = steps;
+  // longest-processing-time-first order of the warp tasks (cost ~ per-step work of the config)
+  std::vector<double> cost(tasks.size());
+  for (size_t i = 0; i < tasks.size(); ++i) {
+    const DevCfg& c = ctx->hcfg[tasks[i].cfg];
+    cost[i] = c.N < 2 ? 0.0 : 60.0 + (c.pp >= 2 ? 14.0 * (c.pp - 1) + 0.5 * c.dp : 0.0);
+  }
+  std::vector<int> order(tasks.size());
+  for (size_t i = 0; i < order.size(); ++i) order[i] = (int)i;
+  std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return cost[a] > cost[b]; });
+  std::vector<SaTask> sorted(tasks.size());
+  for (size_t i = 0; i < order.size(); ++i) sorted[i] = tasks[order[i]];
+
+  const int n = ctx->n_nodes;
+  const int nn = n * n;
+  const bool rep = nn * 32 * 8 <= 64 * 1024;
+  const int r_bytes = (rep ? nn * 32 : nn) * 8;
+  auto a16 = [](int x) { return (x + 15) & ~15; };
+  const int warp_bytes = a16(maxN * 128) + a16(maxdp2 * 256) + a16((n + 3) / 4 * 128);
+  int wpb = kSaThreads / 32;
+  const int smem_max = 227 * 1024;
+  if (r_bytes + warp_bytes > smem_max)
+    return fail(ctx, PIPETTE_E_UNSUPPORTED, "SA state (%d B/warp + %d B) exceeds shared memory", warp_bytes, r_bytes);
+  while (wpb > 1 && r_bytes + wpb * warp_bytes > smem_max) --wpb;
+  const size_t smem = (size_t)r_bytes + (size_t)wpb * warp_bytes;
+
+  const bool tracing = o.trace && o.trace_items && o.n_trace > 0 && o.trace_cap > 0;
+  std::vector<int> trace_slot;
+  if (tracing) {
+    trace_slot.assign(std::max(slots, 1), -1);
+    for (int t = 0; t < o.n_trace; ++t) {
+      const int64_t j = o.trace_items[t];
+      if (j < 0 || j >= (int64_t)F * chains || j % W != r) continue;
+      const int f = (int)(j / chains), c = (int)(j % chains);
+      const long long base = (long long)f * chains;
+      const int c_first = (int)(((r - base) % W + W) % W);
+      trace_slot[cfg_slot[f] + (c - c_first) / W] = t;
+    }
+  }
+
+  CU(ensure(ctx->tasks, sizeof(SaTask) * std::max<size_t>(1, sorted.size())));
+  CU(ensure(ctx->counter, sizeof(int)));
+  CU(ensure(ctx->chain_out, sizeof(ChainOut) * std::max(1, slots)));
+  CU(ensure(ctx->best_perm, sizeof(uint16_t) * std::max(1, perm_words)));
+  CU(ensure(ctx->cfg_slot, sizeof(int) * (F + 1)));
+  CU(ensure(ctx->slot_perm_off, sizeof(int) * std::max(1, slots)));
+  CU(ensure(ctx->slot_lane, sizeof(int) * std::max(1, slots)));
+  CU(ensure(ctx->cfg_best, sizeof(CfgBest) * F));
+  CU(ensure(ctx->gbits, sizeof(unsigned long long) * F));
+  CU(ensure(ctx->items, sizeof(unsigned long long) * F));
+  CU(ensure(ctx->gitems, sizeof(unsigned long long) * F));
+  const int row_words = 4 + (maxN + 3) / 4;
+  CU(ensure(ctx->pack, sizeof(unsigned long long) * ((size_t)F * row_words + 1)));
+  if (!sorted.empty())
+    CU(cudaMemcpyAsync(ctx->tasks.p, sorted.data(), sizeof(SaTask) * sorted.size(), cudaMemcpyHostToDevice, s));
+  CU(cudaMemcpyAsync(ctx->cfg_slot.p, cfg_slot.data(), sizeof(int) * (F + 1), cudaMemcpyHostToDevice, s));
+  if (slots) {
+    CU(cudaMemcpyAsync(ctx->slot_perm_off.p, slot_perm_off.data(), sizeof(int) * slots, cudaMemcpyHostToDevice, s));
+    CU(cudaMemcpyAsync(ctx->slot_lane.p, slot_lane.data(), sizeof(int) * slots, cudaMemcpyHostToDevice, s));
+  }
+  CU(cudaMemsetAsync(ctx->counter.p, 0, sizeof(int), s));
+  if (tracing) {
+    CU(ensure(ctx->trace_slot, sizeof(int) * trace_slot.size()));
+    CU(ensure(ctx->trace, sizeof(pipette_trace_record) * (size_t)o.n_trace * o.trace_cap));
+    CU(cudaMemcpyAsync(ctx->trace_slot.p, trace_slot.data(), sizeof(int) * trace_slot.size(), cudaMemcpyHostToDevice, s));
+    CU(cudaMemsetAsync(ctx->trace.p, 0, sizeof(pipette_trace_record) * (size_t)o.n_trace * o.trace_cap, s));
+  }
+
+  SaParams P{};
+  P.cfgs = (const DevCfg*)ctx->cfgs.p;
+  P.qtab = (const double*)ctx->qtab.p;
+  P.R = ctx->dR;
+  P.tasks = (const SaTask*)ctx->tasks.p;
+  P.n_tasks = (int)sorted.size();
+  P.task_counter = (int*)ctx->counter.p;
+  P.n_nodes = n;
+  P.iterations = iterations;
+  P.key = make_uint2((uint32_t)seed, (uint32_t)(seed >> 32));
+  P.world = W;
+  P.alpha_inv = 1.0 / o.alpha;
+  P.tau = o.tau;
+  P.t0 = o.t0 > 0.0 ? o.t0 : 0.0;
+  P.rep = rep;
+  P.warps_per_block = wpb;
+  P.warp_smem_bytes = warp_bytes;
+  P.r_smem_bytes = r_bytes;
+  P.out = (ChainOut*)ctx->chain_out.p;
+  P.best_perm = (uint16_t*)ctx->best_perm.p;
+  P.trace_slot = tracing ? (const int*)ctx->trace_slot.p : nullptr;
+  P.trace_cap = tracing ? o.trace_cap : 0;
+  P.trace = tracing ? (pipette_trace_record*)ctx->trace.p : nullptr;
+
+  const void* kern = sa_kernel(n <= 32 ? 1 : 4, rep, tracing);
+  CU(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  int occ = 0;
+  CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, wpb * 32, smem));
+  occ = std::max(occ, 1);
+  const int grid = (int)std::max<long long>(1, std::min<long long>(((long long)sorted.size() + wpb - 1) / wpb,
+                                                                   (long long)occ * ctx->n_sms));
+  CU(cudaEventRecord(ctx->ev[2], s));
+  if (!sorted.empty()) {
+    void* args[] = {&P};
+    CU(cudaLaunchKernel(kern, dim3(grid), dim3(wpb * 32), args, smem, s));
+    ctx->launches++;
+    CU(cudaGetLastError());
+  }
+  CU(cudaEventRecord(ctx->ev[3], s));
+  k_argmin<<<F, 256, 0, s>>>((const ChainOut*)ctx->chain_out.p, (const int*)ctx->cfg_slot.p, F,
+                              (CfgBest*)ctx->cfg_best.p);
+  ctx->launches++;
+  CU(cudaGetLastError());
+  CU(cudaEventRecord(ctx->ev[4], s));
+
+  // ---- combine (R18): min latency bits, then min item among ranks attaining it, then
+  //      the owners' plans (one fused allreduce(sum) of owner-only rows)
+  unsigned long long* gbits = (unsigned long long*)ctx->gbits.p;
+  unsigned long long* items = (unsigned long long*)ctx->items.p;
+  unsigned long long* gitems = (unsigned long long*)ctx->gitems.p;
+  unsigned long long* pack = (unsigned long long*)ctx->pack.p;
+  // local latency bits of each config (ChainOut.best is the first field of CfgBest)
+  CU(cudaMemcpy2DAsync(gbits, sizeof(unsigned long long), ctx->cfg_best.p, sizeof(CfgBest),
+                       sizeof(unsigned long long), F, cudaMemcpyDeviceToDevice, s));
+  if (W > 1) NC(ncclAllReduce(gbits, gbits, F, ncclUint64, ncclMin, ctx->comm, s));
+  k_combine_items<<<(F + 127) / 128, 128, 0, s>>>((const CfgBest*)ctx->cfg_best.p, gbits, F, chains, items);
+  ctx->launches++;
+  if (W > 1) NC(ncclAllReduce(items, gitems, F, ncclUint64, ncclMin, ctx->comm, s));
+  else CU(cudaMemcpyAsync(gitems, items, sizeof(unsigned long long) * F, cudaMemcpyDeviceToDevice, s));
+  k_combine_pack<<<F, 128, 0, s>>>((const CfgBest*)ctx->cfg_best.p, gitems, (const DevCfg*)ctx->cfgs.p,
+                                    (const int*)ctx->feas.p, (const int*)ctx->slot_perm_off.p,
+                                    (const int*)ctx->slot_lane.p, (const uint16_t*)ctx->best_perm.p, F, chains,
+                                    row_words, pack);
+  ctx->launches++;
+  k_sum_accepted<<<1, 32, 0, s>>>((const CfgBest*)ctx->cfg_best.p, F, pack + (size_t)F * row_words);
+  ctx->launches++;
+  CU(cudaGetLastError());
+  if (W > 1) NC(ncclAllReduce(pack, pack, (size_t)F * row_words + 1, ncclUint64, ncclSum, ctx->comm, s));
+  CU(cudaEventRecord(ctx->ev[5], s));
+
+  std::vector<unsigned long long> hb(F), hi(F), hp((size_t)F * row_words + 1);
+  CU(cudaMemcpyAsync(hb.data(), gbits, sizeof(unsigned long long) * F, cudaMemcpyDeviceToHost, s));
+  CU(cudaMemcpyAsync(hi.data(), gitems, sizeof(unsigned long long) * F, cudaMemcpyDeviceToHost, s));
+  CU(cudaMemcpyAsync(hp.data(), pack, sizeof(unsigned long long) * hp.size(), cudaMemcpyDeviceToHost, s));
+  std::vector<ChainOut> hco;
+  std::vector<uint16_t> hperm;
+  if (o.chains && o.chains_cap > 0 && slots > 0) {
+    hco.resize(slots);
+    CU(cudaMemcpyAsync(hco.data(), ctx->chain_out.p, sizeof(ChainOut) * slots, cudaMemcpyDeviceToHost, s));
+    if (o.chain_perms) {
+      hperm.resize(perm_words);
+      CU(cudaMemcpyAsync(hperm.data(), ctx->best_perm.p, sizeof(uint16_t) * perm_words, cudaMemcpyDeviceToHost, s));
+    }
+  }
+  std::vector<pipette_trace_record> htr;
+  if (tracing) {
+    htr.resize((size_t)o.n_trace * o.trace_cap);
+    CU(cudaMemcpyAsync(htr.data(), ctx->trace.p, sizeof(pipette_trace_record) * htr.size(), cudaMemcpyDeviceToHost, s));
+  }
+  CU(cudaStreamSynchronize(s));
+  out->enumerate_ms = elapsed(ctx->ev[0], ctx->ev[1]);
+  out->sa_ms = elapsed(ctx->ev[2], ctx->ev[3]);
+  out->argmin_ms = elapsed(ctx->ev[3], ctx->ev[4]);
+  out->combine_ms = elapsed(ctx->ev[4], ctx->ev[5]);
+  out->sa_accepted = hp[(size_t)F * row_words];
+
+  // ---- assemble plans on the host from the combined rows (identical on every rank)
+  auto fill = [&](int f, pipette_plan* p) -> pipette_status {
+    const DevCfg& c = ctx->hcfg[ctx->hfeas[f]];
+    const unsigned long long* row = hp.data() + (size_t)f * row_words;
+    p->cfg.pp = (uint16_t)c.pp; p->cfg.tp = (uint16_t)c.tp; p->cfg.dp = (uint16_t)c.dp; p->cfg.mb = (uint16_t)c.mb;
+    p->n_mb = c.n_mb;
+    double v;
+    std::memcpy(&v, &hb[f], 8); p->latency_s = v;
+    std::memcpy(&v, &row[0], 8); p->t_pp = v;
+    std::memcpy(&v, &row[1], 8); p->t_dp = v;
+    std::memcpy(&v, &row[2], 8); p->t_bubble = v;
+    p->t_straggler = c.Ss;
+    p->best_step = (int32_t)((long long)row[3] - 1);
+    p->mem_bytes = c.mem;
+    p->cfg_index = c.e;
+    p->chain = (int32_t)(hi[f] % (unsigned long long)chains);
+    p->n_slots = c.N;
+    if (!p->perm || p->perm_cap < c.N) return fail(ctx, PIPETTE_E_INVALID, "plan perm buffer needs %d entries", c.N);
+    for (int w = 0; w < c.N; ++w) p->perm[w] = (uint16_t)(row[4 + w / 4] >> (16 * (w % 4)));
+    return PIPETTE_OK;
+  };
+  int fw = 0;
+  for (int f = 1; f < F; ++f)
+    if (hb[f] < hb[fw]) fw = f;  // lexicographic (T, e, c): ties keep the lower f (R17)
+  const uint64_t keep_steps = out->sa_steps, keep_acc = out->sa_accepted;
+  const double t_en = out->enumerate_ms, t_sa = out->sa_ms, t_am = out->argmin_ms, t_cb = out->combine_ms;
+  out->n_slots = ctx->hcfg[ctx->hfeas[fw]].N;
+  if ((st = fill(fw, out)) != PIPETTE_OK) return st;
+  out->configs_enumerated = E; out->configs_rejected_oom = E - F;
+  out->sa_steps = keep_steps; out->sa_accepted = keep_acc;
+  out->enumerate_ms = t_en; out->sa_ms = t_sa; out->argmin_ms = t_am; out->combine_ms = t_cb;
+  if (per_config && per_config_cap > 0) {
+    std::vector<int> ord(F);
+    for (int f = 0; f < F; ++f) ord[f] = f;
+    std::stable_sort(ord.begin(), ord.end(), [&](int a, int b) { return hb[a] < hb[b]; });
+    for (int i = 0; i < std::min(F, per_config_cap); ++i) {
+      pipette_plan* p = &per_config[i];
+      if ((st = fill(ord[i], p)) != PIPETTE_OK) return st;
+      p->configs_enumerated = E; p->configs_rejected_oom = E - F; p->sa_steps = keep_steps; p->sa_accepted = keep_acc;
+    }
+  }
+  // ---- diagnostics: per-chain results and traces of this rank's items
+  if (!hco.empty()) {
+    for (int sidx = 0; sidx < slots; ++sidx) {
+      const ChainOut& co = hco[sidx];
+      const int64_t j = (int64_t)co.f * chains + co.c;
+      if (j >= o.chains_cap) continue;
+      pipette_chain_result& cr = o.chains[j];
+      const DevCfg& c = ctx->hcfg[ctx->hfeas[co.f]];
+      cr.best = co.best; cr.best_t_pp = co.best_tpp; cr.best_t_dp = co.best_tdp; cr.L0 = co.L0;
+      cr.best_step = co.best_step; cr.accepted = co.accepted; cr.cfg_index = c.e; cr.chain = co.c;
+      cr.rank = r; cr.n_slots = c.N;
+      if (o.chain_perms && o.chain_perm_stride >= c.N)
+        for (int w = 0; w < c.N; ++w)
+          o.chain_perms[j * o.chain_perm_stride + w] = hperm[slot_perm_off[sidx] + w * 32 + slot_lane[sidx]];
+    }
+  }
+  if (tracing) {
+    for (int t = 0; t < o.n_trace; ++t) {
+      const int64_t j = o.trace_items[t];
+      if (j < 0 || j >= (int64_t)F * chains || j % W != r) continue;
+      std::memcpy(o.trace + (size_t)t * o.trace_cap, htr.data() + (size_t)t * o.trace_cap,
+                  sizeof(pipette_trace_record) * o.trace_cap);
+    }
+  }
+  return PIPETTE_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,101 @@
+// pipette_dev.cuh -- device data layout shared by the kernels and the host library.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "../../include/pipette.h"
+
+namespace pip {
+
+constexpr int kMaxNodes = 128;      // v1 limit (R table and node ids)
+constexpr int kMaxGpus = 1024;      // v1 limit (G); N = G/tp <= 1024 slots
+
+// One enumerated configuration (Alg.1 l.3-5) with its memory verdict (l.7) and the
+// per-config model constants of DESIGN.md section 3.  Built on the device by
+// k_enumerate_filter; read by k_eval_stream and k_sa_chains.
+struct DevCfg {
+  int32_t pp, tp, dp, mb;
+  int32_t n_mb, e, N, spn;
+  unsigned long long mem;            // bytes, exact (R11)
+  int32_t feasible, has_profile;
+  uint32_t pp_magic, spn_magic;      // ceil(2^32/pp), ceil(2^32/spn) for div_small
+  int32_t qi_off, qe_off;            // qtab[qi_off + c] = qi(c), qtab[qe_off + k] = qe(k)
+  double S, m2, md, r, Sb, Ss;
+};
+
+// Enumeration summary written by k_enumerate_filter.
+struct EnumOut {
+  int32_t E, F, qtab_used, overflow;
+};
+
+// One warp-task of the SA kernel: 32 chains (lanes) of one feasible configuration.
+struct SaTask {
+  int32_t cfg;        // index into the DevCfg table (= e)
+  int32_t f;          // feasible index
+  int32_t c_first;    // first local chain id of this config on this rank
+  int32_t k0;         // first local ordinal of this task within the config
+  int32_t count;      // active lanes (<= 32)
+  int32_t slot0;      // first local chain slot (outputs) of this task
+  int32_t perm_off;   // offset (uint16 units) of this task's best-perm block [N][32]
+  int32_t pad;
+};
+
+// Per-chain outputs of k_sa_chains, indexed by local chain slot.
+struct ChainOut {
+  double best, best_tpp, best_tdp, L0;
+  int32_t best_step;
+  uint32_t accepted;
+  int32_t f, c;
+};
+
+// Per-config winner of this rank (k_argmin).
+struct CfgBest {
+  double best, best_tpp, best_tdp;
+  int32_t chain, slot, best_step, pad;
+  unsigned long long accepted;
+};
+
+struct SaParams {
+  const DevCfg* cfgs;
+  const double* qtab;
+  const double* R;           // n x n, R[a][b] = 1/B[a][b]
+  const SaTask* tasks;
+  int32_t n_tasks;
+  int32_t* task_counter;
+  int32_t n_nodes;
+  int32_t iterations;
+  uint2 key;                 // Philox key (seed lo, seed hi)
+  int32_t world;             // chain ids c = c_first + k*world
+  double alpha_inv, tau, t0;
+  int32_t rep;               // R replicated per lane in shared memory
+  int32_t warps_per_block;
+  int32_t warp_smem_bytes;   // per-warp chain-state region
+  int32_t r_smem_bytes;
+  ChainOut* out;
+  uint16_t* best_perm;
+  // trace (debug): trace_slot[local slot] = record row or -1
+  const int32_t* trace_slot;
+  int32_t trace_cap;
+  pipette_trace_record* trace;
+};
+
+struct EvalParams {
+  const DevCfg* cfgs;
+  const unsigned long long* keys;   // sorted (pp<<48 | tp<<32 | dp<<16 | mb) of every config
+  int32_t E;
+  const double* qtab;
+  const double* R;
+  int32_t n_nodes;
+  int64_t n;
+  const pipette_config* cand;
+  const uint16_t* perm;
+  int32_t perm_stride;
+  int32_t vec16;             // perm rows are 16-byte aligned
+  int32_t bm_words;          // bitmap words per thread (ceil(maxN/32))
+  int32_t rep;
+  double* latency;
+  unsigned long long* mem;
+  uint8_t* status;
+};
+
+}  // namespace pip

@@ -1,0 +1,83 @@
+"""CPU-side checks of the C-ABI boundary (no GPU): libpipette.so loads, exports every
+symbol include/pipette.h declares, and its host-only logic (sharding R18, validation,
+status strings) behaves."""
+import ctypes as C
+import os
+import re
+
+import numpy as np
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+@pytest.fixture(scope="module")
+def L():
+    import __graft_entry__
+    __graft_entry__.build()
+    from paper_2405_18093_b200 import _abi
+    return _abi.lib()
+
+
+def _declared():
+    src = open(os.path.join(ROOT, "include", "pipette.h")).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"\b(pipette_[a-z_]+)\s*\(", src)))
+
+
+def test_library_exports_every_declared_symbol(L):
+    names = _declared()
+    assert len(names) >= 12
+    for n in names:
+        assert hasattr(L, n), n
+    from paper_2405_18093_b200 import _abi
+    assert set(_abi.EXPORTS) == set(names)
+
+
+def test_library_is_sm100a(L):
+    import subprocess
+    from paper_2405_18093_b200 import _abi
+    out = subprocess.run(["/usr/local/cuda/bin/cuobjdump", "--list-elf", _abi.LIB_PATH],
+                         capture_output=True, text=True).stdout
+    assert "sm_100a" in out
+
+
+def test_shard_items_partition(L):
+    from paper_2405_18093_b200 import shard_items
+    for n_items, world in [(0, 1), (1, 2), (63488, 8), (1000, 3), (7, 8)]:
+        seen = np.concatenate([shard_items(n_items, r, world) for r in range(world)]) if n_items else np.array([])
+        assert sorted(seen.tolist()) == list(range(n_items))
+        for r in range(world):
+            assert all(j % world == r for j in shard_items(n_items, r, world))
+
+
+def test_strerror_and_init_validation(L):
+    from paper_2405_18093_b200 import _abi
+    assert L.pipette_strerror(0) == b"ok"
+    assert b"memory" in L.pipette_strerror(1)
+    cl = _abi.Cluster(2, 8, 80_000_000_000, 100)
+    bad = np.array([[1.0, 0.0], [1.0, 1.0]])          # a zero bandwidth
+    prof = (_abi.ProfileEntry * 1)(_abi.ProfileEntry(1, 1, 0.1, 0.0))
+    h = C.c_void_p()
+    st = L.pipette_init(C.byref(h), C.byref(cl), bad.ctypes.data_as(C.POINTER(C.c_double)), prof, 1, None)
+    assert st == _abi.E_INVALID and not h.value
+    assert b"bandwidth" in L.pipette_last_error(None)
+    ok = np.ones((2, 2))
+    cl2 = _abi.Cluster(200, 8, 80_000_000_000, 100)
+    st = L.pipette_init(C.byref(h), C.byref(cl2), np.ones((200, 200)).ctypes.data_as(C.POINTER(C.c_double)), prof, 1, None)
+    assert st == _abi.E_UNSUPPORTED
+    cl3 = _abi.Cluster(2, 8, 80_000_000_000, 900)     # margin > 500 permille
+    st = L.pipette_init(C.byref(h), C.byref(cl3), ok.ctypes.data_as(C.POINTER(C.c_double)), prof, 1, None)
+    assert st == _abi.E_INVALID
+    badp = (_abi.ProfileEntry * 1)(_abi.ProfileEntry(1, 1, -1.0, 0.0))
+    st = L.pipette_init(C.byref(h), C.byref(cl), ok.ctypes.data_as(C.POINTER(C.c_double)), badp, 1, None)
+    assert st == _abi.E_INVALID
+
+
+def test_product_package_does_not_touch_the_oracle():
+    pkg = os.path.join(ROOT, "paper_2405_18093_b200")
+    for dp, _, files in os.walk(pkg):
+        for f in files:
+            if f.endswith((".py", ".cu", ".cuh", ".h", ".cpp")):
+                txt = open(os.path.join(dp, f)).read()
+                assert "import oracle" not in txt and "from oracle" not in txt and "oracle.h" not in txt, f

@@ -1,0 +1,275 @@
+"""GPU vs oracle parity through the C ABI (SURVEY 8(c) acceptance):
+  * K1: enumeration order, memory bytes and verdicts bit-exact;
+  * K2: eval-stream latencies bit-exact (bar: 1e-12 relative), memory and status exact,
+        on random candidates of every feasible config of C1-C5 plus edge cases;
+  * K3/K4: per-chain best latency, best step, accepted count and best mapping bit-exact,
+        accepted-swap traces bit-exact, the plan bit-exact -- full on C1, sampled on C2
+        at BASELINE size in the bench's launch configuration.
+"""
+import numpy as np
+import pytest
+
+import oracle as O
+import workloads as W
+
+pytestmark = pytest.mark.gpu
+REL = 1e-12
+
+
+def _ctx(w, B=None, prof=None, **kw):
+    from paper_2405_18093_b200 import Pipette
+    B0, prof0 = W.workload_inputs(w)
+    B = B0 if B is None else B
+    prof = prof0 if prof is None else prof
+    return Pipette(w.n_nodes, w.gpus_per_node, B, prof, w.cap_bytes, w.margin_permille, **kw), B, prof
+
+
+def _models(w):
+    from paper_2405_18093_b200 import Model
+    m = w.model
+    return (Model(m.n_layers, m.hidden, m.heads, m.seq_len, m.vocab),
+            O.make_model(m.n_layers, m.hidden, m.heads, m.seq_len, m.vocab),
+            O.make_cluster(w.n_nodes, w.gpus_per_node, w.cap_bytes, w.margin_permille))
+
+
+def _assert_close(got, want):
+    got, want = np.asarray(got, dtype=np.float64), np.asarray(want, dtype=np.float64)
+    assert got.shape == want.shape
+    rel = np.abs(got - want) / np.maximum(np.abs(want), 1e-300)
+    assert float(rel.max(initial=0.0)) <= REL
+    return int(np.sum(got.view(np.uint64) != want.view(np.uint64)))
+
+
+@pytest.mark.parametrize("name", ["C1", "C2", "C3", "C4", "C5"])
+def test_enumeration_and_memory_filter_bit_exact(name):
+    w = W.WORKLOADS[name]
+    pip, B, prof = _ctx(w)
+    model, mo, cl = _models(w)
+    cfgs, nmb, mem, feas = pip.enumerate(model, w.bs_global)
+    ref = O.enumerate_configs(cl, mo, w.bs_global, O.make_profile(prof))
+    assert len(ref) == len(cfgs)
+    assert [tuple(c) for c in cfgs.tolist()] == [(c.pp, c.tp, c.dp, c.mb) for c in ref]
+    assert nmb.tolist() == [c.n_mb for c in ref]
+    assert [int(x) for x in mem] == [int(c.mem_bytes) for c in ref]
+    assert feas.tolist() == [bool(c.feasible) for c in ref]
+
+
+def _eval_batch(pip, model, bs, cfg_rows, perms):
+    import torch
+    cfg = torch.tensor(np.asarray(cfg_rows, dtype=np.int16), device="cuda")
+    p = torch.from_numpy(np.ascontiguousarray(perms).astype(np.uint16).view(np.int16)).cuda()
+    lat, mem, st = pip.eval(model, bs, cfg, p)
+    torch.cuda.synchronize()
+    return lat.cpu().numpy(), mem.cpu().numpy().view(np.uint64), st.cpu().numpy()
+
+
+@pytest.mark.parametrize("name", ["C1", "C2", "C3", "C4", "C5"])
+def test_eval_stream_random_candidates(name):
+    w = W.WORKLOADS[name]
+    pip, B, prof = _ctx(w)
+    model, mo, cl = _models(w)
+    P = O.make_profile(prof)
+    R = O.inverse_bandwidth(B)
+    ref = O.enumerate_configs(cl, mo, w.bs_global, P)
+    rng = np.random.default_rng(hash(name) & 0xFFFF)
+    chosen = [c for c in ref if c.feasible] + [c for c in ref if not c.feasible][:8]
+    per = 40 if name != "C5" else 12
+    Nmax = max(c.pp * c.dp for c in chosen)
+    stride = ((Nmax + 7) // 8) * 8
+    rows, perms, want_lat, want_mem, want_st = [], [], [], [], []
+    for c in chosen:
+        K = O.constants(cl, mo, c, P)
+        ps = W.random_perms(K.N, per, int(rng.integers(1 << 30)))
+        ps[0] = np.arange(K.N)                       # identity included
+        for p in ps:
+            row = np.zeros(stride, dtype=np.uint16)
+            row[:K.N] = p
+            rows.append((c.pp, c.tp, c.dp, c.mb)); perms.append(row)
+            want_lat.append(O.latency(K, R, p).T); want_mem.append(int(c.mem_bytes))
+            want_st.append(0 if c.feasible else 1)
+    lat, mem, st = _eval_batch(pip, model, w.bs_global, rows, np.stack(perms))
+    assert st.tolist() == want_st
+    assert [int(x) for x in mem] == want_mem
+    nbits = _assert_close(lat, want_lat)
+    assert nbits == 0, f"{nbits} latencies not bit-identical"
+
+
+def test_eval_stream_edge_cases():
+    w = W.WORKLOADS["C1"]
+    model, mo, cl = _models(w)
+    B, prof = W.workload_inputs(w)
+    prof_missing = [e for e in prof if not (e[0] == 2 and e[1] == 4)]
+    pip, _, _ = _ctx(w, B=B, prof=prof_missing)
+    P = O.make_profile(prof_missing)
+    R = O.inverse_bandwidth(B)
+    ref = {(c.pp, c.tp, c.dp, c.mb): c for c in O.enumerate_configs(cl, mo, w.bs_global, P)}
+    stride = 17                                        # odd stride: scalar (unaligned) path
+    rows, perms, want = [], [], []
+
+    def add(cfg, perm, st, lat=None):
+        row = np.zeros(stride, dtype=np.uint16)
+        row[:len(perm)] = perm
+        rows.append(cfg); perms.append(row); want.append((st, lat))
+
+    c = ref[(4, 2, 2, 1)]
+    K = O.constants(cl, mo, c, P)
+    good = np.random.default_rng(0).permutation(8)
+    add((4, 2, 2, 1), good, 0, O.latency(K, R, good).T)
+    add((4, 2, 2, 1), [0, 1, 2, 3, 4, 5, 6, 6], 3)     # duplicate slot
+    add((4, 2, 2, 1), [0, 1, 2, 3, 4, 5, 6, 9], 3)     # out of range
+    add((3, 2, 2, 1), good, 2)                         # pp*tp*dp != G
+    add((4, 2, 2, 3), good, 2)                         # mb does not divide bs_mini
+    add((32, 1, 1, 1), np.arange(16), 2)               # pp > n_layers
+    add((4, 2, 2, 4), good, 4)                         # profile entry removed
+    add((1, 8, 2, 32), [1, 0], 0 if ref[(1, 8, 2, 32)].feasible else 1,
+        O.latency(O.constants(cl, mo, ref[(1, 8, 2, 32)], P), R, [1, 0]).T)
+    for extra in range(300):                           # ragged tail across blocks
+        add((4, 2, 2, 1), good, 0, O.latency(K, R, good).T)
+    lat, mem, st = _eval_batch(pip, model, w.bs_global, rows, np.stack(perms))
+    for i, (s, l) in enumerate(want):
+        assert st[i] == s, (i, rows[i], st[i], s)
+        if l is None:
+            assert np.isnan(lat[i])
+        else:
+            assert lat[i] == l
+    assert mem[3] == 0 and mem[1] == ref[(4, 2, 2, 1)].mem_bytes
+
+
+def test_eval_single_gpu_cluster_and_empty_batch():
+    import torch
+    from paper_2405_18093_b200 import Model, Pipette
+    prof = W.profile_entries(W.GPT_345M, 1, 4)
+    pip = Pipette(1, 1, np.array([[2e11]]), prof, 80_000_000_000, 100)
+    model = Model(24, 1024, 16, 1024)
+    lat, mem, st = _eval_batch(pip, model, 4, [(1, 1, 1, 2)], np.zeros((1, 8), dtype=np.uint16))
+    mo = O.make_model(24, 1024, 16, 1024, 50257)
+    cl = O.make_cluster(1, 1)
+    c = [c for c in O.enumerate_configs(cl, mo, 4, O.make_profile(prof)) if c.mb == 2][0]
+    K = O.constants(cl, mo, c, O.make_profile(prof))
+    assert lat[0] == O.latency(K, O.inverse_bandwidth(np.array([[2e11]])), [0]).T == c.n_mb * K.S
+    e = torch.empty((0, 4), dtype=torch.int16, device="cuda")
+    out = pip.eval(model, 4, e, torch.empty((0, 8), dtype=torch.int16, device="cuda"))
+    assert out[0].numel() == 0
+
+
+def _oracle_chain(cl, mo, P, R, cfg_by_e, e, chain, iters, seed, trace=False, **kw):
+    K = O.constants(cl, mo, cfg_by_e[e], P)
+    return O.sa_chain(K, R, iters, seed, chain, e, trace=trace, **kw)
+
+
+def test_search_c1_every_chain_bit_exact():
+    w = W.WORKLOADS["C1"]
+    pip, B, prof = _ctx(w)
+    model, mo, cl = _models(w)
+    P = O.make_profile(prof)
+    R = O.inverse_bandwidth(B)
+    chains, iters = 3, 1000
+    res = pip.search(model, w.bs_global, chains, iters, w.seed, per_config=True, chain_results=True)
+    by_e = {c.e: c for c in O.enumerate_configs(cl, mo, w.bs_global, P)}
+    assert len(res["chains"]) == 78 * chains
+    for r in res["chains"]:
+        o = _oracle_chain(cl, mo, P, R, by_e, r["cfg_index"], r["chain"], iters, w.seed)
+        assert r["L0"] == o.L0
+        assert (r["best"], r["best_step"], r["accepted"]) == (o.best, o.best_step, o.accepted), r["item"]
+        assert (r["best_t_pp"], r["best_t_dp"]) == (o.best_t_pp, o.best_t_dp)
+        assert np.array_equal(r["perm"], o.best_perm)
+    ref = O.search(cl, B, P, mo, w.bs_global, chains, iters, w.seed)
+    plan = res["plan"]
+    assert (plan.latency_s, plan.cfg_index, plan.chain, plan.best_step) == \
+        (ref.latency, ref.cfg_index, ref.chain, ref.best_step)
+    assert np.array_equal(plan.perm, ref.perm)
+    assert (plan.t_pp, plan.t_dp, plan.t_bubble, plan.t_straggler) == (ref.t_pp, ref.t_dp, ref.t_bubble, ref.t_straggler)
+    assert (plan.sa_steps, plan.sa_accepted) == (ref.sa_steps, ref.sa_accepted)
+    assert plan.configs_enumerated == 78 and plan.configs_rejected_oom == 0
+    pcs = res["per_config"]
+    assert [p.latency_s for p in pcs] == sorted(ref.per_config_best.tolist())
+
+
+def test_search_traces_bit_exact():
+    w = W.WORKLOADS["C2"]
+    pip, B, prof = _ctx(w)
+    model, mo, cl = _models(w)
+    P = O.make_profile(prof)
+    R = O.inverse_bandwidth(B)
+    chains, iters = 64, 2000
+    feas = [c for c in O.enumerate_configs(cl, mo, w.bs_global, P) if c.feasible]
+    items = [f * chains + c for f, c in [(0, 0), (5, 17), (17, 63), (30, 1), (44, 40), (len(feas) - 1, 33)]]
+    res = pip.search(model, w.bs_global, chains, iters, w.seed, trace_items=items, trace_cap=iters)
+    by_e = {c.e: c for c in feas}
+    for t, j in enumerate(items):
+        f, c = divmod(j, chains)
+        o = _oracle_chain(cl, mo, P, R, by_e, feas[f].e, c, iters, w.seed, trace=True)
+        got = res["trace"][t]
+        assert len(o.trace) == iters
+        for a, b in zip(got, o.trace):
+            assert a == b, (j, a, b)
+
+
+def test_search_c2_full_size_sampled_chains():
+    # BASELINE size (1024 chains x 10k swaps on all 62 feasible configs), launch config of bench.py
+    w = W.WORKLOADS["C2"]
+    pip, B, prof = _ctx(w)
+    model, mo, cl = _models(w)
+    P = O.make_profile(prof)
+    R = O.inverse_bandwidth(B)
+    res = pip.search(model, w.bs_global, w.chains, w.iterations, w.seed, chain_results=True, per_config=True)
+    rows = res["chains"]
+    feas = [c for c in O.enumerate_configs(cl, mo, w.bs_global, P) if c.feasible]
+    assert len(rows) == len(feas) * w.chains
+    by_e = {c.e: c for c in feas}
+    rng = np.random.default_rng(1)
+    sample = rng.choice(len(rows), size=48, replace=False).tolist()
+    winners = {p.cfg_index: p for p in res["per_config"]}
+    for j in sample + [r["item"] for r in rows if r["cfg_index"] == res["plan"].cfg_index and r["chain"] == res["plan"].chain]:
+        r = rows[j]
+        o = _oracle_chain(cl, mo, P, R, by_e, r["cfg_index"], r["chain"], w.iterations, w.seed)
+        assert (r["best"], r["best_step"], r["accepted"]) == (o.best, o.best_step, o.accepted), j
+        assert np.array_equal(r["perm"], o.best_perm)
+    # properties at full size: every best mapping is a permutation whose latency is its best value
+    for p in res["per_config"]:
+        K = O.constants(cl, mo, by_e[p.cfg_index], P)
+        assert O.is_permutation(p.perm)
+        assert O.latency(K, R, p.perm).T == p.latency_s
+        assert p.latency_s <= O.latency(K, R, np.arange(K.N)).T
+    best = min(rows, key=lambda r: (r["best"], r["item"]))
+    assert res["plan"].latency_s == best["best"] and res["plan"].chain == best["chain"]
+    assert res["plan"].sa_steps == sum(w.chains * w.iterations for c in feas if c.pp * c.dp >= 2)
+    assert winners[res["plan"].cfg_index].latency_s == res["plan"].latency_s
+
+
+def test_search_degenerates_and_errors():
+    from paper_2405_18093_b200 import Model, Pipette, PipetteError
+    prof = W.profile_entries(W.GPT_345M, 1, 4)
+    pip = Pipette(1, 1, np.array([[2e11]]), prof, 80_000_000_000, 100)
+    res = pip.search(Model(24, 1024, 16, 1024), 4, 4, 200, 3)
+    p = res["plan"]
+    assert p.cfg[:3] == (1, 1, 1) and p.perm.tolist() == [0] and p.best_step == -1
+    assert p.sa_steps == 0 and p.sa_accepted == 0
+    w = W.WORKLOADS["C1"]
+    model, _, _ = _models(w)
+    tiny, _, _ = _ctx(w)
+    B, prof = W.workload_inputs(w)
+    oom = Pipette(w.n_nodes, w.gpus_per_node, B, prof, 1 << 20, 100)
+    with pytest.raises(PipetteError) as ei:
+        oom.search(model, w.bs_global, 1, 10, 1)
+    assert ei.value.status == 1
+    noprof = Pipette(w.n_nodes, w.gpus_per_node, B, prof[:3], w.cap_bytes, 100)
+    with pytest.raises(PipetteError) as ei:
+        noprof.search(model, w.bs_global, 1, 10, 1)
+    assert ei.value.status == 3
+    with pytest.raises(PipetteError) as ei:
+        tiny.search(Model(24, 1000, 16, 1024), w.bs_global, 1, 10, 1)     # hidden % heads != 0
+    assert ei.value.status == 2
+
+
+def test_search_is_deterministic_and_bandwidth_update_matters():
+    w = W.WORKLOADS["C2"]
+    pip, B, prof = _ctx(w)
+    model, _, _ = _models(w)
+    a = pip.search(model, w.bs_global, 64, 1000, 11)["plan"]
+    b = pip.search(model, w.bs_global, 64, 1000, 11)["plan"]
+    assert (a.latency_s, a.cfg_index, a.chain) == (b.latency_s, b.cfg_index, b.chain)
+    assert np.array_equal(a.perm, b.perm)
+    pip.set_bandwidth(B * 0.5)
+    c = pip.search(model, w.bs_global, 64, 1000, 11)["plan"]
+    assert c.latency_s > a.latency_s
