@@ -24,14 +24,42 @@ __device__ __forceinline__ uint4 philox4x32_10(uint4 c, uint2 k) {
   return c;
 }
 
+// Same generator with the ten round keys precomputed (they depend only on the seed, so the
+// SA kernel receives them as kernel parameters, i.e. constant-bank operands), and each
+// 32x32 multiply as one 64-bit IMAD.WIDE giving both halves.
+struct RoundKeys {
+  uint32_t x[10], y[10];
+};
+
+__host__ __device__ inline RoundKeys philox_round_keys(uint2 k) {
+  RoundKeys r;
+  for (int i = 0; i < 10; ++i) {
+    r.x[i] = k.x;
+    r.y[i] = k.y;
+    k.x += 0x9E3779B9u;
+    k.y += 0xBB67AE85u;
+  }
+  return r;
+}
+
+__device__ __forceinline__ uint4 philox4x32_10_rk(uint4 c, const RoundKeys& rk) {
+#pragma unroll
+  for (int r = 0; r < 10; ++r) {
+    const unsigned long long p0 = (unsigned long long)0xD2511F53u * c.x;
+    const unsigned long long p1 = (unsigned long long)0xCD9E8D57u * c.z;
+    c = make_uint4((uint32_t)(p1 >> 32) ^ c.y ^ rk.x[r], (uint32_t)p1, (uint32_t)(p0 >> 32) ^ c.w ^ rk.y[r],
+                   (uint32_t)p0);
+  }
+  return c;
+}
+
 // One proposal's randomness (R14): p uniform in [0,N), q uniform in [0,N)\{p}, u in [0,1).
 struct Draw {
   uint32_t p, q;
   double u;
 };
 
-__device__ __forceinline__ Draw draw_swap(uint32_t step, uint32_t chain, uint32_t e, uint2 key, uint32_t N) {
-  const uint4 w = philox4x32_10(make_uint4(step, chain, e, 0u), key);
+__device__ __forceinline__ Draw draw_from_words(uint4 w, uint32_t N) {
   Draw d;
   d.p = __umulhi(w.x, N);
   uint32_t q = d.p + 1u + __umulhi(w.y, N - 1u);
@@ -39,6 +67,15 @@ __device__ __forceinline__ Draw draw_swap(uint32_t step, uint32_t chain, uint32_
   const unsigned long long bits = ((unsigned long long)(w.z >> 5) << 26) | (unsigned long long)(w.w >> 6);
   d.u = __dmul_rn(__ull2double_rn(bits), 0x1p-53);
   return d;
+}
+
+__device__ __forceinline__ Draw draw_swap(uint32_t step, uint32_t chain, uint32_t e, uint2 key, uint32_t N) {
+  return draw_from_words(philox4x32_10(make_uint4(step, chain, e, 0u), key), N);
+}
+
+__device__ __forceinline__ Draw draw_swap_rk(uint32_t step, uint32_t chain, uint32_t e, const RoundKeys& rk,
+                                             uint32_t N) {
+  return draw_from_words(philox4x32_10_rk(make_uint4(step, chain, e, 0u), rk), N);
 }
 
 // e^x for x <= 0 from IEEE + - * and floor only (R15): Cody-Waite reduction by ln 2
@@ -71,6 +108,22 @@ __device__ __forceinline__ double exp_det(double x) {
 __device__ __forceinline__ bool metropolis(double d, double beta, double u) {
   if (d <= 0.0) return true;
   return u < exp_det(-__dmul_rn(d, beta));
+}
+
+// The same decision with a cheap screen: e^x is first approximated in fp32 (relative
+// error < 2e-5 for -87 <= x <= 0: argument rounding 5.2e-6, ex2.approx scaling 5.2e-6,
+// ex2.approx 2e-7), and exp_det (< 1 ulp from e^x) is evaluated only when u falls within
+// +-0.1% of the approximation.  Outside that band both give the same answer, so the
+// decision is bit-identical to metropolis().
+__device__ __forceinline__ bool metropolis_fast(double d, double beta, double u) {
+  if (d <= 0.0) return true;
+  const double x = -__dmul_rn(d, beta);
+  if (x < -708.0) return false;                       // exp_det(x) == 0 and u >= 0
+  if (x < -87.0) return u == 0.0;                     // e^x < 1.7e-38 < 2^-53 <= any u > 0
+  const double y = (double)__expf(__double2float_rn(x));
+  if (u < __dmul_rn(y, 0.999)) return true;
+  if (u > __dmul_rn(y, 1.001)) return false;
+  return u < exp_det(x);
 }
 
 // Eq.3-4 composition with the Eq.5 value inside T_bubble (R6):

@@ -584,6 +584,7 @@ pipette_status pipette_search(pipette_ctx* ctx, const pipette_model* model, int6
   P.n_nodes = n;
   P.iterations = iterations;
   P.key = make_uint2((uint32_t)seed, (uint32_t)(seed >> 32));
+  P.rk = philox_round_keys(P.key);
   P.world = W;
   P.alpha_inv = 1.0 / o.alpha;
   P.tau = o.tau;

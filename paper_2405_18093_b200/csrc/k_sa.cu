@@ -97,26 +97,57 @@ __device__ __forceinline__ double maxr_full(const Mask<MW>& m, const RTab<REP>& 
 
 // Eq.5 sum of pipeline z in stage order, with positions p and q holding nodes np and nq
 // after the proposed swap (P_z = ((0 + m2 R[..]) + m2 R[..]) + ...).
-template <bool REP>
-__device__ __forceinline__ double pipe_sum(int z, int pp, const uint32_t* pos, int lane, uint32_t p, uint32_t q,
+// PP > 0: compile-time pipeline depth (fully unrolled); PP == 0: runtime depth pp.
+template <bool REP, int PP>
+__device__ __forceinline__ uint32_t node_at(uint32_t w, const uint32_t* pos, int lane, uint32_t p, uint32_t q,
+                                            uint32_t np, uint32_t nq) {
+  return w == p ? nq : (w == q ? np : (pos[w * 32 + lane] >> 16));
+}
+
+template <bool REP, int PP>
+__device__ __forceinline__ double pipe_sum(int z, int pp_rt, const uint32_t* pos, int lane, uint32_t p, uint32_t q,
                                            uint32_t np, uint32_t nq, double m2, const RTab<REP>& R) {
+  const int pp = PP > 0 ? PP : pp_rt;
   const uint32_t base = (uint32_t)(z * pp);
-  uint32_t prev = base == p ? nq : (base == q ? np : (pos[base * 32 + lane] >> 16));
+  uint32_t prev = node_at<REP, PP>(base, pos, lane, p, q, np, nq);
   double s = 0.0;
-  for (int x = 1; x < pp; ++x) {
-    const uint32_t w = base + x;
-    const uint32_t nd = w == p ? nq : (w == q ? np : (pos[w * 32 + lane] >> 16));
+#pragma unroll
+  for (int x = 1; x < (PP > 0 ? PP : pp); ++x) {
+    const uint32_t nd = node_at<REP, PP>(base + x, pos, lane, p, q, np, nq);
     s = __dadd_rn(s, __dmul_rn(m2, R(prev, nd)));
     prev = nd;
   }
   return s;
 }
 
-template <int MW, bool REP, bool TRACE>
-__device__ void run_task(const SaParams& P, const SaTask& T, const double* Rs, unsigned char* ws, int lane) {
-  const DevCfg C = P.cfgs[T.cfg];
+// Two pipelines re-summed in one interleaved loop (independent dependency chains).
+template <bool REP, int PP>
+__device__ __forceinline__ void pipe_sum2(int za, int zb, int pp_rt, const uint32_t* pos, int lane, uint32_t p,
+                                          uint32_t q, uint32_t np, uint32_t nq, double m2, const RTab<REP>& R,
+                                          double& sa, double& sb) {
+  const int pp = PP > 0 ? PP : pp_rt;
+  const uint32_t ba = (uint32_t)(za * pp), bb = (uint32_t)(zb * pp);
+  uint32_t pa = node_at<REP, PP>(ba, pos, lane, p, q, np, nq);
+  uint32_t pb = node_at<REP, PP>(bb, pos, lane, p, q, np, nq);
+  double a = 0.0, b = 0.0;
+#pragma unroll
+  for (int x = 1; x < (PP > 0 ? PP : pp); ++x) {
+    const uint32_t na = node_at<REP, PP>(ba + x, pos, lane, p, q, np, nq);
+    const uint32_t nb = node_at<REP, PP>(bb + x, pos, lane, p, q, np, nq);
+    a = __dadd_rn(a, __dmul_rn(m2, R(pa, na)));
+    b = __dadd_rn(b, __dmul_rn(m2, R(pb, nb)));
+    pa = na;
+    pb = nb;
+  }
+  sa = a;
+  sb = b;
+}
+
+template <int MW, bool REP, bool TRACE, int PP>
+__device__ void run_task(const SaParams& P, const SaTask& T, const DevCfg& C, const double* Rs, unsigned char* ws,
+                         int lane) {
   if (lane >= T.count) return;
-  const int N = C.N, pp = C.pp, dp = C.dp, n = P.n_nodes;
+  const int N = C.N, pp = PP > 0 ? PP : C.pp, dp = C.dp, n = P.n_nodes;
   const uint32_t spn = (uint32_t)C.spn;
   const uint32_t chain = (uint32_t)(T.c_first + (T.k0 + lane) * P.world);
   const int slot = T.slot0 + lane;
@@ -143,7 +174,7 @@ __device__ void run_task(const SaParams& P, const SaTask& T, const double* Rs, u
     cnt_add(cnt, n0, lane, +1);
     mask.set(n0);
     if (pp >= 2) {
-      const double s = pipe_sum<REP>(z, pp, pos, lane, 0xffffffffu, 0xffffffffu, 0u, 0u, C.m2, R);
+      const double s = pipe_sum<REP, PP>(z, pp, pos, lane, 0xffffffffu, 0xffffffffu, 0u, 0u, C.m2, R);
       psum[z * 32 + lane] = s;
       tpp = fmax(tpp, s);
     }
@@ -165,8 +196,11 @@ __device__ void run_task(const SaParams& P, const SaTask& T, const double* Rs, u
   const int trow = TRACE ? P.trace_slot[slot] : -1;
 
   if (N >= 2) {
+    Draw dnext = draw_swap_rk(0u, chain, (uint32_t)C.e, P.rk, (uint32_t)N);
     for (int i = 0; i < P.iterations; ++i) {
-      const Draw d = draw_swap((uint32_t)i, chain, (uint32_t)C.e, P.key, (uint32_t)N);
+      const Draw d = dnext;
+      // the next proposal's Philox words do not depend on this step: issue them now (ILP)
+      dnext = draw_swap_rk((uint32_t)(i + 1), chain, (uint32_t)C.e, P.rk, (uint32_t)N);
       const uint32_t wp = pos[d.p * 32 + lane], wq = pos[d.q * 32 + lane];
       const uint32_t np = wp >> 16, nq = wq >> 16;
       double Lp = cur;
@@ -184,8 +218,8 @@ __device__ void run_task(const SaParams& P, const SaTask& T, const double* Rs, u
           xp = d.p - (uint32_t)(zp * pp);
           xq = d.q - (uint32_t)(zq * pp);
           two = zq != zp;
-          sA = pipe_sum<REP>(zp, pp, pos, lane, d.p, d.q, np, nq, C.m2, R);
-          if (two) sB = pipe_sum<REP>(zq, pp, pos, lane, d.p, d.q, np, nq, C.m2, R);
+          if (two) pipe_sum2<REP, PP>(zp, zq, pp, pos, lane, d.p, d.q, np, nq, C.m2, R, sA, sB);
+          else sA = pipe_sum<REP, PP>(zp, pp, pos, lane, d.p, d.q, np, nq, C.m2, R);
           const double oldA = psum[zp * 32 + lane];
           const double oldB = two ? psum[zq * 32 + lane] : oldA;
           const bool drop = (oldA == tpp && sA < tpp) || (two && oldB == tpp && sB < tpp);
@@ -241,7 +275,7 @@ __device__ void run_task(const SaParams& P, const SaTask& T, const double* Rs, u
           tex2 = k2 >= 2 ? __dmul_rn(__ldg(qe + k2), maxR2) : 0.0;
         }
         Lp = compose(C.Sb, C.r, C.Ss, tpp2, tin2, tex2);
-        acc = metropolis(__dadd_rn(Lp, -cur), beta, d.u);
+        acc = metropolis_fast(__dadd_rn(Lp, -cur), beta, d.u);
         if (acc) {
           if (pp >= 2) {
             psum[zp * 32 + lane] = sA;
@@ -303,7 +337,15 @@ __global__ void __launch_bounds__(kSaThreads) k_sa_chains(SaParams P) {
     t = __shfl_sync(0xffffffffu, t, 0);
     if (t >= P.n_tasks) break;
     const SaTask T = P.tasks[t];
-    run_task<MW, REP, TRACE>(P, T, Rs, ws, lane);
+    const DevCfg C = P.cfgs[T.cfg];
+    switch (C.pp) {   // compile-time pipeline depth for the common power-of-two depths
+      case 1: run_task<MW, REP, TRACE, 1>(P, T, C, Rs, ws, lane); break;
+      case 2: run_task<MW, REP, TRACE, 2>(P, T, C, Rs, ws, lane); break;
+      case 4: run_task<MW, REP, TRACE, 4>(P, T, C, Rs, ws, lane); break;
+      case 8: run_task<MW, REP, TRACE, 8>(P, T, C, Rs, ws, lane); break;
+      case 16: run_task<MW, REP, TRACE, 16>(P, T, C, Rs, ws, lane); break;
+      default: run_task<MW, REP, TRACE, 0>(P, T, C, Rs, ws, lane); break;
+    }
     __syncwarp();
   }
 }

@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 
 #include "../../include/pipette.h"
+#include "devmath.cuh"
 
 namespace pip {
 
@@ -65,6 +66,7 @@ struct SaParams {
   int32_t n_nodes;
   int32_t iterations;
   uint2 key;                 // Philox key (seed lo, seed hi)
+  RoundKeys rk;              // its ten round keys (philox_round_keys(key))
   int32_t world;             // chain ids c = c_first + k*world
   double alpha_inv, tau, t0;
   int32_t rep;               // R replicated per lane in shared memory
