@@ -199,6 +199,11 @@ int64_t pipette_shard_items(int64_t n_items, int32_t rank, int32_t world, int64_
 /* Write a fresh 128-byte ncclUniqueId to id_out (rank 0, before pipette_init). */
 pipette_status pipette_nccl_unique_id(void* id_out);
 
+/* Diagnostics of the last pipette_search on this rank: per SA warp task (32 chains of one
+ * configuration) [start ns, end ns, SM id, config index e] from the device globaltimer,
+ * written to out (cap tasks x 4 uint64, host).  Returns the task count (-1 on error). */
+int64_t pipette_last_task_profile(pipette_ctx* ctx, uint64_t* out, int64_t cap);
+
 /* Number of kernel launches the last pipette_search / pipette_eval issued. */
 int64_t pipette_last_launch_count(const pipette_ctx* ctx);
 

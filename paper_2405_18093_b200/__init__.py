@@ -155,6 +155,14 @@ class Pipette:
     def last_launch_count(self) -> int:
         return int(self._L.pipette_last_launch_count(self._h))
 
+    def last_task_profile(self) -> np.ndarray:
+        """(tasks, 4) uint64: [start ns, end ns, SM id, config e] of the last search's SA warp tasks."""
+        n = int(self._L.pipette_last_task_profile(self._h, None, 0))
+        out = np.zeros((max(1, n), 4), dtype=np.uint64)
+        if n > 0:
+            self._L.pipette_last_task_profile(self._h, out.ctypes.data_as(C.POINTER(C.c_uint64)), n)
+        return out[:max(0, n)]
+
     def set_bandwidth(self, bandwidth):
         B = np.ascontiguousarray(bandwidth, dtype=np.float64)
         if B.shape != (self.n_nodes, self.n_nodes):

@@ -67,7 +67,7 @@ class Plan(C.Structure):
 
 
 EXPORTS = ("pipette_init", "pipette_enumerate", "pipette_set_bandwidth", "pipette_set_stream", "pipette_eval", "pipette_search",
-           "pipette_shard_items", "pipette_nccl_unique_id", "pipette_last_launch_count", "pipette_destroy",
+           "pipette_shard_items", "pipette_nccl_unique_id", "pipette_last_launch_count", "pipette_last_task_profile", "pipette_destroy",
            "pipette_last_error", "pipette_strerror")
 
 _lib = None
@@ -104,6 +104,8 @@ def lib() -> C.CDLL:
     L.pipette_nccl_unique_id.restype = C.c_int
     L.pipette_last_launch_count.argtypes = [vp]
     L.pipette_last_launch_count.restype = C.c_int64
+    L.pipette_last_task_profile.argtypes = [vp, P(C.c_uint64), C.c_int64]
+    L.pipette_last_task_profile.restype = C.c_int64
     L.pipette_destroy.argtypes = [vp]
     L.pipette_destroy.restype = None
     L.pipette_last_error.argtypes = [vp]

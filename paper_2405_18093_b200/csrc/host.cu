@@ -110,7 +110,8 @@ struct pipette_ctx {
   DevBuf cfgs, keys, feas, qtab, eout;
   // search buffers
   DevBuf tasks, counter, chain_out, best_perm, cfg_slot, cfg_best, gbits, items, gitems, pack, accepted,
-      slot_perm_off, slot_lane, trace_slot, trace;
+      slot_perm_off, slot_lane, trace_slot, trace, task_prof;
+  int64_t n_tasks_last = 0;
   cudaEvent_t ev[6] = {};
 };
 
@@ -249,6 +250,16 @@ const char* pipette_last_error(const pipette_ctx* ctx) { return ctx ? ctx->err.c
 
 int64_t pipette_last_launch_count(const pipette_ctx* ctx) { return ctx ? ctx->launches : 0; }
 
+int64_t pipette_last_task_profile(pipette_ctx* ctx, uint64_t* out, int64_t cap) {
+  if (!ctx || ctx->n_tasks_last <= 0 || !ctx->task_prof.p) return 0;
+  const int64_t n = ctx->n_tasks_last;
+  if (out && cap > 0) {
+    if (cudaMemcpy(out, ctx->task_prof.p, sizeof(uint64_t) * 4 * std::min(n, cap), cudaMemcpyDeviceToHost) != cudaSuccess)
+      return -1;
+  }
+  return n;
+}
+
 int64_t pipette_shard_items(int64_t n_items, int32_t rank, int32_t world, int64_t* items, int64_t cap) {
   if (world < 1 || rank < 0 || rank >= world || n_items < 0) return 0;
   int64_t c = 0;
@@ -362,7 +373,7 @@ void pipette_destroy(pipette_ctx* ctx) {
   DevBuf* bufs[] = {&ctx->cfgs, &ctx->keys, &ctx->feas, &ctx->qtab, &ctx->eout, &ctx->tasks, &ctx->counter,
                     &ctx->chain_out, &ctx->best_perm, &ctx->cfg_slot, &ctx->cfg_best, &ctx->gbits, &ctx->items,
                     &ctx->gitems, &ctx->pack, &ctx->accepted, &ctx->slot_perm_off, &ctx->slot_lane,
-                    &ctx->trace_slot, &ctx->trace};
+                    &ctx->trace_slot, &ctx->trace, &ctx->task_prof};
   for (DevBuf* b : bufs)
     if (b->p) cudaFree(b->p);
   if (ctx->dR) cudaFree(ctx->dR);
@@ -548,6 +559,8 @@ pipette_status pipette_search(pipette_ctx* ctx, const pipette_model* model, int6
 
   CU(ensure(ctx->tasks, sizeof(SaTask) * std::max<size_t>(1, sorted.size())));
   CU(ensure(ctx->counter, sizeof(int)));
+  CU(ensure(ctx->task_prof, sizeof(unsigned long long) * 4 * std::max<size_t>(1, sorted.size())));
+  ctx->n_tasks_last = (int64_t)sorted.size();
   CU(ensure(ctx->chain_out, sizeof(ChainOut) * std::max(1, slots)));
   CU(ensure(ctx->best_perm, sizeof(uint16_t) * std::max(1, perm_words)));
   CU(ensure(ctx->cfg_slot, sizeof(int) * (F + 1)));
@@ -595,6 +608,7 @@ pipette_status pipette_search(pipette_ctx* ctx, const pipette_model* model, int6
   P.r_smem_bytes = r_bytes;
   P.out = (ChainOut*)ctx->chain_out.p;
   P.best_perm = (uint16_t*)ctx->best_perm.p;
+  P.task_prof = (unsigned long long*)ctx->task_prof.p;
   P.trace_slot = tracing ? (const int*)ctx->trace_slot.p : nullptr;
   P.trace_cap = tracing ? o.trace_cap : 0;
   P.trace = tracing ? (pipette_trace_record*)ctx->trace.p : nullptr;

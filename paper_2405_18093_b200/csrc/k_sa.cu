@@ -338,6 +338,8 @@ __global__ void __launch_bounds__(kSaThreads) k_sa_chains(SaParams P) {
     if (t >= P.n_tasks) break;
     const SaTask T = P.tasks[t];
     const DevCfg C = P.cfgs[T.cfg];
+    unsigned long long t_start = 0;
+    if (lane == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_start));
     switch (C.pp) {   // compile-time pipeline depth for the common power-of-two depths
       case 1: run_task<MW, REP, TRACE, 1>(P, T, C, Rs, ws, lane); break;
       case 2: run_task<MW, REP, TRACE, 2>(P, T, C, Rs, ws, lane); break;
@@ -347,6 +349,14 @@ __global__ void __launch_bounds__(kSaThreads) k_sa_chains(SaParams P) {
       default: run_task<MW, REP, TRACE, 0>(P, T, C, Rs, ws, lane); break;
     }
     __syncwarp();
+    if (lane == 0) {
+      unsigned long long t_end;
+      uint32_t smid;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_end));
+      asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+      ulonglong4* tp = reinterpret_cast<ulonglong4*>(P.task_prof) + t;
+      *tp = make_ulonglong4(t_start, t_end, smid, (unsigned long long)T.cfg);
+    }
   }
 }
 

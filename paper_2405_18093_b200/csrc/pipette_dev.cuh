@@ -75,6 +75,7 @@ struct SaParams {
   int32_t r_smem_bytes;
   ChainOut* out;
   uint16_t* best_perm;
+  unsigned long long* task_prof;   // per task: [start ns, end ns, smid, cfg] (diagnostics)
   // trace (debug): trace_slot[local slot] = record row or -1
   const int32_t* trace_slot;
   int32_t trace_cap;
