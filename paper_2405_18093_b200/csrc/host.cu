@@ -19,7 +19,9 @@ __global__ void k_enumerate_filter(int, int, unsigned long long, int, pipette_mo
                                    const pipette_profile_entry*, int, DevCfg*, unsigned long long*, int, int*,
                                    double*, int, EnumOut*);
 const void* eval_kernel(int mw, bool rep);
-const void* sa_kernel(int mw, bool rep, bool trace);
+const void* sa_kernel(int mode, bool trace);
+int sa_warp_state_bytes(int mode, int N, int pp, int dp, int n);
+__global__ void k_subset_max(const double*, int, double*);
 __global__ void k_argmin(const ChainOut*, const int*, int, CfgBest*);
 constexpr int kEnumThreads = 1024, kEvalThreads = 256, kSaThreads = 128;
 
@@ -97,6 +99,7 @@ struct pipette_ctx {
   int64_t launches = 0;
   // device tables
   double* dR = nullptr;
+  double* dTab = nullptr;   // subset-max table (n <= 16)
   pipette_profile_entry* dProf = nullptr;
   int n_prof = 0;
   std::vector<pipette_profile_entry> prof;
@@ -176,6 +179,12 @@ pipette_status upload_bw(pipette_ctx* ctx, const double* bw) {
   std::vector<double> R((size_t)n * n);
   for (int i = 0; i < n * n; ++i) R[i] = 1.0 / bw[i];  // R5: IEEE division, never symmetrised
   CU(cudaMemcpy(ctx->dR, R.data(), sizeof(double) * n * n, cudaMemcpyHostToDevice));
+  if (n <= 16) {
+    if (!ctx->dTab) CU(cudaMalloc(&ctx->dTab, sizeof(double) << n));
+    k_subset_max<<<((1 << n) + 255) / 256, 256>>>(ctx->dR, n, ctx->dTab);
+    CU(cudaGetLastError());
+    CU(cudaDeviceSynchronize());
+  }
   return PIPETTE_OK;
 }
 
@@ -377,6 +386,7 @@ void pipette_destroy(pipette_ctx* ctx) {
   for (DevBuf* b : bufs)
     if (b->p) cudaFree(b->p);
   if (ctx->dR) cudaFree(ctx->dR);
+  if (ctx->dTab) cudaFree(ctx->dTab);
   if (ctx->dProf) cudaFree(ctx->dProf);
   for (auto& e : ctx->ev)
     if (e) cudaEventDestroy(e);
@@ -532,10 +542,16 @@ pipette_status pipette_search(pipette_ctx* ctx, const pipette_model* model, int6
 
   const int n = ctx->n_nodes;
   const int nn = n * n;
-  const bool rep = nn * 32 * 8 <= 64 * 1024;
+  // MODE 0 (small clusters): packed positions, register stage-1 state, lane-replicated R,
+  // subset-max table.  MODE 1: general layout.
+  const int mode = (n <= 16 && maxN <= 256 && ctx->g <= 15 && ctx->dTab) ? 0 : 1;
+  const bool rep = mode == 0;
   const int r_bytes = (rep ? nn * 32 : nn) * 8;
-  auto a16 = [](int x) { return (x + 15) & ~15; };
-  const int warp_bytes = a16(maxN * 128) + a16(maxdp2 * 256) + a16((n + 3) / 4 * 128);
+  int warp_bytes = 16;
+  for (int f = 0; f < F; ++f) {
+    const DevCfg& c = ctx->hcfg[ctx->hfeas[f]];
+    warp_bytes = std::max(warp_bytes, sa_warp_state_bytes(mode, c.N, c.pp, c.dp, n));
+  }
   int wpb = kSaThreads / 32;
   const int smem_max = 227 * 1024;
   if (r_bytes + warp_bytes > smem_max)
@@ -591,6 +607,7 @@ pipette_status pipette_search(pipette_ctx* ctx, const pipette_model* model, int6
   P.cfgs = (const DevCfg*)ctx->cfgs.p;
   P.qtab = (const double*)ctx->qtab.p;
   P.R = ctx->dR;
+  P.subset_max = ctx->dTab;
   P.tasks = (const SaTask*)ctx->tasks.p;
   P.n_tasks = (int)sorted.size();
   P.task_counter = (int*)ctx->counter.p;
@@ -613,7 +630,7 @@ pipette_status pipette_search(pipette_ctx* ctx, const pipette_model* model, int6
   P.trace_cap = tracing ? o.trace_cap : 0;
   P.trace = tracing ? (pipette_trace_record*)ctx->trace.p : nullptr;
 
-  const void* kern = sa_kernel(n <= 32 ? 1 : 4, rep, tracing);
+  const void* kern = sa_kernel(mode, tracing);
   CU(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   int occ = 0;
   CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, wpb * 32, smem));

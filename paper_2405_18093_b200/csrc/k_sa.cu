@@ -7,16 +7,23 @@
 //
 // Design: one chain per LANE; a warp runs 32 chains of one
 // configuration, so every instruction advances 32 independent Markov chains.  Chain
-// state lives in shared memory in a lane-interleaved layout ([element][lane], 4- or
-// 8-byte words), which makes every per-lane random access bank-conflict free:
-//   pos[w]   = slot | node << 16             (N words)
-//   psum[z]  = Eq.5 sum of pipeline z        (dp doubles, pp >= 2)
-//   cnt[a]   = stage-1 DP members on node a  (u8, packed 4 per word; c_a <= spn)
-// R = 1/B is staged once per block, replicated per lane when small (conflict free).
-// Re-evaluation is incremental but bit-exact: only the (at most two) touched pipelines
-// are re-summed from scratch in stage order, and the max terms (T_PP, T_in, T_ex) are
-// maintained with witnesses and rescanned when a witness could drop -- max is exact,
-// so every latency equals the from-scratch definition bit for bit.
+// state lives in shared memory in lane-interleaved layouts ([element][lane] words), so
+// every per-lane random access is bank-conflict free:
+//   positions  (slot, node) of each worker position w = z*pp + x
+//              PosPacked: 16 bits per position, two per word (N <= 256, n <= 256)
+//              PosWide:   32 bits per position (general)
+//   psum[z]    Eq.5 sum of pipeline z (dp doubles, pp >= 2)
+//   stage-1    S1Reg:  per-node DP member counts as nibbles of a 64-bit register, the
+//                      node set N1 as a bit mask, T_ex from a subset-max table
+//                      (n <= 16, c_n <= spn <= 15)
+//              S1Smem: counts in shared memory (u8), a 128-bit node mask, T_ex with a
+//                      witness pair (general)
+// Re-evaluation is incremental but bit-exact: the (at most two) touched pipelines are
+// re-summed from scratch in stage order, the max terms (T_PP, T_in, T_ex) are kept with
+// witnesses / tables and rescanned when a witness could drop.  max is exact, so every
+// latency equals the from-scratch definition of the oracle bit for bit.
+#include <type_traits>
+
 #include "devmath.cuh"
 #include "pipette_dev.cuh"
 
@@ -24,7 +31,7 @@ namespace pip {
 
 constexpr int kSaThreads = 128;
 
-__device__ __forceinline__ int align16(int x) { return (x + 15) & ~15; }
+__host__ __device__ __forceinline__ int align16(int x) { return (x + 15) & ~15; }
 
 template <bool REP>
 struct RTab {
@@ -35,105 +42,96 @@ struct RTab {
   }
 };
 
-
-__device__ __forceinline__ uint32_t cnt_get(const uint32_t* cnt, uint32_t a, int lane) {
-  return (cnt[(a >> 2) * 32 + lane] >> ((a & 3) * 8)) & 0xffu;
-}
-__device__ __forceinline__ void cnt_add(uint32_t* cnt, uint32_t a, int lane, int delta) {
-  const uint32_t sh = (a & 3) * 8;
-  uint32_t& w = cnt[(a >> 2) * 32 + lane];
-  w = delta > 0 ? w + (1u << sh) : w - (1u << sh);
-}
-
-// Eq.6 intra term from scratch over the stage-1 node set: max_{c_a >= 2} qi(c_a) R[a][a].
-template <int MW, bool REP>
-__device__ __forceinline__ double tin_full(const Mask<MW>& m, const uint32_t* cnt, int lane, uint32_t dn,
-                                           uint32_t c_dn, uint32_t up, uint32_t c_up, const double* qi,
-                                           const RTab<REP>& R, int& win) {
-  double t = 0.0;
-  win = -1;
-#pragma unroll
-  for (int wd = 0; wd < MW; ++wd) {
-    uint32_t bits = m.w[wd];
-    while (bits) {
-      const uint32_t a = wd * 32 + __ffs(bits) - 1;
-      bits &= bits - 1;
-      const uint32_t c = a == dn ? c_dn : (a == up ? c_up : cnt_get(cnt, a, lane));
-      if (c >= 2) {
-        const double v = __dmul_rn(__ldg(qi + c), R(a, a));
-        if (v > t) { t = v; win = (int)a; }
-      }
+// ------------------------------------------------------------------ position storage
+struct PosPacked {
+  uint32_t* s;
+  int lane;
+  static __host__ __device__ int bytes(int N) { return ((N + 1) / 2) * 128; }
+  __device__ __forceinline__ uint32_t half(uint32_t w) const {
+    return (s[(w >> 1) * 32 + lane] >> ((w & 1u) * 16u)) & 0xffffu;
+  }
+  __device__ __forceinline__ uint32_t raw(uint32_t w) const { return half(w); }
+  __device__ __forceinline__ uint32_t node(uint32_t w) const { return half(w) >> 8; }
+  static __device__ __forceinline__ uint32_t node_of(uint32_t r) { return r >> 8; }
+  static __device__ __forceinline__ uint32_t slot_of(uint32_t r) { return r & 0xffu; }
+  __device__ __forceinline__ void init(int N, uint32_t spn, uint32_t spn_magic) {
+    for (int w = 0; w < N; w += 2) {
+      const uint32_t a = (uint32_t)w | (div_small((uint32_t)w, spn_magic, spn) << 8);
+      const uint32_t b = w + 1 < N ? ((uint32_t)(w + 1) | (div_small((uint32_t)(w + 1), spn_magic, spn) << 8)) : 0u;
+      s[(w >> 1) * 32 + lane] = a | (b << 16);
     }
   }
-  return t;
-}
-
-// Eq.6 inter term's slowest link from scratch: max over ordered pairs a != b of R[a][b].
-template <int MW, bool REP>
-__device__ __forceinline__ double maxr_full(const Mask<MW>& m, const RTab<REP>& R, int& wa, int& wb) {
-  double mx = 0.0;
-  wa = wb = -1;
-#pragma unroll
-  for (int wd = 0; wd < MW; ++wd) {
-    uint32_t bits = m.w[wd];
-    while (bits) {
-      const uint32_t a = wd * 32 + __ffs(bits) - 1;
-      bits &= bits - 1;
-#pragma unroll
-      for (int wd2 = 0; wd2 < MW; ++wd2) {
-        uint32_t bits2 = m.w[wd2];
-        while (bits2) {
-          const uint32_t b = wd2 * 32 + __ffs(bits2) - 1;
-          bits2 &= bits2 - 1;
-          if (a == b) continue;
-          const double v = R(a, b);
-          if (v > mx) { mx = v; wa = (int)a; wb = (int)b; }
-        }
-      }
+  // positions p and q exchange their contents (rp = raw(p), rq = raw(q))
+  __device__ __forceinline__ void swap(uint32_t p, uint32_t q, uint32_t rp, uint32_t rq) {
+    uint32_t* wpp = &s[(p >> 1) * 32 + lane];
+    uint32_t* wqq = &s[(q >> 1) * 32 + lane];
+    if ((p >> 1) == (q >> 1)) {
+      *wpp = (*wpp >> 16) | (*wpp << 16);
+    } else {
+      const uint32_t shp = (p & 1u) * 16u, shq = (q & 1u) * 16u;
+      *wpp = (*wpp & ~(0xffffu << shp)) | (rq << shp);
+      *wqq = (*wqq & ~(0xffffu << shq)) | (rp << shq);
     }
   }
-  return mx;
+};
+
+struct PosWide {
+  uint32_t* s;
+  int lane;
+  static __host__ __device__ int bytes(int N) { return N * 128; }
+  __device__ __forceinline__ uint32_t raw(uint32_t w) const { return s[w * 32 + lane]; }
+  __device__ __forceinline__ uint32_t node(uint32_t w) const { return raw(w) >> 16; }
+  static __device__ __forceinline__ uint32_t node_of(uint32_t r) { return r >> 16; }
+  static __device__ __forceinline__ uint32_t slot_of(uint32_t r) { return r & 0xffffu; }
+  __device__ __forceinline__ void init(int N, uint32_t spn, uint32_t spn_magic) {
+    for (int w = 0; w < N; ++w) s[w * 32 + lane] = (uint32_t)w | (div_small((uint32_t)w, spn_magic, spn) << 16);
+  }
+  __device__ __forceinline__ void swap(uint32_t p, uint32_t q, uint32_t rp, uint32_t rq) {
+    s[p * 32 + lane] = rq;
+    s[q * 32 + lane] = rp;
+  }
+};
+
+// Node of position w after the proposed swap of positions p and q (nodes np, nq).
+template <class POS>
+__device__ __forceinline__ uint32_t node_at(const POS& pos, uint32_t w, uint32_t p, uint32_t q, uint32_t np,
+                                            uint32_t nq) {
+  const uint32_t v = pos.node(w);
+  return w == p ? nq : (w == q ? np : v);
 }
 
-// Eq.5 sum of pipeline z in stage order, with positions p and q holding nodes np and nq
-// after the proposed swap (P_z = ((0 + m2 R[..]) + m2 R[..]) + ...).
-// PP > 0: compile-time pipeline depth (fully unrolled); PP == 0: runtime depth pp.
-template <bool REP, int PP>
-__device__ __forceinline__ uint32_t node_at(uint32_t w, const uint32_t* pos, int lane, uint32_t p, uint32_t q,
-                                            uint32_t np, uint32_t nq) {
-  return w == p ? nq : (w == q ? np : (pos[w * 32 + lane] >> 16));
-}
-
-template <bool REP, int PP>
-__device__ __forceinline__ double pipe_sum(int z, int pp_rt, const uint32_t* pos, int lane, uint32_t p, uint32_t q,
-                                           uint32_t np, uint32_t nq, double m2, const RTab<REP>& R) {
+// Eq.5 sum of pipeline z in stage order (P_z = ((0 + m2 R[..]) + m2 R[..]) + ..., DESIGN.md
+// 3).  PP > 0: compile-time pipeline depth (fully unrolled, loads hoisted); PP == 0: runtime.
+template <bool REP, int PP, class POS>
+__device__ __forceinline__ double pipe_sum(int z, int pp_rt, const POS& pos, uint32_t p, uint32_t q, uint32_t np,
+                                           uint32_t nq, double m2, const RTab<REP>& R) {
   const int pp = PP > 0 ? PP : pp_rt;
   const uint32_t base = (uint32_t)(z * pp);
-  uint32_t prev = node_at<REP, PP>(base, pos, lane, p, q, np, nq);
+  uint32_t prev = node_at(pos, base, p, q, np, nq);
   double s = 0.0;
 #pragma unroll
   for (int x = 1; x < (PP > 0 ? PP : pp); ++x) {
-    const uint32_t nd = node_at<REP, PP>(base + x, pos, lane, p, q, np, nq);
+    const uint32_t nd = node_at(pos, base + x, p, q, np, nq);
     s = __dadd_rn(s, __dmul_rn(m2, R(prev, nd)));
     prev = nd;
   }
   return s;
 }
 
-// Two pipelines re-summed in one interleaved loop (independent dependency chains).
-template <bool REP, int PP>
-__device__ __forceinline__ void pipe_sum2(int za, int zb, int pp_rt, const uint32_t* pos, int lane, uint32_t p,
-                                          uint32_t q, uint32_t np, uint32_t nq, double m2, const RTab<REP>& R,
-                                          double& sa, double& sb) {
+// Two pipelines re-summed in one interleaved loop (two independent dependency chains).
+template <bool REP, int PP, class POS>
+__device__ __forceinline__ void pipe_sum2(int za, int zb, int pp_rt, const POS& pos, uint32_t p, uint32_t q,
+                                          uint32_t np, uint32_t nq, double m2, const RTab<REP>& R, double& sa,
+                                          double& sb) {
   const int pp = PP > 0 ? PP : pp_rt;
   const uint32_t ba = (uint32_t)(za * pp), bb = (uint32_t)(zb * pp);
-  uint32_t pa = node_at<REP, PP>(ba, pos, lane, p, q, np, nq);
-  uint32_t pb = node_at<REP, PP>(bb, pos, lane, p, q, np, nq);
+  uint32_t pa = node_at(pos, ba, p, q, np, nq);
+  uint32_t pb = node_at(pos, bb, p, q, np, nq);
   double a = 0.0, b = 0.0;
 #pragma unroll
   for (int x = 1; x < (PP > 0 ? PP : pp); ++x) {
-    const uint32_t na = node_at<REP, PP>(ba + x, pos, lane, p, q, np, nq);
-    const uint32_t nb = node_at<REP, PP>(bb + x, pos, lane, p, q, np, nq);
+    const uint32_t na = node_at(pos, ba + x, p, q, np, nq);
+    const uint32_t nb = node_at(pos, bb + x, p, q, np, nq);
     a = __dadd_rn(a, __dmul_rn(m2, R(pa, na)));
     b = __dadd_rn(b, __dmul_rn(m2, R(pb, nb)));
     pa = na;
@@ -143,52 +141,226 @@ __device__ __forceinline__ void pipe_sum2(int za, int zb, int pp_rt, const uint3
   sb = b;
 }
 
-template <int MW, bool REP, bool TRACE, int PP>
+// ------------------------------------------------------------------ stage-1 (Eq.6) state
+struct S1Ctx {
+  const double* qi;   // qi(c), c = 0..dp
+  const double* qe;   // qe(k), k = 0..min(dp, n)
+  const double* tab;  // subset-max table (S1Reg only)
+  int n;
+};
+
+// n <= 16 nodes and <= 15 stage-1 members per node.
+template <bool REP>
+struct S1Reg {
+  uint64_t cnt, cnt2;
+  uint32_t mask, mask2;
+  int k, k2, win, win2;
+  double tin, tex, tin2, tex2;
+
+  static __device__ __forceinline__ uint32_t get(uint64_t c, uint32_t a) { return (uint32_t)(c >> (4u * a)) & 15u; }
+
+  __device__ __forceinline__ double tin_full(uint64_t c, const S1Ctx& X, const RTab<REP>& R, int& w) const {
+    double t = 0.0;
+    w = -1;
+#pragma unroll 4
+    for (int a = 0; a < X.n; ++a) {
+      const uint32_t ca = get(c, (uint32_t)a);
+      if (ca >= 2u) {
+        const double v = __dmul_rn(__ldg(X.qi + ca), R((uint32_t)a, (uint32_t)a));
+        if (v > t) { t = v; w = a; }
+      }
+    }
+    return t;
+  }
+  __device__ __forceinline__ double tex_of(uint32_t m, int kk, const S1Ctx& X) const {
+    return kk >= 2 ? __dmul_rn(__ldg(X.qe + kk), __ldg(X.tab + m)) : 0.0;
+  }
+  __device__ __forceinline__ void clear() { cnt = 0ull; mask = 0u; }
+  __device__ __forceinline__ void add_init(uint32_t a) { cnt += 1ull << (4u * a); mask |= 1u << a; }
+  __device__ __forceinline__ void finish_init(const S1Ctx& X, const RTab<REP>& R) {
+    k = __popc(mask);
+    tin = tin_full(cnt, X, R, win);
+    tex = tex_of(mask, k, X);
+  }
+  // a stage-1 member moves from node dn to node up (tentative state)
+  __device__ __forceinline__ void propose(uint32_t dn, uint32_t up, const S1Ctx& X, const RTab<REP>& R) {
+    const uint32_t c_dn = get(cnt, dn) - 1u, c_up = get(cnt, up) + 1u;
+    cnt2 = cnt - (1ull << (4u * dn)) + (1ull << (4u * up));
+    mask2 = (mask & (c_dn == 0u ? ~(1u << dn) : 0xffffffffu)) | (1u << up);
+    k2 = __popc(mask2);
+    tin2 = tin; win2 = win;
+    if ((int)dn == win) {
+      tin2 = tin_full(cnt2, X, R, win2);
+    } else if (c_up >= 2u) {
+      const double v = __dmul_rn(__ldg(X.qi + c_up), R(up, up));
+      if (v > tin2) { tin2 = v; win2 = (int)up; }
+    }
+    tex2 = (mask2 == mask) ? tex : tex_of(mask2, k2, X);
+  }
+  __device__ __forceinline__ void commit() { cnt = cnt2; mask = mask2; k = k2; tin = tin2; win = win2; tex = tex2; }
+};
+
+// General stage-1 state: counts (u8, c_n <= spn <= 255) in shared memory, 128-bit node
+// mask, T_ex maintained with a witness ordered pair.
+template <bool REP>
+struct S1Smem {
+  uint32_t* c;   // [ceil(n/4)][32] words
+  int lane;
+  Mask<4> mask, mask2;
+  int k, k2, win, win2, wa, wb, wa2, wb2;
+  uint32_t dn_, up_;
+  double tin, tex, maxR, tin2, tex2, maxR2;
+
+  __device__ __forceinline__ uint32_t get(uint32_t a) const { return (c[(a >> 2) * 32 + lane] >> ((a & 3) * 8)) & 0xffu; }
+  __device__ __forceinline__ void add(uint32_t a, int delta) {
+    uint32_t& w = c[(a >> 2) * 32 + lane];
+    const uint32_t sh = (a & 3) * 8;
+    w = delta > 0 ? w + (1u << sh) : w - (1u << sh);
+  }
+  __device__ __forceinline__ double tin_full(const Mask<4>& m, uint32_t dn, uint32_t c_dn, uint32_t up,
+                                             uint32_t c_up, const S1Ctx& X, const RTab<REP>& R, int& w) const {
+    double t = 0.0;
+    w = -1;
+#pragma unroll
+    for (int wd = 0; wd < 4; ++wd) {
+      uint32_t bits = m.w[wd];
+      while (bits) {
+        const uint32_t a = wd * 32 + __ffs(bits) - 1;
+        bits &= bits - 1;
+        const uint32_t ca = a == dn ? c_dn : (a == up ? c_up : get(a));
+        if (ca >= 2) {
+          const double v = __dmul_rn(__ldg(X.qi + ca), R(a, a));
+          if (v > t) { t = v; w = (int)a; }
+        }
+      }
+    }
+    return t;
+  }
+  __device__ __forceinline__ double maxr_full(const Mask<4>& m, const RTab<REP>& R, int& a_, int& b_) const {
+    double mx = 0.0;
+    a_ = b_ = -1;
+#pragma unroll
+    for (int wd = 0; wd < 4; ++wd) {
+      uint32_t bits = m.w[wd];
+      while (bits) {
+        const uint32_t a = wd * 32 + __ffs(bits) - 1;
+        bits &= bits - 1;
+#pragma unroll
+        for (int wd2 = 0; wd2 < 4; ++wd2) {
+          uint32_t bits2 = m.w[wd2];
+          while (bits2) {
+            const uint32_t b = wd2 * 32 + __ffs(bits2) - 1;
+            bits2 &= bits2 - 1;
+            if (a == b) continue;
+            const double v = R(a, b);
+            if (v > mx) { mx = v; a_ = (int)a; b_ = (int)b; }
+          }
+        }
+      }
+    }
+    return mx;
+  }
+  __device__ __forceinline__ void clear(int n) {
+    for (int wd = 0; wd < (n + 3) / 4; ++wd) c[wd * 32 + lane] = 0u;
+    mask.clear();
+  }
+  __device__ __forceinline__ void add_init(uint32_t a) { add(a, +1); mask.set(a); }
+  __device__ __forceinline__ void finish_init(const S1Ctx& X, const RTab<REP>& R) {
+    k = mask.count();
+    tin = tin_full(mask, 0xffffffffu, 0u, 0xffffffffu, 0u, X, R, win);
+    maxR = 0.0;
+    wa = wb = -1;
+    if (k >= 2) maxR = maxr_full(mask, R, wa, wb);
+    tex = k >= 2 ? __dmul_rn(__ldg(X.qe + k), maxR) : 0.0;
+  }
+  __device__ __forceinline__ void propose(uint32_t dn, uint32_t up, const S1Ctx& X, const RTab<REP>& R) {
+    dn_ = dn; up_ = up;
+    const uint32_t c_dn = get(dn) - 1u, c_up = get(up) + 1u;
+    const bool leave = c_dn == 0u, join = c_up == 1u;
+    mask2 = mask;
+    if (leave) mask2.reset(dn);
+    if (join) mask2.set(up);
+    k2 = k - (int)leave + (int)join;
+    tin2 = tin; win2 = win;
+    if ((int)dn == win) {
+      tin2 = tin_full(mask2, dn, c_dn, up, c_up, X, R, win2);
+    } else if (c_up >= 2u) {
+      const double v = __dmul_rn(__ldg(X.qi + c_up), R(up, up));
+      if (v > tin2) { tin2 = v; win2 = (int)up; }
+    }
+    maxR2 = maxR; wa2 = wa; wb2 = wb;
+    if (k2 < 2) {
+      maxR2 = 0.0; wa2 = wb2 = -1;
+    } else if (leave && ((int)dn == wa || (int)dn == wb)) {
+      maxR2 = maxr_full(mask2, R, wa2, wb2);
+    } else if (join) {
+#pragma unroll
+      for (int wd = 0; wd < 4; ++wd) {
+        uint32_t bits = mask2.w[wd];
+        while (bits) {
+          const uint32_t b = wd * 32 + __ffs(bits) - 1;
+          bits &= bits - 1;
+          if (b == up) continue;
+          const double v1 = R(up, b), v2 = R(b, up);
+          if (v1 > maxR2) { maxR2 = v1; wa2 = (int)up; wb2 = (int)b; }
+          if (v2 > maxR2) { maxR2 = v2; wa2 = (int)b; wb2 = (int)up; }
+        }
+      }
+    }
+    tex2 = k2 >= 2 ? __dmul_rn(__ldg(X.qe + k2), maxR2) : 0.0;
+  }
+  __device__ __forceinline__ void commit() {
+    add(dn_, -1); add(up_, +1);
+    mask = mask2; k = k2; tin = tin2; win = win2; tex = tex2; maxR = maxR2; wa = wa2; wb = wb2;
+  }
+};
+
+// Shared-memory footprint of one warp's chain state for a configuration.
+template <class POS>
+__host__ __device__ inline int warp_state_bytes(int N, int pp, int dp, int n, bool s1smem) {
+  return align16(POS::bytes(N)) + (pp >= 2 ? align16(dp * 256) : 0) + (s1smem ? align16((n + 3) / 4 * 128) : 0);
+}
+
+// ------------------------------------------------------------------ one warp task
+template <class POS, class S1, bool REP, bool TRACE, int PP>
 __device__ void run_task(const SaParams& P, const SaTask& T, const DevCfg& C, const double* Rs, unsigned char* ws,
                          int lane) {
   if (lane >= T.count) return;
+  constexpr bool kSmemS1 = !std::is_same<S1, S1Reg<REP>>::value;
   const int N = C.N, pp = PP > 0 ? PP : C.pp, dp = C.dp, n = P.n_nodes;
-  const uint32_t spn = (uint32_t)C.spn;
   const uint32_t chain = (uint32_t)(T.c_first + (T.k0 + lane) * P.world);
   const int slot = T.slot0 + lane;
-  const double* qi = P.qtab + C.qi_off;
-  const double* qe = P.qtab + C.qe_off;
   const RTab<REP> R{Rs, n, lane};
+  const S1Ctx X{P.qtab + C.qi_off, P.qtab + C.qe_off, P.subset_max, n};
 
-  uint32_t* pos = reinterpret_cast<uint32_t*>(ws);
-  double* psum = reinterpret_cast<double*>(ws + align16(N * 128));
-  uint32_t* cnt = reinterpret_cast<uint32_t*>(ws + align16(N * 128) + (pp >= 2 ? align16(dp * 256) : 0));
+  POS pos{reinterpret_cast<uint32_t*>(ws), lane};
+  double* psum = reinterpret_cast<double*>(ws + align16(POS::bytes(N)));
   uint16_t* bperm = P.best_perm + T.perm_off;
+  S1 s1;
+  if constexpr (kSmemS1) {
+    s1.c = reinterpret_cast<uint32_t*>(ws + align16(POS::bytes(N)) + (pp >= 2 ? align16(dp * 256) : 0));
+    s1.lane = lane;
+    s1.clear(n);
+  } else {
+    s1.clear();
+  }
 
   // ---- initial state: identity mapping (R16) and its latency from scratch
-  for (int w = 0; w < N; ++w) {
-    pos[w * 32 + lane] = (uint32_t)w | (div_small((uint32_t)w, C.spn_magic, spn) << 16);
-    bperm[w * 32 + lane] = (uint16_t)w;
-  }
-  for (int wd = 0; wd < (n + 3) / 4; ++wd) cnt[wd * 32 + lane] = 0u;
-  Mask<MW> mask;
-  mask.clear();
+  pos.init(N, (uint32_t)C.spn, C.spn_magic);
+  for (int w = 0; w < N; ++w) bperm[w * 32 + lane] = (uint16_t)w;
   double tpp = 0.0;
   for (int z = 0; z < dp; ++z) {
-    const uint32_t n0 = pos[z * pp * 32 + lane] >> 16;
-    cnt_add(cnt, n0, lane, +1);
-    mask.set(n0);
+    s1.add_init(pos.node((uint32_t)(z * pp)));
     if (pp >= 2) {
-      const double s = pipe_sum<REP, PP>(z, pp, pos, lane, 0xffffffffu, 0xffffffffu, 0u, 0u, C.m2, R);
+      const double s = pipe_sum<REP, PP>(z, pp, pos, 0xffffffffu, 0xffffffffu, 0u, 0u, C.m2, R);
       psum[z * 32 + lane] = s;
       tpp = fmax(tpp, s);
     }
   }
-  int k = mask.count();
-  int win, wa, wb;
-  double t_in = tin_full<MW, REP>(mask, cnt, lane, 0xffffffffu, 0u, 0xffffffffu, 0u, qi, R, win);
-  double maxR = 0.0;
-  wa = wb = -1;
-  if (k >= 2) maxR = maxr_full<MW, REP>(mask, R, wa, wb);
-  double t_ex = k >= 2 ? __dmul_rn(__ldg(qe + k), maxR) : 0.0;
+  s1.finish_init(X, R);
 
-  const double L0 = compose(C.Sb, C.r, C.Ss, tpp, t_in, t_ex);
-  double cur = L0, best = L0, best_tpp = tpp, best_tdp = __dadd_rn(t_in, t_ex);
+  const double L0 = compose(C.Sb, C.r, C.Ss, tpp, s1.tin, s1.tex);
+  double cur = L0, best = L0, best_tpp = tpp, best_tdp = __dadd_rn(s1.tin, s1.tex);
   int best_step = -1;
   uint32_t accepted = 0;
   double beta = P.t0 > 0.0 ? __ddiv_rn(1.0, P.t0) : __ddiv_rn(1.0, __dmul_rn(P.tau, L0));
@@ -201,8 +373,8 @@ __device__ void run_task(const SaParams& P, const SaTask& T, const DevCfg& C, co
       const Draw d = dnext;
       // the next proposal's Philox words do not depend on this step: issue them now (ILP)
       dnext = draw_swap_rk((uint32_t)(i + 1), chain, (uint32_t)C.e, P.rk, (uint32_t)N);
-      const uint32_t wp = pos[d.p * 32 + lane], wq = pos[d.q * 32 + lane];
-      const uint32_t np = wp >> 16, nq = wq >> 16;
+      const uint32_t rp = pos.raw(d.p), rq = pos.raw(d.q);
+      const uint32_t np = POS::node_of(rp), nq = POS::node_of(rq);
       double Lp = cur;
       bool acc = true;
       bool improved = false;
@@ -218,61 +390,37 @@ __device__ void run_task(const SaParams& P, const SaTask& T, const DevCfg& C, co
           xp = d.p - (uint32_t)(zp * pp);
           xq = d.q - (uint32_t)(zq * pp);
           two = zq != zp;
-          if (two) pipe_sum2<REP, PP>(zp, zq, pp, pos, lane, d.p, d.q, np, nq, C.m2, R, sA, sB);
-          else sA = pipe_sum<REP, PP>(zp, pp, pos, lane, d.p, d.q, np, nq, C.m2, R);
+          if (two) pipe_sum2<REP, PP>(zp, zq, pp, pos, d.p, d.q, np, nq, C.m2, R, sA, sB);
+          else sA = pipe_sum<REP, PP>(zp, pp, pos, d.p, d.q, np, nq, C.m2, R);
           const double oldA = psum[zp * 32 + lane];
           const double oldB = two ? psum[zq * 32 + lane] : oldA;
           const bool drop = (oldA == tpp && sA < tpp) || (two && oldB == tpp && sB < tpp);
-          if (drop) {
-            double mx = two ? fmax(sA, sB) : sA;
-            for (int z = 0; z < dp; ++z)
-              if (z != zp && z != zq) mx = fmax(mx, psum[z * 32 + lane]);
-            tpp2 = mx;
+          if (drop) {   // a pipeline at the max decreased: rescan (4 independent max chains)
+            double m0 = two ? fmax(sA, sB) : sA, m1 = 0.0, m2 = 0.0, m3 = 0.0;
+            int z = 0;
+            for (; z + 4 <= dp; z += 4) {
+              const double v0 = psum[(z + 0) * 32 + lane], v1 = psum[(z + 1) * 32 + lane];
+              const double v2 = psum[(z + 2) * 32 + lane], v3 = psum[(z + 3) * 32 + lane];
+              m0 = fmax(m0, (z + 0 == zp || z + 0 == zq) ? 0.0 : v0);
+              m1 = fmax(m1, (z + 1 == zp || z + 1 == zq) ? 0.0 : v1);
+              m2 = fmax(m2, (z + 2 == zp || z + 2 == zq) ? 0.0 : v2);
+              m3 = fmax(m3, (z + 3 == zp || z + 3 == zq) ? 0.0 : v3);
+            }
+            for (; z < dp; ++z) m0 = fmax(m0, (z == zp || z == zq) ? 0.0 : psum[z * 32 + lane]);
+            tpp2 = fmax(fmax(m0, m1), fmax(m2, m3));
           } else {
             tpp2 = fmax(tpp, two ? fmax(sA, sB) : sA);
           }
         }
         // ---- Eq.6: the stage-1 node multiset changes only if exactly one of p, q is stage 1
-        const bool sp = xp == 0u, sq = xq == 0u;
-        double tin2 = t_in, tex2 = t_ex, maxR2 = maxR;
-        int win2 = win, wa2 = wa, wb2 = wb, k2 = k;
-        uint32_t dn = 0, up = 0, c_dn = 0, c_up = 0;
-        Mask<MW> mask2 = mask;
-        const bool dpchg = sp != sq;
+        const bool dpchg = (xp == 0u) != (xq == 0u);
+        double tin2 = s1.tin, tex2 = s1.tex;
         if (dpchg) {
-          dn = sp ? np : nq;   // node losing a stage-1 DP member
-          up = sp ? nq : np;   // node gaining one
-          c_dn = cnt_get(cnt, dn, lane) - 1u;
-          c_up = cnt_get(cnt, up, lane) + 1u;
-          const bool leave = c_dn == 0u, join = c_up == 1u;
-          if (leave) mask2.reset(dn);
-          if (join) mask2.set(up);
-          k2 = k - (int)leave + (int)join;
-          if ((int)dn == win) {
-            tin2 = tin_full<MW, REP>(mask2, cnt, lane, dn, c_dn, up, c_up, qi, R, win2);
-          } else if (c_up >= 2u) {
-            const double v = __dmul_rn(__ldg(qi + c_up), R(up, up));
-            if (v > tin2) { tin2 = v; win2 = (int)up; }
-          }
-          if (k2 < 2) {
-            maxR2 = 0.0; wa2 = wb2 = -1;
-          } else if (leave && ((int)dn == wa || (int)dn == wb)) {
-            maxR2 = maxr_full<MW, REP>(mask2, R, wa2, wb2);
-          } else if (join) {
-#pragma unroll
-            for (int wd = 0; wd < MW; ++wd) {
-              uint32_t bits = mask2.w[wd];
-              while (bits) {
-                const uint32_t b = wd * 32 + __ffs(bits) - 1;
-                bits &= bits - 1;
-                if (b == up) continue;
-                const double v1 = R(up, b), v2 = R(b, up);
-                if (v1 > maxR2) { maxR2 = v1; wa2 = (int)up; wb2 = (int)b; }
-                if (v2 > maxR2) { maxR2 = v2; wa2 = (int)b; wb2 = (int)up; }
-              }
-            }
-          }
-          tex2 = k2 >= 2 ? __dmul_rn(__ldg(qe + k2), maxR2) : 0.0;
+          const uint32_t dn = xp == 0u ? np : nq;   // node losing a stage-1 DP member
+          const uint32_t up = xp == 0u ? nq : np;   // node gaining one
+          s1.propose(dn, up, X, R);
+          tin2 = s1.tin2;
+          tex2 = s1.tex2;
         }
         Lp = compose(C.Sb, C.r, C.Ss, tpp2, tin2, tex2);
         acc = metropolis_fast(__dadd_rn(Lp, -cur), beta, d.u);
@@ -282,27 +430,20 @@ __device__ void run_task(const SaParams& P, const SaTask& T, const DevCfg& C, co
             if (two) psum[zq * 32 + lane] = sB;
             tpp = tpp2;
           }
-          if (dpchg) {
-            cnt_add(cnt, dn, lane, -1);
-            cnt_add(cnt, up, lane, +1);
-            mask = mask2; k = k2;
-            t_in = tin2; win = win2;
-            t_ex = tex2; maxR = maxR2; wa = wa2; wb = wb2;
-          }
+          if (dpchg) s1.commit();
           cur = Lp;
           if (Lp < best) {
-            best = Lp; best_step = i; best_tpp = tpp; best_tdp = __dadd_rn(t_in, t_ex);
+            best = Lp; best_step = i; best_tpp = tpp; best_tdp = __dadd_rn(s1.tin, s1.tex);
             improved = true;
           }
         }
       }
       if (acc) {
-        pos[d.p * 32 + lane] = wq;
-        pos[d.q * 32 + lane] = wp;
+        pos.swap(d.p, d.q, rp, rq);
         ++accepted;
       }
       if (improved)
-        for (int w = 0; w < N; ++w) bperm[w * 32 + lane] = (uint16_t)(pos[w * 32 + lane] & 0xffffu);
+        for (int w = 0; w < N; ++w) bperm[w * 32 + lane] = (uint16_t)POS::slot_of(pos.raw((uint32_t)w));
       if (TRACE && trow >= 0 && i < P.trace_cap) {
         pipette_trace_record rec;
         rec.i = (uint32_t)i; rec.p = (uint16_t)d.p; rec.q = (uint16_t)d.q;
@@ -318,8 +459,13 @@ __device__ void run_task(const SaParams& P, const SaTask& T, const DevCfg& C, co
   P.out[slot] = o;
 }
 
-template <int MW, bool REP, bool TRACE>
+// MODE 0: n <= 16 nodes, N <= 256, spn <= 15 (packed positions, register stage-1 state,
+//         lane-replicated R, subset-max table).  MODE 1: general.
+template <int MODE, bool TRACE>
 __global__ void __launch_bounds__(kSaThreads) k_sa_chains(SaParams P) {
+  using POS = typename std::conditional<MODE == 0, PosPacked, PosWide>::type;
+  constexpr bool REP = MODE == 0;
+  using S1 = typename std::conditional<MODE == 0, S1Reg<REP>, S1Smem<REP>>::type;
   extern __shared__ __align__(16) unsigned char smem[];
   double* Rs = reinterpret_cast<double*>(smem);
   const int nn = P.n_nodes * P.n_nodes;
@@ -341,12 +487,13 @@ __global__ void __launch_bounds__(kSaThreads) k_sa_chains(SaParams P) {
     unsigned long long t_start = 0;
     if (lane == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_start));
     switch (C.pp) {   // compile-time pipeline depth for the common power-of-two depths
-      case 1: run_task<MW, REP, TRACE, 1>(P, T, C, Rs, ws, lane); break;
-      case 2: run_task<MW, REP, TRACE, 2>(P, T, C, Rs, ws, lane); break;
-      case 4: run_task<MW, REP, TRACE, 4>(P, T, C, Rs, ws, lane); break;
-      case 8: run_task<MW, REP, TRACE, 8>(P, T, C, Rs, ws, lane); break;
-      case 16: run_task<MW, REP, TRACE, 16>(P, T, C, Rs, ws, lane); break;
-      default: run_task<MW, REP, TRACE, 0>(P, T, C, Rs, ws, lane); break;
+      case 1: run_task<POS, S1, REP, TRACE, 1>(P, T, C, Rs, ws, lane); break;
+      case 2: run_task<POS, S1, REP, TRACE, 2>(P, T, C, Rs, ws, lane); break;
+      case 4: run_task<POS, S1, REP, TRACE, 4>(P, T, C, Rs, ws, lane); break;
+      case 8: run_task<POS, S1, REP, TRACE, 8>(P, T, C, Rs, ws, lane); break;
+      case 16: run_task<POS, S1, REP, TRACE, 16>(P, T, C, Rs, ws, lane); break;
+      case 32: run_task<POS, S1, REP, TRACE, 32>(P, T, C, Rs, ws, lane); break;
+      default: run_task<POS, S1, REP, TRACE, 0>(P, T, C, Rs, ws, lane); break;
     }
     __syncwarp();
     if (lane == 0) {
@@ -354,10 +501,24 @@ __global__ void __launch_bounds__(kSaThreads) k_sa_chains(SaParams P) {
       uint32_t smid;
       asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_end));
       asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
-      ulonglong4* tp = reinterpret_cast<ulonglong4*>(P.task_prof) + t;
-      *tp = make_ulonglong4(t_start, t_end, smid, (unsigned long long)T.cfg);
+      reinterpret_cast<ulonglong4*>(P.task_prof)[t] = make_ulonglong4(t_start, t_end, smid, (unsigned long long)T.cfg);
     }
   }
+}
+
+// Subset-max table for the inter-node term of Eq.6 (R10): tab[m] = max over ordered pairs
+// a != b of nodes in bit set m of R[a][b] (0 for |m| < 2).  max is exact, so the value
+// is the one a pairwise scan gives.  One thread per subset, n <= 16.
+__global__ void k_subset_max(const double* __restrict__ R, int n, double* __restrict__ tab) {
+  const uint32_t m = blockIdx.x * blockDim.x + threadIdx.x;
+  if (m >= (1u << n)) return;
+  double mx = 0.0;
+  for (int a = 0; a < n; ++a) {
+    if (!((m >> a) & 1u)) continue;
+    for (int b = 0; b < n; ++b)
+      if (b != a && ((m >> b) & 1u)) mx = fmax(mx, R[a * n + b]);
+  }
+  tab[m] = mx;
 }
 
 // K4: per-configuration lexicographic (latency, chain) minimum over this rank's chains,
@@ -409,15 +570,14 @@ __global__ void __launch_bounds__(256) k_argmin(const ChainOut* __restrict__ out
   }
 }
 
-// Host-side handle of the K3 variant: MW = mask words (n <= 32 -> 1, else 4), REP = R
-// replicated per lane, TRACE = debug trace records.
-const void* sa_kernel(int mw, bool rep, bool trace) {
-  if (mw == 1) {
-    if (rep) return trace ? (const void*)k_sa_chains<1, true, true> : (const void*)k_sa_chains<1, true, false>;
-    return trace ? (const void*)k_sa_chains<1, false, true> : (const void*)k_sa_chains<1, false, false>;
-  }
-  if (rep) return trace ? (const void*)k_sa_chains<4, true, true> : (const void*)k_sa_chains<4, true, false>;
-  return trace ? (const void*)k_sa_chains<4, false, true> : (const void*)k_sa_chains<4, false, false>;
+// Host-side handles of the K3 variants (MODE 0 small clusters, 1 general; TRACE records).
+const void* sa_kernel(int mode, bool trace) {
+  if (mode == 0) return trace ? (const void*)k_sa_chains<0, true> : (const void*)k_sa_chains<0, false>;
+  return trace ? (const void*)k_sa_chains<1, true> : (const void*)k_sa_chains<1, false>;
+}
+
+int sa_warp_state_bytes(int mode, int N, int pp, int dp, int n) {
+  return mode == 0 ? warp_state_bytes<PosPacked>(N, pp, dp, n, false) : warp_state_bytes<PosWide>(N, pp, dp, n, true);
 }
 
 }  // namespace pip

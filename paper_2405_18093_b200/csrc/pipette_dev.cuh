@@ -60,6 +60,7 @@ struct SaParams {
   const DevCfg* cfgs;
   const double* qtab;
   const double* R;           // n x n, R[a][b] = 1/B[a][b]
+  const double* subset_max;  // 2^n subset maxima of R off-diagonal (n <= 16), or null
   const SaTask* tasks;
   int32_t n_tasks;
   int32_t* task_counter;
