@@ -18,7 +18,7 @@ namespace pip {
 __global__ void k_enumerate_filter(int, int, unsigned long long, int, pipette_model, long long,
                                    const pipette_profile_entry*, int, DevCfg*, unsigned long long*, int, int*,
                                    double*, int, EnumOut*);
-const void* eval_kernel(int mw, bool rep);
+const void* eval_kernel(int mode);
 const void* sa_kernel(int mode, bool trace);
 int sa_warp_state_bytes(int mode, int N, int pp, int dp, int n);
 __global__ void k_subset_max(const double*, int, double*);
@@ -436,6 +436,7 @@ pipette_status pipette_eval(pipette_ctx* ctx, const pipette_model* model, int64_
   P.E = ctx->E;
   P.qtab = (const double*)ctx->qtab.p;
   P.R = ctx->dR;
+  P.subset_max = ctx->dTab;
   P.n_nodes = ctx->n_nodes;
   P.n = n;
   P.cand = d_cfg;
@@ -444,7 +445,8 @@ pipette_status pipette_eval(pipette_ctx* ctx, const pipette_model* model, int64_
   P.vec16 = ((uintptr_t)d_perm % 16 == 0) && (perm_stride % 8 == 0);
   P.bm_words = (maxN + 31) / 32;
   const int nn = ctx->n_nodes * ctx->n_nodes;
-  const bool rep = nn * 32 * 8 <= 64 * 1024;
+  const int mode = (ctx->n_nodes <= 16 && ctx->g <= 15 && ctx->dTab) ? 0 : 1;
+  const bool rep = mode == 0;
   P.rep = rep;
   P.latency = d_latency;
   P.mem = (unsigned long long*)d_mem;
@@ -452,7 +454,7 @@ pipette_status pipette_eval(pipette_ctx* ctx, const pipette_model* model, int64_
   const size_t smem = (size_t)(rep ? nn * 32 : nn) * 8 + ((ctx->E * 8 + 15) & ~15) +
                       (size_t)(P.bm_words + (ctx->n_nodes + 3) / 4) * kEvalThreads * 4;
   if (smem > 227 * 1024) return fail(ctx, PIPETTE_E_UNSUPPORTED, "eval shared memory %zu B too large", smem);
-  const void* kern = eval_kernel(ctx->n_nodes <= 32 ? 1 : 4, rep);
+  const void* kern = eval_kernel(mode);
   CU(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   int occ = 0;
   CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kEvalThreads, smem));

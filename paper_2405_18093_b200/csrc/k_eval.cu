@@ -6,9 +6,13 @@
 // candidate.  One thread per candidate (DESIGN.md section 7 explains why not one warp:
 // the per-candidate work is a sequential, fixed-order sum, and thread-per-candidate
 // keeps all 32 lanes busy).  The mapping row is read with 16-byte vector loads; the
-// config table keys, R = 1/B (lane-replicated when small) and per-thread scratch
-// (bijection bitmap, stage-1 node counts) live in shared memory in thread-interleaved
-// layouts, so per-thread random accesses are bank-conflict free.
+// config table keys and R = 1/B (lane-replicated when small) live in shared memory.
+//   MODE 0 (n <= 16 nodes, <= 15 slots per node): stage-1 node counts are nibbles of a
+//          64-bit register, the node set a 32-bit mask, the bijection bitmap two
+//          registers (N <= 64), and the slowest inter-node link of Eq.6 one load from
+//          the subset-max table.
+//   MODE 1 (general): bitmap and counts in thread-interleaved shared memory (bank-
+//          conflict free), pairwise scan of the stage-1 node set.
 #include "devmath.cuh"
 #include "pipette_dev.cuh"
 
@@ -16,8 +20,9 @@ namespace pip {
 
 constexpr int kEvalThreads = 256;
 
-template <int MW, bool REP>
+template <int MODE>
 __global__ void __launch_bounds__(kEvalThreads) k_eval_stream(EvalParams P) {
+  constexpr bool REP = MODE == 0;
   extern __shared__ __align__(16) unsigned char smem[];
   const int n = P.n_nodes, nn = n * n;
   const int tid = threadIdx.x, lane = tid & 31;
@@ -56,9 +61,14 @@ __global__ void __launch_bounds__(kEvalThreads) k_eval_stream(EvalParams P) {
     const int N = C.N, pp = C.pp;
     const uint32_t spn = (uint32_t)C.spn;
     const uint16_t* row = P.perm + i * (long long)P.perm_stride;
-    for (int w = 0; w < (N + 31) / 32; ++w) bm[w * kEvalThreads + tid] = 0u;
-    for (int w = 0; w < cwords; ++w) cnt[w * kEvalThreads + tid] = 0u;
-    Mask<MW> mask;
+    const bool regbm = MODE == 0 && N <= 64;
+    if (!regbm)
+      for (int w = 0; w < (N + 31) / 32; ++w) bm[w * kEvalThreads + tid] = 0u;
+    if (MODE != 0)
+      for (int w = 0; w < cwords; ++w) cnt[w * kEvalThreads + tid] = 0u;
+    uint32_t b0 = 0u, b1 = 0u, dup = 0u;        // register bitmap (MODE 0, N <= 64)
+    unsigned long long c64 = 0ull;              // nibble counts (MODE 0)
+    Mask<MODE == 0 ? 1 : 4> mask;
     mask.clear();
     bool ok = true;
     double tpp = 0.0, s = 0.0;
@@ -69,14 +79,23 @@ __global__ void __launch_bounds__(kEvalThreads) k_eval_stream(EvalParams P) {
       if (v >= (uint32_t)N) {
         ok = false;
       } else {
-        uint32_t& bw = bm[(v >> 5) * kEvalThreads + tid];
-        const uint32_t bit = 1u << (v & 31);
-        if (bw & bit) ok = false;
-        bw |= bit;
+        if (regbm) {
+          const uint32_t bit = 1u << (v & 31);
+          const bool hi32 = v >= 32;
+          dup |= (hi32 ? b1 : b0) & bit;
+          b0 |= hi32 ? 0u : bit;
+          b1 |= hi32 ? bit : 0u;
+        } else {
+          uint32_t& bw = bm[(v >> 5) * kEvalThreads + tid];
+          const uint32_t bit = 1u << (v & 31);
+          if (bw & bit) ok = false;
+          bw |= bit;
+        }
         nd = div_small(v, C.spn_magic, spn);
       }
       if (x == 0) {                                  // stage-1 worker of pipeline z (Eq.6)
-        cnt[(nd >> 2) * kEvalThreads + tid] += 1u << ((nd & 3) * 8);
+        if (MODE == 0) c64 += 1ull << (4u * nd);
+        else cnt[(nd >> 2) * kEvalThreads + tid] += 1u << ((nd & 3) * 8);
         mask.set(nd);
         s = 0.0;
       } else {                                       // Eq.5 hop x-1 -> x, stage order
@@ -100,42 +119,53 @@ __global__ void __launch_bounds__(kEvalThreads) k_eval_stream(EvalParams P) {
     } else {
       for (int w = 0; w < N; ++w) visit(__ldg(row + w));
     }
+    if (dup) ok = false;
     P.mem[i] = C.mem;
     if (!ok) { P.latency[i] = qnan; P.status[i] = 3; continue; }
     if (!C.has_profile) { P.latency[i] = qnan; P.status[i] = 4; continue; }
     // Eq.6: per-node intra ring over nodes with >= 2 stage-1 members, slowest inter link
     const double* qi = P.qtab + C.qi_off;
     double t_in = 0.0, mx = 0.0;
-#pragma unroll
-    for (int wd = 0; wd < MW; ++wd) {
-      uint32_t bits = mask.w[wd];
+    const int k = mask.count();
+    if (MODE == 0) {
+      uint32_t bits = mask.w[0];
       while (bits) {
-        const uint32_t a = wd * 32 + __ffs(bits) - 1;
+        const uint32_t a = __ffs(bits) - 1;
         bits &= bits - 1;
-        const uint32_t c = (cnt[(a >> 2) * kEvalThreads + tid] >> ((a & 3) * 8)) & 0xffu;
+        const uint32_t c = (uint32_t)(c64 >> (4u * a)) & 15u;
         if (c >= 2) t_in = fmax(t_in, __dmul_rn(__ldg(qi + c), Rab(a, a)));
+      }
+      if (k >= 2) mx = __ldg(P.subset_max + mask.w[0]);
+    } else {
 #pragma unroll
-        for (int wd2 = 0; wd2 < MW; ++wd2) {
-          uint32_t bits2 = mask.w[wd2];
-          while (bits2) {
-            const uint32_t b = wd2 * 32 + __ffs(bits2) - 1;
-            bits2 &= bits2 - 1;
-            if (a != b) mx = fmax(mx, Rab(a, b));
+      for (int wd = 0; wd < 4; ++wd) {
+        uint32_t bits = mask.w[wd];
+        while (bits) {
+          const uint32_t a = wd * 32 + __ffs(bits) - 1;
+          bits &= bits - 1;
+          const uint32_t c = (cnt[(a >> 2) * kEvalThreads + tid] >> ((a & 3) * 8)) & 0xffu;
+          if (c >= 2) t_in = fmax(t_in, __dmul_rn(__ldg(qi + c), Rab(a, a)));
+#pragma unroll
+          for (int wd2 = 0; wd2 < 4; ++wd2) {
+            uint32_t bits2 = mask.w[wd2];
+            while (bits2) {
+              const uint32_t b = wd2 * 32 + __ffs(bits2) - 1;
+              bits2 &= bits2 - 1;
+              if (a != b) mx = fmax(mx, Rab(a, b));
+            }
           }
         }
       }
     }
-    const int k = mask.count();
     const double t_ex = k >= 2 ? __dmul_rn(__ldg(P.qtab + C.qe_off + k), mx) : 0.0;
     P.latency[i] = compose(C.Sb, C.r, C.Ss, tpp, t_in, t_ex);
     P.status[i] = C.feasible ? 0 : 1;
   }
 }
 
-// Host-side handle of the K2 variant (MW mask words, REP lane-replicated R).
-const void* eval_kernel(int mw, bool rep) {
-  if (mw == 1) return rep ? (const void*)k_eval_stream<1, true> : (const void*)k_eval_stream<1, false>;
-  return rep ? (const void*)k_eval_stream<4, true> : (const void*)k_eval_stream<4, false>;
+// Host-side handle of the K2 variant (MODE 0 small clusters, 1 general).
+const void* eval_kernel(int mode) {
+  return mode == 0 ? (const void*)k_eval_stream<0> : (const void*)k_eval_stream<1>;
 }
 
 }  // namespace pip

@@ -89,6 +89,7 @@ struct EvalParams {
   int32_t E;
   const double* qtab;
   const double* R;
+  const double* subset_max;  // 2^n table (MODE 0)
   int32_t n_nodes;
   int64_t n;
   const pipette_config* cand;
