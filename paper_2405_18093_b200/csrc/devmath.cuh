@@ -110,6 +110,9 @@ __device__ __forceinline__ bool metropolis(double d, double beta, double u) {
   return u < exp_det(-__dmul_rn(d, beta));
 }
 
+// Out-of-line exact tail of metropolis_fast (rare: keeps the hot loop's code small).
+static __device__ __noinline__ bool metropolis_exact(double x, double u) { return u < exp_det(x); }
+
 // The same decision with a cheap screen: e^x is first approximated in fp32 (relative
 // error < 2e-5 for -87 <= x <= 0: argument rounding 5.2e-6, ex2.approx scaling 5.2e-6,
 // ex2.approx 2e-7), and exp_det (< 1 ulp from e^x) is evaluated only when u falls within
@@ -123,7 +126,7 @@ __device__ __forceinline__ bool metropolis_fast(double d, double beta, double u)
   const double y = (double)__expf(__double2float_rn(x));
   if (u < __dmul_rn(y, 0.999)) return true;
   if (u > __dmul_rn(y, 1.001)) return false;
-  return u < exp_det(x);
+  return metropolis_exact(x, u);
 }
 
 // Eq.3-4 composition with the Eq.5 value inside T_bubble (R6):

@@ -534,7 +534,7 @@ pipette_status pipette_search(pipette_ctx* ctx, const pipette_model* model, int6
   std::vector<double> cost(tasks.size());
   for (size_t i = 0; i < tasks.size(); ++i) {
     const DevCfg& c = ctx->hcfg[tasks[i].cfg];
-    cost[i] = c.N < 2 ? 0.0 : 60.0 + (c.pp >= 2 ? 14.0 * (c.pp - 1) + 0.5 * c.dp : 0.0);
+    cost[i] = c.N < 2 ? 0.0 : (c.pp >= 2 ? 100.0 + 12.0 * (c.pp - 1) + 6.0 * c.dp : 10.0);
   }
   std::vector<int> order(tasks.size());
   for (size_t i = 0; i < order.size(); ++i) order[i] = (int)i;

@@ -109,7 +109,7 @@ __device__ __forceinline__ double pipe_sum(int z, int pp_rt, const POS& pos, uin
   const uint32_t base = (uint32_t)(z * pp);
   uint32_t prev = node_at(pos, base, p, q, np, nq);
   double s = 0.0;
-#pragma unroll
+#pragma unroll 4
   for (int x = 1; x < (PP > 0 ? PP : pp); ++x) {
     const uint32_t nd = node_at(pos, base + x, p, q, np, nq);
     s = __dadd_rn(s, __dmul_rn(m2, R(prev, nd)));
@@ -128,7 +128,7 @@ __device__ __forceinline__ void pipe_sum2(int za, int zb, int pp_rt, const POS& 
   uint32_t pa = node_at(pos, ba, p, q, np, nq);
   uint32_t pb = node_at(pos, bb, p, q, np, nq);
   double a = 0.0, b = 0.0;
-#pragma unroll
+#pragma unroll 4
   for (int x = 1; x < (PP > 0 ? PP : pp); ++x) {
     const uint32_t na = node_at(pos, ba + x, p, q, np, nq);
     const uint32_t nb = node_at(pos, bb + x, p, q, np, nq);
@@ -475,13 +475,18 @@ __global__ void __launch_bounds__(kSaThreads) k_sa_chains(SaParams P) {
     for (int i = threadIdx.x; i < nn; i += blockDim.x) Rs[i] = P.R[i];
   }
   __syncthreads();
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
   unsigned char* ws = smem + P.r_smem_bytes + wid * P.warp_smem_bytes;
+  __shared__ int s_base;
   for (;;) {
-    int t = 0;
-    if (lane == 0) t = atomicAdd(P.task_counter, 1);
-    t = __shfl_sync(0xffffffffu, t, 0);
-    if (t >= P.n_tasks) break;
+    // the warps of a block take consecutive tasks: the task list is grouped by config, so
+    // a block runs one code path (I-cache locality) and its warps finish together
+    __syncthreads();
+    if (threadIdx.x == 0) s_base = atomicAdd(P.task_counter, nw);
+    __syncthreads();
+    const int t = s_base + wid;
+    if (s_base >= P.n_tasks) break;
+    if (t >= P.n_tasks) continue;
     const SaTask T = P.tasks[t];
     const DevCfg C = P.cfgs[T.cfg];
     unsigned long long t_start = 0;
@@ -491,8 +496,6 @@ __global__ void __launch_bounds__(kSaThreads) k_sa_chains(SaParams P) {
       case 2: run_task<POS, S1, REP, TRACE, 2>(P, T, C, Rs, ws, lane); break;
       case 4: run_task<POS, S1, REP, TRACE, 4>(P, T, C, Rs, ws, lane); break;
       case 8: run_task<POS, S1, REP, TRACE, 8>(P, T, C, Rs, ws, lane); break;
-      case 16: run_task<POS, S1, REP, TRACE, 16>(P, T, C, Rs, ws, lane); break;
-      case 32: run_task<POS, S1, REP, TRACE, 32>(P, T, C, Rs, ws, lane); break;
       default: run_task<POS, S1, REP, TRACE, 0>(P, T, C, Rs, ws, lane); break;
     }
     __syncwarp();

@@ -20,7 +20,7 @@ flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
 s = torch.cuda.current_stream()
 
 
-def run(tag, n=4, do_flush=False, sampler=False, sleep=0.0):
+def run(tag, n=4, do_flush=False, sampler=False, sleep=0.0, flush_fn=None):
     out = []
     ctx = bench.ClockSampler(0) if sampler else None
     if ctx:
@@ -28,6 +28,8 @@ def run(tag, n=4, do_flush=False, sampler=False, sleep=0.0):
     for k in range(n):
         if do_flush:
             flush.fill_(k)
+        if flush_fn:
+            flush_fn(k)
         if sleep:
             torch.cuda.synchronize(); time.sleep(sleep)
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -43,9 +45,17 @@ def run(tag, n=4, do_flush=False, sampler=False, sleep=0.0):
         print(tag, out)
 
 
+
+
+def tiny(k):
+    flush.fill_(k)
+    pip.search(model, w.bs_global, 1, 10, w.seed)
+
 run("plain")
-run("flush", do_flush=True)
-run("sampler", sampler=True)
-run("flush+sampler", do_flush=True, sampler=True)
-run("sleep0.2", sleep=0.2)
+run("flush256", do_flush=True)
+for mb in (48, 96, 128, 192):
+    buf = torch.empty(mb << 20, dtype=torch.uint8, device="cuda")
+    run(f"fill{mb}MB", flush_fn=lambda k, b=buf: b.fill_(k))
+    del buf
+run("flush256+tinysearch", flush_fn=tiny)
 run("plain again")
