@@ -92,11 +92,15 @@ struct PosWide {
   }
 };
 
-// Node of position w after the proposed swap of positions p and q (nodes np, nq).
+constexpr uint32_t kNone = 0xffffffffu;
+
+// Node of position w with positions p and q reading as nodes nq and np instead (kNone: no
+// substitution -- the compiler then drops the compares).
 template <class POS>
 __device__ __forceinline__ uint32_t node_at(const POS& pos, uint32_t w, uint32_t p, uint32_t q, uint32_t np,
                                             uint32_t nq) {
   const uint32_t v = pos.node(w);
+  if (p == kNone) return v;
   return w == p ? nq : (w == q ? np : v);
 }
 
@@ -109,7 +113,7 @@ __device__ __forceinline__ double pipe_sum(int z, int pp_rt, const POS& pos, uin
   const uint32_t base = (uint32_t)(z * pp);
   uint32_t prev = node_at(pos, base, p, q, np, nq);
   double s = 0.0;
-#pragma unroll 4
+#pragma unroll (PP > 0 ? 32 : 4)
   for (int x = 1; x < (PP > 0 ? PP : pp); ++x) {
     const uint32_t nd = node_at(pos, base + x, p, q, np, nq);
     s = __dadd_rn(s, __dmul_rn(m2, R(prev, nd)));
@@ -128,7 +132,7 @@ __device__ __forceinline__ void pipe_sum2(int za, int zb, int pp_rt, const POS& 
   uint32_t pa = node_at(pos, ba, p, q, np, nq);
   uint32_t pb = node_at(pos, bb, p, q, np, nq);
   double a = 0.0, b = 0.0;
-#pragma unroll 4
+#pragma unroll (PP > 0 ? 32 : 4)
   for (int x = 1; x < (PP > 0 ? PP : pp); ++x) {
     const uint32_t na = node_at(pos, ba + x, p, q, np, nq);
     const uint32_t nb = node_at(pos, bb + x, p, q, np, nq);
@@ -352,7 +356,7 @@ __device__ void run_task(const SaParams& P, const SaTask& T, const DevCfg& C, co
   for (int z = 0; z < dp; ++z) {
     s1.add_init(pos.node((uint32_t)(z * pp)));
     if (pp >= 2) {
-      const double s = pipe_sum<REP, PP>(z, pp, pos, 0xffffffffu, 0xffffffffu, 0u, 0u, C.m2, R);
+      const double s = pipe_sum<REP, PP>(z, pp, pos, kNone, kNone, 0u, 0u, C.m2, R);
       psum[z * 32 + lane] = s;
       tpp = fmax(tpp, s);
     }
@@ -390,8 +394,11 @@ __device__ void run_task(const SaParams& P, const SaTask& T, const DevCfg& C, co
           xp = d.p - (uint32_t)(zp * pp);
           xq = d.q - (uint32_t)(zq * pp);
           two = zq != zp;
-          if (two) pipe_sum2<REP, PP>(zp, zq, pp, pos, d.p, d.q, np, nq, C.m2, R, sA, sB);
-          else sA = pipe_sum<REP, PP>(zp, pp, pos, d.p, d.q, np, nq, C.m2, R);
+          // apply the swap tentatively (reverted below if rejected): the re-sum then reads
+          // plain positions, with no per-hop substitution
+          pos.swap(d.p, d.q, rp, rq);
+          if (two) pipe_sum2<REP, PP>(zp, zq, pp, pos, kNone, kNone, 0u, 0u, C.m2, R, sA, sB);
+          else sA = pipe_sum<REP, PP>(zp, pp, pos, kNone, kNone, 0u, 0u, C.m2, R);
           const double oldA = psum[zp * 32 + lane];
           const double oldB = two ? psum[zq * 32 + lane] : oldA;
           const bool drop = (oldA == tpp && sA < tpp) || (two && oldB == tpp && sB < tpp);
@@ -439,8 +446,10 @@ __device__ void run_task(const SaParams& P, const SaTask& T, const DevCfg& C, co
         }
       }
       if (acc) {
-        pos.swap(d.p, d.q, rp, rq);
+        if (pp < 2 || np == nq) pos.swap(d.p, d.q, rp, rq);   // (already applied when re-summed)
         ++accepted;
+      } else if (pp >= 2) {
+        pos.swap(d.p, d.q, rq, rp);                             // revert the tentative swap
       }
       if (improved)
         for (int w = 0; w < N; ++w) bperm[w * 32 + lane] = (uint16_t)POS::slot_of(pos.raw((uint32_t)w));
@@ -496,6 +505,8 @@ __global__ void __launch_bounds__(kSaThreads) k_sa_chains(SaParams P) {
       case 2: run_task<POS, S1, REP, TRACE, 2>(P, T, C, Rs, ws, lane); break;
       case 4: run_task<POS, S1, REP, TRACE, 4>(P, T, C, Rs, ws, lane); break;
       case 8: run_task<POS, S1, REP, TRACE, 8>(P, T, C, Rs, ws, lane); break;
+      case 16: run_task<POS, S1, REP, TRACE, 16>(P, T, C, Rs, ws, lane); break;
+      case 32: run_task<POS, S1, REP, TRACE, 32>(P, T, C, Rs, ws, lane); break;
       default: run_task<POS, S1, REP, TRACE, 0>(P, T, C, Rs, ws, lane); break;
     }
     __syncwarp();
