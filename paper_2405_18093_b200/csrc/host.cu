@@ -22,6 +22,7 @@ const void* eval_kernel(int mode);
 const void* sa_kernel(int mode, bool trace);
 int sa_warp_state_bytes(int mode, int N, int pp, int dp, int n);
 __global__ void k_subset_max(const double*, int, double*);
+__global__ void k_tin_rank(const DevCfg*, const int*, const double*, const double*, int, uint8_t*, double*);
 __global__ void k_argmin(const ChainOut*, const int*, int, CfgBest*);
 constexpr int kEnumThreads = 1024, kEvalThreads = 256, kSaThreads = 128;
 
@@ -113,7 +114,7 @@ struct pipette_ctx {
   DevBuf cfgs, keys, feas, qtab, eout;
   // search buffers
   DevBuf tasks, counter, chain_out, best_perm, cfg_slot, cfg_best, gbits, items, gitems, pack, accepted,
-      slot_perm_off, slot_lane, trace_slot, trace, task_prof;
+      slot_perm_off, slot_lane, trace_slot, trace, task_prof, tin_rank, tin_vs;
   int64_t n_tasks_last = 0;
   cudaEvent_t ev[6] = {};
 };
@@ -382,7 +383,7 @@ void pipette_destroy(pipette_ctx* ctx) {
   DevBuf* bufs[] = {&ctx->cfgs, &ctx->keys, &ctx->feas, &ctx->qtab, &ctx->eout, &ctx->tasks, &ctx->counter,
                     &ctx->chain_out, &ctx->best_perm, &ctx->cfg_slot, &ctx->cfg_best, &ctx->gbits, &ctx->items,
                     &ctx->gitems, &ctx->pack, &ctx->accepted, &ctx->slot_perm_off, &ctx->slot_lane,
-                    &ctx->trace_slot, &ctx->trace, &ctx->task_prof};
+                    &ctx->trace_slot, &ctx->trace, &ctx->task_prof, &ctx->tin_rank, &ctx->tin_vs};
   for (DevBuf* b : bufs)
     if (b->p) cudaFree(b->p);
   if (ctx->dR) cudaFree(ctx->dR);
@@ -610,6 +611,8 @@ pipette_status pipette_search(pipette_ctx* ctx, const pipette_model* model, int6
   P.qtab = (const double*)ctx->qtab.p;
   P.R = ctx->dR;
   P.subset_max = ctx->dTab;
+  P.tin_rank = mode == 0 ? (const uint8_t*)ctx->tin_rank.p : nullptr;
+  P.tin_vs = mode == 0 ? (const double*)ctx->tin_vs.p : nullptr;
   P.tasks = (const SaTask*)ctx->tasks.p;
   P.n_tasks = (int)sorted.size();
   P.task_counter = (int*)ctx->counter.p;
@@ -639,7 +642,17 @@ pipette_status pipette_search(pipette_ctx* ctx, const pipette_model* model, int6
   occ = std::max(occ, 1);
   const int grid = (int)std::max<long long>(1, std::min<long long>(((long long)sorted.size() + wpb - 1) / wpb,
                                                                    (long long)occ * ctx->n_sms));
+  if (mode == 0) {   // T_in rank tables of every feasible config (S1Reg)
+    CU(ensure(ctx->tin_rank, (size_t)F * 256));
+    CU(ensure(ctx->tin_vs, sizeof(double) * (size_t)F * 256));
+  }
   CU(cudaEventRecord(ctx->ev[2], s));
+  if (mode == 0) {
+    k_tin_rank<<<F, 256, 0, s>>>((const DevCfg*)ctx->cfgs.p, (const int*)ctx->feas.p, (const double*)ctx->qtab.p,
+                                 ctx->dR, n, (uint8_t*)ctx->tin_rank.p, (double*)ctx->tin_vs.p);
+    ctx->launches++;
+    CU(cudaGetLastError());
+  }
   if (!sorted.empty()) {
     void* args[] = {&P};
     CU(cudaLaunchKernel(kern, dim3(grid), dim3(wpb * 32), args, smem, s));

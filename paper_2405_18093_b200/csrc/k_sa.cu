@@ -47,31 +47,24 @@ struct PosPacked {
   uint32_t* s;
   int lane;
   static __host__ __device__ int bytes(int N) { return ((N + 1) / 2) * 128; }
-  __device__ __forceinline__ uint32_t half(uint32_t w) const {
-    return (s[(w >> 1) * 32 + lane] >> ((w & 1u) * 16u)) & 0xffffu;
+  // 16-bit cell of position w: half (w & 1) of word (w >> 1)*32 + lane -- the bank is the
+  // lane's for every w, and the cell is read/written with 16/8-bit LDS/STS (no RMW).
+  __device__ __forceinline__ uint32_t hidx(uint32_t w) const { return ((((w >> 1) << 5) + (uint32_t)lane) << 1) | (w & 1u); }
+  __device__ __forceinline__ uint32_t raw(uint32_t w) const { return reinterpret_cast<const uint16_t*>(s)[hidx(w)]; }
+  __device__ __forceinline__ uint32_t node(uint32_t w) const {
+    return reinterpret_cast<const uint8_t*>(s)[(hidx(w) << 1) + 1];   // high byte of the cell
   }
-  __device__ __forceinline__ uint32_t raw(uint32_t w) const { return half(w); }
-  __device__ __forceinline__ uint32_t node(uint32_t w) const { return half(w) >> 8; }
   static __device__ __forceinline__ uint32_t node_of(uint32_t r) { return r >> 8; }
   static __device__ __forceinline__ uint32_t slot_of(uint32_t r) { return r & 0xffu; }
   __device__ __forceinline__ void init(int N, uint32_t spn, uint32_t spn_magic) {
-    for (int w = 0; w < N; w += 2) {
-      const uint32_t a = (uint32_t)w | (div_small((uint32_t)w, spn_magic, spn) << 8);
-      const uint32_t b = w + 1 < N ? ((uint32_t)(w + 1) | (div_small((uint32_t)(w + 1), spn_magic, spn) << 8)) : 0u;
-      s[(w >> 1) * 32 + lane] = a | (b << 16);
-    }
+    uint16_t* s16 = reinterpret_cast<uint16_t*>(s);
+    for (int w = 0; w < N; ++w) s16[hidx((uint32_t)w)] = (uint16_t)((uint32_t)w | (div_small((uint32_t)w, spn_magic, spn) << 8));
   }
-  // positions p and q exchange their contents (rp = raw(p), rq = raw(q))
+  // positions p and q take the contents rq and rp
   __device__ __forceinline__ void swap(uint32_t p, uint32_t q, uint32_t rp, uint32_t rq) {
-    uint32_t* wpp = &s[(p >> 1) * 32 + lane];
-    uint32_t* wqq = &s[(q >> 1) * 32 + lane];
-    if ((p >> 1) == (q >> 1)) {
-      *wpp = (*wpp >> 16) | (*wpp << 16);
-    } else {
-      const uint32_t shp = (p & 1u) * 16u, shq = (q & 1u) * 16u;
-      *wpp = (*wpp & ~(0xffffu << shp)) | (rq << shp);
-      *wqq = (*wqq & ~(0xffffu << shq)) | (rp << shq);
-    }
+    uint16_t* s16 = reinterpret_cast<uint16_t*>(s);
+    s16[hidx(p)] = (uint16_t)rq;
+    s16[hidx(q)] = (uint16_t)rp;
   }
 };
 
@@ -147,34 +140,38 @@ __device__ __forceinline__ void pipe_sum2(int za, int zb, int pp_rt, const POS& 
 
 // ------------------------------------------------------------------ stage-1 (Eq.6) state
 struct S1Ctx {
-  const double* qi;   // qi(c), c = 0..dp
-  const double* qe;   // qe(k), k = 0..min(dp, n)
-  const double* tab;  // subset-max table (S1Reg only)
+  const double* qi;      // qi(c), c = 0..dp
+  const double* qe;      // qe(k), k = 0..min(dp, n)
+  const double* tab;     // subset-max table (S1Reg only)
+  const uint8_t* rank;   // [a*16 + c] rank of qi(c)*R[a][a], 255 if c < 2 (S1Reg only)
+  const double* vs;      // values in rank order (S1Reg only)
   int n;
 };
 
-// n <= 16 nodes and <= 15 stage-1 members per node.
+// n <= 16 nodes and <= 15 stage-1 members per node.  T_in by ranks: for this config every
+// value qi(c)*R[a][a] (c >= 2) has a precomputed position in descending order
+// (k_tin_rank); a node's current rank is one byte of rk[], and T_in is the value at the
+// smallest rank present (SIMD byte minimum) -- the max of Eq.6's intra term without a scan.
 template <bool REP>
 struct S1Reg {
   uint64_t cnt, cnt2;
   uint32_t mask, mask2;
-  int k, k2, win, win2;
+  uint32_t rk[4], rk2[4];
+  int k, k2;
   double tin, tex, tin2, tex2;
 
   static __device__ __forceinline__ uint32_t get(uint64_t c, uint32_t a) { return (uint32_t)(c >> (4u * a)) & 15u; }
-
-  __device__ __forceinline__ double tin_full(uint64_t c, const S1Ctx& X, const RTab<REP>& R, int& w) const {
-    double t = 0.0;
-    w = -1;
-#pragma unroll 4
-    for (int a = 0; a < X.n; ++a) {
-      const uint32_t ca = get(c, (uint32_t)a);
-      if (ca >= 2u) {
-        const double v = __dmul_rn(__ldg(X.qi + ca), R((uint32_t)a, (uint32_t)a));
-        if (v > t) { t = v; w = a; }
-      }
-    }
-    return t;
+  static __device__ __forceinline__ void set_byte(uint32_t (&r)[4], uint32_t a, uint32_t v) {
+    const uint32_t sh = (a & 3u) * 8u;
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+      r[i] = ((a >> 2) == (uint32_t)i) ? ((r[i] & ~(0xffu << sh)) | (v << sh)) : r[i];
+  }
+  static __device__ __forceinline__ double tin_of(const uint32_t (&r)[4], const S1Ctx& X) {
+    uint32_t m = __vminu4(__vminu4(r[0], r[1]), __vminu4(r[2], r[3]));
+    m = __vminu4(m, m >> 16);
+    m = __vminu4(m, m >> 8) & 0xffu;
+    return m == 0xffu ? 0.0 : __ldg(X.vs + m);
   }
   __device__ __forceinline__ double tex_of(uint32_t m, int kk, const S1Ctx& X) const {
     return kk >= 2 ? __dmul_rn(__ldg(X.qe + kk), __ldg(X.tab + m)) : 0.0;
@@ -182,8 +179,10 @@ struct S1Reg {
   __device__ __forceinline__ void clear() { cnt = 0ull; mask = 0u; }
   __device__ __forceinline__ void add_init(uint32_t a) { cnt += 1ull << (4u * a); mask |= 1u << a; }
   __device__ __forceinline__ void finish_init(const S1Ctx& X, const RTab<REP>& R) {
+    rk[0] = rk[1] = rk[2] = rk[3] = 0xffffffffu;
+    for (int a = 0; a < X.n; ++a) set_byte(rk, (uint32_t)a, X.rank[a * 16 + get(cnt, (uint32_t)a)]);
     k = __popc(mask);
-    tin = tin_full(cnt, X, R, win);
+    tin = tin_of(rk, X);
     tex = tex_of(mask, k, X);
   }
   // a stage-1 member moves from node dn to node up (tentative state)
@@ -192,16 +191,18 @@ struct S1Reg {
     cnt2 = cnt - (1ull << (4u * dn)) + (1ull << (4u * up));
     mask2 = (mask & (c_dn == 0u ? ~(1u << dn) : 0xffffffffu)) | (1u << up);
     k2 = __popc(mask2);
-    tin2 = tin; win2 = win;
-    if ((int)dn == win) {
-      tin2 = tin_full(cnt2, X, R, win2);
-    } else if (c_up >= 2u) {
-      const double v = __dmul_rn(__ldg(X.qi + c_up), R(up, up));
-      if (v > tin2) { tin2 = v; win2 = (int)up; }
-    }
+#pragma unroll
+    for (int i = 0; i < 4; ++i) rk2[i] = rk[i];
+    set_byte(rk2, dn, X.rank[dn * 16 + c_dn]);
+    set_byte(rk2, up, X.rank[up * 16 + c_up]);
+    tin2 = tin_of(rk2, X);
     tex2 = (mask2 == mask) ? tex : tex_of(mask2, k2, X);
   }
-  __device__ __forceinline__ void commit() { cnt = cnt2; mask = mask2; k = k2; tin = tin2; win = win2; tex = tex2; }
+  __device__ __forceinline__ void commit() {
+    cnt = cnt2; mask = mask2; k = k2; tin = tin2; tex = tex2;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) rk[i] = rk2[i];
+  }
 };
 
 // General stage-1 state: counts (u8, c_n <= spn <= 255) in shared memory, 128-bit node
@@ -335,7 +336,9 @@ __device__ void run_task(const SaParams& P, const SaTask& T, const DevCfg& C, co
   const uint32_t chain = (uint32_t)(T.c_first + (T.k0 + lane) * P.world);
   const int slot = T.slot0 + lane;
   const RTab<REP> R{Rs, n, lane};
-  const S1Ctx X{P.qtab + C.qi_off, P.qtab + C.qe_off, P.subset_max, n};
+  const S1Ctx X{P.qtab + C.qi_off, P.qtab + C.qe_off, P.subset_max,
+                P.tin_rank ? P.tin_rank + (size_t)T.f * 256 : nullptr,
+                P.tin_vs ? P.tin_vs + (size_t)T.f * 256 : nullptr, n};
 
   POS pos{reinterpret_cast<uint32_t*>(ws), lane};
   double* psum = reinterpret_cast<double*>(ws + align16(POS::bytes(N)));
@@ -353,12 +356,13 @@ __device__ void run_task(const SaParams& P, const SaTask& T, const DevCfg& C, co
   pos.init(N, (uint32_t)C.spn, C.spn_magic);
   for (int w = 0; w < N; ++w) bperm[w * 32 + lane] = (uint16_t)w;
   double tpp = 0.0;
+  int nmax = 0;   // pipelines whose sum equals tpp
   for (int z = 0; z < dp; ++z) {
     s1.add_init(pos.node((uint32_t)(z * pp)));
     if (pp >= 2) {
       const double s = pipe_sum<REP, PP>(z, pp, pos, kNone, kNone, 0u, 0u, C.m2, R);
       psum[z * 32 + lane] = s;
-      tpp = fmax(tpp, s);
+      if (s > tpp) { tpp = s; nmax = 1; } else if (s == tpp) { ++nmax; }
     }
   }
   s1.finish_init(X, R);
@@ -388,6 +392,7 @@ __device__ void run_task(const SaParams& P, const SaTask& T, const DevCfg& C, co
         int zp = 0, zq = 0;
         bool two = false;
         double sA = 0.0, sB = 0.0, tpp2 = tpp;
+        int nmax2 = nmax;
         if (pp >= 2) {
           zp = (int)div_small(d.p, C.pp_magic, (uint32_t)pp);
           zq = (int)div_small(d.q, C.pp_magic, (uint32_t)pp);
@@ -401,9 +406,15 @@ __device__ void run_task(const SaParams& P, const SaTask& T, const DevCfg& C, co
           else sA = pipe_sum<REP, PP>(zp, pp, pos, kNone, kNone, 0u, 0u, C.m2, R);
           const double oldA = psum[zp * 32 + lane];
           const double oldB = two ? psum[zq * 32 + lane] : oldA;
-          const bool drop = (oldA == tpp && sA < tpp) || (two && oldB == tpp && sB < tpp);
-          if (drop) {   // a pipeline at the max decreased: rescan (4 independent max chains)
-            double m0 = two ? fmax(sA, sB) : sA, m1 = 0.0, m2 = 0.0, m3 = 0.0;
+          const double snew = two ? fmax(sA, sB) : sA;
+          const int keep = nmax - (oldA == tpp ? 1 : 0) - ((two && oldB == tpp) ? 1 : 0);  // untouched at max
+          if (keep > 0 || snew >= tpp) {
+            // the max is max(tpp if an untouched pipeline still holds it, new sums)
+            tpp2 = (keep > 0) ? fmax(tpp, snew) : snew;
+            nmax2 = (keep > 0 && tpp2 == tpp ? keep : 0) + (sA == tpp2 ? 1 : 0) + ((two && sB == tpp2) ? 1 : 0);
+          } else {
+            // the unique max pipeline decreased: rescan (4 independent max chains)
+            double m0 = snew, m1 = 0.0, m2 = 0.0, m3 = 0.0;
             int z = 0;
             for (; z + 4 <= dp; z += 4) {
               const double v0 = psum[(z + 0) * 32 + lane], v1 = psum[(z + 1) * 32 + lane];
@@ -415,8 +426,11 @@ __device__ void run_task(const SaParams& P, const SaTask& T, const DevCfg& C, co
             }
             for (; z < dp; ++z) m0 = fmax(m0, (z == zp || z == zq) ? 0.0 : psum[z * 32 + lane]);
             tpp2 = fmax(fmax(m0, m1), fmax(m2, m3));
-          } else {
-            tpp2 = fmax(tpp, two ? fmax(sA, sB) : sA);
+            nmax2 = 0;
+            for (z = 0; z < dp; ++z) {
+              const double v = (z == zp) ? sA : ((z == zq) ? sB : psum[z * 32 + lane]);
+              nmax2 += v == tpp2 ? 1 : 0;
+            }
           }
         }
         // ---- Eq.6: the stage-1 node multiset changes only if exactly one of p, q is stage 1
@@ -436,6 +450,7 @@ __device__ void run_task(const SaParams& P, const SaTask& T, const DevCfg& C, co
             psum[zp * 32 + lane] = sA;
             if (two) psum[zq * 32 + lane] = sB;
             tpp = tpp2;
+            nmax = nmax2;
           }
           if (dpchg) s1.commit();
           cur = Lp;
@@ -533,6 +548,32 @@ __global__ void k_subset_max(const double* __restrict__ R, int n, double* __rest
       if (b != a && ((m >> b) & 1u)) mx = fmax(mx, R[a * n + b]);
   }
   tab[m] = mx;
+}
+
+// Per feasible config (block f): rank every value qi(c)*R[a][a], a < n, 2 <= c <= min(spn,
+// dp), in descending order (ties by index), so that T_in = the value of the smallest rank
+// present.  rank[f][a*16 + c] (255 when c < 2 or out of range), vs[f][rank] = value.
+__global__ void k_tin_rank(const DevCfg* __restrict__ cfgs, const int* __restrict__ feas, const double* __restrict__ qtab,
+                           const double* __restrict__ R, int n, uint8_t* __restrict__ rank, double* __restrict__ vs) {
+  const int f = blockIdx.x;
+  const DevCfg C = cfgs[feas[f]];
+  const int cmax = min(min(C.spn, C.dp), 15);
+  const int per = cmax >= 2 ? cmax - 1 : 0;      // values c = 2..cmax per node
+  const int P = n * per;
+  __shared__ double v[256];
+  for (int i = threadIdx.x; i < 256; i += blockDim.x) rank[(size_t)f * 256 + i] = 0xff;
+  for (int i = threadIdx.x; i < P; i += blockDim.x) {
+    const int a = i / per, c = 2 + i % per;
+    v[i] = __dmul_rn(qtab[C.qi_off + c], R[a * n + a]);
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < P; i += blockDim.x) {
+    int r = 0;
+    for (int j = 0; j < P; ++j) r += (v[j] > v[i] || (v[j] == v[i] && j < i)) ? 1 : 0;
+    const int a = i / per, c = 2 + i % per;
+    rank[(size_t)f * 256 + a * 16 + c] = (uint8_t)r;
+    vs[(size_t)f * 256 + r] = v[i];
+  }
 }
 
 // K4: per-configuration lexicographic (latency, chain) minimum over this rank's chains,

@@ -61,6 +61,8 @@ struct SaParams {
   const double* qtab;
   const double* R;           // n x n, R[a][b] = 1/B[a][b]
   const double* subset_max;  // 2^n subset maxima of R off-diagonal (n <= 16), or null
+  const uint8_t* tin_rank;   // per feasible config: 256 ranks (k_tin_rank), MODE 0
+  const double* tin_vs;      // per feasible config: 256 values in rank order, MODE 0
   const SaTask* tasks;
   int32_t n_tasks;
   int32_t* task_counter;
