@@ -1,0 +1,41 @@
+"""torchrun worker: pipette_search over NCCL on W GPUs; rank 0 writes the plan as JSON.
+Usage: torchrun --nproc-per-node W tests/helpers/mp_search.py OUT.json WORKLOAD CHAINS ITERS"""
+import json
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, ROOT)
+
+import torch  # noqa: E402
+import torch.distributed as dist  # noqa: E402
+
+import workloads as W  # noqa: E402
+from paper_2405_18093_b200 import Model, Pipette  # noqa: E402
+
+
+def main(out, name, chains, iters):
+    local = int(os.environ["LOCAL_RANK"])
+    torch.cuda.set_device(local)
+    dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    w = W.WORKLOADS[name]
+    B, prof = W.workload_inputs(w)
+    m = w.model
+    pip = Pipette.from_torch_distributed(w.n_nodes, w.gpus_per_node, B, prof, device=local,
+                                         mem_capacity_bytes=w.cap_bytes, mem_margin_permille=w.margin_permille)
+    res = pip.search(Model(m.n_layers, m.hidden, m.heads, m.seq_len, m.vocab), w.bs_global, chains, iters, w.seed,
+                     per_config=True)
+    p = res["plan"]
+    rec = {"rank": dist.get_rank(), "world": dist.get_world_size(), "latency": p.latency_s.hex(),
+           "cfg_index": p.cfg_index, "chain": p.chain, "best_step": p.best_step, "perm": p.perm.tolist(),
+           "t_pp": p.t_pp.hex(), "t_dp": p.t_dp.hex(), "sa_steps": p.sa_steps, "sa_accepted": p.sa_accepted,
+           "per_config": [(q.cfg_index, q.latency_s.hex(), q.chain, q.perm.tolist()) for q in res["per_config"]]}
+    recs = [None] * dist.get_world_size()
+    dist.all_gather_object(recs, rec)
+    if dist.get_rank() == 0:
+        json.dump(recs, open(out, "w"))
+    dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main(sys.argv[1], sys.argv[2], int(sys.argv[3]), int(sys.argv[4]))

@@ -1,0 +1,48 @@
+"""Multi-GPU pipette_search over NCCL (one process per GPU, torchrun): every rank gets the
+identical plan, bit-identical to the 1-GPU search and to the oracle (R18)."""
+import json
+import os
+import subprocess
+import sys
+
+import numpy as np
+import pytest
+
+import oracle as O
+import workloads as W
+
+pytestmark = pytest.mark.gpu
+HERE = os.path.dirname(os.path.abspath(__file__))
+
+
+def _ngpu():
+    import torch
+    return torch.cuda.device_count()
+
+
+@pytest.mark.parametrize("world", [2, 4, 8])
+def test_multi_gpu_plan_bit_identical(world, tmp_path):
+    if _ngpu() < world:
+        pytest.skip(f"needs {world} GPUs")
+    name, chains, iters = "C1", 8, 1000
+    out = tmp_path / "plan.json"
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={world}",
+           "--master-addr=127.0.0.1", "--master-port=29533", os.path.join(HERE, "helpers", "mp_search.py"),
+           str(out), name, str(chains), str(iters)]
+    subprocess.run(cmd, check=True, timeout=600)
+    recs = json.load(open(out))
+    w = W.WORKLOADS[name]
+    B, prof = W.workload_inputs(w)
+    m = w.model
+    cl = O.make_cluster(w.n_nodes, w.gpus_per_node, w.cap_bytes, w.margin_permille)
+    mo = O.make_model(m.n_layers, m.hidden, m.heads, m.seq_len, m.vocab)
+    ref = O.search(cl, B, O.make_profile(prof), mo, w.bs_global, chains, iters, w.seed)
+    assert len(recs) == world
+    for r in recs:
+        assert r == {**recs[0], "rank": r["rank"]}                      # identical on every rank
+        assert float.fromhex(r["latency"]) == ref.latency
+        assert (r["cfg_index"], r["chain"], r["best_step"]) == (ref.cfg_index, ref.chain, ref.best_step)
+        assert r["perm"] == ref.perm.tolist()
+        assert float.fromhex(r["t_pp"]) == ref.t_pp and float.fromhex(r["t_dp"]) == ref.t_dp
+        assert (r["sa_steps"], r["sa_accepted"]) == (ref.sa_steps, ref.sa_accepted)
+        assert sorted(float.fromhex(q[1]) for q in r["per_config"]) == sorted(ref.per_config_best.tolist())
