@@ -606,6 +606,10 @@ pipette_status pipette_search(pipette_ctx* ctx, const pipette_model* model, int6
     CU(cudaMemsetAsync(ctx->trace.p, 0, sizeof(pipette_trace_record) * (size_t)o.n_trace * o.trace_cap, s));
   }
 
+  if (mode == 0) {   // T_in rank tables of every feasible config (S1Reg)
+    CU(ensure(ctx->tin_rank, (size_t)F * 256));
+    CU(ensure(ctx->tin_vs, sizeof(double) * (size_t)F * 256));
+  }
   SaParams P{};
   P.cfgs = (const DevCfg*)ctx->cfgs.p;
   P.qtab = (const double*)ctx->qtab.p;
@@ -642,10 +646,6 @@ pipette_status pipette_search(pipette_ctx* ctx, const pipette_model* model, int6
   occ = std::max(occ, 1);
   const int grid = (int)std::max<long long>(1, std::min<long long>(((long long)sorted.size() + wpb - 1) / wpb,
                                                                    (long long)occ * ctx->n_sms));
-  if (mode == 0) {   // T_in rank tables of every feasible config (S1Reg)
-    CU(ensure(ctx->tin_rank, (size_t)F * 256));
-    CU(ensure(ctx->tin_vs, sizeof(double) * (size_t)F * 256));
-  }
   CU(cudaEventRecord(ctx->ev[2], s));
   if (mode == 0) {
     k_tin_rank<<<F, 256, 0, s>>>((const DevCfg*)ctx->cfgs.p, (const int*)ctx->feas.p, (const double*)ctx->qtab.p,
