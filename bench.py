@@ -282,20 +282,9 @@ def run_ours(args):
         dist.destroy_process_group()
 
 
-def bench_eval(pip, model, w, cfgs, feas, pk, n=1 << 22, reps=5):
-    """pipette_eval on a homogeneous batch of 2^22 random mappings of the feasible config
-    with the largest N; HBM roofline with 25 + 2N algorithmic bytes."""
+def _eval_time(pip, model, w, cfg, perm, reps=5):
     import torch
-    idx = max((i for i in range(len(feas)) if feas[i]), key=lambda i: (cfgs[i][0] * cfgs[i][2], -i))
-    pp, tp, dp, mb = (int(x) for x in cfgs[idx])
-    N = pp * dp
-    stride = ((N + 7) // 8) * 8
-    g = torch.Generator(device="cuda").manual_seed(5)
-    keys = torch.rand((n, N), device="cuda", generator=g)
-    perm = torch.zeros((n, stride), dtype=torch.int16, device="cuda")
-    perm[:, :N] = torch.argsort(keys, dim=1).to(torch.int16)
-    del keys
-    cfg = torch.tensor([pp, tp, dp, mb], dtype=torch.int16, device="cuda").repeat(n, 1).contiguous()
+    n = cfg.shape[0]
     out = (torch.empty(n, dtype=torch.float64, device="cuda"), torch.empty(n, dtype=torch.int64, device="cuda"),
            torch.empty(n, dtype=torch.uint8, device="cuda"))
     for _ in range(3):
@@ -309,15 +298,48 @@ def bench_eval(pip, model, w, cfgs, feas, pk, n=1 << 22, reps=5):
         b.record()
         torch.cuda.synchronize()
         ts.append(a.elapsed_time(b) / 1000.0)
-    t = statistics.median(ts)
-    alg = 8 + 2 * N + 17                      # config + mapping in, latency + mem + status out
-    gbs = alg * n / t / 1e9
-    return {"value": n / t, "unit": "candidates/s", "config": [pp, tp, dp, mb], "N": N, "batch": n,
-            "stride": stride, "roofline": {"kernel": "k_eval_stream", "bound": "hbm", "achieved": gbs,
-                                             "peak": pk.get("hbm_gbs"), "unit": "GB/s",
-                                             "frac": gbs / pk.get("hbm_gbs", 6538.3), "traffic": None,
-                                             "alg_bytes_per_candidate": alg,
-                                             "note": f"batch {n * (stride * 2 + 25) / 1e9:.2f} GB > L2"}}
+    return statistics.median(ts), out
+
+
+def _perms(n, Ns, stride, seed):
+    """n random mappings; row i is a uniform permutation of [0, Ns[i]) (padded to stride)."""
+    import torch
+    g = torch.Generator(device="cuda").manual_seed(seed)
+    keys = torch.rand((n, stride), device="cuda", generator=g)
+    col = torch.arange(stride, device="cuda").unsqueeze(0)
+    keys = torch.where(col < Ns.unsqueeze(1), keys, 2.0 + col.to(keys.dtype))   # padding sorts last
+    perm = torch.argsort(keys, dim=1).to(torch.int16)
+    return perm.contiguous()
+
+
+def bench_eval(pip, model, w, cfgs, feas, pk, n=1 << 22):
+    """pipette_eval (row a10) on 2^22 random mappings: (1) homogeneous batch of the feasible
+    config with the largest N, (2) mixed batch over every feasible config.
+    HBM roofline with 8 + 2N + 17 algorithmic bytes per candidate."""
+    import torch
+    fi = [i for i in range(len(feas)) if feas[i]]
+    out = {}
+    idx = max(fi, key=lambda i: (cfgs[i][0] * cfgs[i][2], -i))
+    for tag, rows in (("homogeneous", [idx] * n), ("mixed", [fi[k % len(fi)] for k in range(n)])):
+        rows = np.asarray(rows)
+        np.random.default_rng(3).shuffle(rows)
+        cf = torch.from_numpy(cfgs[rows].astype(np.int16)).cuda().contiguous()
+        Ns = torch.from_numpy((cfgs[rows, 0] * cfgs[rows, 2]).astype(np.int64)).cuda()
+        stride = int(((Ns.max().item() + 7) // 8) * 8)
+        perm = _perms(n, Ns, stride, 5)
+        t, res = _eval_time(pip, model, w, cf, perm)
+        alg = float((8 + 2 * Ns.double() + 17).sum().item())
+        gbs = alg / t / 1e9
+        st = res[2].cpu().numpy()
+        out[tag] = {"value": n / t, "unit": "candidates/s", "batch": n, "stride": stride,
+                    "configs": [list(map(int, cfgs[idx]))] if tag == "homogeneous" else int(len(fi)),
+                    "status_ok_or_oom": bool(((st == 0) | (st == 1)).all()),
+                    "roofline": {"kernel": "k_eval_stream", "bound": "hbm", "achieved": gbs,
+                                 "peak": pk.get("hbm_gbs"), "unit": "GB/s", "frac": gbs / pk.get("hbm_gbs", 6538.3),
+                                 "traffic": None, "alg_bytes_per_candidate": alg / n,
+                                 "note": f"batch {(n * stride * 2 + 25 * n) / 1e9:.2f} GB > L2"}}
+        del perm, cf
+    return out
 
 
 def main():

@@ -7,10 +7,11 @@
 // the per-candidate work is a sequential, fixed-order sum, and thread-per-candidate
 // keeps all 32 lanes busy).  The mapping row is read with 16-byte vector loads; the
 // config table keys and R = 1/B (lane-replicated when small) live in shared memory.
-//   MODE 0 (n <= 16 nodes, <= 15 slots per node): stage-1 node counts are nibbles of a
-//          64-bit register, the node set a 32-bit mask, the bijection bitmap two
-//          registers (N <= 64), and the slowest inter-node link of Eq.6 one load from
-//          the subset-max table.
+//   MODE 0 (n <= 16 nodes, <= 15 slots per node): the pipeline depth is a template
+//          parameter (the stage of each mapping slot is static inside a 16-byte chunk),
+//          stage-1 node counts are nibbles of a 64-bit register, the bijection bitmap is
+//          a 64-bit register (N <= 64; shared memory above), and the slowest inter-node
+//          link of Eq.6 is one load from the subset-max table.
 //   MODE 1 (general): bitmap and counts in thread-interleaved shared memory (bank-
 //          conflict free), pairwise scan of the stage-1 node set.
 #include "devmath.cuh"
@@ -20,17 +21,203 @@ namespace pip {
 
 constexpr int kEvalThreads = 256;
 
+struct EvalShared {
+  const double* Rs;
+  uint32_t* bm;     // [bm_words][kEvalThreads]
+  uint32_t* cnt;    // [ceil(n/4)][kEvalThreads]
+  int n, tid, lane;
+};
+
+template <bool REP>
+__device__ __forceinline__ double r_at(const EvalShared& S, uint32_t a, uint32_t b) {
+  return REP ? S.Rs[((int)a * S.n + (int)b) * 32 + S.lane] : S.Rs[(int)a * S.n + (int)b];
+}
+
+// MODE 0 evaluation of one candidate with compile-time pipeline depth PP (0: runtime).
+template <int PP>
+__device__ __forceinline__ void eval_small(const EvalParams& P, const EvalShared& S, const DevCfg& C,
+                                           const uint16_t* row, long long i) {
+  const int N = C.N;
+  const int pp = PP > 0 ? PP : C.pp;
+  const uint32_t spn = (uint32_t)C.spn;
+  const bool regbm = N <= 64;
+  if (!regbm)
+    for (int w = 0; w < (N + 31) / 32; ++w) S.bm[w * kEvalThreads + S.tid] = 0u;
+  unsigned long long seen = 0ull, dup = 0ull, c64 = 0ull;
+  uint32_t mask = 0u;
+  bool ok = true;
+  double tpp = 0.0, s = 0.0;
+  uint32_t prev = 0;
+  int x = 0;   // runtime stage counter (PP == 0 only)
+  auto visit = [&](uint32_t v, bool stage1, bool last) {
+    uint32_t nd = 0;
+    if (v >= (uint32_t)N) {
+      ok = false;
+    } else {
+      if (regbm) {
+        const unsigned long long bit = 1ull << v;
+        dup |= seen & bit;
+        seen |= bit;
+      } else {
+        uint32_t& bw = S.bm[(v >> 5) * kEvalThreads + S.tid];
+        const uint32_t bit = 1u << (v & 31);
+        if (bw & bit) ok = false;
+        bw |= bit;
+      }
+      nd = div_small(v, C.spn_magic, spn);
+    }
+    if (stage1) {                                    // stage-1 worker of pipeline z (Eq.6)
+      c64 += 1ull << (4u * nd);
+      mask |= 1u << nd;
+      s = 0.0;
+    } else {                                         // Eq.5 hop x-1 -> x, stage order
+      s = __dadd_rn(s, __dmul_rn(C.m2, r_at<true>(S, prev, nd)));
+    }
+    prev = nd;
+    if (last && pp >= 2) tpp = fmax(tpp, s);
+  };
+  auto flags = [&](int w0, int j, bool& st, bool& la) {
+    if (PP == 1) { st = true; la = true; }
+    else if (PP == 2 || PP == 4 || PP == 8) { st = (j % PP) == 0; la = (j % PP) == PP - 1; }
+    else if (PP >= 16) {
+      st = j == 0 && (w0 & (PP - 1)) == 0;
+      la = j == 7 && (w0 & (PP - 1)) == PP - 8;
+    } else {
+      st = x == 0; la = x == pp - 1;
+      x = (x + 1 == pp) ? 0 : x + 1;
+    }
+  };
+  if (P.vec16) {
+    const uint4* r4 = reinterpret_cast<const uint4*>(row);
+    for (int w0 = 0; w0 < N; w0 += 8) {
+      const uint4 v = __ldg(r4 + (w0 >> 3));
+      const uint32_t pk[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        if (w0 + j < N) {
+          bool st, la;
+          flags(w0, j, st, la);
+          visit((pk[j >> 1] >> ((j & 1) * 16)) & 0xffffu, st, la);
+        }
+      }
+    }
+  } else {
+    for (int w = 0; w < N; ++w) {
+      const bool st = (w % pp) == 0, la = (w % pp) == pp - 1;
+      visit(__ldg(row + w), st, la);
+    }
+  }
+  if (dup) ok = false;
+  P.mem[i] = C.mem;
+  const double qnan = __longlong_as_double(0x7ff8000000000000ll);
+  if (!ok) { P.latency[i] = qnan; P.status[i] = 3; return; }
+  if (!C.has_profile) { P.latency[i] = qnan; P.status[i] = 4; return; }
+  // Eq.6: per-node intra ring over nodes with >= 2 stage-1 members, slowest inter link
+  const double* qi = P.qtab + C.qi_off;
+  double t_in = 0.0;
+  uint32_t bits = mask;
+  while (bits) {
+    const uint32_t a = __ffs(bits) - 1;
+    bits &= bits - 1;
+    const uint32_t c = (uint32_t)(c64 >> (4u * a)) & 15u;
+    if (c >= 2) t_in = fmax(t_in, __dmul_rn(__ldg(qi + c), r_at<true>(S, a, a)));
+  }
+  const int k = __popc(mask);
+  const double t_ex = k >= 2 ? __dmul_rn(__ldg(P.qtab + C.qe_off + k), __ldg(P.subset_max + mask)) : 0.0;
+  P.latency[i] = compose(C.Sb, C.r, C.Ss, tpp, t_in, t_ex);
+  P.status[i] = C.feasible ? 0 : 1;
+}
+
+// MODE 1 (general) evaluation of one candidate.
+__device__ __forceinline__ void eval_general(const EvalParams& P, const EvalShared& S, const DevCfg& C,
+                                             const uint16_t* row, long long i) {
+  const int N = C.N, pp = C.pp;
+  const uint32_t spn = (uint32_t)C.spn;
+  for (int w = 0; w < (N + 31) / 32; ++w) S.bm[w * kEvalThreads + S.tid] = 0u;
+  for (int w = 0; w < (S.n + 3) / 4; ++w) S.cnt[w * kEvalThreads + S.tid] = 0u;
+  Mask<4> mask;
+  mask.clear();
+  bool ok = true;
+  double tpp = 0.0, s = 0.0;
+  uint32_t prev = 0;
+  int x = 0;
+  auto visit = [&](uint32_t v) {
+    uint32_t nd = 0;
+    if (v >= (uint32_t)N) {
+      ok = false;
+    } else {
+      uint32_t& bw = S.bm[(v >> 5) * kEvalThreads + S.tid];
+      const uint32_t bit = 1u << (v & 31);
+      if (bw & bit) ok = false;
+      bw |= bit;
+      nd = div_small(v, C.spn_magic, spn);
+    }
+    if (x == 0) {
+      S.cnt[(nd >> 2) * kEvalThreads + S.tid] += 1u << ((nd & 3) * 8);
+      mask.set(nd);
+      s = 0.0;
+    } else {
+      s = __dadd_rn(s, __dmul_rn(C.m2, r_at<false>(S, prev, nd)));
+    }
+    prev = nd;
+    if (++x == pp) {
+      x = 0;
+      if (pp >= 2) tpp = fmax(tpp, s);
+    }
+  };
+  if (P.vec16) {
+    const uint4* r4 = reinterpret_cast<const uint4*>(row);
+    for (int w0 = 0; w0 < N; w0 += 8) {
+      const uint4 v = __ldg(r4 + (w0 >> 3));
+      const uint32_t pk[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+      for (int j = 0; j < 8; ++j)
+        if (w0 + j < N) visit((pk[j >> 1] >> ((j & 1) * 16)) & 0xffffu);
+    }
+  } else {
+    for (int w = 0; w < N; ++w) visit(__ldg(row + w));
+  }
+  P.mem[i] = C.mem;
+  const double qnan = __longlong_as_double(0x7ff8000000000000ll);
+  if (!ok) { P.latency[i] = qnan; P.status[i] = 3; return; }
+  if (!C.has_profile) { P.latency[i] = qnan; P.status[i] = 4; return; }
+  const double* qi = P.qtab + C.qi_off;
+  double t_in = 0.0, mx = 0.0;
+#pragma unroll
+  for (int wd = 0; wd < 4; ++wd) {
+    uint32_t bits = mask.w[wd];
+    while (bits) {
+      const uint32_t a = wd * 32 + __ffs(bits) - 1;
+      bits &= bits - 1;
+      const uint32_t c = (S.cnt[(a >> 2) * kEvalThreads + S.tid] >> ((a & 3) * 8)) & 0xffu;
+      if (c >= 2) t_in = fmax(t_in, __dmul_rn(__ldg(qi + c), r_at<false>(S, a, a)));
+#pragma unroll
+      for (int wd2 = 0; wd2 < 4; ++wd2) {
+        uint32_t bits2 = mask.w[wd2];
+        while (bits2) {
+          const uint32_t b = wd2 * 32 + __ffs(bits2) - 1;
+          bits2 &= bits2 - 1;
+          if (a != b) mx = fmax(mx, r_at<false>(S, a, b));
+        }
+      }
+    }
+  }
+  const int k = mask.count();
+  const double t_ex = k >= 2 ? __dmul_rn(__ldg(P.qtab + C.qe_off + k), mx) : 0.0;
+  P.latency[i] = compose(C.Sb, C.r, C.Ss, tpp, t_in, t_ex);
+  P.status[i] = C.feasible ? 0 : 1;
+}
+
 template <int MODE>
 __global__ void __launch_bounds__(kEvalThreads) k_eval_stream(EvalParams P) {
   constexpr bool REP = MODE == 0;
   extern __shared__ __align__(16) unsigned char smem[];
   const int n = P.n_nodes, nn = n * n;
-  const int tid = threadIdx.x, lane = tid & 31;
+  const int tid = threadIdx.x;
   double* Rs = reinterpret_cast<double*>(smem);
   const int r_bytes = (REP ? nn * 32 : nn) * 8;
   unsigned long long* keys = reinterpret_cast<unsigned long long*>(smem + r_bytes);
   uint32_t* bm = reinterpret_cast<uint32_t*>(smem + r_bytes + ((P.E * 8 + 15) & ~15));
-  uint32_t* cnt = bm + P.bm_words * kEvalThreads;
   if (REP) {
     for (int i = tid; i < nn * 32; i += blockDim.x) Rs[i] = P.R[i >> 5];
   } else {
@@ -38,11 +225,8 @@ __global__ void __launch_bounds__(kEvalThreads) k_eval_stream(EvalParams P) {
   }
   for (int i = tid; i < P.E; i += blockDim.x) keys[i] = P.keys[i];
   __syncthreads();
-  auto Rab = [&](uint32_t a, uint32_t b) -> double {
-    return REP ? Rs[((int)a * n + (int)b) * 32 + lane] : Rs[(int)a * n + (int)b];
-  };
+  const EvalShared S{Rs, bm, bm + P.bm_words * kEvalThreads, n, tid, tid & 31};
   const double qnan = __longlong_as_double(0x7ff8000000000000ll);
-  const int cwords = (n + 3) / 4;
 
   for (long long i = (long long)blockIdx.x * blockDim.x + tid; i < P.n; i += (long long)gridDim.x * blockDim.x) {
     const pipette_config cf = P.cand[i];
@@ -58,108 +242,20 @@ __global__ void __launch_bounds__(kEvalThreads) k_eval_stream(EvalParams P) {
       continue;
     }
     const DevCfg C = P.cfgs[lo];
-    const int N = C.N, pp = C.pp;
-    const uint32_t spn = (uint32_t)C.spn;
     const uint16_t* row = P.perm + i * (long long)P.perm_stride;
-    const bool regbm = MODE == 0 && N <= 64;
-    if (!regbm)
-      for (int w = 0; w < (N + 31) / 32; ++w) bm[w * kEvalThreads + tid] = 0u;
-    if (MODE != 0)
-      for (int w = 0; w < cwords; ++w) cnt[w * kEvalThreads + tid] = 0u;
-    uint32_t b0 = 0u, b1 = 0u, dup = 0u;        // register bitmap (MODE 0, N <= 64)
-    unsigned long long c64 = 0ull;              // nibble counts (MODE 0)
-    Mask<MODE == 0 ? 1 : 4> mask;
-    mask.clear();
-    bool ok = true;
-    double tpp = 0.0, s = 0.0;
-    uint32_t prev = 0;
-    int x = 0;
-    auto visit = [&](uint32_t v) {
-      uint32_t nd = 0;
-      if (v >= (uint32_t)N) {
-        ok = false;
-      } else {
-        if (regbm) {
-          const uint32_t bit = 1u << (v & 31);
-          const bool hi32 = v >= 32;
-          dup |= (hi32 ? b1 : b0) & bit;
-          b0 |= hi32 ? 0u : bit;
-          b1 |= hi32 ? bit : 0u;
-        } else {
-          uint32_t& bw = bm[(v >> 5) * kEvalThreads + tid];
-          const uint32_t bit = 1u << (v & 31);
-          if (bw & bit) ok = false;
-          bw |= bit;
-        }
-        nd = div_small(v, C.spn_magic, spn);
-      }
-      if (x == 0) {                                  // stage-1 worker of pipeline z (Eq.6)
-        if (MODE == 0) c64 += 1ull << (4u * nd);
-        else cnt[(nd >> 2) * kEvalThreads + tid] += 1u << ((nd & 3) * 8);
-        mask.set(nd);
-        s = 0.0;
-      } else {                                       // Eq.5 hop x-1 -> x, stage order
-        s = __dadd_rn(s, __dmul_rn(C.m2, Rab(prev, nd)));
-      }
-      prev = nd;
-      if (++x == pp) {
-        x = 0;
-        if (pp >= 2) tpp = fmax(tpp, s);
-      }
-    };
-    if (P.vec16) {
-      const uint4* r4 = reinterpret_cast<const uint4*>(row);
-      for (int w0 = 0; w0 < N; w0 += 8) {
-        const uint4 v = __ldg(r4 + (w0 >> 3));
-        const uint32_t pk[4] = {v.x, v.y, v.z, v.w};
-#pragma unroll
-        for (int j = 0; j < 8; ++j)
-          if (w0 + j < N) visit((pk[j >> 1] >> ((j & 1) * 16)) & 0xffffu);
-      }
-    } else {
-      for (int w = 0; w < N; ++w) visit(__ldg(row + w));
-    }
-    if (dup) ok = false;
-    P.mem[i] = C.mem;
-    if (!ok) { P.latency[i] = qnan; P.status[i] = 3; continue; }
-    if (!C.has_profile) { P.latency[i] = qnan; P.status[i] = 4; continue; }
-    // Eq.6: per-node intra ring over nodes with >= 2 stage-1 members, slowest inter link
-    const double* qi = P.qtab + C.qi_off;
-    double t_in = 0.0, mx = 0.0;
-    const int k = mask.count();
     if (MODE == 0) {
-      uint32_t bits = mask.w[0];
-      while (bits) {
-        const uint32_t a = __ffs(bits) - 1;
-        bits &= bits - 1;
-        const uint32_t c = (uint32_t)(c64 >> (4u * a)) & 15u;
-        if (c >= 2) t_in = fmax(t_in, __dmul_rn(__ldg(qi + c), Rab(a, a)));
+      switch (C.pp) {
+        case 1: eval_small<1>(P, S, C, row, i); break;
+        case 2: eval_small<2>(P, S, C, row, i); break;
+        case 4: eval_small<4>(P, S, C, row, i); break;
+        case 8: eval_small<8>(P, S, C, row, i); break;
+        case 16: eval_small<16>(P, S, C, row, i); break;
+        case 32: eval_small<32>(P, S, C, row, i); break;
+        default: eval_small<0>(P, S, C, row, i); break;
       }
-      if (k >= 2) mx = __ldg(P.subset_max + mask.w[0]);
     } else {
-#pragma unroll
-      for (int wd = 0; wd < 4; ++wd) {
-        uint32_t bits = mask.w[wd];
-        while (bits) {
-          const uint32_t a = wd * 32 + __ffs(bits) - 1;
-          bits &= bits - 1;
-          const uint32_t c = (cnt[(a >> 2) * kEvalThreads + tid] >> ((a & 3) * 8)) & 0xffu;
-          if (c >= 2) t_in = fmax(t_in, __dmul_rn(__ldg(qi + c), Rab(a, a)));
-#pragma unroll
-          for (int wd2 = 0; wd2 < 4; ++wd2) {
-            uint32_t bits2 = mask.w[wd2];
-            while (bits2) {
-              const uint32_t b = wd2 * 32 + __ffs(bits2) - 1;
-              bits2 &= bits2 - 1;
-              if (a != b) mx = fmax(mx, Rab(a, b));
-            }
-          }
-        }
-      }
+      eval_general(P, S, C, row, i);
     }
-    const double t_ex = k >= 2 ? __dmul_rn(__ldg(P.qtab + C.qe_off + k), mx) : 0.0;
-    P.latency[i] = compose(C.Sb, C.r, C.Ss, tpp, t_in, t_ex);
-    P.status[i] = C.feasible ? 0 : 1;
   }
 }
 
