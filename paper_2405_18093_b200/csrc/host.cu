@@ -453,14 +453,15 @@ pipette_status pipette_eval(pipette_ctx* ctx, const pipette_model* model, int64_
   P.mem = (unsigned long long*)d_mem;
   P.status = d_status;
   const size_t smem = (size_t)(rep ? nn * 32 : nn) * 8 + ((ctx->E * 8 + 15) & ~15) +
-                      (size_t)(P.bm_words + (ctx->n_nodes + 3) / 4) * kEvalThreads * 4;
+                      (size_t)(P.bm_words + (ctx->n_nodes + 3) / 4) * kEvalThreads * 4 +
+                      2048 * sizeof(int) + 4096 * sizeof(int) + 2048 * sizeof(short);
   if (smem > 227 * 1024) return fail(ctx, PIPETTE_E_UNSUPPORTED, "eval shared memory %zu B too large", smem);
   const void* kern = eval_kernel(mode);
   CU(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   int occ = 0;
   CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kEvalThreads, smem));
   occ = std::max(occ, 1);
-  const long long need = (n + kEvalThreads - 1) / kEvalThreads;
+  const long long need = (n + 2047) / 2048;   // tiles of 2048 candidates
   const int grid = (int)std::min<long long>(need, (long long)occ * ctx->n_sms);
   void* args[] = {&P};
   CU(cudaLaunchKernel(kern, dim3(grid), dim3(kEvalThreads), args, smem, s));

@@ -20,6 +20,41 @@
 namespace pip {
 
 constexpr int kEvalThreads = 256;
+constexpr int kEvalTile = 2048;            // candidates per block iteration (bucketed by config)
+constexpr int kEvalMaxBucketCfgs = 4096;   // histogram capacity
+
+// Exclusive block-wide scan (one int per thread); total = block sum.
+__device__ int block_scan_excl_eval(int v, int* sh, int& total) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  int x = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) sh[wid] = x;
+  __syncthreads();
+  if (wid == 0) {
+    int s = lane < nw ? sh[lane] : 0;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, s, o);
+      if (lane >= o) s += y;
+    }
+    sh[lane] = s;
+  }
+  __syncthreads();
+  const int excl = x - v + (wid > 0 ? sh[wid - 1] : 0);
+  total = sh[nw - 1];
+  __syncthreads();
+  return excl;
+}
+
+// End of the per-thread scratch (bitmap, counts) in the dynamic shared-memory layout.
+__device__ __forceinline__ unsigned char* cnt_end(const EvalParams& P, unsigned char* smem, int r_bytes) {
+  return smem + r_bytes + ((P.E * 8 + 15) & ~15) +
+         (size_t)(P.bm_words + (P.n_nodes + 3) / 4) * kEvalThreads * 4;
+}
 
 struct EvalShared {
   const double* Rs;
@@ -77,9 +112,11 @@ __device__ __forceinline__ void eval_small(const EvalParams& P, const EvalShared
     if (last && pp >= 2) tpp = fmax(tpp, s);
   };
   auto flags = [&](int w0, int j, bool& st, bool& la) {
-    if (PP == 1) { st = true; la = true; }
-    else if (PP == 2 || PP == 4 || PP == 8) { st = (j % PP) == 0; la = (j % PP) == PP - 1; }
-    else if (PP >= 16) {
+    if constexpr (PP == 1) {
+      st = true; la = true;
+    } else if constexpr (PP == 2 || PP == 4 || PP == 8) {   // stage of slot j is static
+      st = (j % PP) == 0; la = (j % PP) == PP - 1;
+    } else if constexpr (PP >= 16) {                       // chunks never straddle pipelines
       st = j == 0 && (w0 & (PP - 1)) == 0;
       la = j == 7 && (w0 & (PP - 1)) == PP - 8;
     } else {
@@ -227,35 +264,74 @@ __global__ void __launch_bounds__(kEvalThreads) k_eval_stream(EvalParams P) {
   __syncthreads();
   const EvalShared S{Rs, bm, bm + P.bm_words * kEvalThreads, n, tid, tid & 31};
   const double qnan = __longlong_as_double(0x7ff8000000000000ll);
+  // tile bucketing: candidates of a tile are processed grouped by configuration, so the
+  // lanes of a warp run the same code path (mixed batches)
+  int* tile_e = reinterpret_cast<int*>(cnt_end(P, smem, r_bytes));
+  int* hist = tile_e + kEvalTile;
+  short* order = reinterpret_cast<short*>(hist + kEvalMaxBucketCfgs);
+  __shared__ int sh_scan[32];
+  const bool bucket = P.E + 1 <= kEvalMaxBucketCfgs;
 
-  for (long long i = (long long)blockIdx.x * blockDim.x + tid; i < P.n; i += (long long)gridDim.x * blockDim.x) {
-    const pipette_config cf = P.cand[i];
-    const unsigned long long key = ((unsigned long long)cf.pp << 48) | ((unsigned long long)cf.tp << 32) |
-                                   ((unsigned long long)cf.dp << 16) | (unsigned long long)cf.mb;
-    int lo = 0, hi = P.E;   // first index with keys[idx] >= key
-    while (lo < hi) {
-      const int mid = (lo + hi) >> 1;
-      if (keys[mid] < key) lo = mid + 1; else hi = mid;
+  for (long long base = (long long)blockIdx.x * kEvalTile; base < P.n; base += (long long)gridDim.x * kEvalTile) {
+    const int cnt_valid = (int)min((long long)kEvalTile, P.n - base);
+    if (bucket) {
+      for (int k = tid; k <= P.E; k += blockDim.x) hist[k] = 0;
+      __syncthreads();
     }
-    if (lo >= P.E || keys[lo] != key) {      // not in the enumeration of Alg.1 l.3-5
-      P.latency[i] = qnan; P.mem[i] = 0ull; P.status[i] = 2;
-      continue;
-    }
-    const DevCfg C = P.cfgs[lo];
-    const uint16_t* row = P.perm + i * (long long)P.perm_stride;
-    if (MODE == 0) {
-      switch (C.pp) {
-        case 1: eval_small<1>(P, S, C, row, i); break;
-        case 2: eval_small<2>(P, S, C, row, i); break;
-        case 4: eval_small<4>(P, S, C, row, i); break;
-        case 8: eval_small<8>(P, S, C, row, i); break;
-        case 16: eval_small<16>(P, S, C, row, i); break;
-        case 32: eval_small<32>(P, S, C, row, i); break;
-        default: eval_small<0>(P, S, C, row, i); break;
+    for (int k = tid; k < cnt_valid; k += blockDim.x) {
+      const pipette_config cf = P.cand[base + k];
+      const unsigned long long key = ((unsigned long long)cf.pp << 48) | ((unsigned long long)cf.tp << 32) |
+                                     ((unsigned long long)cf.dp << 16) | (unsigned long long)cf.mb;
+      int lo = 0, hi = P.E;   // first index with keys[idx] >= key
+      while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if (keys[mid] < key) lo = mid + 1; else hi = mid;
       }
-    } else {
-      eval_general(P, S, C, row, i);
+      const int e = (lo >= P.E || keys[lo] != key) ? -1 : lo;   // -1: not in the enumeration (Alg.1 l.3-5)
+      tile_e[k] = e;
+      if (bucket) atomicAdd(&hist[e + 1], 1);
     }
+    __syncthreads();
+    if (bucket) {
+      // exclusive scan of the per-config histogram, then scatter tile positions
+      int carry = 0;
+      for (int b0 = 0; b0 <= P.E; b0 += blockDim.x) {
+        const int k = b0 + tid;
+        const int v = k <= P.E ? hist[k] : 0;
+        int tot;
+        const int ex = carry + block_scan_excl_eval(v, sh_scan, tot);
+        carry += tot;
+        if (k <= P.E) hist[k] = ex;
+      }
+      __syncthreads();
+      for (int k = tid; k < cnt_valid; k += blockDim.x) order[atomicAdd(&hist[tile_e[k] + 1], 1)] = (short)k;
+      __syncthreads();
+    }
+    for (int sidx = tid; sidx < cnt_valid; sidx += blockDim.x) {
+      const int k = bucket ? order[sidx] : sidx;
+      const long long i = base + k;
+      const int e = tile_e[k];
+      if (e < 0) {
+        P.latency[i] = qnan; P.mem[i] = 0ull; P.status[i] = 2;
+        continue;
+      }
+      const DevCfg C = P.cfgs[e];
+      const uint16_t* row = P.perm + i * (long long)P.perm_stride;
+      if (MODE == 0) {
+        switch (C.pp) {
+          case 1: eval_small<1>(P, S, C, row, i); break;
+          case 2: eval_small<2>(P, S, C, row, i); break;
+          case 4: eval_small<4>(P, S, C, row, i); break;
+          case 8: eval_small<8>(P, S, C, row, i); break;
+          case 16: eval_small<16>(P, S, C, row, i); break;
+          case 32: eval_small<32>(P, S, C, row, i); break;
+          default: eval_small<0>(P, S, C, row, i); break;
+        }
+      } else {
+        eval_general(P, S, C, row, i);
+      }
+    }
+    __syncthreads();
   }
 }
 
