@@ -104,6 +104,59 @@ __device__ __forceinline__ void eval_small(const EvalParams& P, const EvalShared
     prev = nd;
     if (last && pp >= 2) tpp = fmax(tpp, s);
   };
+  auto flags = [&](int w0, int j, bool& st, bool& la) {
+    if constexpr (PP == 1) {
+      st = true; la = true;
+    } else if constexpr (PP == 2 || PP == 4 || PP == 8) {   // stage of slot j is static
+      st = (j % PP) == 0; la = (j % PP) == PP - 1;
+    } else if constexpr (PP >= 16) {                       // chunks never straddle pipelines
+      st = j == 0 && (w0 & (PP - 1)) == 0;
+      la = j == 7 && (w0 & (PP - 1)) == PP - 8;
+    } else {
+      st = x == 0; la = x == pp - 1;
+      x = (x + 1 == pp) ? 0 : x + 1;
+    }
+  };
+  if (P.vec16) {
+    const uint4* r4 = reinterpret_cast<const uint4*>(row);
+    for (int w0 = 0; w0 < N; w0 += 8) {
+      const uint4 v = __ldg(r4 + (w0 >> 3));
+      const uint32_t pk[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        if (w0 + j < N) {
+          bool st, la;
+          flags(w0, j, st, la);
+          visit((pk[j >> 1] >> ((j & 1) * 16)) & 0xffffu, st, la);
+        }
+      }
+    }
+  } else {
+    for (int w = 0; w < N; ++w) {
+      const bool st = (w % pp) == 0, la = (w % pp) == pp - 1;
+      visit(__ldg(row + w), st, la);
+    }
+  }
+  bool ok = !bad;
+  if (regbm) {
+    ok = ok && seen == (N == 64 ? ~0ull : ((1ull << N) - 1ull));
+  } else {
+    int c = 0;
+    for (int w = 0; w < (N + 31) / 32; ++w) c += __popc(S.bm[w * kEvalThreads + S.tid]);
+    ok = ok && c == N;
+  }
+  // stage-1 node set N1 from the nibble counts: bit a set iff nibble a is non-zero
+  unsigned long long t = c64 | (c64 >> 1);
+  t = (t | (t >> 2)) & 0x1111111111111111ull;
+  uint32_t lo = (uint32_t)t, hi = (uint32_t)(t >> 32);
+  lo = (lo | (lo >> 3)) & 0x03030303u; hi = (hi | (hi >> 3)) & 0x03030303u;
+  lo = (lo | (lo >> 6)) & 0x000f000fu; hi = (hi | (hi >> 6)) & 0x000f000fu;
+  lo = (lo | (lo >> 12)) & 0xffu;      hi = (hi | (hi >> 12)) & 0xffu;
+  const uint32_t mask = lo | (hi << 8);
+  P.mem[i] = C.mem;
+  const double qnan = __longlong_as_double(0x7ff8000000000000ll);
+  if (!ok) { P.latency[i] = qnan; P.status[i] = 3; return; }
+  if (!C.has_profile) { P.latency[i] = qnan; P.status[i] = 4; return; }
   // Eq.6: per-node intra ring over nodes with >= 2 stage-1 members, slowest inter link
   const double* qi = P.qtab + C.qi_off;
   double t_in = 0.0;
