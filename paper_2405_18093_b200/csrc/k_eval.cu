@@ -56,6 +56,13 @@ __device__ __forceinline__ unsigned char* cnt_end(const EvalParams& P, unsigned 
          (size_t)(P.bm_words + (P.n_nodes + 3) / 4) * kEvalThreads * 4;
 }
 
+// PTX shl.b32: shift amounts >= 32 give 0 (C's << is undefined there).
+__device__ __forceinline__ uint32_t shl_clamp(uint32_t x, uint32_t sh) {
+  uint32_t r;
+  asm("shl.b32 %0, %1, %2;" : "=r"(r) : "r"(x), "r"(sh));
+  return r;
+}
+
 struct EvalShared {
   const double* Rs;
   uint32_t* bm;     // [bm_words][kEvalThreads]
@@ -69,7 +76,7 @@ __device__ __forceinline__ double r_at(const EvalShared& S, uint32_t a, uint32_t
 }
 
 // MODE 0 evaluation of one candidate with compile-time pipeline depth PP (0: runtime).
-template <int PP>
+template <int PP, bool N8>
 __device__ __forceinline__ void eval_small(const EvalParams& P, const EvalShared& S, const DevCfg& C,
                                            const uint16_t* row, long long i) {
   const int N = C.N;
@@ -78,25 +85,31 @@ __device__ __forceinline__ void eval_small(const EvalParams& P, const EvalShared
   const bool regbm = N <= 64;
   if (!regbm)
     for (int w = 0; w < (N + 31) / 32; ++w) S.bm[w * kEvalThreads + S.tid] = 0u;
-  // Bijection test (Eq.2): OR the bit of every slot id; with every id < N, the row is a
-  // permutation of [0, N) iff all N bits end up set (a duplicate leaves one unset).
-  unsigned long long seen = 0ull, c64 = 0ull;
+  // Bijection test (Eq.2): OR the bit of every slot id into [0, 64) (a 2x32-bit register
+  // pair; shl clamps, so ids >= 64 set nothing).  The row is a permutation of [0, N) iff
+  // exactly the N low bits end up set: an id >= N sets a bit above N or none, and a
+  // duplicate leaves one of the N bits unset.  Larger N: bitmap in shared memory.
+  uint32_t seen_lo = 0u, seen_hi = 0u;
+  uint32_t c_lo = 0u, c_hi = 0u;        // stage-1 counts, nibble a of (c_hi:c_lo) = node a
   bool bad = false;
   double tpp = 0.0, s = 0.0;
   uint32_t prev = 0;
   int x = 0;   // runtime stage counter (PP == 0 only)
-  const uint32_t nmax = (uint32_t)S.n - 1u;
   auto visit = [&](uint32_t v, bool stage1, bool last) {
-    bad |= v >= (uint32_t)N;
     if (regbm) {
-      seen |= 1ull << (v & 63u);
+      seen_lo |= shl_clamp(1u, v);
+      seen_hi |= shl_clamp(1u, v - 32u);
+      v = min(v, (uint32_t)N - 1u);                 // keeps node ids in range (the row is invalid)
     } else {
-      uint32_t& bw = S.bm[(min(v, (uint32_t)N - 1u) >> 5) * kEvalThreads + S.tid];
+      bad |= v >= (uint32_t)N;
+      v = min(v, (uint32_t)N - 1u);
+      uint32_t& bw = S.bm[(v >> 5) * kEvalThreads + S.tid];
       bw |= 1u << (v & 31);
     }
-    const uint32_t nd = min(div_small(v, C.spn_magic, spn), nmax);   // clamp only matters when bad
+    const uint32_t nd = div_small(v, C.spn_magic, spn);
     if (stage1) {                                    // stage-1 worker of pipeline z (Eq.6)
-      c64 += 1ull << (4u * nd);
+      c_lo += shl_clamp(1u, 4u * nd);
+      if (!N8) c_hi += shl_clamp(1u, 4u * nd - 32u);
       s = 0.0;
     } else {                                         // Eq.5 hop x-1 -> x, stage order
       s = __dadd_rn(s, __dmul_rn(C.m2, r_at<true>(S, prev, nd)));
@@ -119,14 +132,25 @@ __device__ __forceinline__ void eval_small(const EvalParams& P, const EvalShared
   };
   if (P.vec16) {
     const uint4* r4 = reinterpret_cast<const uint4*>(row);
-    for (int w0 = 0; w0 < N; w0 += 8) {
+    const int full = N & ~7;                         // whole 8-slot chunks: no per-slot guard
+    for (int w0 = 0; w0 < full; w0 += 8) {
       const uint4 v = __ldg(r4 + (w0 >> 3));
       const uint32_t pk[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
       for (int j = 0; j < 8; ++j) {
-        if (w0 + j < N) {
+        bool st, la;
+        flags(w0, j, st, la);
+        visit((pk[j >> 1] >> ((j & 1) * 16)) & 0xffffu, st, la);
+      }
+    }
+    if (full < N) {
+      const uint4 v = __ldg(r4 + (full >> 3));
+      const uint32_t pk[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        if (full + j < N) {
           bool st, la;
-          flags(w0, j, st, la);
+          flags(full, j, st, la);
           visit((pk[j >> 1] >> ((j & 1) * 16)) & 0xffffu, st, la);
         }
       }
@@ -139,16 +163,18 @@ __device__ __forceinline__ void eval_small(const EvalParams& P, const EvalShared
   }
   bool ok = !bad;
   if (regbm) {
-    ok = ok && seen == (N == 64 ? ~0ull : ((1ull << N) - 1ull));
+    const uint32_t want_lo = N >= 32 ? 0xffffffffu : ((1u << N) - 1u);
+    const uint32_t want_hi = N >= 64 ? 0xffffffffu : (N > 32 ? ((1u << (N - 32)) - 1u) : 0u);
+    ok = seen_lo == want_lo && seen_hi == want_hi;
   } else {
     int c = 0;
     for (int w = 0; w < (N + 31) / 32; ++w) c += __popc(S.bm[w * kEvalThreads + S.tid]);
     ok = ok && c == N;
   }
   // stage-1 node set N1 from the nibble counts: bit a set iff nibble a is non-zero
-  unsigned long long t = c64 | (c64 >> 1);
-  t = (t | (t >> 2)) & 0x1111111111111111ull;
-  uint32_t lo = (uint32_t)t, hi = (uint32_t)(t >> 32);
+  const unsigned long long c64 = ((unsigned long long)c_hi << 32) | c_lo;
+  uint32_t lo = c_lo | (c_lo >> 1), hi = c_hi | (c_hi >> 1);
+  lo = (lo | (lo >> 2)) & 0x11111111u; hi = (hi | (hi >> 2)) & 0x11111111u;
   lo = (lo | (lo >> 3)) & 0x03030303u; hi = (hi | (hi >> 3)) & 0x03030303u;
   lo = (lo | (lo >> 6)) & 0x000f000fu; hi = (hi | (hi >> 6)) & 0x000f000fu;
   lo = (lo | (lo >> 12)) & 0xffu;      hi = (hi | (hi >> 12)) & 0xffu;
@@ -171,6 +197,13 @@ __device__ __forceinline__ void eval_small(const EvalParams& P, const EvalShared
   const double t_ex = k >= 2 ? __dmul_rn(__ldg(P.qtab + C.qe_off + k), __ldg(P.subset_max + mask)) : 0.0;
   P.latency[i] = compose(C.Sb, C.r, C.Ss, tpp, t_in, t_ex);
   P.status[i] = C.feasible ? 0 : 1;
+}
+
+template <int PP>
+__device__ __forceinline__ void dispatch_n(const EvalParams& P, const EvalShared& S, const DevCfg& C,
+                                           const uint16_t* row, long long i) {
+  if (S.n <= 8) eval_small<PP, true>(P, S, C, row, i);    // stage-1 counts fit one 32-bit word
+  else eval_small<PP, false>(P, S, C, row, i);
 }
 
 // MODE 1 (general) evaluation of one candidate.
@@ -327,13 +360,13 @@ __global__ void __launch_bounds__(kEvalThreads) k_eval_stream(EvalParams P) {
       const uint16_t* row = P.perm + i * (long long)P.perm_stride;
       if (MODE == 0) {
         switch (C.pp) {
-          case 1: eval_small<1>(P, S, C, row, i); break;
-          case 2: eval_small<2>(P, S, C, row, i); break;
-          case 4: eval_small<4>(P, S, C, row, i); break;
-          case 8: eval_small<8>(P, S, C, row, i); break;
-          case 16: eval_small<16>(P, S, C, row, i); break;
-          case 32: eval_small<32>(P, S, C, row, i); break;
-          default: eval_small<0>(P, S, C, row, i); break;
+          case 1: dispatch_n<1>(P, S, C, row, i); break;
+          case 2: dispatch_n<2>(P, S, C, row, i); break;
+          case 4: dispatch_n<4>(P, S, C, row, i); break;
+          case 8: dispatch_n<8>(P, S, C, row, i); break;
+          case 16: dispatch_n<16>(P, S, C, row, i); break;
+          case 32: dispatch_n<32>(P, S, C, row, i); break;
+          default: dispatch_n<0>(P, S, C, row, i); break;
         }
       } else {
         eval_general(P, S, C, row, i);
