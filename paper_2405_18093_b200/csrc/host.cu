@@ -20,7 +20,10 @@ __global__ void k_enumerate_filter(int, int, unsigned long long, int, pipette_mo
                                    double*, int, EnumOut*);
 const void* eval_kernel(int mode);
 const void* sa_kernel(int mode, bool trace);
-int sa_warp_state_bytes(int mode, int N, int pp, int dp, int n);
+int sa_warp_state_bytes(int mode, int N, int pp, int dp, int n, int dp_cap);
+__global__ void k_node_lists(const double*, int, uint8_t*, double*);
+__global__ void k_pair_list(const double*, int, uint16_t*, double*);
+__global__ void k_tin_list(const DevCfg*, const int*, const double*, const double*, int, int, uint16_t*, double*, int*);
 __global__ void k_subset_max(const double*, int, double*);
 __global__ void k_tin_rank(const DevCfg*, const int*, const double*, const double*, int, uint8_t*, double*);
 __global__ void k_argmin(const ChainOut*, const int*, int, CfgBest*);
@@ -101,6 +104,11 @@ struct pipette_ctx {
   // device tables
   double* dR = nullptr;
   double* dTab = nullptr;   // subset-max table (n <= 16)
+  // sorted cluster tables for larger clusters (n > 16)
+  uint8_t* dNlNode = nullptr;
+  double* dNlVal = nullptr;
+  uint16_t* dGlAb = nullptr;
+  double* dGlVal = nullptr;
   pipette_profile_entry* dProf = nullptr;
   int n_prof = 0;
   std::vector<pipette_profile_entry> prof;
@@ -114,7 +122,7 @@ struct pipette_ctx {
   DevBuf cfgs, keys, feas, qtab, eout;
   // search buffers
   DevBuf tasks, counter, chain_out, best_perm, cfg_slot, cfg_best, gbits, items, gitems, pack, accepted,
-      slot_perm_off, slot_lane, trace_slot, trace, task_prof, tin_rank, tin_vs;
+      slot_perm_off, slot_lane, trace_slot, trace, task_prof, tin_rank, tin_vs, tl_ac, tl_val, tl_len;
   int64_t n_tasks_last = 0;
   cudaEvent_t ev[6] = {};
 };
@@ -183,6 +191,18 @@ pipette_status upload_bw(pipette_ctx* ctx, const double* bw) {
   if (n <= 16) {
     if (!ctx->dTab) CU(cudaMalloc(&ctx->dTab, sizeof(double) << n));
     k_subset_max<<<((1 << n) + 255) / 256, 256>>>(ctx->dR, n, ctx->dTab);
+    CU(cudaGetLastError());
+    CU(cudaDeviceSynchronize());
+  } else {
+    const size_t L1 = (size_t)n * 2 * (n - 1), L2 = (size_t)n * (n - 1);
+    if (!ctx->dNlNode) {
+      CU(cudaMalloc(&ctx->dNlNode, L1));
+      CU(cudaMalloc(&ctx->dNlVal, sizeof(double) * L1));
+      CU(cudaMalloc(&ctx->dGlAb, sizeof(uint16_t) * L2));
+      CU(cudaMalloc(&ctx->dGlVal, sizeof(double) * L2));
+    }
+    k_node_lists<<<n, 256>>>(ctx->dR, n, ctx->dNlNode, ctx->dNlVal);
+    k_pair_list<<<(unsigned)((L2 + 255) / 256), 256>>>(ctx->dR, n, ctx->dGlAb, ctx->dGlVal);
     CU(cudaGetLastError());
     CU(cudaDeviceSynchronize());
   }
@@ -383,11 +403,16 @@ void pipette_destroy(pipette_ctx* ctx) {
   DevBuf* bufs[] = {&ctx->cfgs, &ctx->keys, &ctx->feas, &ctx->qtab, &ctx->eout, &ctx->tasks, &ctx->counter,
                     &ctx->chain_out, &ctx->best_perm, &ctx->cfg_slot, &ctx->cfg_best, &ctx->gbits, &ctx->items,
                     &ctx->gitems, &ctx->pack, &ctx->accepted, &ctx->slot_perm_off, &ctx->slot_lane,
-                    &ctx->trace_slot, &ctx->trace, &ctx->task_prof, &ctx->tin_rank, &ctx->tin_vs};
+                    &ctx->trace_slot, &ctx->trace, &ctx->task_prof, &ctx->tin_rank, &ctx->tin_vs, &ctx->tl_ac,
+                    &ctx->tl_val, &ctx->tl_len};
   for (DevBuf* b : bufs)
     if (b->p) cudaFree(b->p);
   if (ctx->dR) cudaFree(ctx->dR);
   if (ctx->dTab) cudaFree(ctx->dTab);
+  if (ctx->dNlNode) cudaFree(ctx->dNlNode);
+  if (ctx->dNlVal) cudaFree(ctx->dNlVal);
+  if (ctx->dGlAb) cudaFree(ctx->dGlAb);
+  if (ctx->dGlVal) cudaFree(ctx->dGlVal);
   if (ctx->dProf) cudaFree(ctx->dProf);
   for (auto& e : ctx->ev)
     if (e) cudaEventDestroy(e);
@@ -546,15 +571,18 @@ pipette_status pipette_search(pipette_ctx* ctx, const pipette_model* model, int6
 
   const int n = ctx->n_nodes;
   const int nn = n * n;
-  // MODE 0 (small clusters): packed positions, register stage-1 state, lane-replicated R,
-  // subset-max table.  MODE 1: general layout.
-  const int mode = (n <= 16 && maxN <= 256 && ctx->g <= 15 && ctx->dTab) ? 0 : 1;
+  // MODE 0 (n <= 16): packed positions, register stage-1 state, lane-replicated R,
+  // subset-max table.  MODE 1 (N <= 256): packed positions, sorted-table stage-1 state,
+  // R through L1.  MODE 2: 32-bit positions (N > 256).
+  const int mode = (n <= 16 && maxN <= 256 && ctx->g <= 15 && ctx->dTab) ? 0 : (maxN <= 256 ? 1 : 2);
   const bool rep = mode == 0;
-  const int r_bytes = (rep ? nn * 32 : nn) * 8;
-  int warp_bytes = 16;
+  const int r_bytes = rep ? nn * 32 * 8 : 0;
+  const int dp_cap = mode == 0 ? (1 << 30) : 32;
+  int warp_bytes = 16, tl_stride = 1;
   for (int f = 0; f < F; ++f) {
     const DevCfg& c = ctx->hcfg[ctx->hfeas[f]];
-    warp_bytes = std::max(warp_bytes, sa_warp_state_bytes(mode, c.N, c.pp, c.dp, n));
+    warp_bytes = std::max(warp_bytes, sa_warp_state_bytes(mode, c.N, c.pp, c.dp, n, dp_cap));
+    tl_stride = std::max(tl_stride, n * (std::min(c.spn, c.dp) - 1));
   }
   int wpb = kSaThreads / 32;
   const int smem_max = 227 * 1024;
@@ -610,6 +638,10 @@ pipette_status pipette_search(pipette_ctx* ctx, const pipette_model* model, int6
   if (mode == 0) {   // T_in rank tables of every feasible config (S1Reg)
     CU(ensure(ctx->tin_rank, (size_t)F * 256));
     CU(ensure(ctx->tin_vs, sizeof(double) * (size_t)F * 256));
+  } else {           // sorted T_in lists of every feasible config (S1Large)
+    CU(ensure(ctx->tl_ac, sizeof(uint16_t) * (size_t)F * tl_stride));
+    CU(ensure(ctx->tl_val, sizeof(double) * (size_t)F * tl_stride));
+    CU(ensure(ctx->tl_len, sizeof(int) * (size_t)F));
   }
   SaParams P{};
   P.cfgs = (const DevCfg*)ctx->cfgs.p;
@@ -618,6 +650,15 @@ pipette_status pipette_search(pipette_ctx* ctx, const pipette_model* model, int6
   P.subset_max = ctx->dTab;
   P.tin_rank = mode == 0 ? (const uint8_t*)ctx->tin_rank.p : nullptr;
   P.tin_vs = mode == 0 ? (const double*)ctx->tin_vs.p : nullptr;
+  P.nl_node = ctx->dNlNode;
+  P.nl_val = ctx->dNlVal;
+  P.gl_ab = ctx->dGlAb;
+  P.gl_val = ctx->dGlVal;
+  P.tl_ac = mode != 0 ? (const uint16_t*)ctx->tl_ac.p : nullptr;
+  P.tl_val = mode != 0 ? (const double*)ctx->tl_val.p : nullptr;
+  P.tl_len = mode != 0 ? (const int*)ctx->tl_len.p : nullptr;
+  P.tl_stride = tl_stride;
+  P.psum_dp_cap = dp_cap;
   P.tasks = (const SaTask*)ctx->tasks.p;
   P.n_tasks = (int)sorted.size();
   P.task_counter = (int*)ctx->counter.p;
@@ -651,9 +692,13 @@ pipette_status pipette_search(pipette_ctx* ctx, const pipette_model* model, int6
   if (mode == 0) {
     k_tin_rank<<<F, 256, 0, s>>>((const DevCfg*)ctx->cfgs.p, (const int*)ctx->feas.p, (const double*)ctx->qtab.p,
                                  ctx->dR, n, (uint8_t*)ctx->tin_rank.p, (double*)ctx->tin_vs.p);
-    ctx->launches++;
-    CU(cudaGetLastError());
+  } else {
+    k_tin_list<<<F, 256, 0, s>>>((const DevCfg*)ctx->cfgs.p, (const int*)ctx->feas.p, (const double*)ctx->qtab.p,
+                                 ctx->dR, n, tl_stride, (uint16_t*)ctx->tl_ac.p, (double*)ctx->tl_val.p,
+                                 (int*)ctx->tl_len.p);
   }
+  ctx->launches++;
+  CU(cudaGetLastError());
   if (!sorted.empty()) {
     void* args[] = {&P};
     CU(cudaLaunchKernel(kern, dim3(grid), dim3(wpb * 32), args, smem, s));

@@ -33,13 +33,20 @@ constexpr int kSaThreads = 128;
 
 __host__ __device__ __forceinline__ int align16(int x) { return (x + 15) & ~15; }
 
-template <bool REP>
-struct RTab {
+// R = 1/B lookups.  RRep: lane-replicated copy in shared memory (conflict free, n <= 16).
+// RGlob: the n x n table in global memory through the read-only path (L1-resident; for
+// large clusters the table would not leave room in shared memory for chain state).
+struct RRep {
   const double* s;
   int n, lane;
   __device__ __forceinline__ double operator()(uint32_t a, uint32_t b) const {
-    return REP ? s[((int)a * n + (int)b) * 32 + lane] : s[(int)a * n + (int)b];
+    return s[((int)a * n + (int)b) * 32 + lane];
   }
+};
+struct RGlob {
+  const double* s;
+  int n, lane;
+  __device__ __forceinline__ double operator()(uint32_t a, uint32_t b) const { return __ldg(s + (int)a * n + (int)b); }
 };
 
 // ------------------------------------------------------------------ position storage
@@ -99,9 +106,9 @@ __device__ __forceinline__ uint32_t node_at(const POS& pos, uint32_t w, uint32_t
 
 // Eq.5 sum of pipeline z in stage order (P_z = ((0 + m2 R[..]) + m2 R[..]) + ..., DESIGN.md
 // 3).  PP > 0: compile-time pipeline depth (fully unrolled, loads hoisted); PP == 0: runtime.
-template <bool REP, int PP, class POS>
+template <class RT, int PP, class POS>
 __device__ __forceinline__ double pipe_sum(int z, int pp_rt, const POS& pos, uint32_t p, uint32_t q, uint32_t np,
-                                           uint32_t nq, double m2, const RTab<REP>& R) {
+                                           uint32_t nq, double m2, const RT& R) {
   const int pp = PP > 0 ? PP : pp_rt;
   const uint32_t base = (uint32_t)(z * pp);
   uint32_t prev = node_at(pos, base, p, q, np, nq);
@@ -116,9 +123,9 @@ __device__ __forceinline__ double pipe_sum(int z, int pp_rt, const POS& pos, uin
 }
 
 // Two pipelines re-summed in one interleaved loop (two independent dependency chains).
-template <bool REP, int PP, class POS>
+template <class RT, int PP, class POS>
 __device__ __forceinline__ void pipe_sum2(int za, int zb, int pp_rt, const POS& pos, uint32_t p, uint32_t q,
-                                          uint32_t np, uint32_t nq, double m2, const RTab<REP>& R, double& sa,
+                                          uint32_t np, uint32_t nq, double m2, const RT& R, double& sa,
                                           double& sb) {
   const int pp = PP > 0 ? PP : pp_rt;
   const uint32_t ba = (uint32_t)(za * pp), bb = (uint32_t)(zb * pp);
@@ -145,6 +152,14 @@ struct S1Ctx {
   const double* tab;     // subset-max table (S1Reg only)
   const uint8_t* rank;   // [a*16 + c] rank of qi(c)*R[a][a], 255 if c < 2 (S1Reg only)
   const double* vs;      // values in rank order (S1Reg only)
+  // S1Large tables
+  const uint8_t* nl_node;   // [a][nl_len] other endpoints of pairs with a, by R descending
+  const double* nl_val;     // their R values (both directions)
+  const uint16_t* gl_ab;    // all ordered pairs (a | b << 8) by R descending
+  const double* gl_val;
+  const uint16_t* tl_ac;    // this config's (a | c << 8), c >= 2, by qi(c) R[a][a] descending
+  const double* tl_val;
+  int nl_len, gl_len, tl_len;
   int n;
 };
 
@@ -152,7 +167,7 @@ struct S1Ctx {
 // value qi(c)*R[a][a] (c >= 2) has a precomputed position in descending order
 // (k_tin_rank); a node's current rank is one byte of rk[], and T_in is the value at the
 // smallest rank present (SIMD byte minimum) -- the max of Eq.6's intra term without a scan.
-template <bool REP>
+template <class RT>
 struct S1Reg {
   uint64_t cnt, cnt2;
   uint32_t mask, mask2;
@@ -178,7 +193,7 @@ struct S1Reg {
   }
   __device__ __forceinline__ void clear() { cnt = 0ull; mask = 0u; }
   __device__ __forceinline__ void add_init(uint32_t a) { cnt += 1ull << (4u * a); mask |= 1u << a; }
-  __device__ __forceinline__ void finish_init(const S1Ctx& X, const RTab<REP>& R) {
+  __device__ __forceinline__ void finish_init(const S1Ctx& X, const RT& R) {
     rk[0] = rk[1] = rk[2] = rk[3] = 0xffffffffu;
     for (int a = 0; a < X.n; ++a) set_byte(rk, (uint32_t)a, X.rank[a * 16 + get(cnt, (uint32_t)a)]);
     k = __popc(mask);
@@ -186,7 +201,7 @@ struct S1Reg {
     tex = tex_of(mask, k, X);
   }
   // a stage-1 member moves from node dn to node up (tentative state)
-  __device__ __forceinline__ void propose(uint32_t dn, uint32_t up, const S1Ctx& X, const RTab<REP>& R) {
+  __device__ __forceinline__ void propose(uint32_t dn, uint32_t up, const S1Ctx& X, const RT& R) {
     const uint32_t c_dn = get(cnt, dn) - 1u, c_up = get(cnt, up) + 1u;
     cnt2 = cnt - (1ull << (4u * dn)) + (1ull << (4u * up));
     mask2 = (mask & (c_dn == 0u ? ~(1u << dn) : 0xffffffffu)) | (1u << up);
@@ -205,15 +220,22 @@ struct S1Reg {
   }
 };
 
-// General stage-1 state: counts (u8, c_n <= spn <= 255) in shared memory, 128-bit node
-// mask, T_ex maintained with a witness ordered pair.
-template <bool REP>
-struct S1Smem {
+// General stage-1 state (n <= 128): counts (u8, c_n <= spn <= 255) in shared memory, a
+// 128-bit node mask N1 in registers, witnesses for both max terms of Eq.6 and sorted
+// tables instead of scans:
+//   T_in: witness node; when it loses a member, the config's (a, c) list sorted by
+//         qi(c) R[a][a] is scanned for the first entry whose node has exactly c members.
+//   T_ex: witness pair {wa, wb}; a node joining N1 scans its own pair list (sorted by R)
+//         for the first partner in N1 (expected n/k probes); the witness leaving
+//         recomputes over member pairs (k <= 16) or scans the global sorted pair list for
+//         the first pair inside N1 (expected (n/k)^2 probes).
+template <class RT>
+struct S1Large {
   uint32_t* c;   // [ceil(n/4)][32] words
   int lane;
   Mask<4> mask, mask2;
   int k, k2, win, win2, wa, wb, wa2, wb2;
-  uint32_t dn_, up_;
+  uint32_t dn_, up_, c_dn_, c_up_;
   double tin, tex, maxR, tin2, tex2, maxR2;
 
   __device__ __forceinline__ uint32_t get(uint32_t a) const { return (c[(a >> 2) * 32 + lane] >> ((a & 3) * 8)) & 0xffu; }
@@ -222,26 +244,25 @@ struct S1Smem {
     const uint32_t sh = (a & 3) * 8;
     w = delta > 0 ? w + (1u << sh) : w - (1u << sh);
   }
-  __device__ __forceinline__ double tin_full(const Mask<4>& m, uint32_t dn, uint32_t c_dn, uint32_t up,
-                                             uint32_t c_up, const S1Ctx& X, const RTab<REP>& R, int& w) const {
-    double t = 0.0;
-    w = -1;
+  static __device__ __forceinline__ bool in(const Mask<4>& m, uint32_t a) {
+    uint32_t w = m.w[0];
 #pragma unroll
-    for (int wd = 0; wd < 4; ++wd) {
-      uint32_t bits = m.w[wd];
-      while (bits) {
-        const uint32_t a = wd * 32 + __ffs(bits) - 1;
-        bits &= bits - 1;
-        const uint32_t ca = a == dn ? c_dn : (a == up ? c_up : get(a));
-        if (ca >= 2) {
-          const double v = __dmul_rn(__ldg(X.qi + ca), R(a, a));
-          if (v > t) { t = v; w = (int)a; }
-        }
-      }
-    }
-    return t;
+    for (int i = 1; i < 4; ++i) w = ((a >> 5) == (uint32_t)i) ? m.w[i] : w;
+    return (w >> (a & 31)) & 1u;
   }
-  __device__ __forceinline__ double maxr_full(const Mask<4>& m, const RTab<REP>& R, int& a_, int& b_) const {
+  // tentative count of node a (after dn -> up)
+  __device__ __forceinline__ uint32_t cnt2(uint32_t a) const { return a == dn_ ? c_dn_ : (a == up_ ? c_up_ : get(a)); }
+
+  __device__ __forceinline__ double tin_scan(const S1Ctx& X, bool tentative, int& w) const {
+    for (int i = 0; i < X.tl_len; ++i) {
+      const uint32_t ac = X.tl_ac[i];
+      const uint32_t a = ac & 0xffu, cc = ac >> 8;
+      if ((tentative ? cnt2(a) : get(a)) == cc) { w = (int)a; return X.tl_val[i]; }
+    }
+    w = -1;
+    return 0.0;
+  }
+  __device__ __forceinline__ double maxr_members(const Mask<4>& m, const RT& R, int& a_, int& b_) const {
     double mx = 0.0;
     a_ = b_ = -1;
 #pragma unroll
@@ -265,50 +286,58 @@ struct S1Smem {
     }
     return mx;
   }
+  __device__ __forceinline__ double maxr_global(const Mask<4>& m, const S1Ctx& X, int& a_, int& b_) const {
+    for (int i = 0; i < X.gl_len; ++i) {
+      const uint32_t ab = X.gl_ab[i];
+      const uint32_t a = ab & 0xffu, b = ab >> 8;
+      if (in(m, a) && in(m, b)) { a_ = (int)a; b_ = (int)b; return X.gl_val[i]; }
+    }
+    a_ = b_ = -1;
+    return 0.0;
+  }
+  __device__ __forceinline__ double maxr(const Mask<4>& m, int kk, const S1Ctx& X, const RT& R, int& a_, int& b_) const {
+    if (kk < 2) { a_ = b_ = -1; return 0.0; }
+    return kk <= 16 ? maxr_members(m, R, a_, b_) : maxr_global(m, X, a_, b_);
+  }
   __device__ __forceinline__ void clear(int n) {
     for (int wd = 0; wd < (n + 3) / 4; ++wd) c[wd * 32 + lane] = 0u;
     mask.clear();
   }
   __device__ __forceinline__ void add_init(uint32_t a) { add(a, +1); mask.set(a); }
-  __device__ __forceinline__ void finish_init(const S1Ctx& X, const RTab<REP>& R) {
+  __device__ __forceinline__ void finish_init(const S1Ctx& X, const RT& R) {
     k = mask.count();
-    tin = tin_full(mask, 0xffffffffu, 0u, 0xffffffffu, 0u, X, R, win);
-    maxR = 0.0;
-    wa = wb = -1;
-    if (k >= 2) maxR = maxr_full(mask, R, wa, wb);
+    tin = tin_scan(X, false, win);
+    maxR = maxr(mask, k, X, R, wa, wb);
     tex = k >= 2 ? __dmul_rn(__ldg(X.qe + k), maxR) : 0.0;
   }
-  __device__ __forceinline__ void propose(uint32_t dn, uint32_t up, const S1Ctx& X, const RTab<REP>& R) {
+  __device__ __forceinline__ void propose(uint32_t dn, uint32_t up, const S1Ctx& X, const RT& R) {
     dn_ = dn; up_ = up;
-    const uint32_t c_dn = get(dn) - 1u, c_up = get(up) + 1u;
-    const bool leave = c_dn == 0u, join = c_up == 1u;
+    c_dn_ = get(dn) - 1u; c_up_ = get(up) + 1u;
+    const bool leave = c_dn_ == 0u, join = c_up_ == 1u;
     mask2 = mask;
     if (leave) mask2.reset(dn);
     if (join) mask2.set(up);
     k2 = k - (int)leave + (int)join;
     tin2 = tin; win2 = win;
     if ((int)dn == win) {
-      tin2 = tin_full(mask2, dn, c_dn, up, c_up, X, R, win2);
-    } else if (c_up >= 2u) {
-      const double v = __dmul_rn(__ldg(X.qi + c_up), R(up, up));
+      tin2 = tin_scan(X, true, win2);
+    } else if (c_up_ >= 2u) {
+      const double v = __dmul_rn(__ldg(X.qi + c_up_), R(up, up));
       if (v > tin2) { tin2 = v; win2 = (int)up; }
     }
     maxR2 = maxR; wa2 = wa; wb2 = wb;
     if (k2 < 2) {
       maxR2 = 0.0; wa2 = wb2 = -1;
     } else if (leave && ((int)dn == wa || (int)dn == wb)) {
-      maxR2 = maxr_full(mask2, R, wa2, wb2);
+      maxR2 = maxr(mask2, k2, X, R, wa2, wb2);
     } else if (join) {
-#pragma unroll
-      for (int wd = 0; wd < 4; ++wd) {
-        uint32_t bits = mask2.w[wd];
-        while (bits) {
-          const uint32_t b = wd * 32 + __ffs(bits) - 1;
-          bits &= bits - 1;
-          if (b == up) continue;
-          const double v1 = R(up, b), v2 = R(b, up);
-          if (v1 > maxR2) { maxR2 = v1; wa2 = (int)up; wb2 = (int)b; }
-          if (v2 > maxR2) { maxR2 = v2; wa2 = (int)b; wb2 = (int)up; }
+      const uint8_t* nl = X.nl_node + (size_t)up * X.nl_len;
+      for (int i = 0; i < X.nl_len; ++i) {       // first partner of up inside N1 (by R)
+        const uint32_t b = nl[i];
+        if (in(mask2, b)) {
+          const double v = X.nl_val[(size_t)up * X.nl_len + i];
+          if (v > maxR2) { maxR2 = v; wa2 = (int)up; wb2 = (int)b; }
+          break;
         }
       }
     }
@@ -321,31 +350,41 @@ struct S1Smem {
 };
 
 // Shared-memory footprint of one warp's chain state for a configuration.
+// psum cached in shared memory when pp >= 2 and dp <= dp_cap.
 template <class POS>
-__host__ __device__ inline int warp_state_bytes(int N, int pp, int dp, int n, bool s1smem) {
-  return align16(POS::bytes(N)) + (pp >= 2 ? align16(dp * 256) : 0) + (s1smem ? align16((n + 3) / 4 * 128) : 0);
+__host__ __device__ inline int warp_state_bytes(int N, int pp, int dp, int n, bool s1smem, int dp_cap) {
+  return align16(POS::bytes(N)) + ((pp >= 2 && dp <= dp_cap) ? align16(dp * 256) : 0) +
+         (s1smem ? align16((n + 3) / 4 * 128) : 0);
 }
 
 // ------------------------------------------------------------------ one warp task
-template <class POS, class S1, bool REP, bool TRACE, int PP>
-__device__ void run_task(const SaParams& P, const SaTask& T, const DevCfg& C, const double* Rs, unsigned char* ws,
+template <class POS, class S1, class RT, bool TRACE, int PP>
+__device__ void run_task(const SaParams& P, const SaTask& T, const DevCfg& C, const RT& R, unsigned char* ws,
                          int lane) {
   if (lane >= T.count) return;
-  constexpr bool kSmemS1 = !std::is_same<S1, S1Reg<REP>>::value;
+  constexpr bool kLargeS1 = !std::is_same<S1, S1Reg<RT>>::value;
   const int N = C.N, pp = PP > 0 ? PP : C.pp, dp = C.dp, n = P.n_nodes;
   const uint32_t chain = (uint32_t)(T.c_first + (T.k0 + lane) * P.world);
   const int slot = T.slot0 + lane;
-  const RTab<REP> R{Rs, n, lane};
-  const S1Ctx X{P.qtab + C.qi_off, P.qtab + C.qe_off, P.subset_max,
-                P.tin_rank ? P.tin_rank + (size_t)T.f * 256 : nullptr,
-                P.tin_vs ? P.tin_vs + (size_t)T.f * 256 : nullptr, n};
+  S1Ctx X;
+  X.qi = P.qtab + C.qi_off; X.qe = P.qtab + C.qe_off; X.tab = P.subset_max;
+  X.rank = P.tin_rank ? P.tin_rank + (size_t)T.f * 256 : nullptr;
+  X.vs = P.tin_vs ? P.tin_vs + (size_t)T.f * 256 : nullptr;
+  X.nl_node = P.nl_node; X.nl_val = P.nl_val; X.gl_ab = P.gl_ab; X.gl_val = P.gl_val;
+  X.tl_ac = P.tl_ac ? P.tl_ac + (size_t)T.f * P.tl_stride : nullptr;
+  X.tl_val = P.tl_val ? P.tl_val + (size_t)T.f * P.tl_stride : nullptr;
+  X.nl_len = 2 * (n - 1); X.gl_len = n * (n - 1); X.tl_len = P.tl_len ? P.tl_len[T.f] : 0;
+  X.n = n;
 
+  // psum (Eq.5 sum of every pipeline) cached in shared memory unless dp is large; then the
+  // old sums of the touched pipelines are re-summed before the tentative swap instead
+  const bool cache = pp >= 2 && dp <= P.psum_dp_cap;
   POS pos{reinterpret_cast<uint32_t*>(ws), lane};
   double* psum = reinterpret_cast<double*>(ws + align16(POS::bytes(N)));
   uint16_t* bperm = P.best_perm + T.perm_off;
   S1 s1;
-  if constexpr (kSmemS1) {
-    s1.c = reinterpret_cast<uint32_t*>(ws + align16(POS::bytes(N)) + (pp >= 2 ? align16(dp * 256) : 0));
+  if constexpr (kLargeS1) {
+    s1.c = reinterpret_cast<uint32_t*>(ws + align16(POS::bytes(N)) + (cache ? align16(dp * 256) : 0));
     s1.lane = lane;
     s1.clear(n);
   } else {
@@ -360,8 +399,8 @@ __device__ void run_task(const SaParams& P, const SaTask& T, const DevCfg& C, co
   for (int z = 0; z < dp; ++z) {
     s1.add_init(pos.node((uint32_t)(z * pp)));
     if (pp >= 2) {
-      const double s = pipe_sum<REP, PP>(z, pp, pos, kNone, kNone, 0u, 0u, C.m2, R);
-      psum[z * 32 + lane] = s;
+      const double s = pipe_sum<RT, PP>(z, pp, pos, kNone, kNone, 0u, 0u, C.m2, R);
+      if (cache) psum[z * 32 + lane] = s;
       if (s > tpp) { tpp = s; nmax = 1; } else if (s == tpp) { ++nmax; }
     }
   }
@@ -399,20 +438,26 @@ __device__ void run_task(const SaParams& P, const SaTask& T, const DevCfg& C, co
           xp = d.p - (uint32_t)(zp * pp);
           xq = d.q - (uint32_t)(zq * pp);
           two = zq != zp;
+          double oldA, oldB;
+          if (cache) {
+            oldA = psum[zp * 32 + lane];
+            oldB = two ? psum[zq * 32 + lane] : oldA;
+          } else {
+            if (two) pipe_sum2<RT, PP>(zp, zq, pp, pos, kNone, kNone, 0u, 0u, C.m2, R, oldA, oldB);
+            else oldB = oldA = pipe_sum<RT, PP>(zp, pp, pos, kNone, kNone, 0u, 0u, C.m2, R);
+          }
           // apply the swap tentatively (reverted below if rejected): the re-sum then reads
           // plain positions, with no per-hop substitution
           pos.swap(d.p, d.q, rp, rq);
-          if (two) pipe_sum2<REP, PP>(zp, zq, pp, pos, kNone, kNone, 0u, 0u, C.m2, R, sA, sB);
-          else sA = pipe_sum<REP, PP>(zp, pp, pos, kNone, kNone, 0u, 0u, C.m2, R);
-          const double oldA = psum[zp * 32 + lane];
-          const double oldB = two ? psum[zq * 32 + lane] : oldA;
+          if (two) pipe_sum2<RT, PP>(zp, zq, pp, pos, kNone, kNone, 0u, 0u, C.m2, R, sA, sB);
+          else sA = pipe_sum<RT, PP>(zp, pp, pos, kNone, kNone, 0u, 0u, C.m2, R);
           const double snew = two ? fmax(sA, sB) : sA;
           const int keep = nmax - (oldA == tpp ? 1 : 0) - ((two && oldB == tpp) ? 1 : 0);  // untouched at max
           if (keep > 0 || snew >= tpp) {
             // the max is max(tpp if an untouched pipeline still holds it, new sums)
             tpp2 = (keep > 0) ? fmax(tpp, snew) : snew;
             nmax2 = (keep > 0 && tpp2 == tpp ? keep : 0) + (sA == tpp2 ? 1 : 0) + ((two && sB == tpp2) ? 1 : 0);
-          } else {
+          } else if (cache) {
             // the unique max pipeline decreased: rescan (4 independent max chains)
             double m0 = snew, m1 = 0.0, m2 = 0.0, m3 = 0.0;
             int z = 0;
@@ -431,6 +476,14 @@ __device__ void run_task(const SaParams& P, const SaTask& T, const DevCfg& C, co
               const double v = (z == zp) ? sA : ((z == zq) ? sB : psum[z * 32 + lane]);
               nmax2 += v == tpp2 ? 1 : 0;
             }
+          } else {
+            // no cache: re-sum every pipeline of the tentative mapping
+            tpp2 = 0.0;
+            nmax2 = 0;
+            for (int z = 0; z < dp; ++z) {
+              const double v = (z == zp) ? sA : ((z == zq) ? sB : pipe_sum<RT, PP>(z, pp, pos, kNone, kNone, 0u, 0u, C.m2, R));
+              if (v > tpp2) { tpp2 = v; nmax2 = 1; } else if (v == tpp2) { ++nmax2; }
+            }
           }
         }
         // ---- Eq.6: the stage-1 node multiset changes only if exactly one of p, q is stage 1
@@ -447,8 +500,10 @@ __device__ void run_task(const SaParams& P, const SaTask& T, const DevCfg& C, co
         acc = metropolis_fast(__dadd_rn(Lp, -cur), beta, d.u);
         if (acc) {
           if (pp >= 2) {
-            psum[zp * 32 + lane] = sA;
-            if (two) psum[zq * 32 + lane] = sB;
+            if (cache) {
+              psum[zp * 32 + lane] = sA;
+              if (two) psum[zq * 32 + lane] = sB;
+            }
             tpp = tpp2;
             nmax = nmax2;
           }
@@ -483,23 +538,24 @@ __device__ void run_task(const SaParams& P, const SaTask& T, const DevCfg& C, co
   P.out[slot] = o;
 }
 
-// MODE 0: n <= 16 nodes, N <= 256, spn <= 15 (packed positions, register stage-1 state,
-//         lane-replicated R, subset-max table).  MODE 1: general.
+// MODE 0: n <= 16 nodes, N <= 256, spn <= 15: packed positions, register stage-1 state,
+//         lane-replicated R in shared memory, subset-max table.
+// MODE 1: n <= 128, N <= 256: packed positions, S1Large, R through L1.
+// MODE 2: general (N <= 1024): 32-bit positions, S1Large, R through L1.
 template <int MODE, bool TRACE>
 __global__ void __launch_bounds__(kSaThreads) k_sa_chains(SaParams P) {
-  using POS = typename std::conditional<MODE == 0, PosPacked, PosWide>::type;
-  constexpr bool REP = MODE == 0;
-  using S1 = typename std::conditional<MODE == 0, S1Reg<REP>, S1Smem<REP>>::type;
+  using POS = typename std::conditional<MODE == 2, PosWide, PosPacked>::type;
+  using RT = typename std::conditional<MODE == 0, RRep, RGlob>::type;
+  using S1 = typename std::conditional<MODE == 0, S1Reg<RT>, S1Large<RT>>::type;
   extern __shared__ __align__(16) unsigned char smem[];
   double* Rs = reinterpret_cast<double*>(smem);
   const int nn = P.n_nodes * P.n_nodes;
-  if (REP) {
+  if (MODE == 0) {
     for (int i = threadIdx.x; i < nn * 32; i += blockDim.x) Rs[i] = P.R[i >> 5];
-  } else {
-    for (int i = threadIdx.x; i < nn; i += blockDim.x) Rs[i] = P.R[i];
+    __syncthreads();
   }
-  __syncthreads();
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const RT R{MODE == 0 ? Rs : P.R, P.n_nodes, lane};
   unsigned char* ws = smem + P.r_smem_bytes + wid * P.warp_smem_bytes;
   __shared__ int s_base;
   for (;;) {
@@ -516,13 +572,13 @@ __global__ void __launch_bounds__(kSaThreads) k_sa_chains(SaParams P) {
     unsigned long long t_start = 0;
     if (lane == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_start));
     switch (C.pp) {   // compile-time pipeline depth for the common power-of-two depths
-      case 1: run_task<POS, S1, REP, TRACE, 1>(P, T, C, Rs, ws, lane); break;
-      case 2: run_task<POS, S1, REP, TRACE, 2>(P, T, C, Rs, ws, lane); break;
-      case 4: run_task<POS, S1, REP, TRACE, 4>(P, T, C, Rs, ws, lane); break;
-      case 8: run_task<POS, S1, REP, TRACE, 8>(P, T, C, Rs, ws, lane); break;
-      case 16: run_task<POS, S1, REP, TRACE, 16>(P, T, C, Rs, ws, lane); break;
-      case 32: run_task<POS, S1, REP, TRACE, 32>(P, T, C, Rs, ws, lane); break;
-      default: run_task<POS, S1, REP, TRACE, 0>(P, T, C, Rs, ws, lane); break;
+      case 1: run_task<POS, S1, RT, TRACE, 1>(P, T, C, R, ws, lane); break;
+      case 2: run_task<POS, S1, RT, TRACE, 2>(P, T, C, R, ws, lane); break;
+      case 4: run_task<POS, S1, RT, TRACE, 4>(P, T, C, R, ws, lane); break;
+      case 8: run_task<POS, S1, RT, TRACE, 8>(P, T, C, R, ws, lane); break;
+      case 16: run_task<POS, S1, RT, TRACE, 16>(P, T, C, R, ws, lane); break;
+      case 32: run_task<POS, S1, RT, TRACE, 32>(P, T, C, R, ws, lane); break;
+      default: run_task<POS, S1, RT, TRACE, 0>(P, T, C, R, ws, lane); break;
     }
     __syncwarp();
     if (lane == 0) {
@@ -532,6 +588,69 @@ __global__ void __launch_bounds__(kSaThreads) k_sa_chains(SaParams P) {
       asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
       reinterpret_cast<ulonglong4*>(P.task_prof)[t] = make_ulonglong4(t_start, t_end, smid, (unsigned long long)T.cfg);
     }
+  }
+}
+
+// Sorted tables of the cluster for S1Large (n <= 256).  Node lists: for each node a, the
+// 2(n-1) values R[a][b] and R[b][a] (b != a) in descending order with their partner b.
+// Ties are broken by index, so the order is total.  One block per node.
+__global__ void k_node_lists(const double* __restrict__ R, int n, uint8_t* __restrict__ nl_node,
+                             double* __restrict__ nl_val) {
+  const int a = blockIdx.x, L = 2 * (n - 1);
+  for (int i = threadIdx.x; i < L; i += blockDim.x) {
+    const int bi = i >> 1, b = bi < a ? bi : bi + 1;
+    const double v = (i & 1) ? R[b * n + a] : R[a * n + b];
+    int r = 0;
+    for (int j = 0; j < L; ++j) {
+      const int bj = j >> 1, b2 = bj < a ? bj : bj + 1;
+      const double u = (j & 1) ? R[b2 * n + a] : R[a * n + b2];
+      r += (u > v || (u == v && j < i)) ? 1 : 0;
+    }
+    nl_node[(size_t)a * L + r] = (uint8_t)b;
+    nl_val[(size_t)a * L + r] = v;
+  }
+}
+
+// Global list: all ordered pairs a != b by R[a][b] descending (one thread per pair).
+__global__ void k_pair_list(const double* __restrict__ R, int n, uint16_t* __restrict__ gl_ab,
+                            double* __restrict__ gl_val) {
+  const int L = n * (n - 1);
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= L) return;
+  const int a = i / (n - 1), bi = i % (n - 1), b = bi < a ? bi : bi + 1;
+  const double v = R[a * n + b];
+  int r = 0;
+  for (int j = 0; j < L; ++j) {
+    const int a2 = j / (n - 1), bj = j % (n - 1), b2 = bj < a2 ? bj : bj + 1;
+    const double u = R[a2 * n + b2];
+    r += (u > v || (u == v && j < i)) ? 1 : 0;
+  }
+  gl_ab[r] = (uint16_t)(a | (b << 8));
+  gl_val[r] = v;
+}
+
+// Per feasible config (block f): the (a, c) entries, 2 <= c <= min(spn, dp), sorted by
+// qi(c) R[a][a] descending (ties by index); tl_len[f] entries, row stride `stride`.
+__global__ void k_tin_list(const DevCfg* __restrict__ cfgs, const int* __restrict__ feas,
+                           const double* __restrict__ qtab, const double* __restrict__ R, int n, int stride,
+                           uint16_t* __restrict__ tl_ac, double* __restrict__ tl_val, int* __restrict__ tl_len) {
+  const int f = blockIdx.x;
+  const DevCfg C = cfgs[feas[f]];
+  const int cmax = min(min(C.spn, C.dp), 255);
+  const int per = cmax >= 2 ? cmax - 1 : 0;
+  const int L = min(n * per, stride);
+  if (threadIdx.x == 0) tl_len[f] = L;
+  for (int i = threadIdx.x; i < L; i += blockDim.x) {
+    const int a = i / per, c = 2 + i % per;
+    const double v = __dmul_rn(qtab[C.qi_off + c], R[a * n + a]);
+    int r = 0;
+    for (int j = 0; j < L; ++j) {
+      const int a2 = j / per, c2 = 2 + j % per;
+      const double u = __dmul_rn(qtab[C.qi_off + c2], R[a2 * n + a2]);
+      r += (u > v || (u == v && j < i)) ? 1 : 0;
+    }
+    tl_ac[(size_t)f * stride + r] = (uint16_t)(a | (c << 8));
+    tl_val[(size_t)f * stride + r] = v;
   }
 }
 
@@ -625,14 +744,17 @@ __global__ void __launch_bounds__(256) k_argmin(const ChainOut* __restrict__ out
   }
 }
 
-// Host-side handles of the K3 variants (MODE 0 small clusters, 1 general; TRACE records).
+// Host-side handles of the K3 variants (MODE 0/1/2 as above; TRACE records).
 const void* sa_kernel(int mode, bool trace) {
   if (mode == 0) return trace ? (const void*)k_sa_chains<0, true> : (const void*)k_sa_chains<0, false>;
-  return trace ? (const void*)k_sa_chains<1, true> : (const void*)k_sa_chains<1, false>;
+  if (mode == 1) return trace ? (const void*)k_sa_chains<1, true> : (const void*)k_sa_chains<1, false>;
+  return trace ? (const void*)k_sa_chains<2, true> : (const void*)k_sa_chains<2, false>;
 }
 
-int sa_warp_state_bytes(int mode, int N, int pp, int dp, int n) {
-  return mode == 0 ? warp_state_bytes<PosPacked>(N, pp, dp, n, false) : warp_state_bytes<PosWide>(N, pp, dp, n, true);
+int sa_warp_state_bytes(int mode, int N, int pp, int dp, int n, int dp_cap) {
+  if (mode == 0) return warp_state_bytes<PosPacked>(N, pp, dp, n, false, dp_cap);
+  if (mode == 1) return warp_state_bytes<PosPacked>(N, pp, dp, n, true, dp_cap);
+  return warp_state_bytes<PosWide>(N, pp, dp, n, true, dp_cap);
 }
 
 }  // namespace pip

@@ -63,6 +63,15 @@ struct SaParams {
   const double* subset_max;  // 2^n subset maxima of R off-diagonal (n <= 16), or null
   const uint8_t* tin_rank;   // per feasible config: 256 ranks (k_tin_rank), MODE 0
   const double* tin_vs;      // per feasible config: 256 values in rank order, MODE 0
+  const uint8_t* nl_node;    // S1Large cluster tables (k_node_lists, k_pair_list)
+  const double* nl_val;
+  const uint16_t* gl_ab;
+  const double* gl_val;
+  const uint16_t* tl_ac;     // S1Large per-config T_in lists (k_tin_list), row stride tl_stride
+  const double* tl_val;
+  const int* tl_len;
+  int32_t tl_stride;
+  int32_t psum_dp_cap;       // pipeline sums cached in shared memory when dp <= this
   const SaTask* tasks;
   int32_t n_tasks;
   int32_t* task_counter;

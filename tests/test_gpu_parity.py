@@ -273,3 +273,49 @@ def test_search_is_deterministic_and_bandwidth_update_matters():
     pip.set_bandwidth(B * 0.5)
     c = pip.search(model, w.bs_global, 64, 1000, 11)["plan"]
     assert c.latency_s > a.latency_s
+
+
+def _sampled_chain_parity(w, chains, iters, n_sample, seed=2, trace_n=3):
+    pip, B, prof = _ctx(w)
+    model, mo, cl = _models(w)
+    P = O.make_profile(prof)
+    R = O.inverse_bandwidth(B)
+    feas = [c for c in O.enumerate_configs(cl, mo, w.bs_global, P) if c.feasible]
+    rng = np.random.default_rng(seed)
+    items = rng.choice(len(feas) * chains, size=trace_n, replace=False).tolist()
+    res = pip.search(model, w.bs_global, chains, iters, w.seed, chain_results=True, per_config=True,
+                     trace_items=items, trace_cap=iters)
+    rows = res["chains"]
+    assert len(rows) == len(feas) * chains
+    by_e = {c.e: c for c in feas}
+    for j in rng.choice(len(rows), size=n_sample, replace=False).tolist():
+        r = rows[j]
+        o = _oracle_chain(cl, mo, P, R, by_e, r["cfg_index"], r["chain"], iters, w.seed)
+        assert r["L0"] == o.L0
+        assert (r["best"], r["best_step"], r["accepted"]) == (o.best, o.best_step, o.accepted), (j, r["cfg_index"])
+        assert (r["best_t_pp"], r["best_t_dp"]) == (o.best_t_pp, o.best_t_dp)
+        assert np.array_equal(r["perm"], o.best_perm)
+    for t, j in enumerate(items):
+        f, c = divmod(j, chains)
+        o = _oracle_chain(cl, mo, P, R, by_e, feas[f].e, c, iters, w.seed, trace=True)
+        assert res["trace"][t] == o.trace, j
+    ref_best = min(rows, key=lambda r: (r["best"], r["item"]))
+    assert res["plan"].latency_s == ref_best["best"] and res["plan"].chain == ref_best["chain"]
+    return res
+
+
+def test_search_mode1_c4_sampled_chains_and_traces():
+    # 32 nodes: packed positions, sorted-table stage-1 state (S1Large), R through L1
+    _sampled_chain_parity(W.WORKLOADS["C4"], chains=64, iters=2000, n_sample=40)
+
+
+def test_search_mode1_c5_sampled_chains_and_traces():
+    # 128 nodes, N up to 256
+    _sampled_chain_parity(W.WORKLOADS["C5"], chains=32, iters=1000, n_sample=24, trace_n=2)
+
+
+def test_search_mode2_wide_positions():
+    # N > 256 (tp = 1 on 40 nodes x 8 GPUs) takes the 32-bit position layout
+    w = W.Workload("C0", 40, 8, W.GPT_345M, 320, 80_000_000_000, 100, 8, 600, 0.2, 0.2, 11)
+    res = _sampled_chain_parity(w, chains=8, iters=600, n_sample=24, trace_n=2)
+    assert any(p.cfg[0] * p.cfg[2] > 256 for p in res["per_config"])
