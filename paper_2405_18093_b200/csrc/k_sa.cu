@@ -295,9 +295,11 @@ struct S1Large {
     a_ = b_ = -1;
     return 0.0;
   }
+  // recompute from scratch: k(k-1) member pairs, or the global sorted list with an
+  // expected (n/k)^2 probes -- whichever is cheaper (k^4 <= 4 n^2)
   __device__ __forceinline__ double maxr(const Mask<4>& m, int kk, const S1Ctx& X, const RT& R, int& a_, int& b_) const {
     if (kk < 2) { a_ = b_ = -1; return 0.0; }
-    return kk <= 16 ? maxr_members(m, R, a_, b_) : maxr_global(m, X, a_, b_);
+    return kk * kk * kk * kk <= 4 * X.n * X.n ? maxr_members(m, R, a_, b_) : maxr_global(m, X, a_, b_);
   }
   __device__ __forceinline__ void clear(int n) {
     for (int wd = 0; wd < (n + 3) / 4; ++wd) c[wd * 32 + lane] = 0u;
@@ -330,9 +332,22 @@ struct S1Large {
       maxR2 = 0.0; wa2 = wb2 = -1;
     } else if (leave && ((int)dn == wa || (int)dn == wb)) {
       maxR2 = maxr(mask2, k2, X, R, wa2, wb2);
-    } else if (join) {
+    } else if (join && 2 * k2 * k2 <= X.n) {  // few members: both directions to each member
+#pragma unroll
+      for (int wd = 0; wd < 4; ++wd) {
+        uint32_t bits = mask2.w[wd];
+        while (bits) {
+          const uint32_t b = wd * 32 + __ffs(bits) - 1;
+          bits &= bits - 1;
+          if (b == up) continue;
+          const double v1 = R(up, b), v2 = R(b, up);
+          if (v1 > maxR2) { maxR2 = v1; wa2 = (int)up; wb2 = (int)b; }
+          if (v2 > maxR2) { maxR2 = v2; wa2 = (int)b; wb2 = (int)up; }
+        }
+      }
+    } else if (join) {                         // first partner of up inside N1, by R (~n/k probes)
       const uint8_t* nl = X.nl_node + (size_t)up * X.nl_len;
-      for (int i = 0; i < X.nl_len; ++i) {       // first partner of up inside N1 (by R)
+      for (int i = 0; i < X.nl_len; ++i) {
         const uint32_t b = nl[i];
         if (in(mask2, b)) {
           const double v = X.nl_val[(size_t)up * X.nl_len + i];
