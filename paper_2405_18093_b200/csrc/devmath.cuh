@@ -141,7 +141,8 @@ __device__ __forceinline__ uint32_t div_small(uint32_t x, uint32_t m, uint32_t d
   return d == 1u ? x : __umulhi(x, m);
 }
 
-// Bit set of node ids (< 32*MW) held in registers; statically indexed words.
+// Bit set of node ids (< 32*MW) held in registers.  MW == 4 is spelled out as four scalar
+// words: with an array member the compiler may place the set in local memory and index it.
 template <int MW>
 struct Mask {
   uint32_t w[MW];
@@ -163,6 +164,26 @@ struct Mask {
     for (int i = 0; i < MW; ++i) c += __popc(w[i]);
     return c;
   }
+};
+
+struct Mask4 {
+  uint32_t w0, w1, w2, w3;
+  __device__ __forceinline__ void clear() { w0 = w1 = w2 = w3 = 0u; }
+  __device__ __forceinline__ uint32_t word(int i) const { return i == 0 ? w0 : (i == 1 ? w1 : (i == 2 ? w2 : w3)); }
+  __device__ __forceinline__ void set(uint32_t a) {
+    const uint32_t b = 1u << (a & 31), q = a >> 5;
+    w0 |= q == 0u ? b : 0u; w1 |= q == 1u ? b : 0u; w2 |= q == 2u ? b : 0u; w3 |= q == 3u ? b : 0u;
+  }
+  __device__ __forceinline__ void reset(uint32_t a) {
+    const uint32_t b = ~(1u << (a & 31)), q = a >> 5;
+    w0 &= q == 0u ? b : ~0u; w1 &= q == 1u ? b : ~0u; w2 &= q == 2u ? b : ~0u; w3 &= q == 3u ? b : ~0u;
+  }
+  __device__ __forceinline__ bool test(uint32_t a) const {
+    const uint32_t q = a >> 5;
+    const uint32_t x = q == 0u ? w0 : (q == 1u ? w1 : (q == 2u ? w2 : w3));
+    return (x >> (a & 31)) & 1u;
+  }
+  __device__ __forceinline__ int count() const { return __popc(w0) + __popc(w1) + __popc(w2) + __popc(w3); }
 };
 
 }  // namespace pip

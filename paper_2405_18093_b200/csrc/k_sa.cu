@@ -171,19 +171,23 @@ template <class RT>
 struct S1Reg {
   uint64_t cnt, cnt2;
   uint32_t mask, mask2;
-  uint32_t rk[4], rk2[4];
+  uint32_t rk0, rk1, rk2_, rk3, nk0, nk1, nk2, nk3;   // current / tentative rank bytes
   int k, k2;
   double tin, tex, tin2, tex2;
 
   static __device__ __forceinline__ uint32_t get(uint64_t c, uint32_t a) { return (uint32_t)(c >> (4u * a)) & 15u; }
-  static __device__ __forceinline__ void set_byte(uint32_t (&r)[4], uint32_t a, uint32_t v) {
-    const uint32_t sh = (a & 3u) * 8u;
-#pragma unroll
-    for (int i = 0; i < 4; ++i)
-      r[i] = ((a >> 2) == (uint32_t)i) ? ((r[i] & ~(0xffu << sh)) | (v << sh)) : r[i];
+  // byte a of the 16-byte vector (r0..r3) := v (scalars, never an indexed array)
+  static __device__ __forceinline__ void set_byte(uint32_t& r0, uint32_t& r1, uint32_t& r2, uint32_t& r3, uint32_t a,
+                                                  uint32_t v) {
+    const uint32_t sh = (a & 3u) * 8u, q = a >> 2;
+    const uint32_t keep = ~(0xffu << sh), put = v << sh;
+    r0 = q == 0u ? ((r0 & keep) | put) : r0;
+    r1 = q == 1u ? ((r1 & keep) | put) : r1;
+    r2 = q == 2u ? ((r2 & keep) | put) : r2;
+    r3 = q == 3u ? ((r3 & keep) | put) : r3;
   }
-  static __device__ __forceinline__ double tin_of(const uint32_t (&r)[4], const S1Ctx& X) {
-    uint32_t m = __vminu4(__vminu4(r[0], r[1]), __vminu4(r[2], r[3]));
+  static __device__ __forceinline__ double tin_of(uint32_t r0, uint32_t r1, uint32_t r2, uint32_t r3, const S1Ctx& X) {
+    uint32_t m = __vminu4(__vminu4(r0, r1), __vminu4(r2, r3));
     m = __vminu4(m, m >> 16);
     m = __vminu4(m, m >> 8) & 0xffu;
     return m == 0xffu ? 0.0 : __ldg(X.vs + m);
@@ -194,10 +198,10 @@ struct S1Reg {
   __device__ __forceinline__ void clear() { cnt = 0ull; mask = 0u; }
   __device__ __forceinline__ void add_init(uint32_t a) { cnt += 1ull << (4u * a); mask |= 1u << a; }
   __device__ __forceinline__ void finish_init(const S1Ctx& X, const RT& R) {
-    rk[0] = rk[1] = rk[2] = rk[3] = 0xffffffffu;
-    for (int a = 0; a < X.n; ++a) set_byte(rk, (uint32_t)a, X.rank[a * 16 + get(cnt, (uint32_t)a)]);
+    rk0 = rk1 = rk2_ = rk3 = 0xffffffffu;
+    for (int a = 0; a < X.n; ++a) set_byte(rk0, rk1, rk2_, rk3, (uint32_t)a, X.rank[a * 16 + get(cnt, (uint32_t)a)]);
     k = __popc(mask);
-    tin = tin_of(rk, X);
+    tin = tin_of(rk0, rk1, rk2_, rk3, X);
     tex = tex_of(mask, k, X);
   }
   // a stage-1 member moves from node dn to node up (tentative state)
@@ -206,17 +210,15 @@ struct S1Reg {
     cnt2 = cnt - (1ull << (4u * dn)) + (1ull << (4u * up));
     mask2 = (mask & (c_dn == 0u ? ~(1u << dn) : 0xffffffffu)) | (1u << up);
     k2 = __popc(mask2);
-#pragma unroll
-    for (int i = 0; i < 4; ++i) rk2[i] = rk[i];
-    set_byte(rk2, dn, X.rank[dn * 16 + c_dn]);
-    set_byte(rk2, up, X.rank[up * 16 + c_up]);
-    tin2 = tin_of(rk2, X);
+    nk0 = rk0; nk1 = rk1; nk2 = rk2_; nk3 = rk3;
+    set_byte(nk0, nk1, nk2, nk3, dn, X.rank[dn * 16 + c_dn]);
+    set_byte(nk0, nk1, nk2, nk3, up, X.rank[up * 16 + c_up]);
+    tin2 = tin_of(nk0, nk1, nk2, nk3, X);
     tex2 = (mask2 == mask) ? tex : tex_of(mask2, k2, X);
   }
   __device__ __forceinline__ void commit() {
     cnt = cnt2; mask = mask2; k = k2; tin = tin2; tex = tex2;
-#pragma unroll
-    for (int i = 0; i < 4; ++i) rk[i] = rk2[i];
+    rk0 = nk0; rk1 = nk1; rk2_ = nk2; rk3 = nk3;
   }
 };
 
@@ -233,7 +235,7 @@ template <class RT>
 struct S1Large {
   uint32_t* c;   // [ceil(n/4)][32] words
   int lane;
-  Mask<4> mask, mask2;
+  Mask4 mask, mask2;
   int k, k2, win, win2, wa, wb, wa2, wb2;
   uint32_t dn_, up_, c_dn_, c_up_;
   double tin, tex, maxR, tin2, tex2, maxR2;
@@ -244,12 +246,7 @@ struct S1Large {
     const uint32_t sh = (a & 3) * 8;
     w = delta > 0 ? w + (1u << sh) : w - (1u << sh);
   }
-  static __device__ __forceinline__ bool in(const Mask<4>& m, uint32_t a) {
-    uint32_t w = m.w[0];
-#pragma unroll
-    for (int i = 1; i < 4; ++i) w = ((a >> 5) == (uint32_t)i) ? m.w[i] : w;
-    return (w >> (a & 31)) & 1u;
-  }
+  static __device__ __forceinline__ bool in(const Mask4& m, uint32_t a) { return m.test(a); }
   // tentative count of node a (after dn -> up)
   __device__ __forceinline__ uint32_t cnt2(uint32_t a) const { return a == dn_ ? c_dn_ : (a == up_ ? c_up_ : get(a)); }
 
@@ -262,18 +259,18 @@ struct S1Large {
     w = -1;
     return 0.0;
   }
-  __device__ __forceinline__ double maxr_members(const Mask<4>& m, const RT& R, int& a_, int& b_) const {
+  __device__ __forceinline__ double maxr_members(const Mask4& m, const RT& R, int& a_, int& b_) const {
     double mx = 0.0;
     a_ = b_ = -1;
 #pragma unroll
     for (int wd = 0; wd < 4; ++wd) {
-      uint32_t bits = m.w[wd];
+      uint32_t bits = m.word(wd);
       while (bits) {
         const uint32_t a = wd * 32 + __ffs(bits) - 1;
         bits &= bits - 1;
 #pragma unroll
         for (int wd2 = 0; wd2 < 4; ++wd2) {
-          uint32_t bits2 = m.w[wd2];
+          uint32_t bits2 = m.word(wd2);
           while (bits2) {
             const uint32_t b = wd2 * 32 + __ffs(bits2) - 1;
             bits2 &= bits2 - 1;
@@ -286,7 +283,7 @@ struct S1Large {
     }
     return mx;
   }
-  __device__ __forceinline__ double maxr_global(const Mask<4>& m, const S1Ctx& X, int& a_, int& b_) const {
+  __device__ __forceinline__ double maxr_global(const Mask4& m, const S1Ctx& X, int& a_, int& b_) const {
     for (int i = 0; i < X.gl_len; ++i) {
       const uint32_t ab = X.gl_ab[i];
       const uint32_t a = ab & 0xffu, b = ab >> 8;
@@ -297,7 +294,7 @@ struct S1Large {
   }
   // recompute from scratch: k(k-1) member pairs, or the global sorted list with an
   // expected (n/k)^2 probes -- whichever is cheaper (k^4 <= 4 n^2)
-  __device__ __forceinline__ double maxr(const Mask<4>& m, int kk, const S1Ctx& X, const RT& R, int& a_, int& b_) const {
+  __device__ __forceinline__ double maxr(const Mask4& m, int kk, const S1Ctx& X, const RT& R, int& a_, int& b_) const {
     if (kk < 2) { a_ = b_ = -1; return 0.0; }
     return kk * kk * kk * kk <= 4 * X.n * X.n ? maxr_members(m, R, a_, b_) : maxr_global(m, X, a_, b_);
   }
@@ -335,7 +332,7 @@ struct S1Large {
     } else if (join && 2 * k2 * k2 <= X.n) {  // few members: both directions to each member
 #pragma unroll
       for (int wd = 0; wd < 4; ++wd) {
-        uint32_t bits = mask2.w[wd];
+        uint32_t bits = mask2.word(wd);
         while (bits) {
           const uint32_t b = wd * 32 + __ffs(bits) - 1;
           bits &= bits - 1;
@@ -374,8 +371,8 @@ __host__ __device__ inline int warp_state_bytes(int N, int pp, int dp, int n, bo
 
 // ------------------------------------------------------------------ one warp task
 template <class POS, class S1, class RT, bool TRACE, int PP>
-__device__ void run_task(const SaParams& P, const SaTask& T, const DevCfg& C, const RT& R, unsigned char* ws,
-                         int lane) {
+__device__ __forceinline__ void run_task(const SaParams& P, const SaTask T, const DevCfg C, const RT R,
+                                         unsigned char* ws, int lane) {
   if (lane >= T.count) return;
   constexpr bool kLargeS1 = !std::is_same<S1, S1Reg<RT>>::value;
   const int N = C.N, pp = PP > 0 ? PP : C.pp, dp = C.dp, n = P.n_nodes;
@@ -558,7 +555,7 @@ __device__ void run_task(const SaParams& P, const SaTask& T, const DevCfg& C, co
 // MODE 1: n <= 128, N <= 256: packed positions, S1Large, R through L1.
 // MODE 2: general (N <= 1024): 32-bit positions, S1Large, R through L1.
 template <int MODE, bool TRACE>
-__global__ void __launch_bounds__(kSaThreads) k_sa_chains(SaParams P) {
+__global__ void __launch_bounds__(kSaThreads, MODE == 0 ? 3 : 2) k_sa_chains(SaParams P) {
   using POS = typename std::conditional<MODE == 2, PosWide, PosPacked>::type;
   using RT = typename std::conditional<MODE == 0, RRep, RGlob>::type;
   using S1 = typename std::conditional<MODE == 0, S1Reg<RT>, S1Large<RT>>::type;
