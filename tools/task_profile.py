@@ -14,6 +14,8 @@ from paper_2405_18093_b200 import Model, Pipette  # noqa: E402
 
 
 def main(name="C2", chains=None, iters=None):
+    chains = int(chains) if chains else None
+    iters = int(iters) if iters else None
     w = W.WORKLOADS[name]
     B, prof = W.workload_inputs(w)
     m = w.model
@@ -43,4 +45,4 @@ def main(name="C2", chains=None, iters=None):
 
 
 if __name__ == "__main__":
-    main(*(sys.argv[1:2] or ["C2"]))
+    main(*(sys.argv[1:4] or ["C2"]))
