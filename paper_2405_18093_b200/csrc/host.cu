@@ -129,6 +129,7 @@ struct pipette_ctx {
 
 namespace {
 
+int align16(int x) { return (x + 15) & ~15; }
 thread_local std::string g_init_err;
 
 const char* kStatusText[] = {"ok", "no feasible configuration (every candidate exceeds the memory limit)",
@@ -561,7 +562,10 @@ pipette_status pipette_search(pipette_ctx* ctx, const pipette_model* model, int6
   std::vector<double> cost(tasks.size());
   for (size_t i = 0; i < tasks.size(); ++i) {
     const DevCfg& c = ctx->hcfg[tasks[i].cfg];
-    cost[i] = c.N < 2 ? 0.0 : (c.pp >= 2 ? 100.0 + 12.0 * (c.pp - 1) + 6.0 * c.dp : 10.0);
+    // per-step work: pipeline re-sums (~pp), plus stage-1 updates with probability
+    // 2(1/pp)(1-1/pp) whose cost grows with the cluster (sorted-list probes)
+    const double pchg = 2.0 * (1.0 / c.pp) * (1.0 - 1.0 / c.pp);
+    cost[i] = c.N < 2 ? 0.0 : (c.pp >= 2 ? 60.0 + 12.0 * (c.pp - 1) + pchg * (40.0 + 4.0 * ctx->n_nodes) : 10.0);
   }
   std::vector<int> order(tasks.size());
   for (size_t i = 0; i < order.size(); ++i) order[i] = (int)i;
@@ -576,7 +580,7 @@ pipette_status pipette_search(pipette_ctx* ctx, const pipette_model* model, int6
   // R through L1.  MODE 2: 32-bit positions (N > 256).
   const int mode = (n <= 16 && maxN <= 256 && ctx->g <= 15 && ctx->dTab) ? 0 : (maxN <= 256 ? 1 : 2);
   const bool rep = mode == 0;
-  const int r_bytes = rep ? nn * 32 * 8 : 0;
+  const int r_bytes = rep ? nn * 32 * 8 : (mode == 1 ? align16(nn * 8) : 0);   // R staged in shared memory
   const int dp_cap = mode == 0 ? (1 << 30) : 32;
   int warp_bytes = 16, tl_stride = 1;
   for (int f = 0; f < F; ++f) {

@@ -43,6 +43,11 @@ struct RRep {
     return s[((int)a * n + (int)b) * 32 + lane];
   }
 };
+struct RSmem {
+  const double* s;
+  int n, lane;
+  __device__ __forceinline__ double operator()(uint32_t a, uint32_t b) const { return s[(int)a * n + (int)b]; }
+};
 struct RGlob {
   const double* s;
   int n, lane;
@@ -283,11 +288,17 @@ struct S1Large {
     }
     return mx;
   }
+  // probes are issued 8 at a time (independent loads, then the sequential test)
   __device__ __forceinline__ double maxr_global(const Mask4& m, const S1Ctx& X, int& a_, int& b_) const {
-    for (int i = 0; i < X.gl_len; ++i) {
-      const uint32_t ab = X.gl_ab[i];
-      const uint32_t a = ab & 0xffu, b = ab >> 8;
-      if (in(m, a) && in(m, b)) { a_ = (int)a; b_ = (int)b; return X.gl_val[i]; }
+    for (int i0 = 0; i0 < X.gl_len; i0 += 8) {
+      uint32_t ab[8];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) ab[j] = i0 + j < X.gl_len ? (uint32_t)__ldg(X.gl_ab + i0 + j) : 0xffffu;
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const uint32_t a = ab[j] & 0xffu, b = ab[j] >> 8;
+        if (i0 + j < X.gl_len && in(m, a) && in(m, b)) { a_ = (int)a; b_ = (int)b; return __ldg(X.gl_val + i0 + j); }
+      }
     }
     a_ = b_ = -1;
     return 0.0;
@@ -344,12 +355,18 @@ struct S1Large {
       }
     } else if (join) {                         // first partner of up inside N1, by R (~n/k probes)
       const uint8_t* nl = X.nl_node + (size_t)up * X.nl_len;
-      for (int i = 0; i < X.nl_len; ++i) {
-        const uint32_t b = nl[i];
-        if (in(mask2, b)) {
-          const double v = X.nl_val[(size_t)up * X.nl_len + i];
-          if (v > maxR2) { maxR2 = v; wa2 = (int)up; wb2 = (int)b; }
-          break;
+      bool found = false;
+      for (int i0 = 0; i0 < X.nl_len && !found; i0 += 8) {
+        uint32_t bb[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) bb[j] = i0 + j < X.nl_len ? (uint32_t)__ldg(nl + i0 + j) : 0u;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          if (!found && i0 + j < X.nl_len && in(mask2, bb[j])) {
+            found = true;
+            const double v = __ldg(X.nl_val + (size_t)up * X.nl_len + i0 + j);
+            if (v > maxR2) { maxR2 = v; wa2 = (int)up; wb2 = (int)bb[j]; }
+          }
         }
       }
     }
@@ -557,17 +574,19 @@ __device__ __forceinline__ void run_task(const SaParams& P, const SaTask T, cons
 template <int MODE, bool TRACE>
 __global__ void __launch_bounds__(kSaThreads, MODE == 0 ? 3 : 2) k_sa_chains(SaParams P) {
   using POS = typename std::conditional<MODE == 2, PosWide, PosPacked>::type;
-  using RT = typename std::conditional<MODE == 0, RRep, RGlob>::type;
+  using RT = typename std::conditional<MODE == 0, RRep, typename std::conditional<MODE == 1, RSmem, RGlob>::type>::type;
   using S1 = typename std::conditional<MODE == 0, S1Reg<RT>, S1Large<RT>>::type;
   extern __shared__ __align__(16) unsigned char smem[];
   double* Rs = reinterpret_cast<double*>(smem);
   const int nn = P.n_nodes * P.n_nodes;
   if (MODE == 0) {
     for (int i = threadIdx.x; i < nn * 32; i += blockDim.x) Rs[i] = P.R[i >> 5];
-    __syncthreads();
+  } else if (MODE == 1) {
+    for (int i = threadIdx.x; i < nn; i += blockDim.x) Rs[i] = P.R[i];
   }
+  __syncthreads();
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
-  const RT R{MODE == 0 ? Rs : P.R, P.n_nodes, lane};
+  const RT R{MODE <= 1 ? Rs : P.R, P.n_nodes, lane};
   unsigned char* ws = smem + P.r_smem_bytes + wid * P.warp_smem_bytes;
   __shared__ int s_base;
   for (;;) {
