@@ -221,6 +221,8 @@ struct S1Reg {
     tin2 = tin_of(nk0, nk1, nk2, nk3, X);
     tex2 = (mask2 == mask) ? tex : tex_of(mask2, k2, X);
   }
+  __device__ __forceinline__ void coop(const S1Ctx&, const RT&) {}
+  __device__ __forceinline__ void finish(const S1Ctx&) {}
   __device__ __forceinline__ void commit() {
     cnt = cnt2; mask = mask2; k = k2; tin = tin2; tex = tex2;
     rk0 = nk0; rk1 = nk1; rk2_ = nk2; rk3 = nk3;
@@ -231,11 +233,15 @@ struct S1Reg {
 // 128-bit node mask N1 in registers, witnesses for both max terms of Eq.6 and sorted
 // tables instead of scans:
 //   T_in: witness node; when it loses a member, the config's (a, c) list sorted by
-//         qi(c) R[a][a] is scanned for the first entry whose node has exactly c members.
-//   T_ex: witness pair {wa, wb}; a node joining N1 scans its own pair list (sorted by R)
+//         qi(c) R[a][a] is searched for the first entry whose node has exactly c members.
+//   T_ex: witness pair {wa, wb}; a node joining N1 searches its own pair list (sorted by R)
 //         for the first partner in N1 (expected n/k probes); the witness leaving
-//         recomputes over member pairs (k <= 16) or scans the global sorted pair list for
-//         the first pair inside N1 (expected (n/k)^2 probes).
+//         recomputes the max over member pairs (small k) or searches the global sorted
+//         pair list for the first pair inside N1 (expected (n/k)^2 probes).
+// The three searches are rare per chain but long, so they are done warp-cooperatively:
+// propose() only flags them; coop() (all 32 lanes converged) serves each flagged lane
+// with the whole warp probing 32 entries per round (ballot picks the first hit), or
+// splitting the member rows over the lanes (shuffle max-reduction).
 template <class RT>
 struct S1Large {
   uint32_t* c;   // [ceil(n/4)][32] words
@@ -243,72 +249,36 @@ struct S1Large {
   Mask4 mask, mask2;
   int k, k2, win, win2, wa, wb, wa2, wb2;
   uint32_t dn_, up_, c_dn_, c_up_;
+  bool need_tin, need_maxr, need_join;
   double tin, tex, maxR, tin2, tex2, maxR2;
 
   __device__ __forceinline__ uint32_t get(uint32_t a) const { return (c[(a >> 2) * 32 + lane] >> ((a & 3) * 8)) & 0xffu; }
+  __device__ __forceinline__ uint32_t get_of(uint32_t a, int L) const { return (c[(a >> 2) * 32 + L] >> ((a & 3) * 8)) & 0xffu; }
   __device__ __forceinline__ void add(uint32_t a, int delta) {
     uint32_t& w = c[(a >> 2) * 32 + lane];
     const uint32_t sh = (a & 3) * 8;
     w = delta > 0 ? w + (1u << sh) : w - (1u << sh);
   }
   static __device__ __forceinline__ bool in(const Mask4& m, uint32_t a) { return m.test(a); }
-  // tentative count of node a (after dn -> up)
-  __device__ __forceinline__ uint32_t cnt2(uint32_t a) const { return a == dn_ ? c_dn_ : (a == up_ ? c_up_ : get(a)); }
 
-  __device__ __forceinline__ double tin_scan(const S1Ctx& X, bool tentative, int& w) const {
+  // ---- per-lane versions (initial state only)
+  __device__ __forceinline__ double tin_scan_own(const S1Ctx& X, int& w) const {
     for (int i = 0; i < X.tl_len; ++i) {
       const uint32_t ac = X.tl_ac[i];
-      const uint32_t a = ac & 0xffu, cc = ac >> 8;
-      if ((tentative ? cnt2(a) : get(a)) == cc) { w = (int)a; return X.tl_val[i]; }
+      if (get(ac & 0xffu) == (ac >> 8)) { w = (int)(ac & 0xffu); return X.tl_val[i]; }
     }
     w = -1;
     return 0.0;
   }
-  __device__ __forceinline__ double maxr_members(const Mask4& m, const RT& R, int& a_, int& b_) const {
-    double mx = 0.0;
-    a_ = b_ = -1;
-#pragma unroll
-    for (int wd = 0; wd < 4; ++wd) {
-      uint32_t bits = m.word(wd);
-      while (bits) {
-        const uint32_t a = wd * 32 + __ffs(bits) - 1;
-        bits &= bits - 1;
-#pragma unroll
-        for (int wd2 = 0; wd2 < 4; ++wd2) {
-          uint32_t bits2 = m.word(wd2);
-          while (bits2) {
-            const uint32_t b = wd2 * 32 + __ffs(bits2) - 1;
-            bits2 &= bits2 - 1;
-            if (a == b) continue;
-            const double v = R(a, b);
-            if (v > mx) { mx = v; a_ = (int)a; b_ = (int)b; }
-          }
-        }
-      }
-    }
-    return mx;
-  }
-  // probes are issued 8 at a time (independent loads, then the sequential test)
-  __device__ __forceinline__ double maxr_global(const Mask4& m, const S1Ctx& X, int& a_, int& b_) const {
-    for (int i0 = 0; i0 < X.gl_len; i0 += 8) {
-      uint32_t ab[8];
-#pragma unroll
-      for (int j = 0; j < 8; ++j) ab[j] = i0 + j < X.gl_len ? (uint32_t)__ldg(X.gl_ab + i0 + j) : 0xffffu;
-#pragma unroll
-      for (int j = 0; j < 8; ++j) {
-        const uint32_t a = ab[j] & 0xffu, b = ab[j] >> 8;
-        if (i0 + j < X.gl_len && in(m, a) && in(m, b)) { a_ = (int)a; b_ = (int)b; return __ldg(X.gl_val + i0 + j); }
-      }
+  __device__ __forceinline__ double maxr_global_own(const Mask4& m, const S1Ctx& X, int& a_, int& b_) const {
+    for (int i = 0; i < X.gl_len; ++i) {
+      const uint32_t ab = X.gl_ab[i];
+      if (in(m, ab & 0xffu) && in(m, ab >> 8)) { a_ = (int)(ab & 0xffu); b_ = (int)(ab >> 8); return X.gl_val[i]; }
     }
     a_ = b_ = -1;
     return 0.0;
   }
-  // recompute from scratch: k(k-1) member pairs, or the global sorted list with an
-  // expected (n/k)^2 probes -- whichever is cheaper (k^4 <= 4 n^2)
-  __device__ __forceinline__ double maxr(const Mask4& m, int kk, const S1Ctx& X, const RT& R, int& a_, int& b_) const {
-    if (kk < 2) { a_ = b_ = -1; return 0.0; }
-    return kk * kk * kk * kk <= 4 * X.n * X.n ? maxr_members(m, R, a_, b_) : maxr_global(m, X, a_, b_);
-  }
+
   __device__ __forceinline__ void clear(int n) {
     for (int wd = 0; wd < (n + 3) / 4; ++wd) c[wd * 32 + lane] = 0u;
     mask.clear();
@@ -316,10 +286,13 @@ struct S1Large {
   __device__ __forceinline__ void add_init(uint32_t a) { add(a, +1); mask.set(a); }
   __device__ __forceinline__ void finish_init(const S1Ctx& X, const RT& R) {
     k = mask.count();
-    tin = tin_scan(X, false, win);
-    maxR = maxr(mask, k, X, R, wa, wb);
+    tin = tin_scan_own(X, win);
+    maxR = k >= 2 ? maxr_global_own(mask, X, wa, wb) : 0.0;
+    if (k < 2) wa = wb = -1;
     tex = k >= 2 ? __dmul_rn(__ldg(X.qe + k), maxR) : 0.0;
+    need_tin = need_maxr = need_join = false;
   }
+  // a stage-1 member moves from node dn to node up (tentative); long searches are flagged
   __device__ __forceinline__ void propose(uint32_t dn, uint32_t up, const S1Ctx& X, const RT& R) {
     dn_ = dn; up_ = up;
     c_dn_ = get(dn) - 1u; c_up_ = get(up) + 1u;
@@ -330,7 +303,7 @@ struct S1Large {
     k2 = k - (int)leave + (int)join;
     tin2 = tin; win2 = win;
     if ((int)dn == win) {
-      tin2 = tin_scan(X, true, win2);
+      need_tin = true;
     } else if (c_up_ >= 2u) {
       const double v = __dmul_rn(__ldg(X.qi + c_up_), R(up, up));
       if (v > tin2) { tin2 = v; win2 = (int)up; }
@@ -339,46 +312,112 @@ struct S1Large {
     if (k2 < 2) {
       maxR2 = 0.0; wa2 = wb2 = -1;
     } else if (leave && ((int)dn == wa || (int)dn == wb)) {
-      maxR2 = maxr(mask2, k2, X, R, wa2, wb2);
-    } else if (join && 2 * k2 * k2 <= X.n) {  // few members: both directions to each member
-#pragma unroll
-      for (int wd = 0; wd < 4; ++wd) {
-        uint32_t bits = mask2.word(wd);
-        while (bits) {
-          const uint32_t b = wd * 32 + __ffs(bits) - 1;
-          bits &= bits - 1;
-          if (b == up) continue;
-          const double v1 = R(up, b), v2 = R(b, up);
-          if (v1 > maxR2) { maxR2 = v1; wa2 = (int)up; wb2 = (int)b; }
-          if (v2 > maxR2) { maxR2 = v2; wa2 = (int)b; wb2 = (int)up; }
-        }
+      need_maxr = true;
+    } else if (join) {
+      need_join = true;
+    }
+  }
+
+  // ---- warp-cooperative searches (called by all 32 lanes, converged)
+  // first index >= 0 in [0, len) with hit(i); the warp probes 32 entries per round
+  template <class F>
+  static __device__ __forceinline__ int coop_first(int len, F hit) {
+    const int ln = threadIdx.x & 31;
+    for (int base = 0; base < len; base += 32) {
+      const int i = base + ln;
+      const unsigned b = __ballot_sync(0xffffffffu, i < len && hit(i));
+      if (b) return base + __ffs(b) - 1;
+    }
+    return -1;
+  }
+  __device__ __forceinline__ void coop(const S1Ctx& X, const RT& R) {
+    const unsigned full = 0xffffffffu;
+    // T_in: first (a, c) entry (by value) whose node has c members after the move
+    unsigned todo = __ballot_sync(full, need_tin);
+    while (todo) {
+      const int L = __ffs(todo) - 1;
+      todo &= todo - 1;
+      const uint32_t dnL = __shfl_sync(full, dn_, L), upL = __shfl_sync(full, up_, L);
+      const uint32_t cdL = __shfl_sync(full, c_dn_, L), cuL = __shfl_sync(full, c_up_, L);
+      const int i = coop_first(X.tl_len, [&](int j) {
+        const uint32_t ac = X.tl_ac[j], a = ac & 0xffu;
+        const uint32_t cnt = a == dnL ? cdL : (a == upL ? cuL : get_of(a, L));
+        return cnt == (ac >> 8);
+      });
+      if (lane == L) {
+        need_tin = false;
+        if (i >= 0) { tin2 = X.tl_val[i]; win2 = (int)(X.tl_ac[i] & 0xffu); } else { tin2 = 0.0; win2 = -1; }
       }
-    } else if (join) {                         // first partner of up inside N1, by R (~n/k probes)
-      const uint8_t* nl = X.nl_node + (size_t)up * X.nl_len;
-      bool found = false;
-      for (int i0 = 0; i0 < X.nl_len && !found; i0 += 8) {
-        uint32_t bb[8];
-#pragma unroll
-        for (int j = 0; j < 8; ++j) bb[j] = i0 + j < X.nl_len ? (uint32_t)__ldg(nl + i0 + j) : 0u;
-#pragma unroll
-        for (int j = 0; j < 8; ++j) {
-          if (!found && i0 + j < X.nl_len && in(mask2, bb[j])) {
-            found = true;
-            const double v = __ldg(X.nl_val + (size_t)up * X.nl_len + i0 + j);
-            if (v > maxR2) { maxR2 = v; wa2 = (int)up; wb2 = (int)bb[j]; }
-          }
+    }
+    // T_ex, join: first partner (by R) of the joining node inside N1
+    todo = __ballot_sync(full, need_join);
+    while (todo) {
+      const int L = __ffs(todo) - 1;
+      todo &= todo - 1;
+      const uint32_t upL = __shfl_sync(full, up_, L);
+      Mask4 m;
+      m.w0 = __shfl_sync(full, mask2.w0, L); m.w1 = __shfl_sync(full, mask2.w1, L);
+      m.w2 = __shfl_sync(full, mask2.w2, L); m.w3 = __shfl_sync(full, mask2.w3, L);
+      const uint8_t* nl = X.nl_node + (size_t)upL * X.nl_len;
+      const int i = coop_first(X.nl_len, [&](int j) { return in(m, nl[j]); });
+      if (lane == L) {
+        need_join = false;
+        if (i >= 0) {
+          const double v = X.nl_val[(size_t)upL * X.nl_len + i];
+          if (v > maxR2) { maxR2 = v; wa2 = (int)upL; wb2 = (int)nl[i]; }
         }
       }
     }
-    tex2 = k2 >= 2 ? __dmul_rn(__ldg(X.qe + k2), maxR2) : 0.0;
+    // T_ex, the witness left: recompute the slowest link of N1
+    todo = __ballot_sync(full, need_maxr);
+    while (todo) {
+      const int L = __ffs(todo) - 1;
+      todo &= todo - 1;
+      Mask4 m;
+      m.w0 = __shfl_sync(full, mask2.w0, L); m.w1 = __shfl_sync(full, mask2.w1, L);
+      m.w2 = __shfl_sync(full, mask2.w2, L); m.w3 = __shfl_sync(full, mask2.w3, L);
+      const int kL = __shfl_sync(full, k2, L);
+      double mx = 0.0;
+      int a_ = -1, b_ = -1;
+      if (kL * kL * kL * kL <= 4 * X.n * X.n) {
+        // member rows split over the lanes: lane j takes nodes j, j+32, ... in N1
+        for (int a = lane; a < X.n; a += 32) {
+          if (!in(m, (uint32_t)a)) continue;
+#pragma unroll
+          for (int wd = 0; wd < 4; ++wd) {
+            uint32_t bits = m.word(wd);
+            while (bits) {
+              const int b = wd * 32 + __ffs(bits) - 1;
+              bits &= bits - 1;
+              if (b == a) continue;
+              const double v = R((uint32_t)a, (uint32_t)b);
+              if (v > mx) { mx = v; a_ = a; b_ = b; }
+            }
+          }
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {   // max-reduce (any witness of an equal max is fine)
+          const double v2 = __shfl_xor_sync(full, mx, o);
+          const int a2 = __shfl_xor_sync(full, a_, o), b2 = __shfl_xor_sync(full, b_, o);
+          if (v2 > mx) { mx = v2; a_ = a2; b_ = b2; }
+        }
+      } else {
+        const int i = coop_first(X.gl_len, [&](int j) {
+          const uint32_t ab = X.gl_ab[j];
+          return in(m, ab & 0xffu) && in(m, ab >> 8);
+        });
+        if (i >= 0) { mx = X.gl_val[i]; a_ = X.gl_ab[i] & 0xff; b_ = X.gl_ab[i] >> 8; }
+      }
+      if (lane == L) { need_maxr = false; maxR2 = mx; wa2 = a_; wb2 = b_; }
+    }
   }
+  __device__ __forceinline__ void finish(const S1Ctx& X) { tex2 = k2 >= 2 ? __dmul_rn(__ldg(X.qe + k2), maxR2) : 0.0; }
   __device__ __forceinline__ void commit() {
     add(dn_, -1); add(up_, +1);
     mask = mask2; k = k2; tin = tin2; win = win2; tex = tex2; maxR = maxR2; wa = wa2; wb = wb2;
   }
 };
 
-// Shared-memory footprint of one warp's chain state for a configuration.
 // psum cached in shared memory when pp >= 2 and dp <= dp_cap.
 template <class POS>
 __host__ __device__ inline int warp_state_bytes(int N, int pp, int dp, int n, bool s1smem, int dp_cap) {
@@ -390,7 +429,9 @@ __host__ __device__ inline int warp_state_bytes(int N, int pp, int dp, int n, bo
 template <class POS, class S1, class RT, bool TRACE, int PP>
 __device__ __forceinline__ void run_task(const SaParams& P, const SaTask T, const DevCfg C, const RT R,
                                          unsigned char* ws, int lane) {
-  if (lane >= T.count) return;
+  // lanes past the task's chain count run a throw-away chain (their outputs are never
+  // written) so that the warp stays converged for the cooperative searches
+  const bool active = lane < T.count;
   constexpr bool kLargeS1 = !std::is_same<S1, S1Reg<RT>>::value;
   const int N = C.N, pp = PP > 0 ? PP : C.pp, dp = C.dp, n = P.n_nodes;
   const uint32_t chain = (uint32_t)(T.c_first + (T.k0 + lane) * P.world);
@@ -441,7 +482,7 @@ __device__ __forceinline__ void run_task(const SaParams& P, const SaTask T, cons
   uint32_t accepted = 0;
   double beta = P.t0 > 0.0 ? __ddiv_rn(1.0, P.t0) : __ddiv_rn(1.0, __dmul_rn(P.tau, L0));
   const double ia = P.alpha_inv;
-  const int trow = TRACE ? P.trace_slot[slot] : -1;
+  const int trow = (TRACE && active) ? P.trace_slot[slot] : -1;
 
   if (N >= 2) {
     Draw dnext = draw_swap_rk(0u, chain, (uint32_t)C.e, P.rk, (uint32_t)N);
@@ -454,13 +495,14 @@ __device__ __forceinline__ void run_task(const SaParams& P, const SaTask T, cons
       double Lp = cur;
       bool acc = true;
       bool improved = false;
-      if (np != nq) {
+      const bool evald = np != nq;
+      uint32_t xp = 0, xq = 0;
+      int zp = 0, zq = 0;
+      bool two = false, dpchg = false;
+      double sA = 0.0, sB = 0.0, tpp2 = tpp;
+      int nmax2 = nmax;
+      if (evald) {
         // ---- Eq.5: re-sum the (at most two) touched pipelines, maintain the max
-        uint32_t xp = 0, xq = 0;
-        int zp = 0, zq = 0;
-        bool two = false;
-        double sA = 0.0, sB = 0.0, tpp2 = tpp;
-        int nmax2 = nmax;
         if (pp >= 2) {
           zp = (int)div_small(d.p, C.pp_magic, (uint32_t)pp);
           zq = (int)div_small(d.q, C.pp_magic, (uint32_t)pp);
@@ -516,12 +558,18 @@ __device__ __forceinline__ void run_task(const SaParams& P, const SaTask T, cons
           }
         }
         // ---- Eq.6: the stage-1 node multiset changes only if exactly one of p, q is stage 1
-        const bool dpchg = (xp == 0u) != (xq == 0u);
-        double tin2 = s1.tin, tex2 = s1.tex;
+        dpchg = (xp == 0u) != (xq == 0u);
         if (dpchg) {
           const uint32_t dn = xp == 0u ? np : nq;   // node losing a stage-1 DP member
           const uint32_t up = xp == 0u ? nq : np;   // node gaining one
           s1.propose(dn, up, X, R);
+        }
+      }
+      s1.coop(X, R);   // warp-converged: long stage-1 searches of any lane, done cooperatively
+      if (evald) {
+        double tin2 = s1.tin, tex2 = s1.tex;
+        if (dpchg) {
+          s1.finish(X);
           tin2 = s1.tin2;
           tex2 = s1.tex2;
         }
@@ -561,10 +609,12 @@ __device__ __forceinline__ void run_task(const SaParams& P, const SaTask T, cons
       beta = __dmul_rn(beta, ia);
     }
   }
-  ChainOut o;
-  o.best = best; o.best_tpp = best_tpp; o.best_tdp = best_tdp; o.L0 = L0;
-  o.best_step = best_step; o.accepted = accepted; o.f = T.f; o.c = (int32_t)chain;
-  P.out[slot] = o;
+  if (active) {
+    ChainOut o;
+    o.best = best; o.best_tpp = best_tpp; o.best_tdp = best_tdp; o.L0 = L0;
+    o.best_step = best_step; o.accepted = accepted; o.f = T.f; o.c = (int32_t)chain;
+    P.out[slot] = o;
+  }
 }
 
 // MODE 0: n <= 16 nodes, N <= 256, spn <= 15: packed positions, register stage-1 state,
