@@ -529,24 +529,26 @@ __device__ __forceinline__ void run_task(const SaParams& P, const SaTask T, cons
             tpp2 = (keep > 0) ? fmax(tpp, snew) : snew;
             nmax2 = (keep > 0 && tpp2 == tpp ? keep : 0) + (sA == tpp2 ? 1 : 0) + ((two && sB == tpp2) ? 1 : 0);
           } else if (cache) {
-            // the unique max pipeline decreased: rescan (4 independent max chains)
-            double m0 = snew, m1 = 0.0, m2 = 0.0, m3 = 0.0;
+            // the unique max pipeline decreased: rescan for the max and its multiplicity in
+            // one pass (two independent (max, count) accumulators)
+            double m0 = sA, m1 = two ? sB : 0.0;
+            int c0 = 1, c1 = two ? 1 : 0;
             int z = 0;
-            for (; z + 4 <= dp; z += 4) {
-              const double v0 = psum[(z + 0) * 32 + lane], v1 = psum[(z + 1) * 32 + lane];
-              const double v2 = psum[(z + 2) * 32 + lane], v3 = psum[(z + 3) * 32 + lane];
-              m0 = fmax(m0, (z + 0 == zp || z + 0 == zq) ? 0.0 : v0);
-              m1 = fmax(m1, (z + 1 == zp || z + 1 == zq) ? 0.0 : v1);
-              m2 = fmax(m2, (z + 2 == zp || z + 2 == zq) ? 0.0 : v2);
-              m3 = fmax(m3, (z + 3 == zp || z + 3 == zq) ? 0.0 : v3);
+            for (; z + 2 <= dp; z += 2) {
+              const double v0 = (z == zp || z == zq) ? 0.0 : psum[z * 32 + lane];
+              const double v1 = (z + 1 == zp || z + 1 == zq) ? 0.0 : psum[(z + 1) * 32 + lane];
+              c0 = v0 > m0 ? 1 : c0 + (v0 == m0 ? 1 : 0);
+              m0 = fmax(m0, v0);
+              c1 = v1 > m1 ? 1 : c1 + (v1 == m1 ? 1 : 0);
+              m1 = fmax(m1, v1);
             }
-            for (; z < dp; ++z) m0 = fmax(m0, (z == zp || z == zq) ? 0.0 : psum[z * 32 + lane]);
-            tpp2 = fmax(fmax(m0, m1), fmax(m2, m3));
-            nmax2 = 0;
-            for (z = 0; z < dp; ++z) {
-              const double v = (z == zp) ? sA : ((z == zq) ? sB : psum[z * 32 + lane]);
-              nmax2 += v == tpp2 ? 1 : 0;
+            if (z < dp) {
+              const double v0 = (z == zp || z == zq) ? 0.0 : psum[z * 32 + lane];
+              c0 = v0 > m0 ? 1 : c0 + (v0 == m0 ? 1 : 0);
+              m0 = fmax(m0, v0);
             }
+            tpp2 = fmax(m0, m1);
+            nmax2 = (m0 == tpp2 ? c0 : 0) + (m1 == tpp2 ? c1 : 0);
           } else {
             // no cache: re-sum every pipeline of the tentative mapping
             tpp2 = 0.0;
@@ -622,7 +624,7 @@ __device__ __forceinline__ void run_task(const SaParams& P, const SaTask T, cons
 // MODE 1: n <= 128, N <= 256: packed positions, S1Large, R through L1.
 // MODE 2: general (N <= 1024): 32-bit positions, S1Large, R through L1.
 template <int MODE, bool TRACE>
-__global__ void __launch_bounds__(kSaThreads, MODE == 0 ? 3 : 2) k_sa_chains(SaParams P) {
+__global__ void __launch_bounds__(kSaThreads, MODE == 0 ? 4 : 2) k_sa_chains(SaParams P) {
   using POS = typename std::conditional<MODE == 2, PosWide, PosPacked>::type;
   using RT = typename std::conditional<MODE == 0, RRep, typename std::conditional<MODE == 1, RSmem, RGlob>::type>::type;
   using S1 = typename std::conditional<MODE == 0, S1Reg<RT>, S1Large<RT>>::type;
