@@ -6,6 +6,7 @@
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -581,7 +582,8 @@ pipette_status pipette_search(pipette_ctx* ctx, const pipette_model* model, int6
   const int mode = (n <= 16 && maxN <= 256 && ctx->g <= 15 && ctx->dTab) ? 0 : (maxN <= 256 ? 1 : 2);
   const bool rep = mode == 0;
   const int r_bytes = rep ? nn * 32 * 8 : (mode == 1 ? align16(nn * 8) : 0);   // R staged in shared memory
-  const int dp_cap = mode == 0 ? 16 : 32;   // psum cached in shared memory when dp <= dp_cap
+  int dp_cap = mode == 0 ? 64 : 32;   // psum cached in shared memory when dp <= dp_cap
+  if (const char* e = getenv("PIPETTE_DP_CAP")) dp_cap = atoi(e);   // tuning knob
   int warp_bytes = 16, tl_stride = 1;
   for (int f = 0; f < F; ++f) {
     const DevCfg& c = ctx->hcfg[ctx->hfeas[f]];

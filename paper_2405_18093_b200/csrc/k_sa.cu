@@ -624,7 +624,7 @@ __device__ __forceinline__ void run_task(const SaParams& P, const SaTask T, cons
 // MODE 1: n <= 128, N <= 256: packed positions, S1Large, R through L1.
 // MODE 2: general (N <= 1024): 32-bit positions, S1Large, R through L1.
 template <int MODE, bool TRACE>
-__global__ void __launch_bounds__(kSaThreads, MODE == 0 ? 4 : 2) k_sa_chains(SaParams P) {
+__global__ void __launch_bounds__(kSaThreads, MODE == 0 ? 3 : 2) k_sa_chains(SaParams P) {
   using POS = typename std::conditional<MODE == 2, PosWide, PosPacked>::type;
   using RT = typename std::conditional<MODE == 0, RRep, typename std::conditional<MODE == 1, RSmem, RGlob>::type>::type;
   using S1 = typename std::conditional<MODE == 0, S1Reg<RT>, S1Large<RT>>::type;
