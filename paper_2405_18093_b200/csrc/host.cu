@@ -581,14 +581,31 @@ pipette_status pipette_search(pipette_ctx* ctx, const pipette_model* model, int6
   // R through L1.  MODE 2: 32-bit positions (N > 256).
   const int mode = (n <= 16 && maxN <= 256 && ctx->g <= 15 && ctx->dTab) ? 0 : (maxN <= 256 ? 1 : 2);
   const bool rep = mode == 0;
-  const int r_bytes = rep ? nn * 32 * 8 : (mode == 1 ? align16(nn * 8) : 0);   // R staged in shared memory
-  int dp_cap = mode == 0 ? 64 : 32;   // psum cached in shared memory when dp <= dp_cap
-  if (const char* e = getenv("PIPETTE_DP_CAP")) dp_cap = atoi(e);   // tuning knob
-  int warp_bytes = 16, tl_stride = 1;
-  for (int f = 0; f < F; ++f) {
-    const DevCfg& c = ctx->hcfg[ctx->hfeas[f]];
-    warp_bytes = std::max(warp_bytes, sa_warp_state_bytes(mode, c.N, c.pp, c.dp, n, dp_cap));
-    tl_stride = std::max(tl_stride, n * (std::min(c.spn, c.dp) - 1));
+  const int r_bytes = rep ? nn * 16 * 8 : (mode == 1 ? align16(nn * 8) : 0);   // R staged in shared memory
+  // psum (Eq.5 sums) cached in shared memory for configs with dp <= dp_cap: the largest cap
+  // that still reaches the best achievable number of resident blocks per SM
+  auto warp_bytes_for = [&](int cap, int& tls) {
+    int wb = 16;
+    tls = 1;
+    for (int f = 0; f < F; ++f) {
+      const DevCfg& c = ctx->hcfg[ctx->hfeas[f]];
+      wb = std::max(wb, sa_warp_state_bytes(mode, c.N, c.pp, c.dp, n, cap));
+      tls = std::max(tls, n * (std::min(c.spn, c.dp) - 1));
+    }
+    return wb;
+  };
+  const int reg_blocks = mode == 0 ? 3 : 2;   // the kernels' __launch_bounds__
+  auto blocks_for = [&](int wb) { return std::min(reg_blocks, (227 * 1024) / std::max(1, r_bytes + 4 * wb)); };
+  int dp_cap = 0, warp_bytes = 16, tl_stride = 1, best_blocks = -1;
+  for (int cap : {1024, 64, 32, 16, 8, 4, 2}) {
+    int tls;
+    const int wb = warp_bytes_for(cap, tls);
+    const int b = blocks_for(wb);
+    if (b > best_blocks) { best_blocks = b; dp_cap = cap; warp_bytes = wb; tl_stride = tls; }
+  }
+  if (const char* e = getenv("PIPETTE_DP_CAP")) {   // tuning knob
+    dp_cap = atoi(e);
+    warp_bytes = warp_bytes_for(dp_cap, tl_stride);
   }
   int wpb = kSaThreads / 32;
   const int smem_max = 227 * 1024;

@@ -33,14 +33,15 @@ constexpr int kSaThreads = 128;
 
 __host__ __device__ __forceinline__ int align16(int x) { return (x + 15) & ~15; }
 
-// R = 1/B lookups.  RRep: lane-replicated copy in shared memory (conflict free, n <= 16).
+// R = 1/B lookups.  RRep: 16 copies in shared memory, copy (lane & 15): a 64-bit shared load
+// is served per half-warp, so 16 copies are already conflict free (n <= 16).
 // RGlob: the n x n table in global memory through the read-only path (L1-resident; for
 // large clusters the table would not leave room in shared memory for chain state).
 struct RRep {
   const double* s;
   int n, lane;
   __device__ __forceinline__ double operator()(uint32_t a, uint32_t b) const {
-    return s[((int)a * n + (int)b) * 32 + lane];
+    return s[((int)a * n + (int)b) * 16 + (lane & 15)];
   }
 };
 struct RSmem {
@@ -632,7 +633,7 @@ __global__ void __launch_bounds__(kSaThreads, MODE == 0 ? 3 : 2) k_sa_chains(SaP
   double* Rs = reinterpret_cast<double*>(smem);
   const int nn = P.n_nodes * P.n_nodes;
   if (MODE == 0) {
-    for (int i = threadIdx.x; i < nn * 32; i += blockDim.x) Rs[i] = P.R[i >> 5];
+    for (int i = threadIdx.x; i < nn * 16; i += blockDim.x) Rs[i] = P.R[i >> 4];
   } else if (MODE == 1) {
     for (int i = threadIdx.x; i < nn; i += blockDim.x) Rs[i] = P.R[i];
   }
