@@ -581,7 +581,9 @@ pipette_status pipette_search(pipette_ctx* ctx, const pipette_model* model, int6
   // R through L1.  MODE 2: 32-bit positions (N > 256).
   const int mode = (n <= 16 && maxN <= 256 && ctx->g <= 15 && ctx->dTab) ? 0 : (maxN <= 256 ? 1 : 2);
   const bool rep = mode == 0;
-  const int r_bytes = rep ? nn * 16 * 8 : (mode == 1 ? align16(nn * 8) : 0);   // R staged in shared memory
+  // MODE 0 replicates R in shared memory: 32 copies for n <= 8, else 16
+  const int r_copies_log2 = (mode == 0 && n <= 8) ? 5 : 4;
+  const int r_bytes = rep ? (nn << r_copies_log2) * 8 : (mode == 1 ? align16(nn * 8) : 0);
   // psum (Eq.5 sums) cached in shared memory for configs with dp <= dp_cap: the largest cap
   // that still reaches the best achievable number of resident blocks per SM
   auto warp_bytes_for = [&](int cap, int& tls) {
@@ -697,6 +699,7 @@ pipette_status pipette_search(pipette_ctx* ctx, const pipette_model* model, int6
   P.warps_per_block = wpb;
   P.warp_smem_bytes = warp_bytes;
   P.r_smem_bytes = r_bytes;
+  P.r_copies_log2 = r_copies_log2;
   P.out = (ChainOut*)ctx->chain_out.p;
   P.best_perm = (uint16_t*)ctx->best_perm.p;
   P.task_prof = (unsigned long long*)ctx->task_prof.p;

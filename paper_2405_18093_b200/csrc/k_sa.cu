@@ -39,9 +39,10 @@ __host__ __device__ __forceinline__ int align16(int x) { return (x + 15) & ~15; 
 // large clusters the table would not leave room in shared memory for chain state).
 struct RRep {
   const double* s;
-  int n, lane;
+  int n, lane;   // lane = this lane's copy index (lane & (copies - 1)); copies = 1 << cshift
+  int cshift;
   __device__ __forceinline__ double operator()(uint32_t a, uint32_t b) const {
-    return s[((int)a * n + (int)b) * 16 + (lane & 15)];
+    return s[(((int)a * n + (int)b) << cshift) + lane];
   }
 };
 struct RSmem {
@@ -633,13 +634,18 @@ __global__ void __launch_bounds__(kSaThreads, MODE == 0 ? 3 : 2) k_sa_chains(SaP
   double* Rs = reinterpret_cast<double*>(smem);
   const int nn = P.n_nodes * P.n_nodes;
   if (MODE == 0) {
-    for (int i = threadIdx.x; i < nn * 16; i += blockDim.x) Rs[i] = P.R[i >> 4];
+    for (int i = threadIdx.x; i < (nn << P.r_copies_log2); i += blockDim.x) Rs[i] = P.R[i >> P.r_copies_log2];
   } else if (MODE == 1) {
     for (int i = threadIdx.x; i < nn; i += blockDim.x) Rs[i] = P.R[i];
   }
   __syncthreads();
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
-  const RT R{MODE <= 1 ? Rs : P.R, P.n_nodes, lane};
+  RT R;
+  if constexpr (MODE == 0) {
+    R = RT{Rs, P.n_nodes, lane & ((1 << P.r_copies_log2) - 1), P.r_copies_log2};
+  } else {
+    R = RT{MODE == 1 ? Rs : P.R, P.n_nodes, lane};
+  }
   unsigned char* ws = smem + P.r_smem_bytes + wid * P.warp_smem_bytes;
   __shared__ int s_base;
   for (;;) {

@@ -82,6 +82,7 @@ struct SaParams {
   int32_t world;             // chain ids c = c_first + k*world
   double alpha_inv, tau, t0;
   int32_t rep;               // R replicated per lane in shared memory
+  int32_t r_copies_log2;     // MODE 0: 32 or 16 copies of R (16 suffice: 64-bit loads go per half-warp)
   int32_t warps_per_block;
   int32_t warp_smem_bytes;   // per-warp chain-state region
   int32_t r_smem_bytes;
