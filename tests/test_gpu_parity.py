@@ -319,3 +319,35 @@ def test_search_mode2_wide_positions():
     w = W.Workload("C0", 40, 8, W.GPT_345M, 320, 80_000_000_000, 100, 8, 600, 0.2, 0.2, 11)
     res = _sampled_chain_parity(w, chains=8, iters=600, n_sample=24, trace_n=2)
     assert any(p.cfg[0] * p.cfg[2] > 256 for p in res["per_config"])
+
+
+def test_search_zero_iterations_and_odd_chain_counts():
+    w = W.WORKLOADS["C1"]
+    pip, B, prof = _ctx(w)
+    model, mo, cl = _models(w)
+    P = O.make_profile(prof)
+    # iterations = 0: the plan is the best identity mapping; every chain keeps L0
+    res = pip.search(model, w.bs_global, 5, 0, w.seed, chain_results=True)
+    assert all(r["best_step"] == -1 and r["accepted"] == 0 and r["best"] == r["L0"] for r in res["chains"])
+    ref = O.search(cl, B, P, mo, w.bs_global, 5, 0, w.seed)
+    assert res["plan"].latency_s == ref.latency and res["plan"].sa_steps == 0
+    # 33 and 65 chains: partial warps at the end of every config
+    for chains in (33, 65):
+        res = pip.search(model, w.bs_global, chains, 200, w.seed)
+        ref = O.search(cl, B, P, mo, w.bs_global, chains, 200, w.seed)
+        p = res["plan"]
+        assert (p.latency_s, p.cfg_index, p.chain, p.best_step) == (ref.latency, ref.cfg_index, ref.chain, ref.best_step)
+        assert np.array_equal(p.perm, ref.perm) and p.sa_accepted == ref.sa_accepted
+
+
+def test_search_custom_temperature_and_alpha():
+    w = W.WORKLOADS["C1"]
+    pip, B, prof = _ctx(w)
+    model, mo, cl = _models(w)
+    P = O.make_profile(prof)
+    for kw in ({"alpha": 0.99, "tau": 0.3}, {"alpha": 1.0, "t0": 1e-3}):
+        res = pip.search(model, w.bs_global, 4, 500, 77, **kw)
+        ref = O.search(cl, B, P, mo, w.bs_global, 4, 500, 77, **kw)
+        p = res["plan"]
+        assert (p.latency_s, p.cfg_index, p.chain, p.best_step) == (ref.latency, ref.cfg_index, ref.chain, ref.best_step)
+        assert p.sa_accepted == ref.sa_accepted
