@@ -63,14 +63,6 @@ __device__ __forceinline__ uint32_t shl_clamp(uint32_t x, uint32_t sh) {
   return r;
 }
 
-// Streaming 16-byte load of candidate data (read once: no L1 allocation).
-__device__ __forceinline__ uint4 ld_stream(const uint4* p) {
-  uint4 r;
-  asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0, %1, %2, %3}, [%4];"
-               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "l"(p));
-  return r;
-}
-
 struct EvalShared {
   const double* Rs;
   uint32_t* bm;     // [bm_words][kEvalThreads]
@@ -141,24 +133,14 @@ __device__ __forceinline__ void eval_small(const EvalParams& P, const EvalShared
   if (P.vec16) {
     const uint4* r4 = reinterpret_cast<const uint4*>(row);
     const int full = N & ~7;                         // whole 8-slot chunks: no per-slot guard
-    // groups of 8 chunks (64 slots): all loads of a group are issued before any is used
-    for (int g0 = 0; g0 < full; g0 += 64) {
-      uint4 v[8];
+    for (int w0 = 0; w0 < full; w0 += 8) {
+      const uint4 v = __ldg(r4 + (w0 >> 3));
+      const uint32_t pk[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
-      for (int c = 0; c < 8; ++c)
-        if (g0 + 8 * c < full) v[c] = ld_stream(r4 + ((g0 >> 3) + c));
-#pragma unroll
-      for (int c = 0; c < 8; ++c) {
-        if (g0 + 8 * c < full) {
-          const int w0 = g0 + 8 * c;
-          const uint32_t pk[4] = {v[c].x, v[c].y, v[c].z, v[c].w};
-#pragma unroll
-          for (int j = 0; j < 8; ++j) {
-            bool st, la;
-            flags(w0, j, st, la);
-            visit((pk[j >> 1] >> ((j & 1) * 16)) & 0xffffu, st, la);
-          }
-        }
+      for (int j = 0; j < 8; ++j) {
+        bool st, la;
+        flags(w0, j, st, la);
+        visit((pk[j >> 1] >> ((j & 1) * 16)) & 0xffffu, st, la);
       }
     }
     if (full < N) {
