@@ -20,6 +20,7 @@ __global__ void k_enumerate_filter(int, int, unsigned long long, int, pipette_mo
                                    const pipette_profile_entry*, int, DevCfg*, unsigned long long*, int, int*,
                                    double*, int, EnumOut*);
 const void* eval_kernel(int mode);
+__global__ void k_tin_values(const DevCfg*, const double*, const double*, int, double*);
 const void* sa_kernel(int mode, bool trace);
 int sa_warp_state_bytes(int mode, int N, int pp, int dp, int n, int dp_cap);
 __global__ void k_node_lists(const double*, int, uint8_t*, double*);
@@ -120,7 +121,8 @@ struct pipette_ctx {
   int E = 0, F = 0;
   std::vector<DevCfg> hcfg;
   std::vector<int> hfeas;
-  DevBuf cfgs, keys, feas, qtab, eout;
+  DevBuf cfgs, keys, feas, qtab, eout, vin;
+  bool vin_valid = false;   // K2 intra-node value table matches the config table and R
   // search buffers
   DevBuf tasks, counter, chain_out, best_perm, cfg_slot, cfg_best, gbits, items, gitems, pack, accepted,
       slot_perm_off, slot_lane, trace_slot, trace, task_prof, tin_rank, tin_vs, tl_ac, tl_val, tl_len;
@@ -258,6 +260,7 @@ pipette_status enumerate(pipette_ctx* ctx, const pipette_model* m, long long bs,
   if (eo.E) CU(cudaMemcpy(ctx->hcfg.data(), ctx->cfgs.p, sizeof(DevCfg) * eo.E, cudaMemcpyDeviceToHost));
   if (eo.F) CU(cudaMemcpy(ctx->hfeas.data(), ctx->feas.p, sizeof(int) * eo.F, cudaMemcpyDeviceToHost));
   ctx->enum_valid = true;
+  ctx->vin_valid = false;
   ctx->enum_model = *m;
   ctx->enum_bs = bs;
   return PIPETTE_OK;
@@ -390,6 +393,7 @@ pipette_status pipette_set_bandwidth(pipette_ctx* ctx, const double* bw) {
   if (st != PIPETTE_OK) return st;
   CU(cudaSetDevice(ctx->device));
   CU(cudaStreamSynchronize(ctx->stream));
+  ctx->vin_valid = false;
   return upload_bw(ctx, bw);
 }
 
@@ -402,7 +406,7 @@ pipette_status pipette_set_stream(pipette_ctx* ctx, void* stream) {
 void pipette_destroy(pipette_ctx* ctx) {
   if (!ctx) return;
   if (ctx->comm) ncclCommDestroy(ctx->comm);
-  DevBuf* bufs[] = {&ctx->cfgs, &ctx->keys, &ctx->feas, &ctx->qtab, &ctx->eout, &ctx->tasks, &ctx->counter,
+  DevBuf* bufs[] = {&ctx->cfgs, &ctx->keys, &ctx->feas, &ctx->qtab, &ctx->eout, &ctx->vin, &ctx->tasks, &ctx->counter,
                     &ctx->chain_out, &ctx->best_perm, &ctx->cfg_slot, &ctx->cfg_best, &ctx->gbits, &ctx->items,
                     &ctx->gitems, &ctx->pack, &ctx->accepted, &ctx->slot_perm_off, &ctx->slot_lane,
                     &ctx->trace_slot, &ctx->trace, &ctx->task_prof, &ctx->tin_rank, &ctx->tin_vs, &ctx->tl_ac,
@@ -458,6 +462,7 @@ pipette_status pipette_eval(pipette_ctx* ctx, const pipette_model* model, int64_
   cudaStream_t s = (cudaStream_t)stream;
   int maxN = 1;
   for (const DevCfg& c : ctx->hcfg) maxN = std::max(maxN, c.N);
+  const int mode = (ctx->n_nodes <= 16 && ctx->g <= 15 && ctx->dTab) ? 0 : 1;
   EvalParams P{};
   P.cfgs = (const DevCfg*)ctx->cfgs.p;
   P.keys = (const unsigned long long*)ctx->keys.p;
@@ -465,6 +470,15 @@ pipette_status pipette_eval(pipette_ctx* ctx, const pipette_model* model, int64_
   P.qtab = (const double*)ctx->qtab.p;
   P.R = ctx->dR;
   P.subset_max = ctx->dTab;
+  if (mode == 0 && !ctx->vin_valid) {
+    CU(ensure(ctx->vin, sizeof(double) * 256 * (size_t)std::max(1, ctx->E)));
+    k_tin_values<<<std::max(1, ctx->E), 256, 0, s>>>((const DevCfg*)ctx->cfgs.p, (const double*)ctx->qtab.p, ctx->dR,
+                                                    ctx->n_nodes, (double*)ctx->vin.p);
+    ctx->launches++;
+    CU(cudaGetLastError());
+    ctx->vin_valid = true;
+  }
+  P.vin = (const double*)ctx->vin.p;
   P.n_nodes = ctx->n_nodes;
   P.n = n;
   P.cand = d_cfg;
@@ -473,7 +487,6 @@ pipette_status pipette_eval(pipette_ctx* ctx, const pipette_model* model, int64_
   P.vec16 = ((uintptr_t)d_perm % 16 == 0) && (perm_stride % 8 == 0);
   P.bm_words = (maxN + 31) / 32;
   const int nn = ctx->n_nodes * ctx->n_nodes;
-  const int mode = (ctx->n_nodes <= 16 && ctx->g <= 15 && ctx->dTab) ? 0 : 1;
   const bool rep = mode == 0;
   P.rep = rep;
   P.latency = d_latency;

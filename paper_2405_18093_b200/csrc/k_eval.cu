@@ -76,13 +76,14 @@ __device__ __forceinline__ double r_at(const EvalShared& S, uint32_t a, uint32_t
 }
 
 // MODE 0 evaluation of one candidate with compile-time pipeline depth PP (0: runtime).
-template <int PP, bool N8>
+template <int PP, bool RB>
 __device__ __forceinline__ void eval_small(const EvalParams& P, const EvalShared& S, const DevCfg& C,
-                                           const uint16_t* row, long long i) {
+                                           const uint16_t* row, long long i, int e) {
+  constexpr bool N8 = false;
   const int N = C.N;
   const int pp = PP > 0 ? PP : C.pp;
   const uint32_t spn = (uint32_t)C.spn;
-  const bool regbm = N <= 64;
+  constexpr bool regbm = RB;   // N <= 64: bitmap in a register pair
   if (!regbm)
     for (int w = 0; w < (N + 31) / 32; ++w) S.bm[w * kEvalThreads + S.tid] = 0u;
   // Bijection test (Eq.2): OR the bit of every slot id into [0, 64) (a 2x32-bit register
@@ -133,8 +134,10 @@ __device__ __forceinline__ void eval_small(const EvalParams& P, const EvalShared
   if (P.vec16) {
     const uint4* r4 = reinterpret_cast<const uint4*>(row);
     const int full = N & ~7;                         // whole 8-slot chunks: no per-slot guard
+    uint4 nxt = full > 0 ? __ldg(r4) : make_uint4(0u, 0u, 0u, 0u);
     for (int w0 = 0; w0 < full; w0 += 8) {
-      const uint4 v = __ldg(r4 + (w0 >> 3));
+      const uint4 v = nxt;                           // chunk w0 (loaded one chunk ahead)
+      if (w0 + 8 < full) nxt = __ldg(r4 + ((w0 + 8) >> 3));
       const uint32_t pk[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
       for (int j = 0; j < 8; ++j) {
@@ -183,15 +186,16 @@ __device__ __forceinline__ void eval_small(const EvalParams& P, const EvalShared
   const double qnan = __longlong_as_double(0x7ff8000000000000ll);
   if (!ok) { P.latency[i] = qnan; P.status[i] = 3; return; }
   if (!C.has_profile) { P.latency[i] = qnan; P.status[i] = 4; return; }
-  // Eq.6: per-node intra ring over nodes with >= 2 stage-1 members, slowest inter link
-  const double* qi = P.qtab + C.qi_off;
+  // Eq.6: per-node intra ring over nodes with >= 2 stage-1 members (value table
+  // vin[e][a*16 + c] = qi(c) R[a][a], 0 for c < 2), slowest inter link
+  const double* vin = P.vin + (size_t)e * 256;
   double t_in = 0.0;
   uint32_t bits = mask;
   while (bits) {
     const uint32_t a = __ffs(bits) - 1;
     bits &= bits - 1;
     const uint32_t c = (uint32_t)(c64 >> (4u * a)) & 15u;
-    if (c >= 2) t_in = fmax(t_in, __dmul_rn(__ldg(qi + c), r_at<true>(S, a, a)));
+    t_in = fmax(t_in, __ldg(vin + a * 16 + c));
   }
   const int k = __popc(mask);
   const double t_ex = k >= 2 ? __dmul_rn(__ldg(P.qtab + C.qe_off + k), __ldg(P.subset_max + mask)) : 0.0;
@@ -201,9 +205,9 @@ __device__ __forceinline__ void eval_small(const EvalParams& P, const EvalShared
 
 template <int PP>
 __device__ __forceinline__ void dispatch_n(const EvalParams& P, const EvalShared& S, const DevCfg& C,
-                                           const uint16_t* row, long long i) {
-  if (S.n <= 8) eval_small<PP, true>(P, S, C, row, i);    // stage-1 counts fit one 32-bit word
-  else eval_small<PP, false>(P, S, C, row, i);
+                                           const uint16_t* row, long long i, int e) {
+  if (C.N <= 64) eval_small<PP, true>(P, S, C, row, i, e);    // bijection bitmap in registers
+  else eval_small<PP, false>(P, S, C, row, i, e);
 }
 
 // MODE 1 (general) evaluation of one candidate.
@@ -360,19 +364,29 @@ __global__ void __launch_bounds__(kEvalThreads) k_eval_stream(EvalParams P) {
       const uint16_t* row = P.perm + i * (long long)P.perm_stride;
       if (MODE == 0) {
         switch (C.pp) {
-          case 1: dispatch_n<1>(P, S, C, row, i); break;
-          case 2: dispatch_n<2>(P, S, C, row, i); break;
-          case 4: dispatch_n<4>(P, S, C, row, i); break;
-          case 8: dispatch_n<8>(P, S, C, row, i); break;
-          case 16: dispatch_n<16>(P, S, C, row, i); break;
-          case 32: dispatch_n<32>(P, S, C, row, i); break;
-          default: dispatch_n<0>(P, S, C, row, i); break;
+          case 1: dispatch_n<1>(P, S, C, row, i, e); break;
+          case 2: dispatch_n<2>(P, S, C, row, i, e); break;
+          case 4: dispatch_n<4>(P, S, C, row, i, e); break;
+          case 8: dispatch_n<8>(P, S, C, row, i, e); break;
+          default: dispatch_n<0>(P, S, C, row, i, e); break;
         }
       } else {
         eval_general(P, S, C, row, i);
       }
     }
     __syncthreads();
+  }
+}
+
+// qi(c) R[a][a] for every enumerated config, node a < n <= 16 and c < 16 (0 for c < 2):
+// the intra-node term of Eq.6 by lookup in K2 MODE 0.  One block per config.
+__global__ void k_tin_values(const DevCfg* __restrict__ cfgs, const double* __restrict__ qtab,
+                             const double* __restrict__ R, int n, double* __restrict__ vin) {
+  const int e = blockIdx.x;
+  const DevCfg C = cfgs[e];
+  for (int i = threadIdx.x; i < 256; i += blockDim.x) {
+    const int a = i >> 4, c = i & 15;
+    vin[(size_t)e * 256 + i] = (a < n && c >= 2 && c <= C.dp) ? __dmul_rn(qtab[C.qi_off + c], R[a * n + a]) : 0.0;
   }
 }
 
