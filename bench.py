@@ -32,6 +32,15 @@ FP64_LANES_PER_SM = 64          # B200 (sm_100) FP64 units per SM per clock (DES
 N_SMS = 148
 
 
+def ncu_traffic(kernel):
+    """Per-launch DRAM bytes of `kernel` from the committed ncu capture (or None)."""
+    try:
+        d = json.load(open(os.path.join(ROOT, "profiles", "ncu_traffic.json")))[kernel]
+        return int(d["read_bytes"]) + int(d["write_bytes"])
+    except Exception:
+        return None
+
+
 def peaks():
     try:
         return json.load(open(PEAKS))
@@ -223,7 +232,9 @@ def run_ours(args):
     fp64_peak = N_SMS * FP64_LANES_PER_SM * (pk.get("sm_max_mhz", 1965.0) * 1e6) / 1e12
     achieved = ops_local / sa_avg_s / 1e12
     roofline = {"kernel": "k_sa_chains", "bound": "alu", "achieved": achieved, "peak": fp64_peak,
-                "unit": "TFLOP/s (fp64 DADD/DMUL ops)", "frac": achieved / fp64_peak, "traffic": None,
+                "unit": "TFLOP/s (fp64 DADD/DMUL ops)", "frac": achieved / fp64_peak,
+                "traffic": ncu_traffic("k_sa_chains") if args.workload == "C2" else None,
+                "traffic_note": "DRAM bytes per launch (ncu): chain state lives in shared memory, R/tables in L2",
                 "peak_source": "148 SMs x 64 FP64 lanes x sm_max_mhz (MEASURED_PEAKS.json), DESIGN.md 8",
                 "sa_kernel_ms": sa_avg_s * 1000.0, "sa_share_of_step": (sa_max / t_max) if t_max else None}
 
@@ -336,7 +347,8 @@ def bench_eval(pip, model, w, cfgs, feas, pk, n=1 << 22):
                     "status_ok_or_oom": bool(((st == 0) | (st == 1)).all()),
                     "roofline": {"kernel": "k_eval_stream", "bound": "hbm", "achieved": gbs,
                                  "peak": pk.get("hbm_gbs"), "unit": "GB/s", "frac": gbs / pk.get("hbm_gbs", 6538.3),
-                                 "traffic": None, "alg_bytes_per_candidate": alg / n,
+                                 "traffic": (ncu_traffic("k_eval_stream") if tag == "homogeneous" else None),
+                                 "alg_bytes_per_candidate": alg / n,
                                  "note": f"batch {(n * stride * 2 + 25 * n) / 1e9:.2f} GB > L2"}}
         del perm, cf
     return out
