@@ -317,18 +317,8 @@ __global__ void __launch_bounds__(kEvalThreads) k_eval_stream(EvalParams P) {
   __shared__ int sh_scan[32];
   const bool bucket = P.E + 1 <= kEvalMaxBucketCfgs;
 
-  const long long tile_stride = (long long)gridDim.x * kEvalTile;
-  const int row_bytes = P.perm_stride * 2;
-  for (long long base = (long long)blockIdx.x * kEvalTile; base < P.n; base += tile_stride) {
+  for (long long base = (long long)blockIdx.x * kEvalTile; base < P.n; base += (long long)gridDim.x * kEvalTile) {
     const int cnt_valid = (int)min((long long)kEvalTile, P.n - base);
-    {   // warm L2 with the mapping rows of this block's next tile while this one is evaluated
-      const long long nb = base + tile_stride;
-      const int nvalid = nb < P.n ? (int)min((long long)kEvalTile, P.n - nb) : 0;
-      const long long first = nb * row_bytes, total = (long long)nvalid * row_bytes;
-      const char* rows = reinterpret_cast<const char*>(P.perm);
-      for (long long off = (long long)tid * 128; off < total; off += (long long)blockDim.x * 128)
-        asm volatile("prefetch.global.L2 [%0];" ::"l"(rows + first + off));
-    }
     if (bucket) {
       for (int k = tid; k <= P.E; k += blockDim.x) hist[k] = 0;
       __syncthreads();
