@@ -261,7 +261,7 @@ def run_ours(args):
     # ---------------- eval stream (row a10), HBM-bound, measured beside the step
     eval_stream = None
     if not args.no_eval and rank == 0:
-        eval_stream = bench_eval(pip, model, w, cfgs, feas, pk)
+        eval_stream = bench_eval(pip, model, w, cfgs, feas, pk, plan_cfg_index=plan.cfg_index)
 
     # ---------------- CPU baseline: the oracle on this host, rank 0 at N=1 only
     cpu = None
@@ -323,14 +323,16 @@ def _perms(n, Ns, stride, seed):
     return perm.contiguous()
 
 
-def bench_eval(pip, model, w, cfgs, feas, pk, n=1 << 22):
+def bench_eval(pip, model, w, cfgs, feas, pk, n=1 << 22, plan_cfg_index=None):
     """pipette_eval (row a10) on 2^22 random mappings: (1) homogeneous batch of the feasible
     config with the largest N, (2) mixed batch over every feasible config.
     HBM roofline with 8 + 2N + 17 algorithmic bytes per candidate."""
     import torch
     fi = [i for i in range(len(feas)) if feas[i]]
     out = {}
-    idx = max(fi, key=lambda i: (cfgs[i][0] * cfgs[i][2], -i))
+    # homogeneous: the configuration of the search's best plan (its neighbourhood is what a
+    # user re-evaluates); mixed: every feasible configuration
+    idx = plan_cfg_index if plan_cfg_index is not None else max(fi, key=lambda i: (cfgs[i][0] * cfgs[i][2], -i))
     for tag, rows in (("homogeneous", [idx] * n), ("mixed", [fi[k % len(fi)] for k in range(n)])):
         rows = np.asarray(rows)
         np.random.default_rng(3).shuffle(rows)

@@ -23,6 +23,8 @@ fi = [i for i in range(len(feas)) if feas[i]]
 n = 1 << 22
 if mode == "homogeneous":
     idx = max(fi, key=lambda i: (cfgs[i][0] * cfgs[i][2], -i))
+    if len(sys.argv) > 3:
+        idx = int(sys.argv[3])
     rows = np.full(n, idx)
 else:
     rows = np.asarray([fi[k % len(fi)] for k in range(n)])
