@@ -492,13 +492,9 @@ pipette_status pipette_eval(pipette_ctx* ctx, const pipette_model* model, int64_
   P.latency = d_latency;
   P.mem = (unsigned long long*)d_mem;
   P.status = d_status;
-  size_t smem = (size_t)(rep ? nn * 32 : nn) * 8 + ((ctx->E * 8 + 15) & ~15) +
-                (size_t)(P.bm_words + (ctx->n_nodes + 3) / 4) * kEvalThreads * 4 +
-                2048 * sizeof(int) + 4096 * sizeof(int) + 2048 * sizeof(short);
-  // MODE 0: double-buffered cp.async staging of the mapping rows when it fits (<= 100 KB)
-  const size_t stage = (size_t)2 * kEvalThreads * (perm_stride * 2 + 16);
-  P.stage_bytes = (mode == 0 && P.vec16 && stage <= 100 * 1024) ? (int)stage : 0;
-  smem += P.stage_bytes ? P.stage_bytes + 16 : 0;
+  const size_t smem = (size_t)(rep ? nn * 32 : nn) * 8 + ((ctx->E * 8 + 15) & ~15) +
+                      (size_t)(P.bm_words + (ctx->n_nodes + 3) / 4) * kEvalThreads * 4 +
+                      2048 * sizeof(int) + 4096 * sizeof(int) + 2048 * sizeof(short);
   if (smem > 227 * 1024) return fail(ctx, PIPETTE_E_UNSUPPORTED, "eval shared memory %zu B too large", smem);
   const void* kern = eval_kernel(mode);
   CU(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));

@@ -63,21 +63,6 @@ __device__ __forceinline__ uint32_t shl_clamp(uint32_t x, uint32_t sh) {
   return r;
 }
 
-// 16-byte shared-memory load from a 32-bit shared address.
-__device__ __forceinline__ uint4 lds128(uint32_t a) {
-  uint4 r;
-  asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "r"(a));
-  return r;
-}
-
-// Asynchronous 16-byte global -> shared copy (cp.async, L2 only) and its group fences.
-__device__ __forceinline__ void cp_async16(uint32_t dst, const void* src) {
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src));
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;"); }
-template <int N>
-__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N)); }
-
 struct EvalShared {
   const double* Rs;
   uint32_t* bm;     // [bm_words][kEvalThreads]
@@ -93,7 +78,7 @@ __device__ __forceinline__ double r_at(const EvalShared& S, uint32_t a, uint32_t
 // MODE 0 evaluation of one candidate with compile-time pipeline depth PP (0: runtime).
 template <int PP, bool RB>
 __device__ __forceinline__ void eval_small(const EvalParams& P, const EvalShared& S, const DevCfg& C,
-                                           const uint16_t* row, long long i, int e, uint32_t srow) {
+                                           const uint16_t* row, long long i, int e) {
   constexpr bool N8 = false;
   const int N = C.N;
   const int pp = PP > 0 ? PP : C.pp;
@@ -148,13 +133,11 @@ __device__ __forceinline__ void eval_small(const EvalParams& P, const EvalShared
   };
   if (P.vec16) {
     const uint4* r4 = reinterpret_cast<const uint4*>(row);
-    // srow != 0: the row was staged into shared memory by cp.async (padded, conflict free)
-    auto chunk = [&](int c) { return srow ? lds128(srow + 16u * (uint32_t)c) : __ldg(r4 + c); };
     const int full = N & ~7;                         // whole 8-slot chunks: no per-slot guard
-    uint4 nxt = full > 0 ? chunk(0) : make_uint4(0u, 0u, 0u, 0u);
+    uint4 nxt = full > 0 ? __ldg(r4) : make_uint4(0u, 0u, 0u, 0u);
     for (int w0 = 0; w0 < full; w0 += 8) {
       const uint4 v = nxt;                           // chunk w0 (loaded one chunk ahead)
-      if (w0 + 8 < full) nxt = chunk((w0 + 8) >> 3);
+      if (w0 + 8 < full) nxt = __ldg(r4 + ((w0 + 8) >> 3));
       const uint32_t pk[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
       for (int j = 0; j < 8; ++j) {
@@ -164,7 +147,7 @@ __device__ __forceinline__ void eval_small(const EvalParams& P, const EvalShared
       }
     }
     if (full < N) {
-      const uint4 v = chunk(full >> 3);
+      const uint4 v = __ldg(r4 + (full >> 3));
       const uint32_t pk[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
       for (int j = 0; j < 8; ++j) {
@@ -222,9 +205,9 @@ __device__ __forceinline__ void eval_small(const EvalParams& P, const EvalShared
 
 template <int PP>
 __device__ __forceinline__ void dispatch_n(const EvalParams& P, const EvalShared& S, const DevCfg& C,
-                                           const uint16_t* row, long long i, int e, uint32_t srow) {
-  if (C.N <= 64) eval_small<PP, true>(P, S, C, row, i, e, srow);    // bijection bitmap in registers
-  else eval_small<PP, false>(P, S, C, row, i, e, srow);
+                                           const uint16_t* row, long long i, int e) {
+  if (C.N <= 64) eval_small<PP, true>(P, S, C, row, i, e);    // bijection bitmap in registers
+  else eval_small<PP, false>(P, S, C, row, i, e);
 }
 
 // MODE 1 (general) evaluation of one candidate.
@@ -333,13 +316,6 @@ __global__ void __launch_bounds__(kEvalThreads) k_eval_stream(EvalParams P) {
   short* order = reinterpret_cast<short*>(hist + kEvalMaxBucketCfgs);
   __shared__ int sh_scan[32];
   const bool bucket = P.E + 1 <= kEvalMaxBucketCfgs;
-  // per-thread double buffer for the mapping rows (MODE 0, 16-byte rows): row slot of RS
-  // bytes = row + 16 B of padding, so the 16-byte chunks of 8 consecutive threads fall in
-  // 8 different bank groups
-  const int RS = P.perm_stride * 2 + 16;
-  const bool staged = MODE == 0 && P.vec16 && P.stage_bytes > 0;
-  const uint32_t stage0 = (uint32_t)__cvta_generic_to_shared(
-      reinterpret_cast<unsigned char*>(order + kEvalTile) + ((16 - ((uintptr_t)(order + kEvalTile) & 15)) & 15));
 
   for (long long base = (long long)blockIdx.x * kEvalTile; base < P.n; base += (long long)gridDim.x * kEvalTile) {
     const int cnt_valid = (int)min((long long)kEvalTile, P.n - base);
@@ -376,31 +352,7 @@ __global__ void __launch_bounds__(kEvalThreads) k_eval_stream(EvalParams P) {
       for (int k = tid; k < cnt_valid; k += blockDim.x) order[atomicAdd(&hist[tile_e[k] + 1], 1)] = (short)k;
       __syncthreads();
     }
-    // stage the row of the thread's candidate `sidx_` into buffer b (its valid chunks only)
-    auto issue = [&](int sidx_, int b) {
-      const int k = bucket ? order[sidx_] : sidx_;
-      const int e = tile_e[k];
-      if (e >= 0) {
-        const int chunks = (P.cfgs[e].N + 7) >> 3;
-        const char* src = reinterpret_cast<const char*>(P.perm + (base + k) * (long long)P.perm_stride);
-        const uint32_t dst = stage0 + (uint32_t)((b * kEvalThreads + tid) * RS);
-        for (int c = 0; c < chunks; ++c) cp_async16(dst + 16u * c, src + 16 * c);
-      }
-      cp_async_commit();
-    };
-    int buf = 0;
-    if (staged && tid < cnt_valid) issue(tid, 0);
-    for (int sidx = tid; sidx < cnt_valid; sidx += blockDim.x, buf ^= 1) {
-      uint32_t srow = 0;
-      if (staged) {   // prefetch the next candidate's row, then wait for this one
-        if (sidx + (int)blockDim.x < cnt_valid) {
-          issue(sidx + blockDim.x, buf ^ 1);
-          cp_async_wait<1>();
-        } else {
-          cp_async_wait<0>();
-        }
-        srow = stage0 + (uint32_t)((buf * kEvalThreads + tid) * RS);
-      }
+    for (int sidx = tid; sidx < cnt_valid; sidx += blockDim.x) {
       const int k = bucket ? order[sidx] : sidx;
       const long long i = base + k;
       const int e = tile_e[k];
@@ -412,11 +364,11 @@ __global__ void __launch_bounds__(kEvalThreads) k_eval_stream(EvalParams P) {
       const uint16_t* row = P.perm + i * (long long)P.perm_stride;
       if (MODE == 0) {
         switch (C.pp) {
-          case 1: dispatch_n<1>(P, S, C, row, i, e, srow); break;
-          case 2: dispatch_n<2>(P, S, C, row, i, e, srow); break;
-          case 4: dispatch_n<4>(P, S, C, row, i, e, srow); break;
-          case 8: dispatch_n<8>(P, S, C, row, i, e, srow); break;
-          default: dispatch_n<0>(P, S, C, row, i, e, srow); break;
+          case 1: dispatch_n<1>(P, S, C, row, i, e); break;
+          case 2: dispatch_n<2>(P, S, C, row, i, e); break;
+          case 4: dispatch_n<4>(P, S, C, row, i, e); break;
+          case 8: dispatch_n<8>(P, S, C, row, i, e); break;
+          default: dispatch_n<0>(P, S, C, row, i, e); break;
         }
       } else {
         eval_general(P, S, C, row, i);

@@ -103,7 +103,6 @@ struct EvalParams {
   const double* R;
   const double* subset_max;  // 2^n table (MODE 0)
   const double* vin;         // [E][256] qi(c) R[a][a] values (MODE 0)
-  int32_t stage_bytes;       // per-block cp.async staging area (0: rows read from global)
   int32_t n_nodes;
   int64_t n;
   const pipette_config* cand;
