@@ -135,9 +135,11 @@ __device__ __forceinline__ void eval_small(const EvalParams& P, const EvalShared
     const uint4* r4 = reinterpret_cast<const uint4*>(row);
     const int full = N & ~7;                         // whole 8-slot chunks: no per-slot guard
     uint4 nxt = full > 0 ? __ldg(r4) : make_uint4(0u, 0u, 0u, 0u);
+    uint4 nxt2 = full > 8 ? __ldg(r4 + 1) : make_uint4(0u, 0u, 0u, 0u);
     for (int w0 = 0; w0 < full; w0 += 8) {
-      const uint4 v = nxt;                           // chunk w0 (loaded one chunk ahead)
-      if (w0 + 8 < full) nxt = __ldg(r4 + ((w0 + 8) >> 3));
+      const uint4 v = nxt;                           // chunk w0 (loaded two chunks ahead)
+      nxt = nxt2;
+      if (w0 + 16 < full) nxt2 = __ldg(r4 + ((w0 + 16) >> 3));
       const uint32_t pk[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
       for (int j = 0; j < 8; ++j) {
