@@ -427,52 +427,6 @@ __host__ __device__ inline int warp_state_bytes(int N, int pp, int dp, int n, bo
          (s1smem ? align16((n + 3) / 4 * 128) : 0);
 }
 
-// The largest Eq.5 pipeline sums with their pipelines, v0 >= v1 >= v2 >= v3 (-1: empty slot).
-// Invariant: every pipeline outside the list has a sum <= the smallest listed value; when
-// dp <= 4 (`all`) the list holds every pipeline.  A proposal touches at most two pipelines,
-// so with >= 3 entries the untouched maximum is the first listed pipeline not touched --
-// T_PP of any proposal in O(1), exact (max), with a rebuild only when an accepted move
-// leaves fewer than 3 entries.
-struct Top4 {
-  double v0, v1, v2, v3;
-  int z0, z1, z2, z3, cnt;
-  bool all;
-  __device__ __forceinline__ void clear() { v0 = v1 = v2 = v3 = -1.0; z0 = z1 = z2 = z3 = -1; cnt = 0; }
-  __device__ __forceinline__ double vmin() const { return cnt >= 4 ? v3 : (cnt == 3 ? v2 : (cnt == 2 ? v1 : v0)); }
-  __device__ __forceinline__ void insert(double v, int z) {   // sorted; the smallest drops when full
-    if (v > v0) { v3 = v2; z3 = z2; v2 = v1; z2 = z1; v1 = v0; z1 = z0; v0 = v; z0 = z; }
-    else if (v > v1) { v3 = v2; z3 = z2; v2 = v1; z2 = z1; v1 = v; z1 = z; }
-    else if (v > v2) { v3 = v2; z3 = z2; v2 = v; z2 = z; }
-    else if (v > v3) { v3 = v; z3 = z; }
-    else return;
-    cnt = min(cnt + 1, 4);
-  }
-  __device__ __forceinline__ void remove(int z) {
-    if (z == z0) { v0 = v1; z0 = z1; v1 = v2; z1 = z2; v2 = v3; z2 = z3; }
-    else if (z == z1) { v1 = v2; z1 = z2; v2 = v3; z2 = z3; }
-    else if (z == z2) { v2 = v3; z2 = z3; }
-    else if (z != z3) return;
-    v3 = -1.0; z3 = -1;
-    --cnt;
-  }
-  // largest listed sum of a pipeline other than a and b (-1 if none)
-  __device__ __forceinline__ double max_excluding(int a, int b) const {
-    if (z0 != a && z0 != b) return v0;
-    if (z1 != a && z1 != b) return v1;
-    if (z2 != a && z2 != b) return v2;
-    if (z3 != a && z3 != b) return v3;
-    return -1.0;
-  }
-  // a committed move changed pipelines a (to sa) and b (to sb; b == a if one pipeline)
-  __device__ __forceinline__ void update(int a, double sa, int b, double sb) {
-    remove(a);
-    if (b != a) remove(b);
-    if (all || cnt == 0 || sa >= vmin()) insert(sa, a);
-    if (b != a && (all || cnt == 0 || sb >= vmin())) insert(sb, b);
-  }
-  __device__ __forceinline__ bool needs_rebuild() const { return !all && cnt < 3; }
-};
-
 // ------------------------------------------------------------------ one warp task
 template <class POS, class S1, class RT, bool TRACE, int PP>
 __device__ __forceinline__ void run_task(const SaParams& P, const SaTask T, const DevCfg C, const RT R,
@@ -513,16 +467,13 @@ __device__ __forceinline__ void run_task(const SaParams& P, const SaTask T, cons
   pos.init(N, (uint32_t)C.spn, C.spn_magic);
   for (int w = 0; w < N; ++w) bperm[w * 32 + lane] = (uint16_t)w;
   double tpp = 0.0;
-  Top4 top;
-  top.clear();
-  top.all = dp <= 4;
+  int nmax = 0;   // pipelines whose sum equals tpp
   for (int z = 0; z < dp; ++z) {
     s1.add_init(pos.node((uint32_t)(z * pp)));
     if (pp >= 2) {
       const double s = pipe_sum<RT, PP>(z, pp, pos, kNone, kNone, 0u, 0u, C.m2, R);
       if (cache) psum[z * 32 + lane] = s;
-      top.insert(s, z);
-      tpp = fmax(tpp, s);
+      if (s > tpp) { tpp = s; nmax = 1; } else if (s == tpp) { ++nmax; }
     }
   }
   s1.finish_init(X, R);
@@ -551,20 +502,64 @@ __device__ __forceinline__ void run_task(const SaParams& P, const SaTask T, cons
       int zp = 0, zq = 0;
       bool two = false, dpchg = false;
       double sA = 0.0, sB = 0.0, tpp2 = tpp;
+      int nmax2 = nmax;
       if (evald) {
-        // ---- Eq.5: re-sum the (at most two) touched pipelines; T_PP from the top list
+        // ---- Eq.5: re-sum the (at most two) touched pipelines, maintain the max
         if (pp >= 2) {
           zp = (int)div_small(d.p, C.pp_magic, (uint32_t)pp);
           zq = (int)div_small(d.q, C.pp_magic, (uint32_t)pp);
           xp = d.p - (uint32_t)(zp * pp);
           xq = d.q - (uint32_t)(zq * pp);
           two = zq != zp;
+          double oldA, oldB;
+          if (cache) {
+            oldA = psum[zp * 32 + lane];
+            oldB = two ? psum[zq * 32 + lane] : oldA;
+          } else {
+            if (two) pipe_sum2<RT, PP>(zp, zq, pp, pos, kNone, kNone, 0u, 0u, C.m2, R, oldA, oldB);
+            else oldB = oldA = pipe_sum<RT, PP>(zp, pp, pos, kNone, kNone, 0u, 0u, C.m2, R);
+          }
           // apply the swap tentatively (reverted below if rejected): the re-sum then reads
           // plain positions, with no per-hop substitution
           pos.swap(d.p, d.q, rp, rq);
           if (two) pipe_sum2<RT, PP>(zp, zq, pp, pos, kNone, kNone, 0u, 0u, C.m2, R, sA, sB);
           else sA = pipe_sum<RT, PP>(zp, pp, pos, kNone, kNone, 0u, 0u, C.m2, R);
-          tpp2 = fmax(fmax(top.max_excluding(zp, zq), sA), two ? sB : 0.0);
+          const double snew = two ? fmax(sA, sB) : sA;
+          const int keep = nmax - (oldA == tpp ? 1 : 0) - ((two && oldB == tpp) ? 1 : 0);  // untouched at max
+          if (keep > 0 || snew >= tpp) {
+            // the max is max(tpp if an untouched pipeline still holds it, new sums)
+            tpp2 = (keep > 0) ? fmax(tpp, snew) : snew;
+            nmax2 = (keep > 0 && tpp2 == tpp ? keep : 0) + (sA == tpp2 ? 1 : 0) + ((two && sB == tpp2) ? 1 : 0);
+          } else if (cache) {
+            // the unique max pipeline decreased: rescan for the max and its multiplicity in
+            // one pass (two independent (max, count) accumulators)
+            double m0 = sA, m1 = two ? sB : 0.0;
+            int c0 = 1, c1 = two ? 1 : 0;
+            int z = 0;
+            for (; z + 2 <= dp; z += 2) {
+              const double v0 = (z == zp || z == zq) ? 0.0 : psum[z * 32 + lane];
+              const double v1 = (z + 1 == zp || z + 1 == zq) ? 0.0 : psum[(z + 1) * 32 + lane];
+              c0 = v0 > m0 ? 1 : c0 + (v0 == m0 ? 1 : 0);
+              m0 = fmax(m0, v0);
+              c1 = v1 > m1 ? 1 : c1 + (v1 == m1 ? 1 : 0);
+              m1 = fmax(m1, v1);
+            }
+            if (z < dp) {
+              const double v0 = (z == zp || z == zq) ? 0.0 : psum[z * 32 + lane];
+              c0 = v0 > m0 ? 1 : c0 + (v0 == m0 ? 1 : 0);
+              m0 = fmax(m0, v0);
+            }
+            tpp2 = fmax(m0, m1);
+            nmax2 = (m0 == tpp2 ? c0 : 0) + (m1 == tpp2 ? c1 : 0);
+          } else {
+            // no cache: re-sum every pipeline of the tentative mapping
+            tpp2 = 0.0;
+            nmax2 = 0;
+            for (int z = 0; z < dp; ++z) {
+              const double v = (z == zp) ? sA : ((z == zq) ? sB : pipe_sum<RT, PP>(z, pp, pos, kNone, kNone, 0u, 0u, C.m2, R));
+              if (v > tpp2) { tpp2 = v; nmax2 = 1; } else if (v == tpp2) { ++nmax2; }
+            }
+          }
         }
         // ---- Eq.6: the stage-1 node multiset changes only if exactly one of p, q is stage 1
         dpchg = (xp == 0u) != (xq == 0u);
@@ -591,12 +586,7 @@ __device__ __forceinline__ void run_task(const SaParams& P, const SaTask T, cons
               if (two) psum[zq * 32 + lane] = sB;
             }
             tpp = tpp2;
-            top.update(zp, sA, two ? zq : zp, sB);
-            if (top.needs_rebuild()) {   // rare: rebuild the list from every pipeline sum
-              top.clear();
-              for (int z = 0; z < dp; ++z)
-                top.insert(cache ? psum[z * 32 + lane] : pipe_sum<RT, PP>(z, pp, pos, kNone, kNone, 0u, 0u, C.m2, R), z);
-            }
+            nmax = nmax2;
           }
           if (dpchg) s1.commit();
           cur = Lp;
