@@ -9,7 +9,7 @@ import ctypes as C
 import os
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_PKG, "lib", "libpipette.so")
+LIB_PATH = os.environ.get("PIPETTE_LIB") or os.path.join(_PKG, "lib", "libpipette.so")   # override: A/B tools only
 
 OK, NO_FEASIBLE, E_INVALID, E_PROFILE, E_CUDA, E_NCCL, E_UNSUPPORTED = range(7)
 
