@@ -124,7 +124,7 @@ struct pipette_ctx {
   DevBuf cfgs, keys, feas, qtab, eout, vin;
   bool vin_valid = false;   // K2 intra-node value table matches the config table and R
   // search buffers
-  DevBuf tasks, counter, chain_out, best_perm, cfg_slot, cfg_best, gbits, items, gitems, pack, accepted,
+  DevBuf tasks, chunks, counter, chain_out, best_perm, cfg_slot, cfg_best, gbits, items, gitems, pack, accepted,
       slot_perm_off, slot_lane, trace_slot, trace, task_prof, tin_rank, tin_vs, tl_ac, tl_val, tl_len;
   int64_t n_tasks_last = 0;
   cudaEvent_t ev[6] = {};
@@ -406,7 +406,7 @@ pipette_status pipette_set_stream(pipette_ctx* ctx, void* stream) {
 void pipette_destroy(pipette_ctx* ctx) {
   if (!ctx) return;
   if (ctx->comm) ncclCommDestroy(ctx->comm);
-  DevBuf* bufs[] = {&ctx->cfgs, &ctx->keys, &ctx->feas, &ctx->qtab, &ctx->eout, &ctx->vin, &ctx->tasks, &ctx->counter,
+  DevBuf* bufs[] = {&ctx->cfgs, &ctx->keys, &ctx->feas, &ctx->qtab, &ctx->eout, &ctx->vin, &ctx->tasks, &ctx->chunks, &ctx->counter,
                     &ctx->chain_out, &ctx->best_perm, &ctx->cfg_slot, &ctx->cfg_best, &ctx->gbits, &ctx->items,
                     &ctx->gitems, &ctx->pack, &ctx->accepted, &ctx->slot_perm_off, &ctx->slot_lane,
                     &ctx->trace_slot, &ctx->trace, &ctx->task_prof, &ctx->tin_rank, &ctx->tin_vs, &ctx->tl_ac,
@@ -488,7 +488,6 @@ pipette_status pipette_eval(pipette_ctx* ctx, const pipette_model* model, int64_
   P.bm_words = (maxN + 31) / 32;
   const int nn = ctx->n_nodes * ctx->n_nodes;
   const bool rep = mode == 0;
-  P.rep = rep;
   P.latency = d_latency;
   P.mem = (unsigned long long*)d_mem;
   P.status = d_status;
@@ -593,10 +592,9 @@ pipette_status pipette_search(pipette_ctx* ctx, const pipette_model* model, int6
   // subset-max table.  MODE 1 (N <= 256): packed positions, sorted-table stage-1 state,
   // R through L1.  MODE 2: 32-bit positions (N > 256).
   const int mode = (n <= 16 && maxN <= 256 && ctx->g <= 15 && ctx->dTab) ? 0 : (maxN <= 256 ? 1 : 2);
-  const bool rep = mode == 0;
-  // MODE 0 replicates R in shared memory: 32 copies for n <= 8, else 16
-  const int r_copies_log2 = (mode == 0 && n <= 8) ? 5 : 4;
-  const int r_bytes = rep ? (nn << r_copies_log2) * 8 : (mode == 1 ? align16(nn * 8) : 0);
+  // MODE 0: the block's m2*R table, 256 hop codes x 16 lane copies (64-bit loads are served
+  // per half-warp, so 16 copies make every lookup conflict free); MODE 1: R in shared memory
+  const int r_bytes = mode == 0 ? 256 * 16 * 8 : (mode == 1 ? align16(nn * 8) : 0);
   // psum (Eq.5 sums) cached in shared memory for configs with dp <= dp_cap: the largest cap
   // that still reaches the best achievable number of resident blocks per SM
   auto warp_bytes_for = [&](int cap, int& tls) {
@@ -628,6 +626,14 @@ pipette_status pipette_search(pipette_ctx* ctx, const pipette_model* model, int6
     return fail(ctx, PIPETTE_E_UNSUPPORTED, "SA state (%d B/warp + %d B) exceeds shared memory", warp_bytes, r_bytes);
   while (wpb > 1 && r_bytes + wpb * warp_bytes > smem_max) --wpb;
   const size_t smem = (size_t)r_bytes + (size_t)wpb * warp_bytes;
+  // block work units: up to wpb consecutive tasks of one configuration
+  std::vector<int2> chunks;
+  for (size_t i = 0; i < sorted.size();) {
+    size_t j = i + 1;
+    while (j < sorted.size() && (int)(j - i) < wpb && sorted[j].cfg == sorted[i].cfg) ++j;
+    chunks.push_back(make_int2((int)i, (int)(j - i)));
+    i = j;
+  }
 
   const bool tracing = o.trace && o.trace_items && o.n_trace > 0 && o.trace_cap > 0;
   std::vector<int> trace_slot;
@@ -644,6 +650,7 @@ pipette_status pipette_search(pipette_ctx* ctx, const pipette_model* model, int6
   }
 
   CU(ensure(ctx->tasks, sizeof(SaTask) * std::max<size_t>(1, sorted.size())));
+  CU(ensure(ctx->chunks, sizeof(int2) * std::max<size_t>(1, chunks.size())));
   CU(ensure(ctx->counter, sizeof(int)));
   CU(ensure(ctx->task_prof, sizeof(unsigned long long) * 4 * std::max<size_t>(1, sorted.size())));
   ctx->n_tasks_last = (int64_t)sorted.size();
@@ -660,6 +667,8 @@ pipette_status pipette_search(pipette_ctx* ctx, const pipette_model* model, int6
   CU(ensure(ctx->pack, sizeof(unsigned long long) * ((size_t)F * row_words + 1)));
   if (!sorted.empty())
     CU(cudaMemcpyAsync(ctx->tasks.p, sorted.data(), sizeof(SaTask) * sorted.size(), cudaMemcpyHostToDevice, s));
+  if (!chunks.empty())
+    CU(cudaMemcpyAsync(ctx->chunks.p, chunks.data(), sizeof(int2) * chunks.size(), cudaMemcpyHostToDevice, s));
   CU(cudaMemcpyAsync(ctx->cfg_slot.p, cfg_slot.data(), sizeof(int) * (F + 1), cudaMemcpyHostToDevice, s));
   if (slots) {
     CU(cudaMemcpyAsync(ctx->slot_perm_off.p, slot_perm_off.data(), sizeof(int) * slots, cudaMemcpyHostToDevice, s));
@@ -699,6 +708,8 @@ pipette_status pipette_search(pipette_ctx* ctx, const pipette_model* model, int6
   P.psum_dp_cap = dp_cap;
   P.tasks = (const SaTask*)ctx->tasks.p;
   P.n_tasks = (int)sorted.size();
+  P.chunks = (const int2*)ctx->chunks.p;
+  P.n_chunks = (int)chunks.size();
   P.task_counter = (int*)ctx->counter.p;
   P.n_nodes = n;
   P.iterations = iterations;
@@ -708,11 +719,9 @@ pipette_status pipette_search(pipette_ctx* ctx, const pipette_model* model, int6
   P.alpha_inv = 1.0 / o.alpha;
   P.tau = o.tau;
   P.t0 = o.t0 > 0.0 ? o.t0 : 0.0;
-  P.rep = rep;
   P.warps_per_block = wpb;
   P.warp_smem_bytes = warp_bytes;
   P.r_smem_bytes = r_bytes;
-  P.r_copies_log2 = r_copies_log2;
   P.out = (ChainOut*)ctx->chain_out.p;
   P.best_perm = (uint16_t*)ctx->best_perm.p;
   P.task_prof = (unsigned long long*)ctx->task_prof.p;
@@ -725,8 +734,7 @@ pipette_status pipette_search(pipette_ctx* ctx, const pipette_model* model, int6
   int occ = 0;
   CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, wpb * 32, smem));
   occ = std::max(occ, 1);
-  const int grid = (int)std::max<long long>(1, std::min<long long>(((long long)sorted.size() + wpb - 1) / wpb,
-                                                                   (long long)occ * ctx->n_sms));
+  const int grid = (int)std::max<long long>(1, std::min<long long>((long long)chunks.size(), (long long)occ * ctx->n_sms));
   CU(cudaEventRecord(ctx->ev[2], s));
   if (mode == 0) {
     k_tin_rank<<<F, 256, 0, s>>>((const DevCfg*)ctx->cfgs.p, (const int*)ctx->feas.p, (const double*)ctx->qtab.p,

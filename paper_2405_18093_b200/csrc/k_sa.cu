@@ -621,54 +621,388 @@ __device__ __forceinline__ void run_task(const SaParams& P, const SaTask T, cons
   }
 }
 
-// MODE 0: n <= 16 nodes, N <= 256, spn <= 15: packed positions, register stage-1 state,
-//         lane-replicated R in shared memory, subset-max table.
+// ------------------------------------------------------------------ MODE 0: hop codes
+// Chain state of MODE 0 (n <= 16 nodes, N <= 256 positions), lane-interleaved bytes
+// ([w/4][lane] words, so every per-lane byte access hits the lane's own bank):
+//   H[w]  hop code of position w = z*pp + x: node(w-1) | node(w) << 4 for x >= 1 (the
+//         Eq.5 hop x-1 -> x of pipeline z), node(w) * 17 for x = 0 (the stage-1 worker).
+//         node(w) = H[w] >> 4 in both cases.
+//   S[w]  slot id of position w (the mapping string of Eq.2; slot < N <= 256)
+// The block's table Tt[code][16 copies] = fl(m2 * R[a][b]), a = code & 15, b = code >> 4,
+// of the block's configuration: a hop of Eq.5 is one byte extraction, one address, one
+// 64-bit shared load and one DADD -- the same product the oracle forms, so the sums are
+// bit-identical.  A pipeline's codes are read as whole words.
+struct HcState {
+  uint8_t* hb;   // byte view of H for this lane: position w at hb + ((w >> 2) << 7) + (w & 3)
+  uint8_t* sb;   // same for S
+  const uint32_t* hw;   // word view of H for this lane: word j at hw[j * 32]
+  __device__ __forceinline__ static uint32_t off(uint32_t w) { return ((w >> 2) << 7) | (w & 3u); }
+};
+
+// Eq.5 sum of pipeline z (bytes z*PP .. z*PP+PP-1), stage order.  Tl = this lane's copy
+// of the block table (Tt + (lane & 15)); the entry of code c is Tl[c * 16].
+template <int PP>
+__device__ __forceinline__ double hc_sum(const HcState& st, uint32_t z, int pp_rt, const double* Tl) {
+  double s = 0.0;
+  if constexpr (PP == 2) {
+    s = __dadd_rn(s, Tl[(uint32_t)st.hb[HcState::off(z * 2u + 1u)] * 16u]);
+  } else if constexpr (PP >= 4) {
+    constexpr int NW = PP / 4;
+    uint32_t wd[NW];
+#pragma unroll
+    for (int k = 0; k < NW; ++k) wd[k] = st.hw[(z * (uint32_t)NW + (uint32_t)k) * 32u];
+#pragma unroll
+    for (int x = 1; x < PP; ++x) {
+      const uint32_t code = __byte_perm(wd[x >> 2], 0u, 0x4440u | (uint32_t)(x & 3));
+      s = __dadd_rn(s, Tl[code * 16u]);
+    }
+  } else {
+    const uint32_t b = z * (uint32_t)pp_rt;
+    for (int x = 1; x < pp_rt; ++x) s = __dadd_rn(s, Tl[(uint32_t)st.hb[HcState::off(b + (uint32_t)x)] * 16u]);
+  }
+  return s;
+}
+
+// Two pipelines in one interleaved loop (two independent DADD chains); za == zb is allowed.
+template <int PP>
+__device__ __forceinline__ void hc_sum2(const HcState& st, uint32_t za, uint32_t zb, int pp_rt, const double* Tl,
+                                        double& sa, double& sb) {
+  double a = 0.0, b = 0.0;
+  if constexpr (PP == 2) {
+    a = __dadd_rn(a, Tl[(uint32_t)st.hb[HcState::off(za * 2u + 1u)] * 16u]);
+    b = __dadd_rn(b, Tl[(uint32_t)st.hb[HcState::off(zb * 2u + 1u)] * 16u]);
+  } else if constexpr (PP >= 4) {
+    constexpr int NW = PP / 4;
+    uint32_t wa[NW], wb[NW];
+#pragma unroll
+    for (int k = 0; k < NW; ++k) {
+      wa[k] = st.hw[(za * (uint32_t)NW + (uint32_t)k) * 32u];
+      wb[k] = st.hw[(zb * (uint32_t)NW + (uint32_t)k) * 32u];
+    }
+#pragma unroll
+    for (int x = 1; x < PP; ++x) {
+      const uint32_t ca = __byte_perm(wa[x >> 2], 0u, 0x4440u | (uint32_t)(x & 3));
+      const uint32_t cb = __byte_perm(wb[x >> 2], 0u, 0x4440u | (uint32_t)(x & 3));
+      a = __dadd_rn(a, Tl[ca * 16u]);
+      b = __dadd_rn(b, Tl[cb * 16u]);
+    }
+  } else {
+    const uint32_t ba = za * (uint32_t)pp_rt, bb = zb * (uint32_t)pp_rt;
+    for (int x = 1; x < pp_rt; ++x) {
+      a = __dadd_rn(a, Tl[(uint32_t)st.hb[HcState::off(ba + (uint32_t)x)] * 16u]);
+      b = __dadd_rn(b, Tl[(uint32_t)st.hb[HcState::off(bb + (uint32_t)x)] * 16u]);
+    }
+  }
+  sa = a;
+  sb = b;
+}
+
+// max over all dp pipelines of the Eq.5 sums and its multiplicity, from the hop codes.
+// PP = 2: a pipeline's sum is its single hop term, two pipelines per code word.
+template <int PP>
+__device__ __forceinline__ void hc_rescan(const HcState& st, int dp, int pp_rt, const double* Tl, double& mx,
+                                          int& cnt) {
+  double m0 = 0.0, m1 = 0.0;
+  int c0 = 0, c1 = 0;
+  auto acc = [](double v, double& m, int& c) {
+    c = v > m ? 1 : c + (v == m ? 1 : 0);
+    m = fmax(m, v);
+  };
+  if constexpr (PP == 2) {
+    const int full = dp >> 1;
+    for (int j = 0; j < full; ++j) {
+      const uint32_t w = st.hw[j * 32];
+      acc(Tl[__byte_perm(w, 0u, 0x4441u) * 16u], m0, c0);
+      acc(Tl[__byte_perm(w, 0u, 0x4443u) * 16u], m1, c1);
+    }
+    if (dp & 1) acc(Tl[__byte_perm(st.hw[full * 32], 0u, 0x4441u) * 16u], m0, c0);
+  } else {
+    int z = 0;
+    for (; z + 2 <= dp; z += 2) {
+      double a, b;
+      hc_sum2<PP>(st, (uint32_t)z, (uint32_t)z + 1u, pp_rt, Tl, a, b);
+      acc(a, m0, c0);
+      acc(b, m1, c1);
+    }
+    if (z < dp) acc(hc_sum<PP>(st, (uint32_t)z, pp_rt, Tl), m0, c0);
+  }
+  mx = fmax(m0, m1);
+  cnt = (m0 == mx ? c0 : 0) + (m1 == mx ? c1 : 0);
+}
+
+__host__ __device__ inline int hc_warp_state_bytes(int N, int pp, int dp, int dp_cap) {
+  const int plane = align16(((N + 3) / 4) * 128);
+  return 2 * plane + ((pp >= 4 && dp <= dp_cap) ? align16(dp * 256) : 0);
+}
+
+// One warp task of MODE 0.  Every lane runs the same instruction stream whatever its
+// proposal (the swap is always applied tentatively, both touched pipelines are always
+// re-summed), so the only divergent paths are the rare rescans and best-mapping writes.
+template <bool TRACE, int PP>
+__device__ __forceinline__ void run_task_hc(const SaParams& P, const SaTask T, const DevCfg C, const double* Tl,
+                                            unsigned char* ws, int lane) {
+  using RT = RRep;
+  const bool active = lane < T.count;
+  const int N = C.N, pp = PP > 0 ? PP : C.pp, dp = C.dp, n = P.n_nodes;
+  const uint32_t chain = (uint32_t)(T.c_first + (T.k0 + lane) * P.world);
+  const int slot = T.slot0 + lane;
+  S1Ctx X;
+  X.qi = P.qtab + C.qi_off; X.qe = P.qtab + C.qe_off; X.tab = P.subset_max;
+  X.rank = P.tin_rank + (size_t)T.f * 256;
+  X.vs = P.tin_vs + (size_t)T.f * 256;
+  X.n = n;
+  const RT Rdummy{nullptr, n, 0, 0};
+
+  const bool cache = pp >= 4 && dp <= P.psum_dp_cap;   // (pp = 2: re-summing one hop is as cheap)
+  const int plane = align16(((N + 3) / 4) * 128);
+  HcState st;
+  st.hb = ws + lane * 4;
+  st.sb = ws + plane + lane * 4;
+  st.hw = reinterpret_cast<const uint32_t*>(ws) + lane;
+  double* psum = reinterpret_cast<double*>(ws + 2 * plane);
+  uint16_t* bperm = P.best_perm + T.perm_off;
+  S1Reg<RT> s1;
+  s1.clear();
+
+  // ---- initial state: identity mapping (R16) and its latency from scratch
+  {
+    uint32_t prevnd = 0;
+    for (int w = 0; w < N; ++w) {
+      const uint32_t nd = div_small((uint32_t)w, C.spn_magic, (uint32_t)C.spn);
+      const int x = w % pp;
+      st.hb[HcState::off((uint32_t)w)] = (uint8_t)(x == 0 ? nd * 17u : (prevnd | (nd << 4)));
+      st.sb[HcState::off((uint32_t)w)] = (uint8_t)w;
+      bperm[w * 32 + lane] = (uint16_t)w;
+      prevnd = nd;
+    }
+  }
+  __syncwarp();
+  double tpp = 0.0;
+  int nmax = 0;   // pipelines whose sum equals tpp
+  for (int z = 0; z < dp; ++z) {
+    s1.add_init((uint32_t)st.hb[HcState::off((uint32_t)(z * pp))] >> 4);
+    if (pp >= 2) {
+      const double s = hc_sum<PP>(st, (uint32_t)z, pp, Tl);
+      if (cache) psum[z * 32 + lane] = s;
+      if (s > tpp) { tpp = s; nmax = 1; } else if (s == tpp) { ++nmax; }
+    }
+  }
+  s1.finish_init(X, Rdummy);
+
+  const double L0 = compose(C.Sb, C.r, C.Ss, tpp, s1.tin, s1.tex);
+  double cur = L0, best = L0, best_tpp = tpp, best_tdp = __dadd_rn(s1.tin, s1.tex);
+  int best_step = -1;
+  uint32_t accepted = 0;
+  double beta = P.t0 > 0.0 ? __ddiv_rn(1.0, P.t0) : __ddiv_rn(1.0, __dmul_rn(P.tau, L0));
+  const double ia = P.alpha_inv;
+  const int trow = (TRACE && active) ? P.trace_slot[slot] : -1;
+
+  if (N >= 2) {
+    Draw dnext = draw_swap_rk(0u, chain, (uint32_t)C.e, P.rk, (uint32_t)N);
+    for (int i = 0; i < P.iterations; ++i) {
+      const Draw d = dnext;
+      dnext = draw_swap_rk((uint32_t)(i + 1), chain, (uint32_t)C.e, P.rk, (uint32_t)N);
+      const uint32_t p = d.p, q = d.q;
+      uint8_t* const bp = st.hb + HcState::off(p);
+      uint8_t* const bq = st.hb + HcState::off(q);
+      uint8_t* const sp_ = st.sb + HcState::off(p);
+      uint8_t* const sq_ = st.sb + HcState::off(q);
+      const uint32_t hp = *bp, hq = *bq, sp = *sp_, sq = *sq_;
+      const uint32_t np = hp >> 4, nq = hq >> 4;
+      double Lp = cur;
+      bool acc = true, improved = false;
+      if (pp >= 2) {
+        const uint32_t zp = PP > 0 ? p / (uint32_t)PP : div_small(p, C.pp_magic, (uint32_t)pp);
+        const uint32_t zq = PP > 0 ? q / (uint32_t)PP : div_small(q, C.pp_magic, (uint32_t)pp);
+        const uint32_t xp = p - zp * (uint32_t)pp, xq = q - zq * (uint32_t)pp;
+        const bool two = zq != zp;
+        const uint32_t zb = two ? zq : zp;
+        const bool pn = xp + 1u < (uint32_t)pp, qn = xq + 1u < (uint32_t)pp;   // p+1 / q+1 in the same pipeline
+        uint8_t* const bp1 = st.hb + HcState::off(p + 1u);
+        uint8_t* const bq1 = st.hb + HcState::off(q + 1u);
+        const uint32_t hp1 = pn ? *bp1 : 0u, hq1 = qn ? *bq1 : 0u;
+        double oldA, oldB;
+        if (cache) {
+          oldA = psum[zp * 32 + lane];
+          oldB = psum[zb * 32 + lane];
+        } else {
+          hc_sum2<PP>(st, zp, zb, pp, Tl, oldA, oldB);
+        }
+        // the hop codes after swapping the nodes of positions p and q (node'(p) = nq,
+        // node'(q) = np); when p and q are adjacent both formulas give the shared byte
+        const uint32_t vp = xp == 0u ? nq * 17u : (((p - 1u == q) ? np : (hp & 15u)) | (nq << 4));
+        const uint32_t vp1 = nq | (((p + 1u == q) ? np : (hp1 >> 4)) << 4);
+        const uint32_t vq = xq == 0u ? np * 17u : (((q - 1u == p) ? nq : (hq & 15u)) | (np << 4));
+        const uint32_t vq1 = np | (((q + 1u == p) ? nq : (hq1 >> 4)) << 4);
+        *bp = (uint8_t)vp;
+        if (pn) *bp1 = (uint8_t)vp1;
+        *bq = (uint8_t)vq;
+        if (qn) *bq1 = (uint8_t)vq1;
+        double sA, sB;
+        hc_sum2<PP>(st, zp, zb, pp, Tl, sA, sB);
+        // ---- T_PP (Eq.5): max over pipelines with its multiplicity
+        double tpp2 = tpp;
+        int nmax2 = nmax;
+        const double snew = fmax(sA, sB);
+        const int keep = nmax - (oldA == tpp ? 1 : 0) - ((two && oldB == tpp) ? 1 : 0);  // untouched at max
+        if (keep > 0 || snew >= tpp) {
+          tpp2 = (keep > 0) ? fmax(tpp, snew) : snew;
+          nmax2 = (keep > 0 && tpp2 == tpp ? keep : 0) + (sA == tpp2 ? 1 : 0) + ((two && sB == tpp2) ? 1 : 0);
+        } else if (cache) {
+          // the unique max pipeline decreased: rescan the cached sums
+          double m0 = sA, m1 = two ? sB : 0.0;
+          int c0 = 1, c1 = two ? 1 : 0;
+          int z = 0;
+          for (; z + 2 <= dp; z += 2) {
+            const double v0 = ((uint32_t)z == zp || (uint32_t)z == zq) ? 0.0 : psum[z * 32 + lane];
+            const double v1 = ((uint32_t)z + 1u == zp || (uint32_t)z + 1u == zq) ? 0.0 : psum[(z + 1) * 32 + lane];
+            c0 = v0 > m0 ? 1 : c0 + (v0 == m0 ? 1 : 0);
+            m0 = fmax(m0, v0);
+            c1 = v1 > m1 ? 1 : c1 + (v1 == m1 ? 1 : 0);
+            m1 = fmax(m1, v1);
+          }
+          if (z < dp) {
+            const double v0 = ((uint32_t)z == zp || (uint32_t)z == zq) ? 0.0 : psum[z * 32 + lane];
+            c0 = v0 > m0 ? 1 : c0 + (v0 == m0 ? 1 : 0);
+            m0 = fmax(m0, v0);
+          }
+          tpp2 = fmax(m0, m1);
+          nmax2 = (m0 == tpp2 ? c0 : 0) + (m1 == tpp2 ? c1 : 0);
+        } else {
+          // no cache: re-sum every pipeline of the tentative mapping (H already holds it)
+          hc_rescan<PP>(st, dp, pp, Tl, tpp2, nmax2);
+        }
+        // ---- Eq.6: the stage-1 node multiset changes only if exactly one of p, q is a
+        //      stage-1 position and the two nodes differ
+        const bool dpchg = ((xp == 0u) != (xq == 0u)) && np != nq;
+        double tin2 = s1.tin, tex2 = s1.tex;
+        if (dpchg) {
+          const uint32_t dn = xp == 0u ? np : nq;   // node losing a stage-1 DP member
+          const uint32_t up = xp == 0u ? nq : np;   // node gaining one
+          s1.propose(dn, up, X, Rdummy);
+          tin2 = s1.tin2;
+          tex2 = s1.tex2;
+        }
+        Lp = compose(C.Sb, C.r, C.Ss, tpp2, tin2, tex2);
+        acc = metropolis_fast(__dadd_rn(Lp, -cur), beta, d.u);
+        if (acc) {
+          if (cache) {
+            psum[zp * 32 + lane] = sA;
+            psum[zb * 32 + lane] = sB;
+          }
+          tpp = tpp2;
+          nmax = nmax2;
+          if (dpchg) s1.commit();
+          cur = Lp;
+          if (Lp < best) {
+            best = Lp; best_step = i; best_tpp = tpp; best_tdp = __dadd_rn(s1.tin, s1.tex);
+            improved = true;
+          }
+        } else {   // revert the tentative hop codes (reverse order: adjacent bytes end right)
+          if (qn) *bq1 = (uint8_t)hq1;
+          *bq = (uint8_t)hq;
+          if (pn) *bp1 = (uint8_t)hp1;
+          *bp = (uint8_t)hp;
+        }
+      } else {
+        // pp = 1: every position is a stage-1 position, the multiset never changes (Eq.6)
+        // and there are no hops (Eq.5): L' = cur, accepted
+        *bp = (uint8_t)hq;
+        *bq = (uint8_t)hp;
+      }
+      if (acc) {
+        *sp_ = (uint8_t)sq;
+        *sq_ = (uint8_t)sp;
+        ++accepted;
+      }
+      if (improved)
+        for (int w = 0; w < N; ++w) bperm[w * 32 + lane] = (uint16_t)st.sb[HcState::off((uint32_t)w)];
+      if (TRACE && trow >= 0 && i < P.trace_cap) {
+        pipette_trace_record rec;
+        rec.i = (uint32_t)i; rec.p = (uint16_t)d.p; rec.q = (uint16_t)d.q;
+        rec.accept = acc ? 1u : 0u; rec.latency = Lp;
+        P.trace[(size_t)trow * P.trace_cap + i] = rec;
+      }
+      beta = __dmul_rn(beta, ia);
+    }
+  }
+  if (active) {
+    ChainOut o;
+    o.best = best; o.best_tpp = best_tpp; o.best_tdp = best_tdp; o.L0 = L0;
+    o.best_step = best_step; o.accepted = accepted; o.f = T.f; o.c = (int32_t)chain;
+    P.out[slot] = o;
+  }
+}
+
+// MODE 0: n <= 16 nodes, N <= 256, spn <= 15: hop-code chain state (run_task_hc), register
+//         stage-1 state, the block's m2*R table in shared memory, subset-max table.
 // MODE 1: n <= 128, N <= 256: packed positions, S1Large, R through L1.
 // MODE 2: general (N <= 1024): 32-bit positions, S1Large, R through L1.
 template <int MODE, bool TRACE>
 __global__ void __launch_bounds__(kSaThreads, MODE == 0 ? 3 : 2) k_sa_chains(SaParams P) {
   using POS = typename std::conditional<MODE == 2, PosWide, PosPacked>::type;
-  using RT = typename std::conditional<MODE == 0, RRep, typename std::conditional<MODE == 1, RSmem, RGlob>::type>::type;
-  using S1 = typename std::conditional<MODE == 0, S1Reg<RT>, S1Large<RT>>::type;
+  using RT = typename std::conditional<MODE == 1, RSmem, RGlob>::type;
+  using S1 = S1Large<RT>;
   extern __shared__ __align__(16) unsigned char smem[];
   double* Rs = reinterpret_cast<double*>(smem);
-  const int nn = P.n_nodes * P.n_nodes;
-  if (MODE == 0) {
-    for (int i = threadIdx.x; i < (nn << P.r_copies_log2); i += blockDim.x) Rs[i] = P.R[i >> P.r_copies_log2];
-  } else if (MODE == 1) {
+  const int n = P.n_nodes, nn = n * n;
+  if (MODE == 1) {
     for (int i = threadIdx.x; i < nn; i += blockDim.x) Rs[i] = P.R[i];
   }
-  __syncthreads();
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
-  RT R;
-  if constexpr (MODE == 0) {
-    R = RT{Rs, P.n_nodes, lane & ((1 << P.r_copies_log2) - 1), P.r_copies_log2};
-  } else {
-    R = RT{MODE == 1 ? Rs : P.R, P.n_nodes, lane};
-  }
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  RT R{MODE == 1 ? Rs : P.R, n, lane};
+  const double* Tl = Rs + (lane & 15);   // MODE 0: this lane's copy of the block's m2*R table
   unsigned char* ws = smem + P.r_smem_bytes + wid * P.warp_smem_bytes;
-  __shared__ int s_base;
+  __shared__ int s_chunk;
+  int table_cfg = -1;
   for (;;) {
-    // the warps of a block take consecutive tasks: the task list is grouped by config, so
-    // a block runs one code path (I-cache locality) and its warps finish together
+    // a block takes one chunk: up to warps-per-block consecutive tasks of ONE configuration
+    // (host-built), so the block runs one code path (I-cache locality), shares the
+    // configuration's m2*R table (MODE 0), and its warps finish together
     __syncthreads();
-    if (threadIdx.x == 0) s_base = atomicAdd(P.task_counter, nw);
+    if (threadIdx.x == 0) s_chunk = atomicAdd(P.task_counter, 1);
     __syncthreads();
-    const int t = s_base + wid;
-    if (s_base >= P.n_tasks) break;
-    if (t >= P.n_tasks) continue;
+    const int ch = s_chunk;
+    if (ch >= P.n_chunks) break;
+    const int2 chunk = P.chunks[ch];
+    if constexpr (MODE == 0) {
+      const int cfg0 = P.tasks[chunk.x].cfg;
+      if (cfg0 != table_cfg) {   // block-uniform: rebuild the table for this configuration
+        const double m2 = P.cfgs[cfg0].m2;
+        for (int i = threadIdx.x; i < 256 * 16; i += blockDim.x) {
+          const int code = i >> 4, a = code & 15, b = code >> 4;
+          Rs[i] = (a < n && b < n) ? __dmul_rn(m2, P.R[a * n + b]) : 0.0;
+        }
+        table_cfg = cfg0;
+      }
+    }
+    __syncthreads();
+    if (wid >= chunk.y) continue;
+    const int t = chunk.x + wid;
     const SaTask T = P.tasks[t];
     const DevCfg C = P.cfgs[T.cfg];
     unsigned long long t_start = 0;
     if (lane == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_start));
-    switch (C.pp) {   // compile-time pipeline depth for the common power-of-two depths
-      case 1: run_task<POS, S1, RT, TRACE, 1>(P, T, C, R, ws, lane); break;
-      case 2: run_task<POS, S1, RT, TRACE, 2>(P, T, C, R, ws, lane); break;
-      case 4: run_task<POS, S1, RT, TRACE, 4>(P, T, C, R, ws, lane); break;
-      case 8: run_task<POS, S1, RT, TRACE, 8>(P, T, C, R, ws, lane); break;
-      case 16: run_task<POS, S1, RT, TRACE, 16>(P, T, C, R, ws, lane); break;
-      case 32: run_task<POS, S1, RT, TRACE, 32>(P, T, C, R, ws, lane); break;
-      default: run_task<POS, S1, RT, TRACE, 0>(P, T, C, R, ws, lane); break;
+    if constexpr (MODE == 0) {
+      switch (C.pp) {   // compile-time pipeline depth for the common power-of-two depths
+        case 1: run_task_hc<TRACE, 1>(P, T, C, Tl, ws, lane); break;
+        case 2: run_task_hc<TRACE, 2>(P, T, C, Tl, ws, lane); break;
+        case 4: run_task_hc<TRACE, 4>(P, T, C, Tl, ws, lane); break;
+        case 8: run_task_hc<TRACE, 8>(P, T, C, Tl, ws, lane); break;
+        case 16: run_task_hc<TRACE, 16>(P, T, C, Tl, ws, lane); break;
+        case 32: run_task_hc<TRACE, 32>(P, T, C, Tl, ws, lane); break;
+        default: run_task_hc<TRACE, 0>(P, T, C, Tl, ws, lane); break;
+      }
+    } else {
+      switch (C.pp) {
+        case 1: run_task<POS, S1, RT, TRACE, 1>(P, T, C, R, ws, lane); break;
+        case 2: run_task<POS, S1, RT, TRACE, 2>(P, T, C, R, ws, lane); break;
+        case 4: run_task<POS, S1, RT, TRACE, 4>(P, T, C, R, ws, lane); break;
+        case 8: run_task<POS, S1, RT, TRACE, 8>(P, T, C, R, ws, lane); break;
+        case 16: run_task<POS, S1, RT, TRACE, 16>(P, T, C, R, ws, lane); break;
+        case 32: run_task<POS, S1, RT, TRACE, 32>(P, T, C, R, ws, lane); break;
+        default: run_task<POS, S1, RT, TRACE, 0>(P, T, C, R, ws, lane); break;
+      }
     }
     __syncwarp();
     if (lane == 0) {
@@ -842,7 +1176,7 @@ const void* sa_kernel(int mode, bool trace) {
 }
 
 int sa_warp_state_bytes(int mode, int N, int pp, int dp, int n, int dp_cap) {
-  if (mode == 0) return warp_state_bytes<PosPacked>(N, pp, dp, n, false, dp_cap);
+  if (mode == 0) return hc_warp_state_bytes(N, pp, dp, dp_cap);
   if (mode == 1) return warp_state_bytes<PosPacked>(N, pp, dp, n, true, dp_cap);
   return warp_state_bytes<PosWide>(N, pp, dp, n, true, dp_cap);
 }

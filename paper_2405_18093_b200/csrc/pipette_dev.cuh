@@ -74,6 +74,8 @@ struct SaParams {
   int32_t psum_dp_cap;       // pipeline sums cached in shared memory when dp <= this
   const SaTask* tasks;
   int32_t n_tasks;
+  const int2* chunks;        // block work units: (first task, task count <= warps per block), one config each
+  int32_t n_chunks;
   int32_t* task_counter;
   int32_t n_nodes;
   int32_t iterations;
@@ -81,8 +83,6 @@ struct SaParams {
   RoundKeys rk;              // its ten round keys (philox_round_keys(key))
   int32_t world;             // chain ids c = c_first + k*world
   double alpha_inv, tau, t0;
-  int32_t rep;               // R replicated per lane in shared memory
-  int32_t r_copies_log2;     // MODE 0: 32 or 16 copies of R (16 suffice: 64-bit loads go per half-warp)
   int32_t warps_per_block;
   int32_t warp_smem_bytes;   // per-warp chain-state region
   int32_t r_smem_bytes;
