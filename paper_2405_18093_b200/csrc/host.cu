@@ -21,7 +21,7 @@ __global__ void k_enumerate_filter(int, int, unsigned long long, int, pipette_mo
                                    double*, int, EnumOut*);
 const void* eval_kernel(int mode);
 __global__ void k_tin_values(const DevCfg*, const double*, const double*, int, double*);
-const void* sa_kernel(int mode, bool trace);
+const void* sa_kernel(int mode, bool trace, int n_nodes);
 int sa_warp_state_bytes(int mode, int N, int pp, int dp, int n, int dp_cap);
 __global__ void k_node_lists(const double*, int, uint8_t*, double*);
 __global__ void k_pair_list(const double*, int, uint16_t*, double*);
@@ -729,7 +729,7 @@ pipette_status pipette_search(pipette_ctx* ctx, const pipette_model* model, int6
   P.trace_cap = tracing ? o.trace_cap : 0;
   P.trace = tracing ? (pipette_trace_record*)ctx->trace.p : nullptr;
 
-  const void* kern = sa_kernel(mode, tracing);
+  const void* kern = sa_kernel(mode, tracing, n);
   CU(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   int occ = 0;
   CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, wpb * 32, smem));

@@ -174,27 +174,32 @@ struct S1Ctx {
 // value qi(c)*R[a][a] (c >= 2) has a precomputed position in descending order
 // (k_tin_rank); a node's current rank is one byte of rk[], and T_in is the value at the
 // smallest rank present (SIMD byte minimum) -- the max of Eq.6's intra term without a scan.
-template <class RT>
+template <class RT, int NW = 4>
 struct S1Reg {
-  uint64_t cnt, cnt2;
+  // NW = 4: n <= 16 nodes, counts in a 64-bit register, rank bytes in four words;
+  // NW = 2: n <= 8 nodes, counts in a 32-bit register, rank bytes in two words
+  using CT = typename std::conditional<NW == 2, uint32_t, uint64_t>::type;
+  CT cnt, cnt2;
   uint32_t mask, mask2;
   uint32_t rk0, rk1, rk2_, rk3, nk0, nk1, nk2, nk3;   // current / tentative rank bytes
   int k, k2;
   double tin, tex, tin2, tex2;
 
-  static __device__ __forceinline__ uint32_t get(uint64_t c, uint32_t a) { return (uint32_t)(c >> (4u * a)) & 15u; }
-  // byte a of the 16-byte vector (r0..r3) := v (scalars, never an indexed array)
+  static __device__ __forceinline__ uint32_t get(CT c, uint32_t a) { return (uint32_t)(c >> (4u * a)) & 15u; }
+  // byte a of the rank vector (r0..r3) := v (scalars, never an indexed array)
   static __device__ __forceinline__ void set_byte(uint32_t& r0, uint32_t& r1, uint32_t& r2, uint32_t& r3, uint32_t a,
                                                   uint32_t v) {
     const uint32_t sh = (a & 3u) * 8u, q = a >> 2;
     const uint32_t keep = ~(0xffu << sh), put = v << sh;
     r0 = q == 0u ? ((r0 & keep) | put) : r0;
     r1 = q == 1u ? ((r1 & keep) | put) : r1;
-    r2 = q == 2u ? ((r2 & keep) | put) : r2;
-    r3 = q == 3u ? ((r3 & keep) | put) : r3;
+    if constexpr (NW == 4) {
+      r2 = q == 2u ? ((r2 & keep) | put) : r2;
+      r3 = q == 3u ? ((r3 & keep) | put) : r3;
+    }
   }
   static __device__ __forceinline__ double tin_of(uint32_t r0, uint32_t r1, uint32_t r2, uint32_t r3, const S1Ctx& X) {
-    uint32_t m = __vminu4(__vminu4(r0, r1), __vminu4(r2, r3));
+    uint32_t m = NW == 4 ? __vminu4(__vminu4(r0, r1), __vminu4(r2, r3)) : __vminu4(r0, r1);
     m = __vminu4(m, m >> 16);
     m = __vminu4(m, m >> 8) & 0xffu;
     return m == 0xffu ? 0.0 : __ldg(X.vs + m);
@@ -202,8 +207,8 @@ struct S1Reg {
   __device__ __forceinline__ double tex_of(uint32_t m, int kk, const S1Ctx& X) const {
     return kk >= 2 ? __dmul_rn(__ldg(X.qe + kk), __ldg(X.tab + m)) : 0.0;
   }
-  __device__ __forceinline__ void clear() { cnt = 0ull; mask = 0u; }
-  __device__ __forceinline__ void add_init(uint32_t a) { cnt += 1ull << (4u * a); mask |= 1u << a; }
+  __device__ __forceinline__ void clear() { cnt = 0; mask = 0u; }
+  __device__ __forceinline__ void add_init(uint32_t a) { cnt += (CT)1 << (4u * a); mask |= 1u << a; }
   __device__ __forceinline__ void finish_init(const S1Ctx& X, const RT& R) {
     rk0 = rk1 = rk2_ = rk3 = 0xffffffffu;
     for (int a = 0; a < X.n; ++a) set_byte(rk0, rk1, rk2_, rk3, (uint32_t)a, X.rank[a * 16 + get(cnt, (uint32_t)a)]);
@@ -214,7 +219,7 @@ struct S1Reg {
   // a stage-1 member moves from node dn to node up (tentative state)
   __device__ __forceinline__ void propose(uint32_t dn, uint32_t up, const S1Ctx& X, const RT& R) {
     const uint32_t c_dn = get(cnt, dn) - 1u, c_up = get(cnt, up) + 1u;
-    cnt2 = cnt - (1ull << (4u * dn)) + (1ull << (4u * up));
+    cnt2 = cnt - ((CT)1 << (4u * dn)) + ((CT)1 << (4u * up));
     mask2 = (mask & (c_dn == 0u ? ~(1u << dn) : 0xffffffffu)) | (1u << up);
     k2 = __popc(mask2);
     nk0 = rk0; nk1 = rk1; nk2 = rk2_; nk3 = rk3;
@@ -738,7 +743,7 @@ __host__ __device__ inline int hc_warp_state_bytes(int N, int pp, int dp, int dp
 // One warp task of MODE 0.  Every lane runs the same instruction stream whatever its
 // proposal (the swap is always applied tentatively, both touched pipelines are always
 // re-summed), so the only divergent paths are the rare rescans and best-mapping writes.
-template <bool TRACE, int PP>
+template <bool TRACE, int PP, int NW>
 __device__ __forceinline__ void run_task_hc(const SaParams& P, const SaTask T, const DevCfg C, const double* Tl,
                                             unsigned char* ws, int lane) {
   using RT = RRep;
@@ -761,7 +766,7 @@ __device__ __forceinline__ void run_task_hc(const SaParams& P, const SaTask T, c
   st.hw = reinterpret_cast<const uint32_t*>(ws) + lane;
   double* psum = reinterpret_cast<double*>(ws + 2 * plane);
   uint16_t* bperm = P.best_perm + T.perm_off;
-  S1Reg<RT> s1;
+  S1Reg<RT, NW> s1;
   s1.clear();
 
   // ---- initial state: identity mapping (R16) and its latency from scratch
@@ -938,7 +943,7 @@ __device__ __forceinline__ void run_task_hc(const SaParams& P, const SaTask T, c
 //         stage-1 state, the block's m2*R table in shared memory, subset-max table.
 // MODE 1: n <= 128, N <= 256: packed positions, S1Large, R through L1.
 // MODE 2: general (N <= 1024): 32-bit positions, S1Large, R through L1.
-template <int MODE, bool TRACE>
+template <int MODE, bool TRACE, int NW = 4>
 __global__ void __launch_bounds__(kSaThreads, MODE == 0 ? 3 : 2) k_sa_chains(SaParams P) {
   using POS = typename std::conditional<MODE == 2, PosWide, PosPacked>::type;
   using RT = typename std::conditional<MODE == 1, RSmem, RGlob>::type;
@@ -985,13 +990,13 @@ __global__ void __launch_bounds__(kSaThreads, MODE == 0 ? 3 : 2) k_sa_chains(SaP
     if (lane == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_start));
     if constexpr (MODE == 0) {
       switch (C.pp) {   // compile-time pipeline depth for the common power-of-two depths
-        case 1: run_task_hc<TRACE, 1>(P, T, C, Tl, ws, lane); break;
-        case 2: run_task_hc<TRACE, 2>(P, T, C, Tl, ws, lane); break;
-        case 4: run_task_hc<TRACE, 4>(P, T, C, Tl, ws, lane); break;
-        case 8: run_task_hc<TRACE, 8>(P, T, C, Tl, ws, lane); break;
-        case 16: run_task_hc<TRACE, 16>(P, T, C, Tl, ws, lane); break;
-        case 32: run_task_hc<TRACE, 32>(P, T, C, Tl, ws, lane); break;
-        default: run_task_hc<TRACE, 0>(P, T, C, Tl, ws, lane); break;
+        case 1: run_task_hc<TRACE, 1, NW>(P, T, C, Tl, ws, lane); break;
+        case 2: run_task_hc<TRACE, 2, NW>(P, T, C, Tl, ws, lane); break;
+        case 4: run_task_hc<TRACE, 4, NW>(P, T, C, Tl, ws, lane); break;
+        case 8: run_task_hc<TRACE, 8, NW>(P, T, C, Tl, ws, lane); break;
+        case 16: run_task_hc<TRACE, 16, NW>(P, T, C, Tl, ws, lane); break;
+        case 32: run_task_hc<TRACE, 32, NW>(P, T, C, Tl, ws, lane); break;
+        default: run_task_hc<TRACE, 0, NW>(P, T, C, Tl, ws, lane); break;
       }
     } else {
       switch (C.pp) {
@@ -1169,8 +1174,9 @@ __global__ void __launch_bounds__(256) k_argmin(const ChainOut* __restrict__ out
 }
 
 // Host-side handles of the K3 variants (MODE 0/1/2 as above; TRACE records).
-const void* sa_kernel(int mode, bool trace) {
-  if (mode == 0) return trace ? (const void*)k_sa_chains<0, true> : (const void*)k_sa_chains<0, false>;
+const void* sa_kernel(int mode, bool trace, int n_nodes) {
+  if (mode == 0 && n_nodes <= 8) return trace ? (const void*)k_sa_chains<0, true, 2> : (const void*)k_sa_chains<0, false, 2>;
+  if (mode == 0) return trace ? (const void*)k_sa_chains<0, true, 4> : (const void*)k_sa_chains<0, false, 4>;
   if (mode == 1) return trace ? (const void*)k_sa_chains<1, true> : (const void*)k_sa_chains<1, false>;
   return trace ? (const void*)k_sa_chains<2, true> : (const void*)k_sa_chains<2, false>;
 }
