@@ -20,6 +20,7 @@ __global__ void k_enumerate_filter(int, int, unsigned long long, int, pipette_mo
                                    const pipette_profile_entry*, int, DevCfg*, unsigned long long*, int, int*,
                                    double*, int, EnumOut*);
 const void* eval_kernel(int mode);
+size_t eval_smem_bytes(int mode, int perm_stride, bool staged, int n_nodes, int E, int bm_words);
 __global__ void k_tin_values(const DevCfg*, const double*, const double*, int, double*);
 const void* sa_kernel(int mode, bool trace, int n_nodes);
 int sa_warp_state_bytes(int mode, int N, int pp, int dp, int n, int dp_cap);
@@ -29,7 +30,7 @@ __global__ void k_tin_list(const DevCfg*, const int*, const double*, const doubl
 __global__ void k_subset_max(const double*, int, double*);
 __global__ void k_tin_rank(const DevCfg*, const int*, const double*, const double*, int, uint8_t*, double*);
 __global__ void k_argmin(const ChainOut*, const int*, int, CfgBest*);
-constexpr int kEnumThreads = 1024, kEvalThreads = 256, kSaThreads = 128;
+constexpr int kEnumThreads = 1024, kSaThreads = 128;
 
 // K5 (combine, phase 1): per-config local winner item id if it attains the global
 // minimum latency, else UINT64_MAX (second allreduce(min) of R18).
@@ -486,24 +487,24 @@ pipette_status pipette_eval(pipette_ctx* ctx, const pipette_model* model, int64_
   P.perm_stride = perm_stride;
   P.vec16 = ((uintptr_t)d_perm % 16 == 0) && (perm_stride % 8 == 0);
   P.bm_words = (maxN + 31) / 32;
-  const int nn = ctx->n_nodes * ctx->n_nodes;
-  const bool rep = mode == 0;
   P.latency = d_latency;
   P.mem = (unsigned long long*)d_mem;
   P.status = d_status;
-  const size_t smem = (size_t)(rep ? nn * 32 : nn) * 8 + ((ctx->E * 8 + 15) & ~15) +
-                      (size_t)(P.bm_words + (ctx->n_nodes + 3) / 4) * kEvalThreads * 4 +
-                      2048 * sizeof(int) + 4096 * sizeof(int) + 2048 * sizeof(short);
+  // rows gathered into per-warp shared staging buffers when they are 16-byte aligned and
+  // the buffers fit beside the tables (else read straight from global memory)
+  size_t smem = eval_smem_bytes(mode, perm_stride, P.vec16 != 0, ctx->n_nodes, ctx->E, P.bm_words);
+  P.staged = P.vec16 && perm_stride <= 64 && smem <= 96 * 1024;   // long rows: direct 16-byte loads measured faster
+  if (!P.staged) smem = eval_smem_bytes(mode, perm_stride, false, ctx->n_nodes, ctx->E, P.bm_words);
   if (smem > 227 * 1024) return fail(ctx, PIPETTE_E_UNSUPPORTED, "eval shared memory %zu B too large", smem);
   const void* kern = eval_kernel(mode);
   CU(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   int occ = 0;
-  CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kEvalThreads, smem));
+  CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, 256, smem));
   occ = std::max(occ, 1);
   const long long need = (n + 2047) / 2048;   // tiles of 2048 candidates
   const int grid = (int)std::min<long long>(need, (long long)occ * ctx->n_sms);
   void* args[] = {&P};
-  CU(cudaLaunchKernel(kern, dim3(grid), dim3(kEvalThreads), args, smem, s));
+  CU(cudaLaunchKernel(kern, dim3(grid), dim3(256), args, smem, s));
   ctx->launches++;
   CU(cudaGetLastError());
   return PIPETTE_OK;

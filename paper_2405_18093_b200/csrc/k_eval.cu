@@ -5,8 +5,13 @@
 // HBM-bound by design: 8 B of configuration + 2N B of mapping in, 17 B out per
 // candidate.  One thread per candidate (DESIGN.md section 7 explains why not one warp:
 // the per-candidate work is a sequential, fixed-order sum, and thread-per-candidate
-// keeps all 32 lanes busy).  The mapping row is read with 16-byte vector loads; the
-// config table keys and R = 1/B (lane-replicated when small) live in shared memory.
+// keeps all 32 lanes busy).  A block works on tiles of TR candidates (TR = its thread
+// count); the tile's mapping rows -- one contiguous range of HBM -- are staged into
+// shared memory with coalesced 16-byte cp.async copies, double-buffered so the next
+// tile streams in while this one is evaluated, and stored with the 128-byte XOR swizzle
+// (16-byte chunk c of 128-byte line l at chunk c ^ (l & 7)) so that the per-thread row
+// reads are bank-conflict free.  The config table keys and R = 1/B (16 lane copies when
+// small) live in shared memory.
 //   MODE 0 (n <= 16 nodes, <= 15 slots per node): the pipeline depth is a template
 //          parameter (the stage of each mapping slot is static inside a 16-byte chunk),
 //          stage-1 node counts are nibbles of a 64-bit register, the bijection bitmap is
@@ -19,9 +24,6 @@
 
 namespace pip {
 
-constexpr int kEvalThreads = 256;
-constexpr int kEvalTile = 2048;            // candidates per block iteration (bucketed by config)
-constexpr int kEvalMaxBucketCfgs = 4096;   // histogram capacity
 
 // Exclusive block-wide scan (one int per thread); total = block sum.
 __device__ int block_scan_excl_eval(int v, int* sh, int& total) {
@@ -50,11 +52,8 @@ __device__ int block_scan_excl_eval(int v, int* sh, int& total) {
   return excl;
 }
 
-// End of the per-thread scratch (bitmap, counts) in the dynamic shared-memory layout.
-__device__ __forceinline__ unsigned char* cnt_end(const EvalParams& P, unsigned char* smem, int r_bytes) {
-  return smem + r_bytes + ((P.E * 8 + 15) & ~15) +
-         (size_t)(P.bm_words + (P.n_nodes + 3) / 4) * kEvalThreads * 4;
-}
+// 128-byte XOR swizzle of a byte offset inside a staging buffer (16-byte granules).
+__device__ __forceinline__ uint32_t swz(uint32_t x) { return x ^ (((x >> 7) & 7u) << 4); }
 
 // PTX shl.b32: shift amounts >= 32 give 0 (C's << is undefined there).
 __device__ __forceinline__ uint32_t shl_clamp(uint32_t x, uint32_t sh) {
@@ -63,29 +62,42 @@ __device__ __forceinline__ uint32_t shl_clamp(uint32_t x, uint32_t sh) {
   return r;
 }
 
+// Where a candidate's mapping row is read from: the swizzled staging buffer (16-byte
+// aligned rows) or global memory (any stride).
+struct RowSrc {
+  const unsigned char* sbuf;   // staging buffer of the warp (nullptr: global)
+  uint32_t roff;               // byte offset of the row inside the buffer
+  const uint16_t* g;           // global row
+  bool vec;                    // 16-byte chunks (staged, or 16-byte aligned global rows)
+  __device__ __forceinline__ uint4 chunk(int k) const {   // 8 slots [8k, 8k+8)
+    if (sbuf) return *reinterpret_cast<const uint4*>(sbuf + swz(roff + (uint32_t)k * 16u));
+    return __ldg(reinterpret_cast<const uint4*>(g) + k);
+  }
+  __device__ __forceinline__ uint32_t slot(int w) const { return __ldg(g + w); }
+};
+
 struct EvalShared {
   const double* Rs;
-  uint32_t* bm;     // [bm_words][kEvalThreads]
-  uint32_t* cnt;    // [ceil(n/4)][kEvalThreads]
-  int n, tid, lane;
+  uint32_t* bm;     // [bm_words][T]
+  uint32_t* cnt;    // [ceil(n/4)][T]
+  int n, tid, lane, T;
 };
 
 template <bool REP>
 __device__ __forceinline__ double r_at(const EvalShared& S, uint32_t a, uint32_t b) {
-  return REP ? S.Rs[((int)a * S.n + (int)b) * 32 + S.lane] : S.Rs[(int)a * S.n + (int)b];
+  return REP ? S.Rs[((int)a * S.n + (int)b) * 16 + (S.lane & 15)] : S.Rs[(int)a * S.n + (int)b];
 }
 
 // MODE 0 evaluation of one candidate with compile-time pipeline depth PP (0: runtime).
 template <int PP, bool RB>
 __device__ __forceinline__ void eval_small(const EvalParams& P, const EvalShared& S, const DevCfg& C,
-                                           const uint16_t* row, long long i, int e) {
-  constexpr bool N8 = false;
+                                           const RowSrc& row, long long i, int e) {
   const int N = C.N;
   const int pp = PP > 0 ? PP : C.pp;
   const uint32_t spn = (uint32_t)C.spn;
   constexpr bool regbm = RB;   // N <= 64: bitmap in a register pair
   if (!regbm)
-    for (int w = 0; w < (N + 31) / 32; ++w) S.bm[w * kEvalThreads + S.tid] = 0u;
+    for (int w = 0; w < (N + 31) / 32; ++w) S.bm[w * S.T + S.tid] = 0u;
   // Bijection test (Eq.2): OR the bit of every slot id into [0, 64) (a 2x32-bit register
   // pair; shl clamps, so ids >= 64 set nothing).  The row is a permutation of [0, N) iff
   // exactly the N low bits end up set: an id >= N sets a bit above N or none, and a
@@ -104,13 +116,13 @@ __device__ __forceinline__ void eval_small(const EvalParams& P, const EvalShared
     } else {
       bad |= v >= (uint32_t)N;
       v = min(v, (uint32_t)N - 1u);
-      uint32_t& bw = S.bm[(v >> 5) * kEvalThreads + S.tid];
+      uint32_t& bw = S.bm[(v >> 5) * S.T + S.tid];
       bw |= 1u << (v & 31);
     }
     const uint32_t nd = div_small(v, C.spn_magic, spn);
     if (stage1) {                                    // stage-1 worker of pipeline z (Eq.6)
       c_lo += shl_clamp(1u, 4u * nd);
-      if (!N8) c_hi += shl_clamp(1u, 4u * nd - 32u);
+      c_hi += shl_clamp(1u, 4u * nd - 32u);
       s = 0.0;
     } else {                                         // Eq.5 hop x-1 -> x, stage order
       s = __dadd_rn(s, __dmul_rn(C.m2, r_at<true>(S, prev, nd)));
@@ -131,15 +143,10 @@ __device__ __forceinline__ void eval_small(const EvalParams& P, const EvalShared
       x = (x + 1 == pp) ? 0 : x + 1;
     }
   };
-  if (P.vec16) {
-    const uint4* r4 = reinterpret_cast<const uint4*>(row);
+  if (row.vec) {
     const int full = N & ~7;                         // whole 8-slot chunks: no per-slot guard
-    uint4 nxt = full > 0 ? __ldg(r4) : make_uint4(0u, 0u, 0u, 0u);
-    uint4 nxt2 = full > 8 ? __ldg(r4 + 1) : make_uint4(0u, 0u, 0u, 0u);
     for (int w0 = 0; w0 < full; w0 += 8) {
-      const uint4 v = nxt;                           // chunk w0 (loaded two chunks ahead)
-      nxt = nxt2;
-      if (w0 + 16 < full) nxt2 = __ldg(r4 + ((w0 + 16) >> 3));
+      const uint4 v = row.chunk(w0 >> 3);
       const uint32_t pk[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
       for (int j = 0; j < 8; ++j) {
@@ -149,7 +156,7 @@ __device__ __forceinline__ void eval_small(const EvalParams& P, const EvalShared
       }
     }
     if (full < N) {
-      const uint4 v = __ldg(r4 + (full >> 3));
+      const uint4 v = row.chunk(full >> 3);
       const uint32_t pk[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
       for (int j = 0; j < 8; ++j) {
@@ -163,7 +170,7 @@ __device__ __forceinline__ void eval_small(const EvalParams& P, const EvalShared
   } else {
     for (int w = 0; w < N; ++w) {
       const bool st = (w % pp) == 0, la = (w % pp) == pp - 1;
-      visit(__ldg(row + w), st, la);
+      visit(row.slot(w), st, la);
     }
   }
   bool ok = !bad;
@@ -173,7 +180,7 @@ __device__ __forceinline__ void eval_small(const EvalParams& P, const EvalShared
     ok = seen_lo == want_lo && seen_hi == want_hi;
   } else {
     int c = 0;
-    for (int w = 0; w < (N + 31) / 32; ++w) c += __popc(S.bm[w * kEvalThreads + S.tid]);
+    for (int w = 0; w < (N + 31) / 32; ++w) c += __popc(S.bm[w * S.T + S.tid]);
     ok = ok && c == N;
   }
   // stage-1 node set N1 from the nibble counts: bit a set iff nibble a is non-zero
@@ -207,18 +214,18 @@ __device__ __forceinline__ void eval_small(const EvalParams& P, const EvalShared
 
 template <int PP>
 __device__ __forceinline__ void dispatch_n(const EvalParams& P, const EvalShared& S, const DevCfg& C,
-                                           const uint16_t* row, long long i, int e) {
+                                           const RowSrc& row, long long i, int e) {
   if (C.N <= 64) eval_small<PP, true>(P, S, C, row, i, e);    // bijection bitmap in registers
   else eval_small<PP, false>(P, S, C, row, i, e);
 }
 
 // MODE 1 (general) evaluation of one candidate.
 __device__ __forceinline__ void eval_general(const EvalParams& P, const EvalShared& S, const DevCfg& C,
-                                             const uint16_t* row, long long i) {
+                                             const RowSrc& row, long long i) {
   const int N = C.N, pp = C.pp;
   const uint32_t spn = (uint32_t)C.spn;
-  for (int w = 0; w < (N + 31) / 32; ++w) S.bm[w * kEvalThreads + S.tid] = 0u;
-  for (int w = 0; w < (S.n + 3) / 4; ++w) S.cnt[w * kEvalThreads + S.tid] = 0u;
+  for (int w = 0; w < (N + 31) / 32; ++w) S.bm[w * S.T + S.tid] = 0u;
+  for (int w = 0; w < (S.n + 3) / 4; ++w) S.cnt[w * S.T + S.tid] = 0u;
   Mask<4> mask;
   mask.clear();
   bool ok = true;
@@ -230,14 +237,14 @@ __device__ __forceinline__ void eval_general(const EvalParams& P, const EvalShar
     if (v >= (uint32_t)N) {
       ok = false;
     } else {
-      uint32_t& bw = S.bm[(v >> 5) * kEvalThreads + S.tid];
+      uint32_t& bw = S.bm[(v >> 5) * S.T + S.tid];
       const uint32_t bit = 1u << (v & 31);
       if (bw & bit) ok = false;
       bw |= bit;
       nd = div_small(v, C.spn_magic, spn);
     }
     if (x == 0) {
-      S.cnt[(nd >> 2) * kEvalThreads + S.tid] += 1u << ((nd & 3) * 8);
+      S.cnt[(nd >> 2) * S.T + S.tid] += 1u << ((nd & 3) * 8);
       mask.set(nd);
       s = 0.0;
     } else {
@@ -249,17 +256,16 @@ __device__ __forceinline__ void eval_general(const EvalParams& P, const EvalShar
       if (pp >= 2) tpp = fmax(tpp, s);
     }
   };
-  if (P.vec16) {
-    const uint4* r4 = reinterpret_cast<const uint4*>(row);
+  if (row.vec) {
     for (int w0 = 0; w0 < N; w0 += 8) {
-      const uint4 v = __ldg(r4 + (w0 >> 3));
+      const uint4 v = row.chunk(w0 >> 3);
       const uint32_t pk[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
       for (int j = 0; j < 8; ++j)
         if (w0 + j < N) visit((pk[j >> 1] >> ((j & 1) * 16)) & 0xffffu);
     }
   } else {
-    for (int w = 0; w < N; ++w) visit(__ldg(row + w));
+    for (int w = 0; w < N; ++w) visit(row.slot(w));
   }
   P.mem[i] = C.mem;
   const double qnan = __longlong_as_double(0x7ff8000000000000ll);
@@ -273,7 +279,7 @@ __device__ __forceinline__ void eval_general(const EvalParams& P, const EvalShar
     while (bits) {
       const uint32_t a = wd * 32 + __ffs(bits) - 1;
       bits &= bits - 1;
-      const uint32_t c = (S.cnt[(a >> 2) * kEvalThreads + S.tid] >> ((a & 3) * 8)) & 0xffu;
+      const uint32_t c = (S.cnt[(a >> 2) * S.T + S.tid] >> ((a & 3) * 8)) & 0xffu;
       if (c >= 2) t_in = fmax(t_in, __dmul_rn(__ldg(qi + c), r_at<false>(S, a, a)));
 #pragma unroll
       for (int wd2 = 0; wd2 < 4; ++wd2) {
@@ -292,40 +298,70 @@ __device__ __forceinline__ void eval_general(const EvalParams& P, const EvalShar
   P.status[i] = C.feasible ? 0 : 1;
 }
 
+constexpr int kEvalThreads = 256;
+constexpr int kEvalTile = 2048;   // candidates per block tile (bucketed by configuration)
+
+// Gather the mapping rows of 32 candidates (tile positions ks[0..31], -1 = none) into a
+// warp's staging buffer: 16-byte cp.async pieces, lanes 8r..8r+7 of a 128-byte row
+// reading one whole line (coalesced), stored swizzled at row r * rb.
+__device__ __forceinline__ void gather_rows(const EvalParams& P, unsigned char* wbuf, const short* ks, long long base,
+                                            uint32_t rb, int lane) {
+  const uint32_t pr = rb >> 4;   // pieces per row
+  const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(wbuf);
+  const unsigned char* src = reinterpret_cast<const unsigned char*>(P.perm);
+  const bool pow2 = (pr & (pr - 1u)) == 0u;
+  const uint32_t sh = 31u - __clz(pr);
+  for (uint32_t pc = (uint32_t)lane; pc < 32u * pr; pc += 32u) {
+    const uint32_t r = pow2 ? pc >> sh : pc / pr, c = pc - r * pr;
+    const int k = ks[r];
+    if (k >= 0)
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sbase + swz(r * rb + c * 16u)),
+                   "l"(src + (size_t)(base + k) * rb + c * 16u)
+                   : "memory");
+  }
+  asm volatile("cp.async.commit_group;\n" ::: "memory");
+}
+
 template <int MODE>
 __global__ void __launch_bounds__(kEvalThreads) k_eval_stream(EvalParams P) {
   constexpr bool REP = MODE == 0;
-  extern __shared__ __align__(16) unsigned char smem[];
+  extern __shared__ __align__(128) unsigned char smem[];
   const int n = P.n_nodes, nn = n * n;
-  const int tid = threadIdx.x;
-  double* Rs = reinterpret_cast<double*>(smem);
-  const int r_bytes = (REP ? nn * 32 : nn) * 8;
-  unsigned long long* keys = reinterpret_cast<unsigned long long*>(smem + r_bytes);
-  uint32_t* bm = reinterpret_cast<uint32_t*>(smem + r_bytes + ((P.E * 8 + 15) & ~15));
-  if (REP) {
-    for (int i = tid; i < nn * 32; i += blockDim.x) Rs[i] = P.R[i >> 5];
-  } else {
-    for (int i = tid; i < nn; i += blockDim.x) Rs[i] = P.R[i];
-  }
-  for (int i = tid; i < P.E; i += blockDim.x) keys[i] = P.keys[i];
-  __syncthreads();
-  const EvalShared S{Rs, bm, bm + P.bm_words * kEvalThreads, n, tid, tid & 31};
-  const double qnan = __longlong_as_double(0x7ff8000000000000ll);
-  // tile bucketing: candidates of a tile are processed grouped by configuration, so the
-  // lanes of a warp run the same code path (mixed batches)
-  int* tile_e = reinterpret_cast<int*>(cnt_end(P, smem, r_bytes));
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5, nwarps = kEvalThreads / 32;
+  // layout: [warp staging buffers nwarps x 32 x rb][R][keys][per-thread scratch]
+  //         [tile_e][hist][order]
+  const uint32_t rb = (uint32_t)P.perm_stride * 2u;
+  const bool staged = P.staged != 0;
+  const uint32_t wb_bytes = staged ? 32u * rb : 0u;   // one buffer
+  unsigned char* wbuf = smem + (size_t)wid * wb_bytes;
+  size_t off = (size_t)nwarps * wb_bytes;
+  double* Rs = reinterpret_cast<double*>(smem + off);
+  off += (size_t)(REP ? nn * 16 : nn) * 8;
+  unsigned long long* keys = reinterpret_cast<unsigned long long*>(smem + off);
+  off += ((size_t)P.E * 8 + 15) & ~(size_t)15;
+  uint32_t* bm = reinterpret_cast<uint32_t*>(smem + off);
+  off += (size_t)(P.bm_words + (n + 3) / 4) * kEvalThreads * 4;
+  int* tile_e = reinterpret_cast<int*>(smem + off);
   int* hist = tile_e + kEvalTile;
-  short* order = reinterpret_cast<short*>(hist + kEvalMaxBucketCfgs);
+  short* order = reinterpret_cast<short*>(hist + ((P.E + 2 + 3) & ~3));
   __shared__ int sh_scan[32];
-  const bool bucket = P.E + 1 <= kEvalMaxBucketCfgs;
+
+  if (REP) {
+    for (int i = tid; i < nn * 16; i += kEvalThreads) Rs[i] = P.R[i >> 4];
+  } else {
+    for (int i = tid; i < nn; i += kEvalThreads) Rs[i] = P.R[i];
+  }
+  for (int i = tid; i < P.E; i += kEvalThreads) keys[i] = P.keys[i];
+  __syncthreads();
+  const EvalShared S{Rs, bm, bm + P.bm_words * kEvalThreads, n, tid, lane, kEvalThreads};
+  const double qnan = __longlong_as_double(0x7ff8000000000000ll);
+  const bool bucket_ok = P.E + 1 <= 32767;
 
   for (long long base = (long long)blockIdx.x * kEvalTile; base < P.n; base += (long long)gridDim.x * kEvalTile) {
     const int cnt_valid = (int)min((long long)kEvalTile, P.n - base);
-    if (bucket) {
-      for (int k = tid; k <= P.E; k += blockDim.x) hist[k] = 0;
-      __syncthreads();
-    }
-    for (int k = tid; k < cnt_valid; k += blockDim.x) {
+    // configuration lookup (Alg.1 l.3-5 membership) of every candidate of the tile
+    bool mixed = false;
+    for (int k = tid; k < cnt_valid; k += kEvalThreads) {
       const pipette_config cf = P.cand[base + k];
       const unsigned long long key = ((unsigned long long)cf.pp << 48) | ((unsigned long long)cf.tp << 32) |
                                      ((unsigned long long)cf.dp << 16) | (unsigned long long)cf.mb;
@@ -334,15 +370,21 @@ __global__ void __launch_bounds__(kEvalThreads) k_eval_stream(EvalParams P) {
         const int mid = (lo + hi) >> 1;
         if (keys[mid] < key) lo = mid + 1; else hi = mid;
       }
-      const int e = (lo >= P.E || keys[lo] != key) ? -1 : lo;   // -1: not in the enumeration (Alg.1 l.3-5)
+      const int e = (lo >= P.E || keys[lo] != key) ? -1 : lo;   // -1: not in the enumeration
       tile_e[k] = e;
-      if (bucket) atomicAdd(&hist[e + 1], 1);
     }
     __syncthreads();
-    if (bucket) {
-      // exclusive scan of the per-config histogram, then scatter tile positions
+    for (int k = tid; k < cnt_valid; k += kEvalThreads) mixed |= tile_e[k] != tile_e[0];
+    // a tile of one configuration is evaluated in candidate order (coalesced rows and
+    // outputs); a mixed tile is bucketed by configuration so a warp shares a code path
+    mixed = __syncthreads_or(mixed) && bucket_ok;
+    if (mixed) {
+      for (int k = tid; k <= P.E; k += kEvalThreads) hist[k] = 0;
+      __syncthreads();
+      for (int k = tid; k < cnt_valid; k += kEvalThreads) atomicAdd(&hist[tile_e[k] + 1], 1);
+      __syncthreads();
       int carry = 0;
-      for (int b0 = 0; b0 <= P.E; b0 += blockDim.x) {
+      for (int b0 = 0; b0 <= P.E; b0 += kEvalThreads) {
         const int k = b0 + tid;
         const int v = k <= P.E ? hist[k] : 0;
         int tot;
@@ -351,33 +393,64 @@ __global__ void __launch_bounds__(kEvalThreads) k_eval_stream(EvalParams P) {
         if (k <= P.E) hist[k] = ex;
       }
       __syncthreads();
-      for (int k = tid; k < cnt_valid; k += blockDim.x) order[atomicAdd(&hist[tile_e[k] + 1], 1)] = (short)k;
-      __syncthreads();
+      for (int k = tid; k < cnt_valid; k += kEvalThreads) order[atomicAdd(&hist[tile_e[k] + 1], 1)] = (short)k;
+    } else {
+      for (int k = tid; k < kEvalTile; k += kEvalThreads) order[k] = (short)k;
     }
-    for (int sidx = tid; sidx < cnt_valid; sidx += blockDim.x) {
-      const int k = bucket ? order[sidx] : sidx;
-      const long long i = base + k;
-      const int e = tile_e[k];
-      if (e < 0) {
-        P.latency[i] = qnan; P.mem[i] = 0ull; P.status[i] = 2;
-        continue;
+    if (staged)   // sentinel past the tile: gathers of the last group skip missing rows
+      for (int k = cnt_valid + tid; k < kEvalTile; k += kEvalThreads) order[k] = -1;
+    __syncthreads();
+
+    // warp w takes the groups of 32 sorted positions g = w, w + 8, ...; its rows stream
+    // into one half of its staging buffer while the other half is evaluated
+    const int groups = (cnt_valid + 31) >> 5;
+    for (int g = wid; g < groups; g += nwarps) {
+      unsigned char* cur = wbuf;
+      if (staged) {   // (one buffer per warp: the other resident warps hide the gather)
+        gather_rows(P, wbuf, order + g * 32, base, rb, lane);
+        asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+        __syncwarp();
       }
-      const DevCfg C = P.cfgs[e];
-      const uint16_t* row = P.perm + i * (long long)P.perm_stride;
-      if (MODE == 0) {
-        switch (C.pp) {
-          case 1: dispatch_n<1>(P, S, C, row, i, e); break;
-          case 2: dispatch_n<2>(P, S, C, row, i, e); break;
-          case 4: dispatch_n<4>(P, S, C, row, i, e); break;
-          case 8: dispatch_n<8>(P, S, C, row, i, e); break;
-          default: dispatch_n<0>(P, S, C, row, i, e); break;
+      const int sidx = g * 32 + lane;
+      if (sidx < cnt_valid) {
+        const int k = order[sidx];
+        const long long i = base + k;
+        const int e = tile_e[k];
+        if (e < 0) {
+          P.latency[i] = qnan; P.mem[i] = 0ull; P.status[i] = 2;
+        } else {
+          const DevCfg C = P.cfgs[e];
+          RowSrc row;
+          row.sbuf = staged ? cur : nullptr;
+          row.roff = (uint32_t)lane * rb;
+          row.g = P.perm + i * (long long)P.perm_stride;
+          row.vec = P.vec16 != 0;
+          if (MODE == 0) {
+            switch (C.pp) {
+              case 1: dispatch_n<1>(P, S, C, row, i, e); break;
+              case 2: dispatch_n<2>(P, S, C, row, i, e); break;
+              case 4: dispatch_n<4>(P, S, C, row, i, e); break;
+              case 8: dispatch_n<8>(P, S, C, row, i, e); break;
+              default: dispatch_n<0>(P, S, C, row, i, e); break;
+            }
+          } else {
+            eval_general(P, S, C, row, i);
+          }
         }
-      } else {
-        eval_general(P, S, C, row, i);
       }
+      __syncwarp();   // the buffer is refilled by the next group
     }
     __syncthreads();
   }
+}
+
+// Dynamic shared memory of k_eval_stream (staged: per-warp double-buffered row staging).
+size_t eval_smem_bytes(int mode, int perm_stride, bool staged, int n_nodes, int E, int bm_words) {
+  const size_t nn = (size_t)n_nodes * n_nodes;
+  const size_t wb = staged ? (size_t)32 * perm_stride * 2 : 0;
+  return (size_t)(kEvalThreads / 32) * wb + (mode == 0 ? nn * 16 : nn) * 8 + (((size_t)E * 8 + 15) & ~(size_t)15) +
+         (size_t)(bm_words + (n_nodes + 3) / 4) * kEvalThreads * 4 + (size_t)kEvalTile * sizeof(int) +
+         (size_t)((E + 2 + 3) & ~3) * sizeof(int) + (size_t)kEvalTile * sizeof(short);
 }
 
 // qi(c) R[a][a] for every enumerated config, node a < n <= 16 and c < 16 (0 for c < 2):

@@ -109,6 +109,7 @@ struct EvalParams {
   const uint16_t* perm;
   int32_t perm_stride;
   int32_t vec16;             // perm rows are 16-byte aligned
+  int32_t staged;            // rows gathered into per-warp shared staging buffers (vec16, fits)
   int32_t bm_words;          // bitmap words per thread (ceil(maxN/32))
   int32_t rep;
   double* latency;
