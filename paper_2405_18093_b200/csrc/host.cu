@@ -198,7 +198,8 @@ pipette_status upload_bw(pipette_ctx* ctx, const double* bw) {
     k_subset_max<<<((1 << n) + 255) / 256, 256>>>(ctx->dR, n, ctx->dTab);
     CU(cudaGetLastError());
     CU(cudaDeviceSynchronize());
-  } else {
+  }
+  if (n >= 2) {   // sorted partner / pair lists (MODE 1 and 2 stage-1 searches)
     const size_t L1 = (size_t)n * 2 * (n - 1), L2 = (size_t)n * (n - 1);
     if (!ctx->dNlNode) {
       CU(cudaMalloc(&ctx->dNlNode, L1));
@@ -594,8 +595,11 @@ pipette_status pipette_search(pipette_ctx* ctx, const pipette_model* model, int6
   // R through L1.  MODE 2: 32-bit positions (N > 256).
   const int mode = (n <= 16 && maxN <= 256 && ctx->g <= 15 && ctx->dTab) ? 0 : (maxN <= 256 ? 1 : 2);
   // MODE 0: the block's m2*R table, 256 hop codes x 16 lane copies (64-bit loads are served
-  // per half-warp, so 16 copies make every lookup conflict free); MODE 1: R in shared memory
+  // per half-warp, so 16 copies make every lookup conflict free); MODE 1: the block's
+  // n x n m2*R table (one copy; above 32 KB the block has 8 warps to share it)
   const int r_bytes = mode == 0 ? 256 * 16 * 8 : (mode == 1 ? align16(nn * 8) : 0);
+  const bool big = mode == 1 && r_bytes > 32 * 1024;
+  const int threads = big ? 256 : kSaThreads;
   // psum (Eq.5 sums) cached in shared memory for configs with dp <= dp_cap: the largest cap
   // that still reaches the best achievable number of resident blocks per SM
   auto warp_bytes_for = [&](int cap, int& tls) {
@@ -608,8 +612,10 @@ pipette_status pipette_search(pipette_ctx* ctx, const pipette_model* model, int6
     }
     return wb;
   };
-  const int reg_blocks = mode == 0 ? 3 : 2;   // the kernels' __launch_bounds__
-  auto blocks_for = [&](int wb) { return std::min(reg_blocks, (227 * 1024) / std::max(1, r_bytes + 4 * wb)); };
+  const int reg_blocks = mode == 0 ? 3 : (mode == 1 ? (big ? 1 : 3) : 2);   // the kernels' __launch_bounds__
+  auto blocks_for = [&](int wb) {
+    return std::min(reg_blocks, (227 * 1024) / std::max(1, r_bytes + (threads / 32) * wb));
+  };
   int dp_cap = 0, warp_bytes = 16, tl_stride = 1, best_blocks = -1;
   for (int cap : {1024, 64, 32, 16, 8, 4, 2}) {
     int tls;
@@ -621,7 +627,7 @@ pipette_status pipette_search(pipette_ctx* ctx, const pipette_model* model, int6
     dp_cap = atoi(e);
     warp_bytes = warp_bytes_for(dp_cap, tl_stride);
   }
-  int wpb = kSaThreads / 32;
+  int wpb = threads / 32;
   const int smem_max = 227 * 1024;
   if (r_bytes + warp_bytes > smem_max)
     return fail(ctx, PIPETTE_E_UNSUPPORTED, "SA state (%d B/warp + %d B) exceeds shared memory", warp_bytes, r_bytes);
@@ -730,7 +736,7 @@ pipette_status pipette_search(pipette_ctx* ctx, const pipette_model* model, int6
   P.trace_cap = tracing ? o.trace_cap : 0;
   P.trace = tracing ? (pipette_trace_record*)ctx->trace.p : nullptr;
 
-  const void* kern = sa_kernel(mode, tracing, n);
+  const void* kern = sa_kernel(big ? 3 : mode, tracing, n);
   CU(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   int occ = 0;
   CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, wpb * 32, smem));

@@ -7,21 +7,20 @@
 //
 // Design: one chain per LANE; a warp runs 32 chains of one
 // configuration, so every instruction advances 32 independent Markov chains.  Chain
-// state lives in shared memory in lane-interleaved layouts ([element][lane] words), so
-// every per-lane random access is bank-conflict free:
-//   positions  (slot, node) of each worker position w = z*pp + x
-//              PosPacked: 16 bits per position, two per word (N <= 256, n <= 256)
-//              PosWide:   32 bits per position (general)
-//   psum[z]    Eq.5 sum of pipeline z (dp doubles, pp >= 2)
-//   stage-1    S1Reg:  per-node DP member counts as nibbles of a 64-bit register, the
-//                      node set N1 as a bit mask, T_ex from a subset-max table
-//                      (n <= 16, c_n <= spn <= 15)
-//              S1Smem: counts in shared memory (u8), a 128-bit node mask, T_ex with a
-//                      witness pair (general)
+// state lives in shared memory in lane-interleaved layouts ([element / 4][lane] words), so
+// every per-lane access is bank-conflict free:
+//   MODE 0 (n <= 16, N <= 256)   hop codes node(w-1) | node(w) << 4 and slot ids, one
+//                                byte per position; the block's 16-copy m2*R table;
+//                                stage-1 state in registers (S1Reg), subset-max T_ex
+//   MODE 1 (n <= 128, N <= 256)  slot ids, one byte per position; the block's n x n m2*R
+//                                table; member counts in shared memory with sorted-table
+//                                witnesses and warp-cooperative searches (S1Large)
+//   MODE 2 (general)             32-bit positions, R through L1 (PosWide, S1Large)
+//   psum[z]                      Eq.5 sum of pipeline z (cached when pp >= 4, dp small)
 // Re-evaluation is incremental but bit-exact: the (at most two) touched pipelines are
 // re-summed from scratch in stage order, the max terms (T_PP, T_in, T_ex) are kept with
-// witnesses / tables and rescanned when a witness could drop.  max is exact, so every
-// latency equals the from-scratch definition of the oracle bit for bit.
+// counts, witnesses or tables and rescanned when a witness could drop.  max is exact, so
+// every latency equals the from-scratch definition of the oracle bit for bit.
 #include <type_traits>
 
 #include "devmath.cuh"
@@ -29,27 +28,10 @@
 
 namespace pip {
 
-constexpr int kSaThreads = 128;
 
 __host__ __device__ __forceinline__ int align16(int x) { return (x + 15) & ~15; }
 
-// R = 1/B lookups.  RRep: 16 copies in shared memory, copy (lane & 15): a 64-bit shared load
-// is served per half-warp, so 16 copies are already conflict free (n <= 16).
-// RGlob: the n x n table in global memory through the read-only path (L1-resident; for
-// large clusters the table would not leave room in shared memory for chain state).
-struct RRep {
-  const double* s;
-  int n, lane;   // lane = this lane's copy index (lane & (copies - 1)); copies = 1 << cshift
-  int cshift;
-  __device__ __forceinline__ double operator()(uint32_t a, uint32_t b) const {
-    return s[(((int)a * n + (int)b) << cshift) + lane];
-  }
-};
-struct RSmem {
-  const double* s;
-  int n, lane;
-  __device__ __forceinline__ double operator()(uint32_t a, uint32_t b) const { return s[(int)a * n + (int)b]; }
-};
+// R = 1/B through the read-only path (MODE 1 searches, MODE 2 hops).
 struct RGlob {
   const double* s;
   int n, lane;
@@ -57,31 +39,6 @@ struct RGlob {
 };
 
 // ------------------------------------------------------------------ position storage
-struct PosPacked {
-  uint32_t* s;
-  int lane;
-  static __host__ __device__ int bytes(int N) { return ((N + 1) / 2) * 128; }
-  // 16-bit cell of position w: half (w & 1) of word (w >> 1)*32 + lane -- the bank is the
-  // lane's for every w, and the cell is read/written with 16/8-bit LDS/STS (no RMW).
-  __device__ __forceinline__ uint32_t hidx(uint32_t w) const { return ((((w >> 1) << 5) + (uint32_t)lane) << 1) | (w & 1u); }
-  __device__ __forceinline__ uint32_t raw(uint32_t w) const { return reinterpret_cast<const uint16_t*>(s)[hidx(w)]; }
-  __device__ __forceinline__ uint32_t node(uint32_t w) const {
-    return reinterpret_cast<const uint8_t*>(s)[(hidx(w) << 1) + 1];   // high byte of the cell
-  }
-  static __device__ __forceinline__ uint32_t node_of(uint32_t r) { return r >> 8; }
-  static __device__ __forceinline__ uint32_t slot_of(uint32_t r) { return r & 0xffu; }
-  __device__ __forceinline__ void init(int N, uint32_t spn, uint32_t spn_magic) {
-    uint16_t* s16 = reinterpret_cast<uint16_t*>(s);
-    for (int w = 0; w < N; ++w) s16[hidx((uint32_t)w)] = (uint16_t)((uint32_t)w | (div_small((uint32_t)w, spn_magic, spn) << 8));
-  }
-  // positions p and q take the contents rq and rp
-  __device__ __forceinline__ void swap(uint32_t p, uint32_t q, uint32_t rp, uint32_t rq) {
-    uint16_t* s16 = reinterpret_cast<uint16_t*>(s);
-    s16[hidx(p)] = (uint16_t)rq;
-    s16[hidx(q)] = (uint16_t)rp;
-  }
-};
-
 struct PosWide {
   uint32_t* s;
   int lane;
@@ -746,7 +703,7 @@ __host__ __device__ inline int hc_warp_state_bytes(int N, int pp, int dp, int dp
 template <bool TRACE, int PP, int NW>
 __device__ __forceinline__ void run_task_hc(const SaParams& P, const SaTask T, const DevCfg C, const double* Tl,
                                             unsigned char* ws, int lane) {
-  using RT = RRep;
+  using RT = RGlob;   // (S1Reg takes no R)
   const bool active = lane < T.count;
   const int N = C.N, pp = PP > 0 ? PP : C.pp, dp = C.dp, n = P.n_nodes;
   const uint32_t chain = (uint32_t)(T.c_first + (T.k0 + lane) * P.world);
@@ -756,7 +713,7 @@ __device__ __forceinline__ void run_task_hc(const SaParams& P, const SaTask T, c
   X.rank = P.tin_rank + (size_t)T.f * 256;
   X.vs = P.tin_vs + (size_t)T.f * 256;
   X.n = n;
-  const RT Rdummy{nullptr, n, 0, 0};
+  const RT Rdummy{nullptr, n, 0};
 
   const bool cache = pp >= 4 && dp <= P.psum_dp_cap;   // (pp = 2: re-summing one hop is as cheap)
   const int plane = align16(((N + 3) / 4) * 128);
@@ -939,23 +896,300 @@ __device__ __forceinline__ void run_task_hc(const SaParams& P, const SaTask T, c
   }
 }
 
+// ------------------------------------------------------------------ MODE 1: slot bytes
+// Chain state of MODE 1 (n <= 128 nodes, N <= 256 positions): the slot of every position
+// as a byte (same lane-interleaved layout as MODE 0); node(w) = slot(w) / spn.  The
+// block's table Tt[a * n + b] = fl(m2 * R[a][b]) of its configuration (one copy; a hop is
+// a byte extraction, the node, the pair index, one 64-bit shared load and one DADD).
+struct SbCtx {
+  const double* T;   // block table, n x n
+  int n;
+  uint32_t spn, spn_magic, spn_sh;   // spn_sh < 32: spn is a power of two
+  __device__ __forceinline__ uint32_t node(uint32_t slot) const {
+    return spn_sh < 32u ? slot >> spn_sh : div_small(slot, spn_magic, spn);
+  }
+};
+
+template <int PP>
+__device__ __forceinline__ double sb_sum(const HcState& st, uint32_t z, int pp_rt, const SbCtx& K) {
+  double s = 0.0;
+  if constexpr (PP >= 4) {
+    constexpr int NW = PP / 4;
+    uint32_t wd[NW];
+#pragma unroll
+    for (int k = 0; k < NW; ++k) wd[k] = st.hw[(z * (uint32_t)NW + (uint32_t)k) * 32u];
+    uint32_t prev = K.node(wd[0] & 0xffu);
+#pragma unroll
+    for (int x = 1; x < PP; ++x) {
+      const uint32_t cur = K.node(__byte_perm(wd[x >> 2], 0u, 0x4440u | (uint32_t)(x & 3)));
+      s = __dadd_rn(s, K.T[prev * (uint32_t)K.n + cur]);
+      prev = cur;
+    }
+  } else {
+    const int pp = PP > 0 ? PP : pp_rt;
+    const uint32_t b = z * (uint32_t)pp;
+    uint32_t prev = K.node(st.hb[HcState::off(b)]);
+    for (int x = 1; x < pp; ++x) {
+      const uint32_t cur = K.node(st.hb[HcState::off(b + (uint32_t)x)]);
+      s = __dadd_rn(s, K.T[prev * (uint32_t)K.n + cur]);
+      prev = cur;
+    }
+  }
+  return s;
+}
+
+template <int PP>
+__device__ __forceinline__ void sb_sum2(const HcState& st, uint32_t za, uint32_t zb, int pp_rt, const SbCtx& K,
+                                        double& sa, double& sb) {
+  double a = 0.0, b = 0.0;
+  if constexpr (PP >= 4) {
+    constexpr int NW = PP / 4;
+    uint32_t wa[NW], wb[NW];
+#pragma unroll
+    for (int k = 0; k < NW; ++k) {
+      wa[k] = st.hw[(za * (uint32_t)NW + (uint32_t)k) * 32u];
+      wb[k] = st.hw[(zb * (uint32_t)NW + (uint32_t)k) * 32u];
+    }
+    uint32_t pa = K.node(wa[0] & 0xffu), pb = K.node(wb[0] & 0xffu);
+#pragma unroll
+    for (int x = 1; x < PP; ++x) {
+      const uint32_t ca = K.node(__byte_perm(wa[x >> 2], 0u, 0x4440u | (uint32_t)(x & 3)));
+      const uint32_t cb = K.node(__byte_perm(wb[x >> 2], 0u, 0x4440u | (uint32_t)(x & 3)));
+      a = __dadd_rn(a, K.T[pa * (uint32_t)K.n + ca]);
+      b = __dadd_rn(b, K.T[pb * (uint32_t)K.n + cb]);
+      pa = ca;
+      pb = cb;
+    }
+  } else {
+    const int pp = PP > 0 ? PP : pp_rt;
+    const uint32_t ba = za * (uint32_t)pp, bb = zb * (uint32_t)pp;
+    uint32_t pa = K.node(st.hb[HcState::off(ba)]), pb = K.node(st.hb[HcState::off(bb)]);
+    for (int x = 1; x < pp; ++x) {
+      const uint32_t ca = K.node(st.hb[HcState::off(ba + (uint32_t)x)]);
+      const uint32_t cb = K.node(st.hb[HcState::off(bb + (uint32_t)x)]);
+      a = __dadd_rn(a, K.T[pa * (uint32_t)K.n + ca]);
+      b = __dadd_rn(b, K.T[pb * (uint32_t)K.n + cb]);
+      pa = ca;
+      pb = cb;
+    }
+  }
+  sa = a;
+  sb = b;
+}
+
+template <int PP>
+__device__ __forceinline__ void sb_rescan(const HcState& st, int dp, int pp_rt, const SbCtx& K, double& mx, int& cnt) {
+  double m0 = 0.0, m1 = 0.0;
+  int c0 = 0, c1 = 0;
+  auto acc = [](double v, double& m, int& c) {
+    c = v > m ? 1 : c + (v == m ? 1 : 0);
+    m = fmax(m, v);
+  };
+  int z = 0;
+  for (; z + 2 <= dp; z += 2) {
+    double a, b;
+    sb_sum2<PP>(st, (uint32_t)z, (uint32_t)z + 1u, pp_rt, K, a, b);
+    acc(a, m0, c0);
+    acc(b, m1, c1);
+  }
+  if (z < dp) acc(sb_sum<PP>(st, (uint32_t)z, pp_rt, K), m0, c0);
+  mx = fmax(m0, m1);
+  cnt = (m0 == mx ? c0 : 0) + (m1 == mx ? c1 : 0);
+}
+
+__host__ __device__ inline int sb_warp_state_bytes(int N, int pp, int dp, int n, int dp_cap) {
+  return align16(((N + 3) / 4) * 128) + align16(((n + 3) / 4) * 128) + ((pp >= 4 && dp <= dp_cap) ? align16(dp * 256) : 0);
+}
+
+// One warp task of MODE 1 (same step structure as run_task_hc).
+template <bool TRACE, int PP>
+__device__ __forceinline__ void run_task_sb(const SaParams& P, const SaTask T, const DevCfg C, const double* Tt,
+                                            unsigned char* ws, int lane) {
+  const bool active = lane < T.count;
+  const int N = C.N, pp = PP > 0 ? PP : C.pp, dp = C.dp, n = P.n_nodes;
+  const uint32_t chain = (uint32_t)(T.c_first + (T.k0 + lane) * P.world);
+  const int slot = T.slot0 + lane;
+  S1Ctx X;
+  X.qi = P.qtab + C.qi_off; X.qe = P.qtab + C.qe_off;
+  X.nl_node = P.nl_node; X.nl_val = P.nl_val; X.gl_ab = P.gl_ab; X.gl_val = P.gl_val;
+  X.tl_ac = P.tl_ac + (size_t)T.f * P.tl_stride;
+  X.tl_val = P.tl_val + (size_t)T.f * P.tl_stride;
+  X.nl_len = 2 * (n - 1); X.gl_len = n * (n - 1); X.tl_len = P.tl_len[T.f];
+  X.n = n;
+  SbCtx K;
+  K.T = Tt; K.n = n; K.spn = (uint32_t)C.spn; K.spn_magic = C.spn_magic;
+  K.spn_sh = (C.spn & (C.spn - 1)) == 0 ? (uint32_t)(31 - __clz(C.spn)) : 32u;
+
+  const bool cache = pp >= 4 && dp <= P.psum_dp_cap;
+  const int plane = align16(((N + 3) / 4) * 128);
+  HcState st;
+  st.hb = ws + lane * 4;   // slot bytes (st.hb doubles as the slot plane)
+  st.sb = st.hb;
+  st.hw = reinterpret_cast<const uint32_t*>(ws) + lane;
+  // stage-1 state with warp-cooperative searches (S1Large; member counts as bytes, the
+  // same lane-interleaved layout as the slots).  (Per-lane searches were measured slower:
+  // a lane's long search stalls its whole warp.)
+  S1Large<RGlob> s1;
+  const RGlob Rg{P.R, n, lane};
+  s1.c = reinterpret_cast<uint32_t*>(ws + plane);
+  s1.lane = lane;
+  double* psum = reinterpret_cast<double*>(ws + plane + align16(((n + 3) / 4) * 128));
+  uint16_t* bperm = P.best_perm + T.perm_off;
+  s1.clear(n);
+
+  for (int w = 0; w < N; ++w) {
+    st.hb[HcState::off((uint32_t)w)] = (uint8_t)w;
+    bperm[w * 32 + lane] = (uint16_t)w;
+  }
+  __syncwarp();
+  double tpp = 0.0;
+  int nmax = 0;
+  for (int z = 0; z < dp; ++z) {
+    s1.add_init(K.node((uint32_t)(z * pp)));
+    if (pp >= 2) {
+      const double s = sb_sum<PP>(st, (uint32_t)z, pp, K);
+      if (cache) psum[z * 32 + lane] = s;
+      if (s > tpp) { tpp = s; nmax = 1; } else if (s == tpp) { ++nmax; }
+    }
+  }
+  s1.finish_init(X, Rg);
+
+  const double L0 = compose(C.Sb, C.r, C.Ss, tpp, s1.tin, s1.tex);
+  double cur = L0, best = L0, best_tpp = tpp, best_tdp = __dadd_rn(s1.tin, s1.tex);
+  int best_step = -1;
+  uint32_t accepted = 0;
+  double beta = P.t0 > 0.0 ? __ddiv_rn(1.0, P.t0) : __ddiv_rn(1.0, __dmul_rn(P.tau, L0));
+  const double ia = P.alpha_inv;
+  const int trow = (TRACE && active) ? P.trace_slot[slot] : -1;
+
+  if (N >= 2) {
+    Draw dnext = draw_swap_rk(0u, chain, (uint32_t)C.e, P.rk, (uint32_t)N);
+    for (int i = 0; i < P.iterations; ++i) {
+      const Draw d = dnext;
+      dnext = draw_swap_rk((uint32_t)(i + 1), chain, (uint32_t)C.e, P.rk, (uint32_t)N);
+      const uint32_t p = d.p, q = d.q;
+      uint8_t* const bp = st.hb + HcState::off(p);
+      uint8_t* const bq = st.hb + HcState::off(q);
+      const uint32_t sp = *bp, sq = *bq;
+      bool dpchg = false;
+      const uint32_t np = K.node(sp), nq = K.node(sq);
+      double Lp = cur;
+      bool acc = true, improved = false;
+      if (pp >= 2) {
+        const uint32_t zp = PP > 0 ? p / (uint32_t)PP : div_small(p, C.pp_magic, (uint32_t)pp);
+        const uint32_t zq = PP > 0 ? q / (uint32_t)PP : div_small(q, C.pp_magic, (uint32_t)pp);
+        const uint32_t xp = p - zp * (uint32_t)pp, xq = q - zq * (uint32_t)pp;
+        const bool two = zq != zp;
+        const uint32_t zb = two ? zq : zp;
+        double oldA, oldB;
+        if (cache) {
+          oldA = psum[zp * 32 + lane];
+          oldB = psum[zb * 32 + lane];
+        } else {
+          sb_sum2<PP>(st, zp, zb, pp, K, oldA, oldB);
+        }
+        *bp = (uint8_t)sq;   // tentative swap
+        *bq = (uint8_t)sp;
+        double sA, sB;
+        sb_sum2<PP>(st, zp, zb, pp, K, sA, sB);
+        double tpp2 = tpp;
+        int nmax2 = nmax;
+        const double snew = fmax(sA, sB);
+        const int keep = nmax - (oldA == tpp ? 1 : 0) - ((two && oldB == tpp) ? 1 : 0);
+        if (keep > 0 || snew >= tpp) {
+          tpp2 = (keep > 0) ? fmax(tpp, snew) : snew;
+          nmax2 = (keep > 0 && tpp2 == tpp ? keep : 0) + (sA == tpp2 ? 1 : 0) + ((two && sB == tpp2) ? 1 : 0);
+        } else if (cache) {
+          double m0 = sA, m1 = two ? sB : 0.0;
+          int c0 = 1, c1 = two ? 1 : 0;
+          for (int z = 0; z < dp; ++z) {
+            const double v = ((uint32_t)z == zp || (uint32_t)z == zq) ? 0.0 : psum[z * 32 + lane];
+            if (z & 1) { c1 = v > m1 ? 1 : c1 + (v == m1 ? 1 : 0); m1 = fmax(m1, v); }
+            else { c0 = v > m0 ? 1 : c0 + (v == m0 ? 1 : 0); m0 = fmax(m0, v); }
+          }
+          tpp2 = fmax(m0, m1);
+          nmax2 = (m0 == tpp2 ? c0 : 0) + (m1 == tpp2 ? c1 : 0);
+        } else {
+          sb_rescan<PP>(st, dp, pp, K, tpp2, nmax2);
+        }
+        dpchg = ((xp == 0u) != (xq == 0u)) && np != nq;
+        if (dpchg) {
+          const uint32_t dn = xp == 0u ? np : nq;
+          const uint32_t up = xp == 0u ? nq : np;
+          s1.propose(dn, up, X, Rg);
+        }
+        s1.coop(X, Rg);   // converged: all lanes' flagged searches
+        double tin2 = s1.tin, tex2 = s1.tex;
+        if (dpchg) {
+          s1.finish(X);
+          tin2 = s1.tin2;
+          tex2 = s1.tex2;
+        }
+        Lp = compose(C.Sb, C.r, C.Ss, tpp2, tin2, tex2);
+        acc = metropolis_fast(__dadd_rn(Lp, -cur), beta, d.u);
+        if (acc) {
+          if (cache) {
+            psum[zp * 32 + lane] = sA;
+            psum[zb * 32 + lane] = sB;
+          }
+          tpp = tpp2;
+          nmax = nmax2;
+          if (dpchg) s1.commit();
+          cur = Lp;
+          if (Lp < best) {
+            best = Lp; best_step = i; best_tpp = tpp; best_tdp = __dadd_rn(s1.tin, s1.tex);
+            improved = true;
+          }
+        } else {
+          *bq = (uint8_t)sq;   // revert
+          *bp = (uint8_t)sp;
+        }
+      } else {
+        *bp = (uint8_t)sq;   // pp = 1: L' = cur (no hops, stage-1 multiset unchanged)
+        *bq = (uint8_t)sp;
+      }
+      if (acc) ++accepted;
+      if (improved)
+        for (int w = 0; w < N; ++w) bperm[w * 32 + lane] = (uint16_t)st.hb[HcState::off((uint32_t)w)];
+      if (TRACE && trow >= 0 && i < P.trace_cap) {
+        pipette_trace_record rec;
+        rec.i = (uint32_t)i; rec.p = (uint16_t)d.p; rec.q = (uint16_t)d.q;
+        rec.accept = acc ? 1u : 0u; rec.latency = Lp;
+        P.trace[(size_t)trow * P.trace_cap + i] = rec;
+      }
+      beta = __dmul_rn(beta, ia);
+    }
+  }
+  if (active) {
+    ChainOut o;
+    o.best = best; o.best_tpp = best_tpp; o.best_tdp = best_tdp; o.L0 = L0;
+    o.best_step = best_step; o.accepted = accepted; o.f = T.f; o.c = (int32_t)chain;
+    P.out[slot] = o;
+  }
+}
+
 // MODE 0: n <= 16 nodes, N <= 256, spn <= 15: hop-code chain state (run_task_hc), register
 //         stage-1 state, the block's m2*R table in shared memory, subset-max table.
 // MODE 1: n <= 128, N <= 256: packed positions, S1Large, R through L1.
 // MODE 2: general (N <= 1024): 32-bit positions, S1Large, R through L1.
-template <int MODE, bool TRACE, int NW = 4>
-__global__ void __launch_bounds__(kSaThreads, MODE == 0 ? 3 : 2) k_sa_chains(SaParams P) {
-  using POS = typename std::conditional<MODE == 2, PosWide, PosPacked>::type;
-  using RT = typename std::conditional<MODE == 1, RSmem, RGlob>::type;
+// launch bounds per mode: MODE 0 4 warps x 3 blocks; MODE 1 4 warps x 3 blocks (small
+// table) or 8 warps x 1 block (BIG: a table of up to 128 KB shared by more warps); MODE 2.
+template <int MODE, bool BIG>
+struct SaLB {
+  static constexpr int threads = (MODE == 1 && BIG) ? 256 : 128;
+  static constexpr int blocks = MODE == 0 ? 3 : (MODE == 1 ? (BIG ? 1 : 3) : 2);
+};
+
+template <int MODE, bool TRACE, int NW = 4, bool BIG = false>
+__global__ void __launch_bounds__(SaLB<MODE, BIG>::threads, SaLB<MODE, BIG>::blocks) k_sa_chains(SaParams P) {
+  using POS = PosWide;
+  using RT = RGlob;
   using S1 = S1Large<RT>;
   extern __shared__ __align__(16) unsigned char smem[];
   double* Rs = reinterpret_cast<double*>(smem);
   const int n = P.n_nodes, nn = n * n;
-  if (MODE == 1) {
-    for (int i = threadIdx.x; i < nn; i += blockDim.x) Rs[i] = P.R[i];
-  }
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  RT R{MODE == 1 ? Rs : P.R, n, lane};
+  RT R{P.R, n, lane};
   const double* Tl = Rs + (lane & 15);   // MODE 0: this lane's copy of the block's m2*R table
   unsigned char* ws = smem + P.r_smem_bytes + wid * P.warp_smem_bytes;
   __shared__ int s_chunk;
@@ -963,20 +1197,24 @@ __global__ void __launch_bounds__(kSaThreads, MODE == 0 ? 3 : 2) k_sa_chains(SaP
   for (;;) {
     // a block takes one chunk: up to warps-per-block consecutive tasks of ONE configuration
     // (host-built), so the block runs one code path (I-cache locality), shares the
-    // configuration's m2*R table (MODE 0), and its warps finish together
+    // configuration's m2*R table (MODE 0/1), and its warps finish together
     __syncthreads();
     if (threadIdx.x == 0) s_chunk = atomicAdd(P.task_counter, 1);
     __syncthreads();
     const int ch = s_chunk;
     if (ch >= P.n_chunks) break;
     const int2 chunk = P.chunks[ch];
-    if constexpr (MODE == 0) {
+    if constexpr (MODE == 0 || MODE == 1) {
       const int cfg0 = P.tasks[chunk.x].cfg;
       if (cfg0 != table_cfg) {   // block-uniform: rebuild the table for this configuration
         const double m2 = P.cfgs[cfg0].m2;
-        for (int i = threadIdx.x; i < 256 * 16; i += blockDim.x) {
-          const int code = i >> 4, a = code & 15, b = code >> 4;
-          Rs[i] = (a < n && b < n) ? __dmul_rn(m2, P.R[a * n + b]) : 0.0;
+        if constexpr (MODE == 0) {
+          for (int i = threadIdx.x; i < 256 * 16; i += blockDim.x) {
+            const int code = i >> 4, a = code & 15, b = code >> 4;
+            Rs[i] = (a < n && b < n) ? __dmul_rn(m2, P.R[a * n + b]) : 0.0;
+          }
+        } else {
+          for (int i = threadIdx.x; i < nn; i += blockDim.x) Rs[i] = __dmul_rn(m2, P.R[i]);
         }
         table_cfg = cfg0;
       }
@@ -997,6 +1235,16 @@ __global__ void __launch_bounds__(kSaThreads, MODE == 0 ? 3 : 2) k_sa_chains(SaP
         case 16: run_task_hc<TRACE, 16, NW>(P, T, C, Tl, ws, lane); break;
         case 32: run_task_hc<TRACE, 32, NW>(P, T, C, Tl, ws, lane); break;
         default: run_task_hc<TRACE, 0, NW>(P, T, C, Tl, ws, lane); break;
+      }
+    } else if constexpr (MODE == 1) {
+      switch (C.pp) {
+        case 1: run_task_sb<TRACE, 1>(P, T, C, Rs, ws, lane); break;
+        case 2: run_task_sb<TRACE, 2>(P, T, C, Rs, ws, lane); break;
+        case 4: run_task_sb<TRACE, 4>(P, T, C, Rs, ws, lane); break;
+        case 8: run_task_sb<TRACE, 8>(P, T, C, Rs, ws, lane); break;
+        case 16: run_task_sb<TRACE, 16>(P, T, C, Rs, ws, lane); break;
+        case 32: run_task_sb<TRACE, 32>(P, T, C, Rs, ws, lane); break;
+        default: run_task_sb<TRACE, 0>(P, T, C, Rs, ws, lane); break;
       }
     } else {
       switch (C.pp) {
@@ -1178,12 +1426,13 @@ const void* sa_kernel(int mode, bool trace, int n_nodes) {
   if (mode == 0 && n_nodes <= 8) return trace ? (const void*)k_sa_chains<0, true, 2> : (const void*)k_sa_chains<0, false, 2>;
   if (mode == 0) return trace ? (const void*)k_sa_chains<0, true, 4> : (const void*)k_sa_chains<0, false, 4>;
   if (mode == 1) return trace ? (const void*)k_sa_chains<1, true> : (const void*)k_sa_chains<1, false>;
+  if (mode == 3) return trace ? (const void*)k_sa_chains<1, true, 4, true> : (const void*)k_sa_chains<1, false, 4, true>;
   return trace ? (const void*)k_sa_chains<2, true> : (const void*)k_sa_chains<2, false>;
 }
 
 int sa_warp_state_bytes(int mode, int N, int pp, int dp, int n, int dp_cap) {
   if (mode == 0) return hc_warp_state_bytes(N, pp, dp, dp_cap);
-  if (mode == 1) return warp_state_bytes<PosPacked>(N, pp, dp, n, true, dp_cap);
+  if (mode == 1 || mode == 3) return sb_warp_state_bytes(N, pp, dp, n, dp_cap);
   return warp_state_bytes<PosWide>(N, pp, dp, n, true, dp_cap);
 }
 
