@@ -125,6 +125,20 @@ def lib():
                                 C.c_int32, C.c_int32, C.c_uint64, C.c_double, C.c_double, C.c_double,
                                 C.c_int32, P(Plan), P(C.c_uint16), C.c_int32, P(C.c_double), P(C.c_int32)]
         L.or_search.restype = C.c_int32
+        L.or_draw_move.argtypes = [C.c_uint32, C.c_uint32, C.c_uint32, C.c_uint64, C.c_int32,
+                                   P(C.c_uint32), P(C.c_uint32), P(C.c_double), P(C.c_uint32)]
+        L.or_move_kind.argtypes = [C.c_uint32, C.c_int32, C.c_int32]
+        L.or_move_kind.restype = C.c_int32
+        L.or_apply_move.argtypes = [P(C.c_uint16), C.c_int32, C.c_uint32, C.c_uint32]
+        L.or_undo_move.argtypes = [P(C.c_uint16), C.c_int32, C.c_uint32, C.c_uint32]
+        L.or_sa_chain_moves.argtypes = [P(Consts), P(C.c_double), C.c_int32, C.c_uint64, C.c_uint32, C.c_uint32,
+                                        C.c_double, C.c_double, C.c_double, C.c_int32, C.c_int32, P(ChainResult),
+                                        P(C.c_uint16), P(TraceRecord), C.c_int32]
+        L.or_search_moves.argtypes = [P(Cluster), P(C.c_double), P(Profile), C.c_int32, P(Model), C.c_int64,
+                                      C.c_int32, C.c_int32, C.c_uint64, C.c_double, C.c_double, C.c_double,
+                                      C.c_int32, C.c_int32, C.c_int32, P(Plan), P(C.c_uint16), C.c_int32,
+                                      P(C.c_double), P(C.c_int32)]
+        L.or_search_moves.restype = C.c_int32
         _lib = L
     return _lib
 
@@ -245,6 +259,26 @@ def draw(i, c, e, seed, N):
     return p.value, q.value, u.value
 
 
+def draw_move(i, c, e, seed, N):
+    """(p, q, u, t): the draw of R14 plus the 11-bit move selector t of R21."""
+    p, q, u, t = C.c_uint32(), C.c_uint32(), C.c_double(), C.c_uint32()
+    lib().or_draw_move(i, c, e, seed, N, C.byref(p), C.byref(q), C.byref(u), C.byref(t))
+    return p.value, q.value, u.value, t.value
+
+
+SWAP, MIGRATE, REVERSE = 0, 1, 2
+
+
+def move_kind(t, w_migrate, w_reverse) -> int:
+    return lib().or_move_kind(t, w_migrate, w_reverse)
+
+
+def apply_move(perm, kind, p, q, undo=False) -> np.ndarray:
+    a = np.ascontiguousarray(np.asarray(perm, dtype=np.uint16)).copy()
+    (lib().or_undo_move if undo else lib().or_apply_move)(_u16ptr(a), kind, p, q)
+    return a
+
+
 @dataclass
 class ChainOut:
     best: float
@@ -258,14 +292,19 @@ class ChainOut:
 
 
 def sa_chain(K: Consts, R: np.ndarray, iterations: int, seed: int, chain: int, e: int,
-             alpha=0.999, tau=0.05, t0=0.0, trace: bool = False) -> ChainOut:
-    """One SA chain of worker dedication, swap move only."""
+             alpha=0.999, tau=0.05, t0=0.0, trace: bool = False, w_migrate=0, w_reverse=0) -> ChainOut:
+    """One SA chain of worker dedication; swap only unless move weights
+    (1/2048 units, R21) are given."""
     R = np.ascontiguousarray(R, dtype=np.float64)
     res = ChainResult()
     bp = np.zeros(max(1, K.N), dtype=np.uint16)
     tr = (TraceRecord * iterations)() if trace and iterations > 0 else None
-    lib().or_sa_chain(C.byref(K), _dptr(R), iterations, seed, chain, e, alpha, tau, t0,
-                      C.byref(res), _u16ptr(bp), tr, iterations if tr is not None else 0)
+    if w_migrate == 0 and w_reverse == 0:
+        lib().or_sa_chain(C.byref(K), _dptr(R), iterations, seed, chain, e, alpha, tau, t0,
+                          C.byref(res), _u16ptr(bp), tr, iterations if tr is not None else 0)
+    else:
+        lib().or_sa_chain_moves(C.byref(K), _dptr(R), iterations, seed, chain, e, alpha, tau, t0, w_migrate,
+                                w_reverse, C.byref(res), _u16ptr(bp), tr, iterations if tr is not None else 0)
     tlist = None
     if tr is not None:
         tlist = [(r.i, r.p, r.q, r.accept, r.L) for r in tr] if K.N >= 2 else []
@@ -297,7 +336,7 @@ class SearchOut:
 
 
 def search(cluster, B, profile, model, bs_global, chains, iterations, seed,
-           alpha=0.999, tau=0.05, t0=0.0, world=1) -> SearchOut:
+           alpha=0.999, tau=0.05, t0=0.0, world=1, w_migrate=0, w_reverse=0) -> SearchOut:
     """Alg.1 with `world` simulated ranks (sharding + two-step min)."""
     B = np.ascontiguousarray(B, dtype=np.float64)
     prof, nprof = profile
@@ -307,9 +346,10 @@ def search(cluster, B, profile, model, bs_global, chains, iterations, seed,
     E = len(enumerate_configs(cluster, model, bs_global, profile))
     pcb = np.full(max(1, E), np.inf)
     pcc = np.full(max(1, E), -1, dtype=np.int32)
-    st = lib().or_search(C.byref(cluster), _dptr(B), prof, nprof, C.byref(model), bs_global,
-                         chains, iterations, seed, alpha, tau, t0, world, C.byref(plan),
-                         _u16ptr(perm), cap, _dptr(pcb), pcc.ctypes.data_as(C.POINTER(C.c_int32)))
+    st = lib().or_search_moves(C.byref(cluster), _dptr(B), prof, nprof, C.byref(model), bs_global,
+                               chains, iterations, seed, alpha, tau, t0, w_migrate, w_reverse, world,
+                               C.byref(plan), _u16ptr(perm), cap, _dptr(pcb),
+                               pcc.ctypes.data_as(C.POINTER(C.c_int32)))
     c = plan.cfg
     return SearchOut(st, plan.E, plan.F, (c.pp, c.tp, c.dp, c.mb), c.n_mb, int(c.mem_bytes),
                      plan.bd.T, plan.bd.t_pp, plan.bd.t_dp, plan.bd.t_bubble, plan.bd.t_straggler,

@@ -267,10 +267,65 @@ double or_exp_det(double x) {
 /* every iteration (R13); pi0 = identity "alphabetical" (R16); best updated */
 /* on strict < (R17).  Every proposal is re-evaluated from the definition.         */
 /* ------------------------------------------------------------------------- */
-void or_sa_chain(const or_consts* K, const double* R, int32_t iterations, uint64_t seed,
-                 uint32_t chain, uint32_t e, double alpha, double tau, double t0,
-                 or_chain_result* res, uint16_t* best_perm,
-                 or_trace_record* trace, int32_t trace_cap) {
+/* ------------------------------------------------------------------------- */
+/* The three SA movements of P:252 ("Regarding f as a string, ... migration      */
+/* (remove a single element to a random position), swap (exchange two elements),  */
+/* and reverse (take a substring and reverse its order)"), reading R21: the move  */
+/* kind comes from the 11 bits of the step's Philox block that u leaves unused,   */
+/* t = ((w2 & 31) << 6) | (w3 & 63) in [0, 2048): swap if t < 2048 - wm - wr,     */
+/* migrate if t < 2048 - wr, else reverse (weights wm, wr in 1/2048 units).       */
+/* (p, q) are the draw's two distinct positions.                                  */
+/*   swap:    exchange positions p and q                                          */
+/*   migrate: remove the element at p and insert it at index q of the remaining   */
+/*            string (element 0 to position 2 of abcd gives bcad)     */
+/*   reverse: reverse positions min(p,q)..max(p,q) inclusive                      */
+/* ------------------------------------------------------------------------- */
+void or_draw_move(uint32_t i, uint32_t c, uint32_t e, uint64_t seed, int32_t N,
+                  uint32_t* p, uint32_t* q, double* u, uint32_t* t) {
+  uint32_t ctr[4] = {i, c, e, 0u};
+  uint32_t key[2] = {(uint32_t)seed, (uint32_t)(seed >> 32)};
+  uint32_t w[4];
+  or_philox4x32_10(ctr, key, w);
+  or_draw(i, c, e, seed, N, p, q, u);
+  *t = ((w[2] & 31u) << 6) | (w[3] & 63u);
+}
+
+int32_t or_move_kind(uint32_t t, int32_t w_migrate, int32_t w_reverse) {
+  if ((int32_t)t < 2048 - w_migrate - w_reverse) return 0;   /* swap */
+  if ((int32_t)t < 2048 - w_reverse) return 1;               /* migrate */
+  return 2;                                                  /* reverse */
+}
+
+void or_apply_move(uint16_t* perm, int32_t kind, uint32_t p, uint32_t q) {
+  if (kind == 0) {
+    uint16_t t = perm[p]; perm[p] = perm[q]; perm[q] = t;
+  } else if (kind == 1) {
+    uint16_t x = perm[p];
+    if (p < q) { for (uint32_t w = p; w < q; ++w) perm[w] = perm[w + 1]; }
+    else       { for (uint32_t w = p; w > q; --w) perm[w] = perm[w - 1]; }
+    perm[q] = x;
+  } else {
+    uint32_t lo = p < q ? p : q, hi = p < q ? q : p;
+    while (lo < hi) { uint16_t t = perm[lo]; perm[lo] = perm[hi]; perm[hi] = t; ++lo; --hi; }
+  }
+}
+
+/* The inverse move: swap and reverse are involutions; migrating p -> q is undone by q -> p. */
+void or_undo_move(uint16_t* perm, int32_t kind, uint32_t p, uint32_t q) {
+  if (kind == 1) or_apply_move(perm, 1, q, p);
+  else or_apply_move(perm, kind, p, q);
+}
+
+/* ------------------------------------------------------------------------- */
+/* One SA chain of fine-grained worker dedication (Alg.1 l.9-15) on   */
+/* configuration e: Metropolis acceptance (R13, R16), every proposal evaluated   */
+/* from scratch by or_latency.  w_migrate = w_reverse = 0 is the swap-only chain. */
+/* ------------------------------------------------------------------------- */
+void or_sa_chain_moves(const or_consts* K, const double* R, int32_t iterations, uint64_t seed,
+                       uint32_t chain, uint32_t e, double alpha, double tau, double t0,
+                       int32_t w_migrate, int32_t w_reverse,
+                       or_chain_result* res, uint16_t* best_perm,
+                       or_trace_record* trace, int32_t trace_cap) {
   const int32_t N = K->N;
   uint16_t* perm = (uint16_t*)malloc(sizeof(uint16_t) * (size_t)N);
   for (int32_t w = 0; w < N; ++w) perm[w] = (uint16_t)w;
@@ -285,9 +340,10 @@ void or_sa_chain(const or_consts* K, const double* R, int32_t iterations, uint64
   double ia = 1.0 / alpha;
   if (N >= 2) {
     for (int32_t i = 0; i < iterations; ++i) {
-      uint32_t p, q; double u;
-      or_draw((uint32_t)i, chain, e, seed, N, &p, &q, &u);
-      uint16_t t = perm[p]; perm[p] = perm[q]; perm[q] = t;          /* swap move */
+      uint32_t p, q, t; double u;
+      or_draw_move((uint32_t)i, chain, e, seed, N, &p, &q, &u, &t);
+      int32_t kind = or_move_kind(t, w_migrate, w_reverse);
+      or_apply_move(perm, kind, p, q);
       double Lp = or_latency(K, R, perm, &bd);
       double d = Lp - cur;
       int acc = (d <= 0.0) || (u < or_exp_det(-(d * beta)));        /* Metropolis */
@@ -298,7 +354,7 @@ void or_sa_chain(const or_consts* K, const double* R, int32_t iterations, uint64
           if (best_perm) memcpy(best_perm, perm, sizeof(uint16_t) * (size_t)N);
         }
       } else {
-        t = perm[p]; perm[p] = perm[q]; perm[q] = t;                  /* undo */
+        or_undo_move(perm, kind, p, q);
       }
       beta = beta * ia;
       if (trace && i < trace_cap) {
@@ -312,6 +368,13 @@ void or_sa_chain(const or_consts* K, const double* R, int32_t iterations, uint64
   free(perm);
 }
 
+void or_sa_chain(const or_consts* K, const double* R, int32_t iterations, uint64_t seed,
+                 uint32_t chain, uint32_t e, double alpha, double tau, double t0,
+                 or_chain_result* res, uint16_t* best_perm,
+                 or_trace_record* trace, int32_t trace_cap) {
+  or_sa_chain_moves(K, R, iterations, seed, chain, e, alpha, tau, t0, 0, 0, res, best_perm, trace, trace_cap);
+}
+
 /* ------------------------------------------------------------------------- */
 /* Alg.1: every feasible (Conf, bs_micro) runs `chains` SA chains;     */
 /* winner = lexicographic min of (latency, config index e, chain c) (R17).         */
@@ -319,11 +382,11 @@ void or_sa_chain(const or_consts* K, const double* R, int32_t iterations, uint64
 /* j mod W; each rank takes its local argmin; the ranks are combined by a min over */
 /* the latency bits, then a min over the item ids that attain it (R18).           */
 /* ------------------------------------------------------------------------- */
-int32_t or_search(const or_cluster* cl, const double* B, const or_profile* prof, int32_t n_prof,
-                  const or_model* m, int64_t bs_global, int32_t chains, int32_t iterations,
-                  uint64_t seed, double alpha, double tau, double t0, int32_t world,
-                  or_plan* plan, uint16_t* perm_out, int32_t perm_cap,
-                  double* per_config_best, int32_t* per_config_chain) {
+int32_t or_search_moves(const or_cluster* cl, const double* B, const or_profile* prof, int32_t n_prof,
+                        const or_model* m, int64_t bs_global, int32_t chains, int32_t iterations,
+                        uint64_t seed, double alpha, double tau, double t0, int32_t w_migrate, int32_t w_reverse,
+                        int32_t world, or_plan* plan, uint16_t* perm_out, int32_t perm_cap,
+                        double* per_config_best, int32_t* per_config_chain) {
   memset(plan, 0, sizeof *plan);
   int32_t n = cl->n_nodes;
   int32_t E = or_enumerate(cl, m, bs_global, prof, n_prof, NULL, 0);
@@ -357,7 +420,8 @@ int32_t or_search(const or_cluster* cl, const double* B, const or_profile* prof,
     if (per_config_chain) per_config_chain[f] = -1;
     for (int32_t c = 0; c < chains; ++c) {
       or_chain_result res;
-      or_sa_chain(&K, R, iterations, seed, (uint32_t)c, (uint32_t)cfgs[i].e, alpha, tau, t0, &res, NULL, NULL, 0);
+      or_sa_chain_moves(&K, R, iterations, seed, (uint32_t)c, (uint32_t)cfgs[i].e, alpha, tau, t0, w_migrate,
+                        w_reverse, &res, NULL, NULL, 0);
       if (K.N >= 2) steps += (uint64_t)iterations;
       acc += res.accepted;
       int64_t j = (int64_t)f * chains + c;
@@ -386,7 +450,8 @@ int32_t or_search(const or_cluster* cl, const double* B, const or_profile* prof,
       or_consts K;
       or_constants(cl, m, &cfgs[i], prof, n_prof, &K);
       or_chain_result res;
-      or_sa_chain(&K, R, iterations, seed, (uint32_t)wc, (uint32_t)cfgs[i].e, alpha, tau, t0, &res, bp, NULL, 0);
+      or_sa_chain_moves(&K, R, iterations, seed, (uint32_t)wc, (uint32_t)cfgs[i].e, alpha, tau, t0, w_migrate,
+                        w_reverse, &res, bp, NULL, 0);
       plan->cfg = cfgs[i];
       or_latency(&K, R, bp, &plan->bd);
       plan->cfg_index = cfgs[i].e; plan->chain = wc; plan->best_step = res.best_step;
@@ -399,4 +464,13 @@ int32_t or_search(const or_cluster* cl, const double* B, const or_profile* prof,
   plan->sa_steps = steps; plan->sa_accepted = acc; plan->status = 0;
   free(bp); free(rank_best); free(rank_item); free(cfgs); free(R);
   return 0;
+}
+
+int32_t or_search(const or_cluster* cl, const double* B, const or_profile* prof, int32_t n_prof,
+                  const or_model* m, int64_t bs_global, int32_t chains, int32_t iterations,
+                  uint64_t seed, double alpha, double tau, double t0, int32_t world,
+                  or_plan* plan, uint16_t* perm_out, int32_t perm_cap,
+                  double* per_config_best, int32_t* per_config_chain) {
+  return or_search_moves(cl, B, prof, n_prof, m, bs_global, chains, iterations, seed, alpha, tau, t0, 0, 0, world,
+                         plan, perm_out, perm_cap, per_config_best, per_config_chain);
 }

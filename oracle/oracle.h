@@ -104,6 +104,23 @@ void or_sa_chain(const or_consts* K, const double* R, int32_t iterations, uint64
                  or_chain_result* res, uint16_t* best_perm,
                  or_trace_record* trace, int32_t trace_cap);
 
+/* NEXT-1: the paper's three SA movements, reading R21. */
+void or_draw_move(uint32_t i, uint32_t c, uint32_t e, uint64_t seed, int32_t N,
+                  uint32_t* p, uint32_t* q, double* u, uint32_t* t);
+int32_t or_move_kind(uint32_t t, int32_t w_migrate, int32_t w_reverse);   /* 0 swap, 1 migrate, 2 reverse */
+void or_apply_move(uint16_t* perm, int32_t kind, uint32_t p, uint32_t q);
+void or_undo_move(uint16_t* perm, int32_t kind, uint32_t p, uint32_t q);
+void or_sa_chain_moves(const or_consts* K, const double* R, int32_t iterations, uint64_t seed,
+                       uint32_t chain, uint32_t e, double alpha, double tau, double t0,
+                       int32_t w_migrate, int32_t w_reverse,
+                       or_chain_result* res, uint16_t* best_perm,
+                       or_trace_record* trace, int32_t trace_cap);
+int32_t or_search_moves(const or_cluster* cl, const double* B, const or_profile* prof, int32_t n_prof,
+                        const or_model* m, int64_t bs_global, int32_t chains, int32_t iterations,
+                        uint64_t seed, double alpha, double tau, double t0, int32_t w_migrate, int32_t w_reverse,
+                        int32_t world, or_plan* plan, uint16_t* perm_out, int32_t perm_cap,
+                        double* per_config_best, int32_t* per_config_chain);
+
 int32_t or_search(const or_cluster* cl, const double* B, const or_profile* prof, int32_t n_prof,
                   const or_model* m, int64_t bs_global, int32_t chains, int32_t iterations,
                   uint64_t seed, double alpha, double tau, double t0, int32_t world,
