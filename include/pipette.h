@@ -107,6 +107,12 @@ typedef struct {
   int32_t n_trace;
   int32_t trace_cap;              /* records kept per traced item (first trace_cap steps) */
   pipette_trace_record* trace;    /* n_trace x trace_cap records (host) */
+  /* The paper's full move set (reading R21): probabilities of the migration
+   * and reverse movements in 1/2048 units (swap takes the rest, 2048 - w_migrate -
+   * w_reverse).  Both 0 (the zero-initialised default) = swap only.  Requires
+   * N = pp*dp <= 256 (else PIPETTE_E_UNSUPPORTED); every proposal is then evaluated in
+   * full (O(N) per step). */
+  int32_t w_migrate, w_reverse;
 } pipette_sa_opts;
 
 /* A plan (Alg.1 output "Conf, Map, T") plus counters and timings. */

@@ -213,9 +213,11 @@ class Pipette:
     # ------------------------------------------------------------------ search
     def search(self, model: Model, bs_global: int, chains: int, iterations: int, seed: int,
                alpha: float = 0.999, tau: float = 0.05, t0: float = 0.0, per_config: bool = False,
-               chain_results: bool = False, trace_items=None, trace_cap: int = 0, stream=None):
+               chain_results: bool = False, trace_items=None, trace_cap: int = 0, stream=None,
+               w_migrate: int = 0, w_reverse: int = 0):
         """Alg.1 on the device (collective when world > 1).  Returns the best Plan, plus
-        (per-config plans, per-chain results, traces) when requested."""
+        (per-config plans, per-chain results, traces) when requested.  w_migrate and
+        w_reverse (1/2048 units) enable the paper's full move set (R21); 0, 0 = swap only."""
         import torch
         s = torch.cuda.current_stream(self.device) if stream is None else stream
         self._check(self._L.pipette_set_stream(self._h, C.c_void_p(s.cuda_stream)))
@@ -223,6 +225,7 @@ class Pipette:
         cap = self.n_nodes * self.gpus_per_node
         opts = _abi.SaOpts()
         opts.alpha, opts.tau, opts.t0 = float(alpha), float(tau), float(t0)
+        opts.w_migrate, opts.w_reverse = int(w_migrate), int(w_reverse)
         keep = []
         n_items = 0
         if chain_results:

@@ -53,7 +53,7 @@ class SaOpts(C.Structure):
                 ("chains", C.POINTER(ChainResult)), ("chain_perms", C.POINTER(C.c_uint16)),
                 ("chain_perm_stride", C.c_int32), ("chains_cap", C.c_int64),
                 ("trace_items", C.POINTER(C.c_int64)), ("n_trace", C.c_int32), ("trace_cap", C.c_int32),
-                ("trace", C.POINTER(TraceRecord))]
+                ("trace", C.POINTER(TraceRecord)), ("w_migrate", C.c_int32), ("w_reverse", C.c_int32)]
 
 
 class Plan(C.Structure):

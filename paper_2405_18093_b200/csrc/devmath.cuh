@@ -69,6 +69,16 @@ __device__ __forceinline__ Draw draw_from_words(uint4 w, uint32_t N) {
   return d;
 }
 
+// A proposal of the full move set (R21): the same (p, q, u) plus the move selector
+// t = ((w2 & 31) << 6) | (w3 & 63) in [0, 2048), the 11 bits u leaves unused.
+struct DrawM {
+  Draw d;
+  uint32_t t;
+};
+
+__device__ __forceinline__ DrawM draw_move_rk(uint32_t step, uint32_t chain, uint32_t e, const RoundKeys& rk,
+                                              uint32_t N);
+
 __device__ __forceinline__ Draw draw_swap(uint32_t step, uint32_t chain, uint32_t e, uint2 key, uint32_t N) {
   return draw_from_words(philox4x32_10(make_uint4(step, chain, e, 0u), key), N);
 }
@@ -76,6 +86,15 @@ __device__ __forceinline__ Draw draw_swap(uint32_t step, uint32_t chain, uint32_
 __device__ __forceinline__ Draw draw_swap_rk(uint32_t step, uint32_t chain, uint32_t e, const RoundKeys& rk,
                                              uint32_t N) {
   return draw_from_words(philox4x32_10_rk(make_uint4(step, chain, e, 0u), rk), N);
+}
+
+__device__ __forceinline__ DrawM draw_move_rk(uint32_t step, uint32_t chain, uint32_t e, const RoundKeys& rk,
+                                              uint32_t N) {
+  const uint4 w = philox4x32_10_rk(make_uint4(step, chain, e, 0u), rk);
+  DrawM m;
+  m.d = draw_from_words(w, N);
+  m.t = ((w.z & 31u) << 6) | (w.w & 63u);
+  return m;
 }
 
 // e^x for x <= 0 from IEEE + - * and floor only (R15): Cody-Waite reduction by ln 2

@@ -526,6 +526,8 @@ pipette_status pipette_search(pipette_ctx* ctx, const pipette_model* model, int6
   if (opts) o = *opts;
   if (!(o.alpha > 0.0 && o.alpha <= 1.0)) return fail(ctx, PIPETTE_E_INVALID, "alpha must be in (0, 1]");
   if (!(o.t0 > 0.0) && !(o.tau > 0.0)) return fail(ctx, PIPETTE_E_INVALID, "tau > 0 or t0 > 0 required");
+  if (o.w_migrate < 0 || o.w_reverse < 0 || o.w_migrate + o.w_reverse > 2048)
+    return fail(ctx, PIPETTE_E_INVALID, "move weights must satisfy 0 <= w_migrate, w_reverse and sum <= 2048");
   CU(cudaSetDevice(ctx->device));
   cudaStream_t s = ctx->stream;
 
@@ -599,6 +601,8 @@ pipette_status pipette_search(pipette_ctx* ctx, const pipette_model* model, int6
   // n x n m2*R table (one copy; above 32 KB the block has 8 warps to share it)
   const int r_bytes = mode == 0 ? 256 * 16 * 8 : (mode == 1 ? align16(nn * 8) : 0);
   const bool big = mode == 1 && r_bytes > 32 * 1024;
+  if (mode == 2 && (o.w_migrate || o.w_reverse))
+    return fail(ctx, PIPETTE_E_UNSUPPORTED, "the full move set needs N = pp*dp <= 256 (max N here %d)", maxN);
   const int threads = big ? 256 : kSaThreads;
   // psum (Eq.5 sums) cached in shared memory for configs with dp <= dp_cap: the largest cap
   // that still reaches the best achievable number of resident blocks per SM
@@ -735,6 +739,8 @@ pipette_status pipette_search(pipette_ctx* ctx, const pipette_model* model, int6
   P.trace_slot = tracing ? (const int*)ctx->trace_slot.p : nullptr;
   P.trace_cap = tracing ? o.trace_cap : 0;
   P.trace = tracing ? (pipette_trace_record*)ctx->trace.p : nullptr;
+  P.w_migrate = o.w_migrate;
+  P.w_reverse = o.w_reverse;
 
   const void* kern = sa_kernel(big ? 3 : mode, tracing, n);
   CU(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));

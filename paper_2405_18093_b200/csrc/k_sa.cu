@@ -1168,6 +1168,232 @@ __device__ __forceinline__ void run_task_sb(const SaParams& P, const SaTask T, c
   }
 }
 
+// ------------------------------------------------------------------ full move set (NEXT-1)
+// The paper's three movements (R21): swap, migration (remove the element at p,
+// insert it at index q) and reverse (positions min(p,q)..max(p,q)).  A migration or a
+// reverse changes up to N positions at once, and a warp almost always holds one, so
+// every proposal is evaluated in full from the slot bytes (the oracle's definition in
+// the kernel's fixed order, O(N) per step) and rejected moves are undone in place.
+__device__ __forceinline__ void move_bytes(uint8_t* sb, int kind, uint32_t p, uint32_t q) {
+  if (kind == 0) {
+    const uint8_t a = sb[HcState::off(p)], b = sb[HcState::off(q)];
+    sb[HcState::off(p)] = b;
+    sb[HcState::off(q)] = a;
+  } else if (kind == 1) {
+    const uint8_t x = sb[HcState::off(p)];
+    if (p < q) {
+      for (uint32_t w = p; w < q; ++w) sb[HcState::off(w)] = sb[HcState::off(w + 1u)];
+    } else {
+      for (uint32_t w = p; w > q; --w) sb[HcState::off(w)] = sb[HcState::off(w - 1u)];
+    }
+    sb[HcState::off(q)] = x;
+  } else {
+    uint32_t lo = min(p, q), hi = max(p, q);
+    for (; lo < hi; ++lo, --hi) {
+      const uint8_t a = sb[HcState::off(lo)], b = sb[HcState::off(hi)];
+      sb[HcState::off(lo)] = b;
+      sb[HcState::off(hi)] = a;
+    }
+  }
+}
+__device__ __forceinline__ void unmove_bytes(uint8_t* sb, int kind, uint32_t p, uint32_t q) {
+  if (kind == 1) move_bytes(sb, 1, q, p);
+  else move_bytes(sb, kind, p, q);
+}
+
+// max over ordered pairs a != b of the node set m (|m| = kk >= 2) of R[a][b]: the member
+// rows (k^2 loads) or the first pair of the global R-sorted list inside m (about (n/k)^2)
+__device__ __forceinline__ double pair_max_lane(const Mask4& m, int kk, const S1Ctx& X, const double* R) {
+  const int n = X.n;
+  double mx = 0.0;
+  if (kk * kk * kk * kk <= 4 * n * n) {
+#pragma unroll
+    for (int wd = 0; wd < 4; ++wd) {
+      uint32_t ba = m.word(wd);
+      while (ba) {
+        const int a = wd * 32 + __ffs(ba) - 1;
+        ba &= ba - 1;
+#pragma unroll
+        for (int wd2 = 0; wd2 < 4; ++wd2) {
+          uint32_t bb = m.word(wd2);
+          while (bb) {
+            const int b = wd2 * 32 + __ffs(bb) - 1;
+            bb &= bb - 1;
+            if (b != a) mx = fmax(mx, __ldg(R + a * n + b));
+          }
+        }
+      }
+    }
+    return mx;
+  }
+  for (int i = 0; i < X.gl_len; ++i) {
+    const uint32_t ab = __ldg(X.gl_ab + i);
+    if (m.test(ab & 0xffu) && m.test(ab >> 8)) return __ldg(X.gl_val + i);
+  }
+  return 0.0;
+}
+
+// Eq.3-6 of the mapping in the slot plane, from scratch.  MODE 0: nibble-coded table
+// (16 lane copies), stage-1 counts as register nibbles, T_in by ranks, T_ex by the
+// subset-max table.  MODE 1: n x n table, counts in shared memory, T_in over the member
+// nodes, T_ex by pair_max_lane.
+template <int MODE, int PP, int NW>
+__device__ __forceinline__ double full_eval(const uint8_t* sb, const uint32_t* sw, uint8_t* cb, const DevCfg& C,
+                                            const SbCtx& K, const S1Ctx& X, const double* R, double& tpp_o,
+                                            double& tdp_o) {
+  using CT = typename std::conditional<NW == 2, uint32_t, uint64_t>::type;
+  const int pp = PP > 0 ? PP : C.pp, dp = C.dp, n = K.n;
+  CT cnt = 0;
+  Mask4 mask;
+  mask.clear();
+  if constexpr (MODE == 1)
+    for (int a = 0; a < n; a += 4) *reinterpret_cast<uint32_t*>(cb + HcState::off((uint32_t)a)) = 0u;
+  auto stage1 = [&](uint32_t nd) {
+    if constexpr (MODE == 0) {
+      cnt += (CT)1 << (4u * nd);
+    } else {
+      cb[HcState::off(nd)] = (uint8_t)(cb[HcState::off(nd)] + 1u);
+      mask.set(nd);
+    }
+  };
+  auto term = [&](uint32_t a, uint32_t b) -> double {
+    return MODE == 0 ? K.T[(a | (b << 4)) * 16u] : K.T[a * (uint32_t)n + b];
+  };
+  double tpp = 0.0;
+  for (int z = 0; z < dp; ++z) {
+    double s = 0.0;
+    if constexpr (PP >= 4) {
+      constexpr int NWD = PP / 4;
+      uint32_t wd[NWD];
+#pragma unroll
+      for (int k = 0; k < NWD; ++k) wd[k] = sw[((uint32_t)z * NWD + (uint32_t)k) * 32u];
+      uint32_t prev = K.node(wd[0] & 0xffu);
+      stage1(prev);
+#pragma unroll
+      for (int x = 1; x < PP; ++x) {
+        const uint32_t cur = K.node(__byte_perm(wd[x >> 2], 0u, 0x4440u | (uint32_t)(x & 3)));
+        s = __dadd_rn(s, term(prev, cur));
+        prev = cur;
+      }
+    } else {
+      const uint32_t b = (uint32_t)(z * pp);
+      uint32_t prev = K.node(sb[HcState::off(b)]);
+      stage1(prev);
+      for (int x = 1; x < pp; ++x) {
+        const uint32_t cur = K.node(sb[HcState::off(b + (uint32_t)x)]);
+        s = __dadd_rn(s, term(prev, cur));
+        prev = cur;
+      }
+    }
+    tpp = fmax(tpp, s);
+  }
+  double tin = 0.0, tex = 0.0;
+  if constexpr (MODE == 0) {
+    uint32_t m = 0u, rmin = 0xffu;
+    for (int a = 0; a < n; ++a) {
+      const uint32_t c = (uint32_t)(cnt >> (4u * (uint32_t)a)) & 15u;
+      if (c) {
+        m |= 1u << a;
+        rmin = min(rmin, (uint32_t)__ldg(X.rank + a * 16 + c));
+      }
+    }
+    tin = rmin == 0xffu ? 0.0 : __ldg(X.vs + rmin);
+    const int k = __popc(m);
+    tex = k >= 2 ? __dmul_rn(__ldg(X.qe + k), __ldg(X.tab + m)) : 0.0;
+  } else {
+#pragma unroll
+    for (int wd = 0; wd < 4; ++wd) {
+      uint32_t bits = mask.word(wd);
+      while (bits) {
+        const uint32_t a = (uint32_t)(wd * 32 + __ffs(bits) - 1);
+        bits &= bits - 1;
+        const uint32_t c = cb[HcState::off(a)];
+        if (c >= 2u) tin = fmax(tin, __dmul_rn(__ldg(X.qi + c), __ldg(R + a * (uint32_t)n + a)));
+      }
+    }
+    const int k = mask.count();
+    tex = k >= 2 ? __dmul_rn(__ldg(X.qe + k), pair_max_lane(mask, k, X, R)) : 0.0;
+  }
+  tpp_o = tpp;
+  tdp_o = __dadd_rn(tin, tex);
+  return compose(C.Sb, C.r, C.Ss, tpp, tin, tex);
+}
+
+// One warp task with the full move set (MODE 0 or 1 state layout, slot plane only).
+template <int MODE, bool TRACE, int PP, int NW>
+__device__ __forceinline__ void run_task_full(const SaParams& P, const SaTask T, const DevCfg C, const double* Tt,
+                                              unsigned char* ws, int lane) {
+  const bool active = lane < T.count;
+  const int N = C.N, n = P.n_nodes;
+  const uint32_t chain = (uint32_t)(T.c_first + (T.k0 + lane) * P.world);
+  const int slot = T.slot0 + lane;
+  S1Ctx X;
+  X.qi = P.qtab + C.qi_off; X.qe = P.qtab + C.qe_off; X.tab = P.subset_max;
+  X.rank = MODE == 0 ? P.tin_rank + (size_t)T.f * 256 : nullptr;
+  X.vs = MODE == 0 ? P.tin_vs + (size_t)T.f * 256 : nullptr;
+  X.gl_ab = P.gl_ab; X.gl_val = P.gl_val; X.gl_len = n * (n - 1);
+  X.n = n;
+  SbCtx K;
+  K.T = MODE == 0 ? Tt + (lane & 15) : Tt; K.n = n; K.spn = (uint32_t)C.spn; K.spn_magic = C.spn_magic;
+  K.spn_sh = (C.spn & (C.spn - 1)) == 0 ? (uint32_t)(31 - __clz(C.spn)) : 32u;
+  const int plane = align16(((N + 3) / 4) * 128);
+  // MODE 0 layout: [hop-code plane (unused)][slot plane]; MODE 1: [slot plane][counts]
+  unsigned char* splane = MODE == 0 ? ws + plane : ws;
+  uint8_t* sb = splane + lane * 4;
+  const uint32_t* sw = reinterpret_cast<const uint32_t*>(splane) + lane;
+  uint8_t* cb = MODE == 1 ? ws + plane + lane * 4 : nullptr;
+  uint16_t* bperm = P.best_perm + T.perm_off;
+  for (int w = 0; w < N; ++w) {
+    sb[HcState::off((uint32_t)w)] = (uint8_t)w;
+    bperm[w * 32 + lane] = (uint16_t)w;
+  }
+  __syncwarp();
+  double tpp, tdp;
+  const double L0 = full_eval<MODE, PP, NW>(sb, sw, cb, C, K, X, P.R, tpp, tdp);
+  double cur = L0, best = L0, best_tpp = tpp, best_tdp = tdp;
+  int best_step = -1;
+  uint32_t accepted = 0;
+  double beta = P.t0 > 0.0 ? __ddiv_rn(1.0, P.t0) : __ddiv_rn(1.0, __dmul_rn(P.tau, L0));
+  const double ia = P.alpha_inv;
+  const int trow = (TRACE && active) ? P.trace_slot[slot] : -1;
+  const int th_swap = 2048 - P.w_migrate - P.w_reverse, th_mig = 2048 - P.w_reverse;
+  if (N >= 2) {
+    DrawM next = draw_move_rk(0u, chain, (uint32_t)C.e, P.rk, (uint32_t)N);
+    for (int i = 0; i < P.iterations; ++i) {
+      const DrawM m = next;
+      next = draw_move_rk((uint32_t)(i + 1), chain, (uint32_t)C.e, P.rk, (uint32_t)N);
+      const int kind = (int)m.t < th_swap ? 0 : ((int)m.t < th_mig ? 1 : 2);
+      move_bytes(sb, kind, m.d.p, m.d.q);
+      double tpp2, tdp2;
+      const double Lp = full_eval<MODE, PP, NW>(sb, sw, cb, C, K, X, P.R, tpp2, tdp2);
+      const bool acc = metropolis_fast(__dadd_rn(Lp, -cur), beta, m.d.u);
+      if (acc) {
+        cur = Lp;
+        ++accepted;
+        if (Lp < best) {
+          best = Lp; best_step = i; best_tpp = tpp2; best_tdp = tdp2;
+          for (int w = 0; w < N; ++w) bperm[w * 32 + lane] = (uint16_t)sb[HcState::off((uint32_t)w)];
+        }
+      } else {
+        unmove_bytes(sb, kind, m.d.p, m.d.q);
+      }
+      if (TRACE && trow >= 0 && i < P.trace_cap) {
+        pipette_trace_record rec;
+        rec.i = (uint32_t)i; rec.p = (uint16_t)m.d.p; rec.q = (uint16_t)m.d.q;
+        rec.accept = acc ? 1u : 0u; rec.latency = Lp;
+        P.trace[(size_t)trow * P.trace_cap + i] = rec;
+      }
+      beta = __dmul_rn(beta, ia);
+    }
+  }
+  if (active) {
+    ChainOut o;
+    o.best = best; o.best_tpp = best_tpp; o.best_tdp = best_tdp; o.L0 = L0;
+    o.best_step = best_step; o.accepted = accepted; o.f = T.f; o.c = (int32_t)chain;
+    P.out[slot] = o;
+  }
+}
+
 // MODE 0: n <= 16 nodes, N <= 256, spn <= 15: hop-code chain state (run_task_hc), register
 //         stage-1 state, the block's m2*R table in shared memory, subset-max table.
 // MODE 1: n <= 128, N <= 256: packed positions, S1Large, R through L1.
@@ -1226,7 +1452,20 @@ __global__ void __launch_bounds__(SaLB<MODE, BIG>::threads, SaLB<MODE, BIG>::blo
     const DevCfg C = P.cfgs[T.cfg];
     unsigned long long t_start = 0;
     if (lane == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_start));
-    if constexpr (MODE == 0) {
+    bool full = false;
+    if constexpr (MODE == 0 || MODE == 1) {
+      if (P.w_migrate | P.w_reverse) {   // the full move set (launch-uniform)
+        switch (C.pp) {
+          case 4: run_task_full<MODE, TRACE, 4, NW>(P, T, C, Rs, ws, lane); break;
+          case 8: run_task_full<MODE, TRACE, 8, NW>(P, T, C, Rs, ws, lane); break;
+          case 16: run_task_full<MODE, TRACE, 16, NW>(P, T, C, Rs, ws, lane); break;
+          default: run_task_full<MODE, TRACE, 0, NW>(P, T, C, Rs, ws, lane); break;
+        }
+        full = true;
+      }
+    }
+    if (full) {
+    } else if constexpr (MODE == 0) {
       switch (C.pp) {   // compile-time pipeline depth for the common power-of-two depths
         case 1: run_task_hc<TRACE, 1, NW>(P, T, C, Tl, ws, lane); break;
         case 2: run_task_hc<TRACE, 2, NW>(P, T, C, Tl, ws, lane); break;

@@ -93,6 +93,7 @@ struct SaParams {
   const int32_t* trace_slot;
   int32_t trace_cap;
   pipette_trace_record* trace;
+  int32_t w_migrate, w_reverse;   // full move set (R21); both 0: swap only
 };
 
 struct EvalParams {

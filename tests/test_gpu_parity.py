@@ -275,7 +275,7 @@ def test_search_is_deterministic_and_bandwidth_update_matters():
     assert c.latency_s > a.latency_s
 
 
-def _sampled_chain_parity(w, chains, iters, n_sample, seed=2, trace_n=3):
+def _sampled_chain_parity(w, chains, iters, n_sample, seed=2, trace_n=3, **moves):
     pip, B, prof = _ctx(w)
     model, mo, cl = _models(w)
     P = O.make_profile(prof)
@@ -284,20 +284,20 @@ def _sampled_chain_parity(w, chains, iters, n_sample, seed=2, trace_n=3):
     rng = np.random.default_rng(seed)
     items = rng.choice(len(feas) * chains, size=trace_n, replace=False).tolist()
     res = pip.search(model, w.bs_global, chains, iters, w.seed, chain_results=True, per_config=True,
-                     trace_items=items, trace_cap=iters)
+                     trace_items=items, trace_cap=iters, **moves)
     rows = res["chains"]
     assert len(rows) == len(feas) * chains
     by_e = {c.e: c for c in feas}
     for j in rng.choice(len(rows), size=n_sample, replace=False).tolist():
         r = rows[j]
-        o = _oracle_chain(cl, mo, P, R, by_e, r["cfg_index"], r["chain"], iters, w.seed)
+        o = _oracle_chain(cl, mo, P, R, by_e, r["cfg_index"], r["chain"], iters, w.seed, **moves)
         assert r["L0"] == o.L0
         assert (r["best"], r["best_step"], r["accepted"]) == (o.best, o.best_step, o.accepted), (j, r["cfg_index"])
         assert (r["best_t_pp"], r["best_t_dp"]) == (o.best_t_pp, o.best_t_dp)
         assert np.array_equal(r["perm"], o.best_perm)
     for t, j in enumerate(items):
         f, c = divmod(j, chains)
-        o = _oracle_chain(cl, mo, P, R, by_e, feas[f].e, c, iters, w.seed, trace=True)
+        o = _oracle_chain(cl, mo, P, R, by_e, feas[f].e, c, iters, w.seed, trace=True, **moves)
         assert res["trace"][t] == o.trace, j
     ref_best = min(rows, key=lambda r: (r["best"], r["item"]))
     assert res["plan"].latency_s == ref_best["best"] and res["plan"].chain == ref_best["chain"]
@@ -351,3 +351,53 @@ def test_search_custom_temperature_and_alpha():
         p = res["plan"]
         assert (p.latency_s, p.cfg_index, p.chain, p.best_step) == (ref.latency, ref.cfg_index, ref.chain, ref.best_step)
         assert p.sa_accepted == ref.sa_accepted
+
+
+# ------------------------------------------------------------------ full move set (NEXT-1, R21)
+UNIFORM = {"w_migrate": 683, "w_reverse": 682}
+
+
+def test_full_moves_c1_every_chain_and_plan_bit_exact():
+    w = W.WORKLOADS["C1"]
+    pip, B, prof = _ctx(w)
+    model, mo, cl = _models(w)
+    P = O.make_profile(prof)
+    R = O.inverse_bandwidth(B)
+    chains, iters = 3, 800
+    res = pip.search(model, w.bs_global, chains, iters, w.seed, chain_results=True, **UNIFORM)
+    by_e = {c.e: c for c in O.enumerate_configs(cl, mo, w.bs_global, P)}
+    for r in res["chains"]:
+        o = _oracle_chain(cl, mo, P, R, by_e, r["cfg_index"], r["chain"], iters, w.seed, **UNIFORM)
+        assert (r["L0"], r["best"], r["best_step"], r["accepted"]) == (o.L0, o.best, o.best_step, o.accepted), r["item"]
+        assert (r["best_t_pp"], r["best_t_dp"]) == (o.best_t_pp, o.best_t_dp)
+        assert np.array_equal(r["perm"], o.best_perm)
+    ref = O.search(cl, B, P, mo, w.bs_global, chains, iters, w.seed, **UNIFORM)
+    p = res["plan"]
+    assert (p.latency_s, p.cfg_index, p.chain, p.best_step) == (ref.latency, ref.cfg_index, ref.chain, ref.best_step)
+    assert np.array_equal(p.perm, ref.perm) and p.sa_accepted == ref.sa_accepted
+
+
+@pytest.mark.parametrize("moves", [UNIFORM, {"w_migrate": 2048, "w_reverse": 0}, {"w_migrate": 0, "w_reverse": 2048}],
+                         ids=["uniform", "migrate", "reverse"])
+def test_full_moves_c2_sampled_chains_and_traces(moves):
+    _sampled_chain_parity(W.WORKLOADS["C2"], chains=32, iters=600, n_sample=32, trace_n=3, **moves)
+
+
+def test_full_moves_mode1_c4_and_c5():
+    _sampled_chain_parity(W.WORKLOADS["C4"], chains=32, iters=400, n_sample=24, trace_n=2, **UNIFORM)
+    _sampled_chain_parity(W.WORKLOADS["C5"], chains=8, iters=200, n_sample=12, trace_n=2, **UNIFORM)
+
+
+def test_full_moves_unsupported_above_256_positions_and_bad_weights():
+    from paper_2405_18093_b200 import PipetteError
+    w = W.Workload("C0", 40, 8, W.GPT_345M, 320, 80_000_000_000, 100, 8, 600, 0.2, 0.2, 11)
+    pip, _, _ = _ctx(w)
+    model, _, _ = _models(w)
+    with pytest.raises(PipetteError) as ei:
+        pip.search(model, w.bs_global, 2, 10, 1, **UNIFORM)
+    assert ei.value.status == 6
+    w1 = W.WORKLOADS["C1"]
+    pip1, _, _ = _ctx(w1)
+    with pytest.raises(PipetteError) as ei:
+        pip1.search(_models(w1)[0], w1.bs_global, 2, 10, 1, w_migrate=2000, w_reverse=100)
+    assert ei.value.status == 2
