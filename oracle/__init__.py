@@ -139,6 +139,10 @@ def lib():
                                       C.c_int32, C.c_int32, C.c_int32, P(Plan), P(C.c_uint16), C.c_int32,
                                       P(C.c_double), P(C.c_int32)]
         L.or_search_moves.restype = C.c_int32
+        L.or_des_1f1b.argtypes = [C.c_int32, C.c_int32, C.c_double, C.c_double, P(C.c_double), P(C.c_double)]
+        L.or_des_1f1b.restype = C.c_double
+        L.or_models.argtypes = [P(Consts), P(C.c_double), P(C.c_uint16), P(C.c_double), P(C.c_double),
+                                P(C.c_double)]
         _lib = L
     return _lib
 
@@ -257,6 +261,22 @@ def draw(i, c, e, seed, N):
     p, q, u = C.c_uint32(), C.c_uint32(), C.c_double()
     lib().or_draw(i, c, e, seed, N, C.byref(p), C.byref(q), C.byref(u))
     return p.value, q.value, u.value
+
+
+def des_1f1b(pp, n_mb, f, b, hop_f, hop_b=None) -> float:
+    """Makespan of one pipeline under the 1F1B schedule (NEXT-2, R22)."""
+    hf = np.ascontiguousarray(np.asarray(hop_f if pp > 1 else [0.0], dtype=np.float64))
+    hb = hf if hop_b is None else np.ascontiguousarray(np.asarray(hop_b if pp > 1 else [0.0], dtype=np.float64))
+    return lib().or_des_1f1b(pp, n_mb, f, b, _dptr(hf), _dptr(hb))
+
+
+def models(K: Consts, R: np.ndarray, perm):
+    """(T_Pipette Eq.3, T_prev Eq.1, T_DES) of one plan (NEXT-2, R22)."""
+    R = np.ascontiguousarray(R, dtype=np.float64)
+    p = np.ascontiguousarray(np.asarray(perm, dtype=np.uint16))
+    a, b, c = C.c_double(), C.c_double(), C.c_double()
+    lib().or_models(C.byref(K), _dptr(R), _u16ptr(p), C.byref(a), C.byref(b), C.byref(c))
+    return a.value, b.value, c.value
 
 
 def draw_move(i, c, e, seed, N):

@@ -203,6 +203,107 @@ double or_latency(const or_consts* K, const double* R, const uint16_t* perm, or_
 }
 
 /* ------------------------------------------------------------------------- */
+/* NEXT-2: the prior-work closed form Eq.1 and a       */
+/* discrete-event simulation of the memory-efficient 1F1B schedule (P:107-111,   */
+/* Fig.2b; the "hidden critical paths" of P:269-271), reading R22.     */
+/*                                                                                */
+/* or_des_1f1b: one pipeline of pp stages and n_mb microbatches.  Stage s         */
+/* (0-based) runs Megatron's 1F1B op order: w = min(pp-s-1, n_mb) warm-up         */
+/* forwards, then one forward / one backward until its forwards are exhausted,    */
+/* then the remaining w backwards.  F(s,m) may start when F(s-1,m) has ended plus */
+/* hop_f[s-1] (s-1 -> s); B(s,m) when B(s+1,m) has ended plus hop_b[s] (s+1 -> s);*/
+/* B(pp-1,m) after F(pp-1,m).  A stage runs one op at a time, in its order;       */
+/* start = max(stage free, dependency ready), end = start + f (or b).  Plain      */
+/* event loop: every stage advances while its next op's dependency has ended.     */
+/* Returns the makespan (the last end).                                           */
+/* ------------------------------------------------------------------------- */
+static void des_op(int32_t pp, int32_t n_mb, int32_t s, int32_t k, int32_t* is_f, int32_t* m) {
+  int32_t w = pp - s - 1 < n_mb ? pp - s - 1 : n_mb;
+  if (k < w) { *is_f = 1; *m = k; }
+  else if (k < 2 * n_mb - w) { int32_t j = k - w; *is_f = (j % 2) == 0; *m = (j % 2) == 0 ? w + j / 2 : j / 2; }
+  else { *is_f = 0; *m = k - n_mb; }
+}
+
+double or_des_1f1b(int32_t pp, int32_t n_mb, double f, double b, const double* hop_f, const double* hop_b) {
+  double* fend = (double*)malloc(sizeof(double) * (size_t)pp * (size_t)n_mb);
+  double* bend = (double*)malloc(sizeof(double) * (size_t)pp * (size_t)n_mb);
+  char* fdone = (char*)calloc((size_t)pp * (size_t)n_mb, 1);
+  char* bdone = (char*)calloc((size_t)pp * (size_t)n_mb, 1);
+  int32_t* ptr = (int32_t*)calloc((size_t)pp, sizeof(int32_t));
+  double* freet = (double*)calloc((size_t)pp, sizeof(double));
+  int64_t remaining = 2 * (int64_t)pp * n_mb;
+  double makespan = 0.0;
+  while (remaining > 0) {
+    int progressed = 0;
+    for (int32_t s = 0; s < pp; ++s) {
+      while (ptr[s] < 2 * n_mb) {
+        int32_t is_f, m;
+        des_op(pp, n_mb, s, ptr[s], &is_f, &m);
+        double dep = 0.0, dur;
+        if (is_f) {
+          if (s > 0) {
+            if (!fdone[(s - 1) * n_mb + m]) break;
+            dep = fend[(s - 1) * n_mb + m] + hop_f[s - 1];
+          }
+          dur = f;
+        } else {
+          if (s < pp - 1) {
+            if (!bdone[(s + 1) * n_mb + m]) break;
+            dep = bend[(s + 1) * n_mb + m] + hop_b[s];
+          } else {
+            dep = fend[s * n_mb + m];
+          }
+          dur = b;
+        }
+        double start = freet[s] > dep ? freet[s] : dep;
+        double end = start + dur;
+        if (is_f) { fend[s * n_mb + m] = end; fdone[s * n_mb + m] = 1; }
+        else      { bend[s * n_mb + m] = end; bdone[s * n_mb + m] = 1; }
+        freet[s] = end;
+        if (end > makespan) makespan = end;
+        ++ptr[s];
+        --remaining;
+        progressed = 1;
+      }
+    }
+    if (!progressed) break;   /* cannot happen for the 1F1B order (deadlock-free) */
+  }
+  free(fend); free(bend); free(fdone); free(bdone); free(ptr); free(freet);
+  return makespan;
+}
+
+/* The three latency models of one plan (reading R22):
+ *   T_Pipette  Eq.3-6 (or_latency);
+ *   T_prev     Eq.1 with the same terms: (n_mb-1)(C+T_TP) + pp(C+T_TP) + T_PP + T_DP,
+ *              where Eq.5's sum stands for (pp-1) T_com^PP (R6), evaluated as
+ *              ((((n_mb-1) * S) + Sb) + T_PP) + (T_in + T_ex);
+ *   T_DES      max over the dp pipelines of the 1F1B simulation + (T_in + T_ex), with
+ *              per-stage f = S / 3, b = S - f (backward = 2 x forward), one-way hops
+ *              msg_PP * R in the direction of the transfer (msg_PP = m2 / 2, exact). */
+void or_models(const or_consts* K, const double* R, const uint16_t* perm, double* t_pipette, double* t_prev,
+               double* t_des) {
+  or_breakdown bd;
+  *t_pipette = or_latency(K, R, perm, &bd);
+  *t_prev = ((((double)(K->n_mb - 1) * K->S) + K->Sb) + bd.t_pp) + bd.t_dp;
+  const int32_t pp = K->pp, n = K->n_nodes, spn = K->spn;
+  const double f = K->S / 3.0, b = K->S - f, half = K->m2 * 0.5;
+  double* hf = (double*)malloc(sizeof(double) * (size_t)(pp > 1 ? pp - 1 : 1));
+  double* hb = (double*)malloc(sizeof(double) * (size_t)(pp > 1 ? pp - 1 : 1));
+  double mk = 0.0;
+  for (int32_t z = 0; z < K->dp; ++z) {
+    for (int32_t x = 0; x + 1 < pp; ++x) {
+      int32_t a = perm[z * pp + x] / spn, c = perm[z * pp + x + 1] / spn;
+      hf[x] = half * R[a * n + c];
+      hb[x] = half * R[c * n + a];
+    }
+    double v = or_des_1f1b(pp, K->n_mb, f, b, hf, hb);
+    if (v > mk) mk = v;
+  }
+  free(hf); free(hb);
+  *t_des = mk + bd.t_dp;
+}
+
+/* ------------------------------------------------------------------------- */
 /* Philox4x32-10 (Salmon et al. SC'11), R14: counter (step, chain, cfg, 0),       */
 /* key (seed lo32, seed hi32).  Round = Random123 / cuRAND definition.            */
 /* ------------------------------------------------------------------------- */

@@ -104,6 +104,11 @@ void or_sa_chain(const or_consts* K, const double* R, int32_t iterations, uint64
                  or_chain_result* res, uint16_t* best_perm,
                  or_trace_record* trace, int32_t trace_cap);
 
+/* NEXT-2: Eq.1 and a 1F1B discrete-event simulation, reading R22. */
+double or_des_1f1b(int32_t pp, int32_t n_mb, double f, double b, const double* hop_f, const double* hop_b);
+void or_models(const or_consts* K, const double* R, const uint16_t* perm, double* t_pipette, double* t_prev,
+               double* t_des);
+
 /* NEXT-1: the paper's three SA movements, reading R21. */
 void or_draw_move(uint32_t i, uint32_t c, uint32_t e, uint64_t seed, int32_t N,
                   uint32_t* p, uint32_t* q, double* u, uint32_t* t);
