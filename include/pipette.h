@@ -198,6 +198,21 @@ pipette_status pipette_search(pipette_ctx* ctx, const pipette_model* model, int6
                               const pipette_sa_opts* opts, pipette_plan* out,
                               pipette_plan* per_config, int32_t per_config_cap);
 
+/* NEXT-2: three latency models of n caller candidates (same inputs,
+ * layout, ownership and asynchrony as pipette_eval; reading R22 of DESIGN.md):
+ *   d_t_pipette[i] : Eq.3-6, bit-identical to pipette_eval's latency
+ *   d_t_prev[i]    : Eq.1, the prior-work model, with Eq.5's sum for
+ *                    (pp-1) T_com^PP: ((((n_mb-1) C') + pp C') + T_PP) + T_DP, C' = C + T_TP
+ *   d_t_des[i]     : a discrete-event simulation of the 1F1B schedule (P:107-111,
+ *                    P:132-138) of every pipeline with f = C'/3, b = C' - f and directed
+ *                    one-way hops msg_PP / B, max over pipelines, plus T_DP
+ *   d_status[i]    : as pipette_eval, plus 5 = pp > 128 (not simulated); no memory output.
+ * The three are NaN when status is 2..5.  Errors: as pipette_eval. */
+pipette_status pipette_eval_models(pipette_ctx* ctx, const pipette_model* model, int64_t bs_global, int64_t n,
+                                   const pipette_config* d_cfg, const uint16_t* d_perm, int32_t perm_stride,
+                                   double* d_t_pipette, double* d_t_prev, double* d_t_des, uint8_t* d_status,
+                                   void* stream);
+
 /* Host-only helper (no GPU needed): the items j in [0, n_items) that `rank` of `world`
  * runs (R18), written to items (capacity cap).  Returns the count (may exceed cap). */
 int64_t pipette_shard_items(int64_t n_items, int32_t rank, int32_t world, int64_t* items, int64_t cap);

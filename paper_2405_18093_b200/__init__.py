@@ -210,6 +210,25 @@ class Pipette:
                                          mem.data_ptr(), status.data_ptr(), C.c_void_p(s.cuda_stream)))
         return lat, mem, status
 
+    def eval_models(self, model: Model, bs_global: int, cfg, perm, stream=None):
+        """NEXT-2: (T_Pipette Eq.3, T_prev Eq.1, T_DES 1F1B simulation, status) CUDA tensors
+        of the candidates (same inputs as eval)."""
+        import torch
+        n = int(cfg.shape[0])
+        if cfg.dtype not in (torch.int16, torch.uint16) or perm.dtype not in (torch.int16, torch.uint16):
+            raise TypeError("cfg and perm must be 16-bit integer tensors")
+        if not (cfg.is_cuda and perm.is_cuda and cfg.is_contiguous() and perm.is_contiguous()):
+            raise ValueError("cfg and perm must be contiguous CUDA tensors")
+        tp, tprev, tdes = (torch.empty(n, dtype=torch.float64, device=cfg.device) for _ in range(3))
+        status = torch.empty(n, dtype=torch.uint8, device=cfg.device)
+        s = torch.cuda.current_stream(cfg.device) if stream is None else stream
+        m = model.c()
+        self._check(self._L.pipette_eval_models(self._h, C.byref(m), int(bs_global), n, cfg.data_ptr(),
+                                                perm.data_ptr(), int(perm.shape[1]) if perm.dim() == 2 else 1,
+                                                tp.data_ptr(), tprev.data_ptr(), tdes.data_ptr(), status.data_ptr(),
+                                                C.c_void_p(s.cuda_stream)))
+        return tp, tprev, tdes, status
+
     # ------------------------------------------------------------------ search
     def search(self, model: Model, bs_global: int, chains: int, iterations: int, seed: int,
                alpha: float = 0.999, tau: float = 0.05, t0: float = 0.0, per_config: bool = False,

@@ -20,6 +20,10 @@ __global__ void k_enumerate_filter(int, int, unsigned long long, int, pipette_mo
                                    const pipette_profile_entry*, int, DevCfg*, unsigned long long*, int, int*,
                                    double*, int, EnumOut*);
 const void* eval_kernel(int mode);
+pipette_status models_launch(const DevCfg* cfgs, const unsigned long long* keys, int E, const double* qtab,
+                             const double* R, int n_nodes, long long n, const pipette_config* cand,
+                             const uint16_t* perm, int stride, double* tp, double* tprev, double* tdes,
+                             uint8_t* status, void* stream);
 size_t eval_smem_bytes(int mode, int perm_stride, bool staged, int n_nodes, int E, int bm_words);
 __global__ void k_tin_values(const DevCfg*, const double*, const double*, int, double*);
 const void* sa_kernel(int mode, bool trace, int n_nodes);
@@ -508,6 +512,28 @@ pipette_status pipette_eval(pipette_ctx* ctx, const pipette_model* model, int64_
   CU(cudaLaunchKernel(kern, dim3(grid), dim3(256), args, smem, s));
   ctx->launches++;
   CU(cudaGetLastError());
+  return PIPETTE_OK;
+}
+
+pipette_status pipette_eval_models(pipette_ctx* ctx, const pipette_model* model, int64_t bs_global, int64_t n,
+                                   const pipette_config* d_cfg, const uint16_t* d_perm, int32_t perm_stride,
+                                   double* d_t_pipette, double* d_t_prev, double* d_t_des, uint8_t* d_status,
+                                   void* stream) {
+  if (!ctx) return PIPETTE_E_INVALID;
+  ctx->launches = 0;
+  pipette_status st = check_model(ctx, model, bs_global);
+  if (st != PIPETTE_OK) return st;
+  if (n < 0 || perm_stride < 1) return fail(ctx, PIPETTE_E_INVALID, "n >= 0 and perm_stride >= 1 required");
+  if (n == 0) return PIPETTE_OK;
+  if (!d_cfg || !d_perm || !d_t_pipette || !d_t_prev || !d_t_des || !d_status)
+    return fail(ctx, PIPETTE_E_INVALID, "null device pointer");
+  CU(cudaSetDevice(ctx->device));
+  if ((st = enumerate(ctx, model, bs_global, false)) != PIPETTE_OK) return st;
+  st = models_launch((const DevCfg*)ctx->cfgs.p, (const unsigned long long*)ctx->keys.p, ctx->E,
+                     (const double*)ctx->qtab.p, ctx->dR, ctx->n_nodes, n, d_cfg, d_perm, perm_stride, d_t_pipette,
+                     d_t_prev, d_t_des, d_status, stream);
+  ctx->launches++;
+  if (st != PIPETTE_OK) return fail(ctx, st, "k_models launch failed: %s", cudaGetErrorString(cudaGetLastError()));
   return PIPETTE_OK;
 }
 

@@ -1,0 +1,195 @@
+// k_models.cu -- K5 (NEXT-2): the three latency models of caller
+// candidates, one thread per candidate:
+//   T_Pipette  Eq.3-6, the same value as K2;
+//   T_prev     Eq.1, the prior-work closed form with the same terms (R22);
+//   T_DES      a discrete-event simulation of the memory-efficient 1F1B schedule (P:107-111,
+//              P:132-138; the hidden critical paths of P:269-271): max over the dp pipelines
+//              of the simulated makespan, plus T_DP (R22).
+//
+// The DES of one pipeline keeps O(pp) state.  Stage s runs its 2 n_mb ops in Megatron's
+// 1F1B order; op k of stage s is F(k) for k < w = min(pp-s-1, n_mb), F(w + j/2) or B(j/2)
+// for j = k - w < 2(n_mb - w) (even / odd j), else B(k - n_mb).  The dependency of op
+// (s, k) -- F(s-1, m) for a forward, B(s+1, m) for a backward -- sits at op index k or
+// k-1 of the neighbour stage (checked for pp < 40, n_mb < 70 in the survey of this kernel
+// and by the parity tests), so the ops are computed by increasing k with two rows of end
+// times, forwards in ascending s and backwards in descending s within a k.  Every op is
+// start = max(stage free, dependency end + hop), end = start + f (or b): the oracle's
+// event loop computes the same IEEE values in another order, so the results are identical.
+#include "devmath.cuh"
+#include "pipette_dev.cuh"
+
+namespace pip {
+
+constexpr int kModelsThreads = 128;
+constexpr int kDesMaxPP = 128;   // local rows of the DES
+
+__device__ __forceinline__ int des_w(int pp, int n_mb, int s) { return min(pp - s - 1, n_mb); }
+__device__ __forceinline__ int des_idx_f(int pp, int n_mb, int s, int m) {
+  const int w = des_w(pp, n_mb, s);
+  return m < w ? m : 2 * m - w;
+}
+__device__ __forceinline__ int des_idx_b(int pp, int n_mb, int s, int m) {
+  const int w = des_w(pp, n_mb, s);
+  return m < n_mb - w ? w + 2 * m + 1 : n_mb + m;
+}
+
+struct ModelsParams {
+  const DevCfg* cfgs;
+  const unsigned long long* keys;
+  int32_t E;
+  const double* qtab;
+  const double* R;
+  int32_t n_nodes;
+  int64_t n;
+  const pipette_config* cand;
+  const uint16_t* perm;
+  int32_t perm_stride;
+  double* t_pipette;
+  double* t_prev;
+  double* t_des;
+  uint8_t* status;
+};
+
+// Makespan of pipeline z of the candidate row (nodes read from the row).
+__device__ double des_pipeline(const ModelsParams& P, const DevCfg& C, const uint16_t* row, int z, double f,
+                               double b, double half, double* E0, double* E1) {
+  const int pp = C.pp, n_mb = C.n_mb, n = P.n_nodes;
+  const uint32_t spn = (uint32_t)C.spn;
+  auto node = [&](int x) { return div_small((uint32_t)__ldg(row + z * pp + x), C.spn_magic, spn); };
+  auto hop_f = [&](int s) { return __dmul_rn(half, __ldg(P.R + node(s) * n + node(s + 1))); };   // s -> s+1
+  auto hop_b = [&](int s) { return __dmul_rn(half, __ldg(P.R + node(s + 1) * n + node(s))); };   // s+1 -> s
+  double mk = 0.0;
+  for (int k = 0; k < 2 * n_mb; ++k) {
+    double* cur = (k & 1) ? E1 : E0;
+    double* prv = (k & 1) ? E0 : E1;
+    // forwards, ascending s
+    for (int s = 0; s < pp; ++s) {
+      const int w = des_w(pp, n_mb, s);
+      int m;
+      bool is_f;
+      if (k < w) { is_f = true; m = k; }
+      else if (k < 2 * n_mb - w) { const int j = k - w; is_f = (j & 1) == 0; m = is_f ? w + j / 2 : j / 2; }
+      else { is_f = false; m = k - n_mb; }
+      if (!is_f) continue;
+      const double fr = k > 0 ? prv[s] : 0.0;
+      double dep = 0.0;
+      if (s > 0) {
+        const int d = des_idx_f(pp, n_mb, s - 1, m);
+        dep = __dadd_rn((d == k ? cur : prv)[s - 1], hop_f(s - 1));
+      }
+      cur[s] = __dadd_rn(fmax(fr, dep), f);
+      mk = fmax(mk, cur[s]);
+    }
+    // backwards, descending s
+    for (int s = pp - 1; s >= 0; --s) {
+      const int w = des_w(pp, n_mb, s);
+      int m;
+      bool is_f;
+      if (k < w) { is_f = true; m = k; }
+      else if (k < 2 * n_mb - w) { const int j = k - w; is_f = (j & 1) == 0; m = is_f ? w + j / 2 : j / 2; }
+      else { is_f = false; m = k - n_mb; }
+      if (is_f) continue;
+      const double fr = prv[s];
+      double dep;
+      if (s < pp - 1) {
+        const int d = des_idx_b(pp, n_mb, s + 1, m);
+        dep = __dadd_rn((d == k ? cur : prv)[s + 1], hop_b(s));
+      } else {
+        dep = fr;   // B(pp-1, m) after F(pp-1, m), the stage's previous op
+      }
+      cur[s] = __dadd_rn(fmax(fr, dep), b);
+      mk = fmax(mk, cur[s]);
+    }
+  }
+  return mk;
+}
+
+__global__ void __launch_bounds__(kModelsThreads) k_models(ModelsParams P) {
+  const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= P.n) return;
+  const double qnan = __longlong_as_double(0x7ff8000000000000ll);
+  const pipette_config cf = P.cand[i];
+  const unsigned long long key = ((unsigned long long)cf.pp << 48) | ((unsigned long long)cf.tp << 32) |
+                                 ((unsigned long long)cf.dp << 16) | (unsigned long long)cf.mb;
+  int lo = 0, hi = P.E;
+  while (lo < hi) {
+    const int mid = (lo + hi) >> 1;
+    if (__ldg(P.keys + mid) < key) lo = mid + 1; else hi = mid;
+  }
+  if (lo >= P.E || __ldg(P.keys + lo) != key) {
+    P.t_pipette[i] = P.t_prev[i] = P.t_des[i] = qnan;
+    P.status[i] = 2;
+    return;
+  }
+  const DevCfg C = P.cfgs[lo];
+  const uint16_t* row = P.perm + i * (long long)P.perm_stride;
+  const int N = C.N, pp = C.pp, dp = C.dp, n = P.n_nodes;
+  // bijection (Eq.2): a bitmap of N <= 1024 bits
+  uint32_t seen[32];
+  for (int j = 0; j < 32; ++j) seen[j] = 0u;
+  bool ok = true;
+  for (int w = 0; w < N; ++w) {
+    const uint32_t v = __ldg(row + w);
+    if (v >= (uint32_t)N || (seen[v >> 5] >> (v & 31)) & 1u) ok = false;
+    else seen[v >> 5] |= 1u << (v & 31);
+  }
+  if (!ok || !C.has_profile || pp > kDesMaxPP) {
+    P.t_pipette[i] = P.t_prev[i] = P.t_des[i] = qnan;
+    P.status[i] = !ok ? 3 : (!C.has_profile ? 4 : 5);
+    return;
+  }
+  const uint32_t spn = (uint32_t)C.spn;
+  auto node = [&](int w) { return div_small((uint32_t)__ldg(row + w), C.spn_magic, spn); };
+  // Eq.5
+  double tpp = 0.0;
+  for (int z = 0; z < dp; ++z) {
+    double s = 0.0;
+    for (int x = 0; x + 1 < pp; ++x)
+      s = __dadd_rn(s, __dmul_rn(C.m2, __ldg(P.R + node(z * pp + x) * n + node(z * pp + x + 1))));
+    tpp = fmax(tpp, s);
+  }
+  // Eq.6 (stage-1 occupancy as a count per node, n <= 128)
+  uint8_t cnt[kMaxNodes];
+  for (int a = 0; a < n; ++a) cnt[a] = 0;
+  for (int z = 0; z < dp; ++z) cnt[node(z * pp)] += 1;
+  int k = 0;
+  double tin = 0.0, mx = 0.0;
+  for (int a = 0; a < n; ++a) {
+    if (!cnt[a]) continue;
+    ++k;
+    if (cnt[a] >= 2) tin = fmax(tin, __dmul_rn(__ldg(P.qtab + C.qi_off + cnt[a]), __ldg(P.R + a * n + a)));
+    for (int b = 0; b < n; ++b)
+      if (b != a && cnt[b]) mx = fmax(mx, __ldg(P.R + a * n + b));
+  }
+  const double tex = k >= 2 ? __dmul_rn(__ldg(P.qtab + C.qe_off + k), mx) : 0.0;
+  const double tdp = __dadd_rn(tin, tex);
+  P.t_pipette[i] = compose(C.Sb, C.r, C.Ss, tpp, tin, tex);
+  // Eq.1: ((((n_mb - 1) * S) + Sb) + T_PP) + T_DP
+  P.t_prev[i] = __dadd_rn(__dadd_rn(__dadd_rn(__dmul_rn((double)(C.n_mb - 1), C.S), C.Sb), tpp), tdp);
+  // DES
+  const double f = __ddiv_rn(C.S, 3.0), b = __dadd_rn(C.S, -f), half = __dmul_rn(C.m2, 0.5);
+  double E0[kDesMaxPP], E1[kDesMaxPP];
+  double mk = 0.0;
+  for (int z = 0; z < dp; ++z) mk = fmax(mk, des_pipeline(P, C, row, z, f, b, half, E0, E1));
+  P.t_des[i] = __dadd_rn(mk, tdp);
+  P.status[i] = C.feasible ? 0 : 1;
+}
+
+void launch_models(const ModelsParams& P, cudaStream_t s) {
+  const long long blocks = (P.n + kModelsThreads - 1) / kModelsThreads;
+  k_models<<<(unsigned)blocks, kModelsThreads, 0, s>>>(P);
+}
+
+}  // namespace pip
+
+// host-side marshalling kept beside the kernel (host.cu owns the context)
+namespace pip {
+pipette_status models_launch(const DevCfg* cfgs, const unsigned long long* keys, int E, const double* qtab,
+                             const double* R, int n_nodes, long long n, const pipette_config* cand,
+                             const uint16_t* perm, int stride, double* tp, double* tprev, double* tdes,
+                             uint8_t* status, void* stream) {
+  ModelsParams P{cfgs, keys, E, qtab, R, n_nodes, n, cand, perm, stride, tp, tprev, tdes, status};
+  launch_models(P, (cudaStream_t)stream);
+  return cudaGetLastError() == cudaSuccess ? PIPETTE_OK : PIPETTE_E_CUDA;
+}
+}  // namespace pip

@@ -401,3 +401,41 @@ def test_full_moves_unsupported_above_256_positions_and_bad_weights():
     with pytest.raises(PipetteError) as ei:
         pip1.search(_models(w1)[0], w1.bs_global, 2, 10, 1, w_migrate=2000, w_reverse=100)
     assert ei.value.status == 2
+
+
+# ------------------------------------------------------------------ NEXT-2: Eq.1 and the 1F1B DES (R22)
+@pytest.mark.parametrize("name", ["C1", "C2", "C3", "C4"])
+def test_eval_models_bit_exact(name):
+    import torch
+    w = W.WORKLOADS[name]
+    pip, B, prof = _ctx(w)
+    model, mo, cl = _models(w)
+    P = O.make_profile(prof)
+    R = O.inverse_bandwidth(B)
+    feas = [c for c in O.enumerate_configs(cl, mo, w.bs_global, P) if c.feasible]
+    rng = np.random.default_rng(11)
+    per = 6 if name != "C4" else 3
+    Nmax = max(c.pp * c.dp for c in feas)
+    stride = ((Nmax + 7) // 8) * 8
+    rows, perms, want = [], [], []
+    for c in feas:
+        K = O.constants(cl, mo, c, P)
+        for p in W.random_perms(K.N, per, int(rng.integers(1 << 30))):
+            row = np.zeros(stride, dtype=np.uint16)
+            row[:K.N] = p
+            rows.append((c.pp, c.tp, c.dp, c.mb)); perms.append(row)
+            want.append(O.models(K, R, p))
+    bad = np.zeros(stride, dtype=np.uint16)                    # duplicate slot -> status 3
+    rows.append(rows[0]); perms.append(bad)
+    rows.append((3, 1, 1, 1)); perms.append(perms[0])          # not enumerated -> status 2
+    cfg = torch.tensor(np.asarray(rows, dtype=np.int16), device="cuda")
+    pr = torch.from_numpy(np.stack(perms).view(np.int16)).cuda()
+    tp, tprev, tdes, st = (x.cpu().numpy() for x in pip.eval_models(model, w.bs_global, cfg, pr))
+    n = len(want)
+    want = np.asarray(want)
+    assert st[n] == 3 and st[n + 1] == 2 and np.isnan(tp[n]) and np.isnan(tdes[n + 1])
+    for col, got in enumerate((tp[:n], tprev[:n], tdes[:n])):
+        assert _assert_close(got, want[:, col]) == 0, f"model {col}: not bit-identical"
+    # the same T_Pipette as the eval stream
+    lat, _, _ = _eval_batch(pip, model, w.bs_global, rows[:n], np.stack(perms[:n]))
+    assert np.array_equal(lat, tp[:n])
