@@ -213,6 +213,20 @@ pipette_status pipette_eval_models(pipette_ctx* ctx, const pipette_model* model,
                                    double* d_t_pipette, double* d_t_prev, double* d_t_des, uint8_t* d_status,
                                    void* stream);
 
+/* NEXT-3: Alg.1 l.1 "network_profile()" (the paper's mpiGraph
+ * profile of node pairs, Fig.3) on the GPUs of this box, from ONE process that
+ * sees them all.  Every ordered pair (i, j) of devices[0..n_gpus) is timed with an
+ * SM-driven copy kernel on GPU i that pushes `bytes` into GPU j's memory (peer stores over
+ * NVLink / NVSwitch), the diagonal with the same copy inside GPU i; median of `reps`
+ * launches after two warm-ups, CUDA events on GPU i.
+ *   bw_out : n_gpus x n_gpus row-major bytes/s (HOST), directed, diagonal = intra -- the
+ *            matrix pipette_init takes for a cluster of n_gpus one-GPU nodes (R5)
+ *   ms_out : the median times (HOST, optional)
+ *   err    : message buffer (optional)
+ * Errors: E_INVALID, E_UNSUPPORTED (a pair without a peer path), E_CUDA. */
+pipette_status pipette_profile_bandwidth(int32_t n_gpus, const int32_t* devices, uint64_t bytes, int32_t reps,
+                                         double* bw_out, double* ms_out, char* err, int32_t err_cap);
+
 /* Host-only helper (no GPU needed): the items j in [0, n_items) that `rank` of `world`
  * runs (R18), written to items (capacity cap).  Returns the count (may exceed cap). */
 int64_t pipette_shard_items(int64_t n_items, int32_t rank, int32_t world, int64_t* items, int64_t cap);

@@ -92,6 +92,27 @@ def nccl_unique_id() -> bytes:
     return buf.raw
 
 
+def profile_bandwidth(devices=None, bytes_per_copy: int = 256 << 20, reps: int = 5):
+    """NEXT-3: Alg.1 l.1 on this box (pipette_profile_bandwidth).  Returns (B, ms): the
+    directed n x n bytes/s matrix over `devices` (default: every visible GPU) with the
+    intra-GPU copy bandwidth on the diagonal, and the median copy times."""
+    L = _abi.lib()
+    if devices is None:
+        import torch
+        devices = list(range(torch.cuda.device_count()))
+    devs = np.ascontiguousarray(devices, dtype=np.int32)
+    n = len(devs)
+    bw = np.zeros((n, n), dtype=np.float64)
+    ms = np.zeros((n, n), dtype=np.float64)
+    err = C.create_string_buffer(512)
+    st = L.pipette_profile_bandwidth(n, devs.ctypes.data_as(C.POINTER(C.c_int32)), int(bytes_per_copy), int(reps),
+                                     bw.ctypes.data_as(C.POINTER(C.c_double)), ms.ctypes.data_as(C.POINTER(C.c_double)),
+                                     err, 512)
+    if st != 0:
+        raise PipetteError(st, err.value.decode())
+    return bw, ms
+
+
 class Pipette:
     """A pipette_ctx on one GPU.  For world > 1 pass rank/world/device and the 128-byte
     NCCL id from rank 0 (see `from_torch_distributed`)."""

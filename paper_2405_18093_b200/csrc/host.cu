@@ -20,6 +20,8 @@ __global__ void k_enumerate_filter(int, int, unsigned long long, int, pipette_mo
                                    const pipette_profile_entry*, int, DevCfg*, unsigned long long*, int, int*,
                                    double*, int, EnumOut*);
 const void* eval_kernel(int mode);
+pipette_status netprof_run(int n, const int* devs, size_t bytes, int reps, double* bw, double* ms_out, char* err,
+                           size_t err_cap);
 pipette_status models_launch(const DevCfg* cfgs, const unsigned long long* keys, int E, const double* qtab,
                              const double* R, int n_nodes, long long n, const pipette_config* cand,
                              const uint16_t* perm, int stride, double* tp, double* tprev, double* tdes,
@@ -309,6 +311,18 @@ int64_t pipette_shard_items(int64_t n_items, int32_t rank, int32_t world, int64_
     ++c;
   }
   return c;
+}
+
+pipette_status pipette_profile_bandwidth(int32_t n_gpus, const int32_t* devices, uint64_t bytes, int32_t reps,
+                                         double* bw_out, double* ms_out, char* err, int32_t err_cap) {
+  static char dummy[8];
+  if (!err || err_cap <= 0) { err = dummy; err_cap = sizeof dummy; }
+  err[0] = 0;
+  if (n_gpus < 1 || !devices || !bw_out || bytes < 16 || reps < 1) {
+    std::snprintf(err, (size_t)err_cap, "n_gpus >= 1, devices, bw_out, bytes >= 16 and reps >= 1 required");
+    return PIPETTE_E_INVALID;
+  }
+  return pip::netprof_run(n_gpus, devices, (size_t)bytes, reps, bw_out, ms_out, err, (size_t)err_cap);
 }
 
 pipette_status pipette_nccl_unique_id(void* id_out) {

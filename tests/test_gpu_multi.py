@@ -46,3 +46,28 @@ def test_multi_gpu_plan_bit_identical(world, chains, tmp_path):
         assert float.fromhex(r["t_pp"]) == ref.t_pp and float.fromhex(r["t_dp"]) == ref.t_dp
         assert (r["sa_steps"], r["sa_accepted"]) == (ref.sa_steps, ref.sa_accepted)
         assert sorted(float.fromhex(q[1]) for q in r["per_config"]) == sorted(ref.per_config_best.tolist())
+
+
+def test_profile_bandwidth_feeds_the_search():
+    # NEXT-3: Alg.1 l.1 on this box; the measured matrix drives pipette_init / the oracle alike
+    import torch
+
+    import oracle as O
+    import workloads as W
+    from paper_2405_18093_b200 import Model, Pipette, profile_bandwidth
+    n = torch.cuda.device_count()
+    B, ms = profile_bandwidth(list(range(n)), bytes_per_copy=64 << 20, reps=3)
+    assert B.shape == (n, n) and np.all(np.isfinite(B)) and np.all(B > 0)
+    assert np.all(np.diag(B) > 5e11)                  # an HBM-to-HBM copy moves > 0.5 TB/s
+    if n > 1:
+        off = B[~np.eye(n, dtype=bool)]
+        assert np.all(off > 1e11)                     # NVLink 5 through NVSwitch: > 100 GB/s per pair
+    prof = W.profile_entries(W.GPT_345M, 1, 8 * n)
+    pip = Pipette(n, 1, B, prof, 80_000_000_000, 100)
+    model = Model(24, 1024, 16, 1024)
+    res = pip.search(model, 8 * n, 4, 300, 5)
+    cl = O.make_cluster(n, 1)
+    mo = O.make_model(24, 1024, 16, 1024, 50257)
+    ref = O.search(cl, B, O.make_profile(prof), mo, 8 * n, 4, 300, 5)
+    p = res["plan"]
+    assert (p.latency_s, p.cfg_index, p.chain) == (ref.latency, ref.cfg_index, ref.chain)
