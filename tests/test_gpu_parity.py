@@ -439,3 +439,39 @@ def test_eval_models_bit_exact(name):
     # the same T_Pipette as the eval stream
     lat, _, _ = _eval_batch(pip, model, w.bs_global, rows[:n], np.stack(perms[:n]))
     assert np.array_equal(lat, tp[:n])
+
+
+# ------------------------------------------------------------------ non-power-of-two shapes
+# pp in {3, 6, 9, 18, ...} takes the runtime pipeline-depth paths, spn in {6, 3} the
+# divide-by-magic node ids (MODE 0: 3 nodes x 6 GPUs; MODE 1: 20 nodes x 6 GPUs)
+ODD0 = W.Workload("C0", 3, 6, W.GPT_345M, 72, 80_000_000_000, 100, 8, 600, 0.3, 0.3, 21)
+ODD1 = W.Workload("C0", 20, 6, W.GPT_345M, 120, 80_000_000_000, 100, 4, 400, 0.3, 0.3, 22)
+
+
+@pytest.mark.parametrize("w", [ODD0, ODD1], ids=["mode0", "mode1"])
+def test_non_power_of_two_shapes_swap_and_full_moves(w):
+    res = _sampled_chain_parity(w, chains=w.chains, iters=w.iterations, n_sample=32, trace_n=3)
+    assert any(p.cfg[0] not in (1, 2, 4, 8, 16, 32) for p in res["per_config"])
+    _sampled_chain_parity(w, chains=w.chains, iters=w.iterations // 2, n_sample=24, trace_n=2, **UNIFORM)
+
+
+@pytest.mark.parametrize("w", [ODD0, ODD1], ids=["mode0", "mode1"])
+def test_non_power_of_two_eval_stream(w):
+    pip, B, prof = _ctx(w)
+    model, mo, cl = _models(w)
+    P = O.make_profile(prof)
+    R = O.inverse_bandwidth(B)
+    feas = [c for c in O.enumerate_configs(cl, mo, w.bs_global, P) if c.feasible]
+    rng = np.random.default_rng(4)
+    Nmax = max(c.pp * c.dp for c in feas)
+    stride = ((Nmax + 7) // 8) * 8
+    rows, perms, want = [], [], []
+    for c in feas:
+        K = O.constants(cl, mo, c, P)
+        for p in W.random_perms(K.N, 8, int(rng.integers(1 << 30))):
+            row = np.zeros(stride, dtype=np.uint16)
+            row[:K.N] = p
+            rows.append((c.pp, c.tp, c.dp, c.mb)); perms.append(row); want.append(O.latency(K, R, p).T)
+    lat, mem, st = _eval_batch(pip, model, w.bs_global, rows, np.stack(perms))
+    assert np.all((st == 0) | (st == 1))
+    assert _assert_close(lat, want) == 0
