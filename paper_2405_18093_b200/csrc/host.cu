@@ -134,6 +134,8 @@ struct pipette_ctx {
   DevBuf tasks, chunks, counter, chain_out, best_perm, cfg_slot, cfg_best, gbits, items, gitems, pack, accepted,
       slot_perm_off, slot_lane, trace_slot, trace, task_prof, tin_rank, tin_vs, tl_ac, tl_val, tl_len;
   int64_t n_tasks_last = 0;
+  // host copies of the last uploaded SA work lists (skip identical re-uploads)
+  std::vector<unsigned char> up_tasks, up_chunks, up_cfg_slot, up_slot_perm_off, up_slot_lane;
   cudaEvent_t ev[6] = {};
 };
 
@@ -176,6 +178,15 @@ cudaError_t ensure(DevBuf& b, size_t bytes) {
   b.bytes = 0;
   cudaError_t e = cudaMalloc(&b.p, std::max<size_t>(bytes, 16));
   if (e == cudaSuccess) b.bytes = std::max<size_t>(bytes, 16);
+  return e;
+}
+
+// ensure() for a buffer whose host copy of the last upload is kept: a reallocation drops
+// the device contents, so it also forgets the copy
+cudaError_t ensure_up(DevBuf& b, size_t bytes, std::vector<unsigned char>& up) {
+  void* before = b.p;
+  cudaError_t e = ensure(b, bytes);
+  if (b.p != before) up.clear();
   return e;
 }
 
@@ -233,13 +244,8 @@ pipette_status check_model(pipette_ctx* ctx, const pipette_model* m, long long b
 
 // K1 on ctx->stream; synchronous readback of the table (cached per (model, bs)).
 pipette_status enumerate(pipette_ctx* ctx, const pipette_model* m, long long bs, bool time_it) {
-  if (!time_it && ctx->enum_valid && std::memcmp(&ctx->enum_model, m, sizeof *m) == 0 && ctx->enum_bs == bs) {
-    if (time_it) {
-      CU(cudaEventRecord(ctx->ev[0], ctx->stream));
-      CU(cudaEventRecord(ctx->ev[1], ctx->stream));
-    }
-    return PIPETTE_OK;
-  }
+  const bool cached = ctx->enum_valid && std::memcmp(&ctx->enum_model, m, sizeof *m) == 0 && ctx->enum_bs == bs;
+  if (cached && !time_it) return PIPETTE_OK;
   const int G = ctx->n_nodes * ctx->g;
   const long long E_cap = (long long)n_div(G) * n_div(ctx->g) * n_div(bs);
   const long long q_cap = E_cap * (G + ctx->n_nodes + 4);
@@ -257,6 +263,9 @@ pipette_status enumerate(pipette_ctx* ctx, const pipette_model* m, long long bs,
   ctx->launches++;
   CU(cudaGetLastError());
   if (time_it) CU(cudaEventRecord(ctx->ev[1], ctx->stream));
+  // a search re-runs K1 every call (it is step a1-a3 of the path); with the same model and
+  // batch its tables are identical, so the host keeps its copy and does not wait for them
+  if (cached) return PIPETTE_OK;
   EnumOut eo;
   CU(cudaMemcpyAsync(&eo, ctx->eout.p, sizeof eo, cudaMemcpyDeviceToHost, ctx->stream));
   CU(cudaStreamSynchronize(ctx->stream));
@@ -700,31 +709,34 @@ pipette_status pipette_search(pipette_ctx* ctx, const pipette_model* model, int6
     }
   }
 
-  CU(ensure(ctx->tasks, sizeof(SaTask) * std::max<size_t>(1, sorted.size())));
-  CU(ensure(ctx->chunks, sizeof(int2) * std::max<size_t>(1, chunks.size())));
+  CU(ensure_up(ctx->tasks, sizeof(SaTask) * std::max<size_t>(1, sorted.size()), ctx->up_tasks));
+  CU(ensure_up(ctx->chunks, sizeof(int2) * std::max<size_t>(1, chunks.size()), ctx->up_chunks));
   CU(ensure(ctx->counter, sizeof(int)));
   CU(ensure(ctx->task_prof, sizeof(unsigned long long) * 4 * std::max<size_t>(1, sorted.size())));
   ctx->n_tasks_last = (int64_t)sorted.size();
   CU(ensure(ctx->chain_out, sizeof(ChainOut) * std::max(1, slots)));
   CU(ensure(ctx->best_perm, sizeof(uint16_t) * std::max(1, perm_words)));
-  CU(ensure(ctx->cfg_slot, sizeof(int) * (F + 1)));
-  CU(ensure(ctx->slot_perm_off, sizeof(int) * std::max(1, slots)));
-  CU(ensure(ctx->slot_lane, sizeof(int) * std::max(1, slots)));
+  CU(ensure_up(ctx->cfg_slot, sizeof(int) * (F + 1), ctx->up_cfg_slot));
+  CU(ensure_up(ctx->slot_perm_off, sizeof(int) * std::max(1, slots), ctx->up_slot_perm_off));
+  CU(ensure_up(ctx->slot_lane, sizeof(int) * std::max(1, slots), ctx->up_slot_lane));
   CU(ensure(ctx->cfg_best, sizeof(CfgBest) * F));
   CU(ensure(ctx->gbits, sizeof(unsigned long long) * F));
   CU(ensure(ctx->items, sizeof(unsigned long long) * F));
   CU(ensure(ctx->gitems, sizeof(unsigned long long) * F));
   const int row_words = 4 + (maxN + 3) / 4;
   CU(ensure(ctx->pack, sizeof(unsigned long long) * ((size_t)F * row_words + 1)));
-  if (!sorted.empty())
-    CU(cudaMemcpyAsync(ctx->tasks.p, sorted.data(), sizeof(SaTask) * sorted.size(), cudaMemcpyHostToDevice, s));
-  if (!chunks.empty())
-    CU(cudaMemcpyAsync(ctx->chunks.p, chunks.data(), sizeof(int2) * chunks.size(), cudaMemcpyHostToDevice, s));
-  CU(cudaMemcpyAsync(ctx->cfg_slot.p, cfg_slot.data(), sizeof(int) * (F + 1), cudaMemcpyHostToDevice, s));
-  if (slots) {
-    CU(cudaMemcpyAsync(ctx->slot_perm_off.p, slot_perm_off.data(), sizeof(int) * slots, cudaMemcpyHostToDevice, s));
-    CU(cudaMemcpyAsync(ctx->slot_lane.p, slot_lane.data(), sizeof(int) * slots, cudaMemcpyHostToDevice, s));
-  }
+  // the work lists of the previous call are still on the device: upload only what changed
+  auto upload = [&](std::vector<unsigned char>& last, DevBuf& dst, const void* src, size_t bytes) -> cudaError_t {
+    if (bytes == 0) return cudaSuccess;
+    if (last.size() == bytes && std::memcmp(last.data(), src, bytes) == 0) return cudaSuccess;
+    last.assign((const unsigned char*)src, (const unsigned char*)src + bytes);
+    return cudaMemcpyAsync(dst.p, last.data(), bytes, cudaMemcpyHostToDevice, s);
+  };
+  CU(upload(ctx->up_tasks, ctx->tasks, sorted.data(), sizeof(SaTask) * sorted.size()));
+  CU(upload(ctx->up_chunks, ctx->chunks, chunks.data(), sizeof(int2) * chunks.size()));
+  CU(upload(ctx->up_cfg_slot, ctx->cfg_slot, cfg_slot.data(), sizeof(int) * (F + 1)));
+  CU(upload(ctx->up_slot_perm_off, ctx->slot_perm_off, slot_perm_off.data(), sizeof(int) * slots));
+  CU(upload(ctx->up_slot_lane, ctx->slot_lane, slot_lane.data(), sizeof(int) * slots));
   CU(cudaMemsetAsync(ctx->counter.p, 0, sizeof(int), s));
   if (tracing) {
     CU(ensure(ctx->trace_slot, sizeof(int) * trace_slot.size()));
