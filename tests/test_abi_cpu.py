@@ -2,6 +2,7 @@
 symbol include/pipette.h declares, and its host-only logic (sharding R18, validation,
 status strings) behaves."""
 import ctypes as C
+import sys
 import os
 import re
 
@@ -81,3 +82,21 @@ def test_product_package_does_not_touch_the_oracle():
             if f.endswith((".py", ".cu", ".cuh", ".h", ".cpp")):
                 txt = open(os.path.join(dp, f)).read()
                 assert "import oracle" not in txt and "from oracle" not in txt and "oracle.h" not in txt, f
+
+
+def test_no_fma_contraction_in_model_arithmetic():
+    # every + - * of the model is its own IEEE op; the only DFMA in the hot
+    # kernels' SASS are the Newton steps of correctly rounded divisions (__ddiv_rn)
+    import shutil
+    import subprocess
+    if shutil.which("cuobjdump") is None:
+        pytest.skip("cuobjdump not available")
+    sys.path.insert(0, os.path.join(ROOT, "tools"))
+    import sass_fma_check
+    from paper_2405_18093_b200 import build
+    res = sass_fma_check.analyse(build.build())
+    assert any("k_sa_chains" in k for k in res) and any("k_eval_stream" in k for k in res)
+    for name, r in res.items():
+        assert r["dfma_outside_division"] == 0, (name, r)
+        if "k_eval_stream" in name:
+            assert r["dfma"] == 0
