@@ -41,6 +41,23 @@ def ncu_traffic(kernel):
         return None
 
 
+def ncu_pipes(summary):
+    """Pipe utilisation of a kernel from its committed ncu summary (profiles/), or None."""
+    try:
+        vals = {}
+        for line in open(os.path.join(ROOT, "profiles", summary)):
+            parts = line.split()
+            if len(parts) >= 2 and not line.startswith("#"):
+                vals[parts[0]] = float(parts[1])
+        return {"issue_active": vals["smsp__issue_active.avg.pct_of_peak_sustained_active"] / 100,
+                "alu_pipe": vals["sm__inst_executed_pipe_alu.avg.pct_of_peak_sustained_active"] / 100,
+                "fp64_pipe": vals["sm__inst_executed_pipe_fp64.avg.pct_of_peak_sustained_active"] / 100,
+                "lsu_pipe": vals["sm__inst_executed_pipe_lsu.avg.pct_of_peak_sustained_active"] / 100,
+                "source": f"profiles/{summary}"}
+    except Exception:
+        return None
+
+
 def peaks():
     try:
         return json.load(open(PEAKS))
@@ -236,7 +253,9 @@ def run_ours(args):
                 "traffic": ncu_traffic("k_sa_chains") if args.workload == "C2" else None,
                 "traffic_note": "DRAM bytes per launch (ncu): chain state lives in shared memory, R/tables in L2",
                 "peak_source": "148 SMs x 64 FP64 lanes x sm_max_mhz (MEASURED_PEAKS.json), DESIGN.md 8",
-                "sa_kernel_ms": sa_avg_s * 1000.0, "sa_share_of_step": (sa_max / t_max) if t_max else None}
+                "sa_kernel_ms": sa_avg_s * 1000.0, "sa_share_of_step": (sa_max / t_max) if t_max else None,
+                "pipes": ncu_pipes("r01b_sa_ncu_summary.txt") if args.workload == "C2" else None,
+                "note": "issue/ALU-bound, not FP64-bound: the FP64 fraction is small by construction (DESIGN.md 8)"}
 
     # ---------------- e2e through the public API: host bandwidth matrix in, plan out
     e2e = None
