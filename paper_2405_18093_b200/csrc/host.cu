@@ -20,6 +20,7 @@ __global__ void k_enumerate_filter(int, int, unsigned long long, int, pipette_mo
                                    const pipette_profile_entry*, int, DevCfg*, unsigned long long*, int, int*,
                                    double*, int, EnumOut*);
 const void* eval_kernel(int mode);
+int eval_tile_size();
 pipette_status netprof_run(int n, const int* devs, size_t bytes, int reps, double* bw, double* ms_out, char* err,
                            size_t err_cap);
 pipette_status models_launch(const DevCfg* cfgs, const unsigned long long* keys, int E, const double* qtab,
@@ -524,12 +525,13 @@ pipette_status pipette_eval(pipette_ctx* ctx, const pipette_model* model, int64_
   P.staged = P.vec16 && perm_stride <= 64 && smem <= 96 * 1024;   // long rows: direct 16-byte loads measured faster
   if (!P.staged) smem = eval_smem_bytes(mode, perm_stride, false, ctx->n_nodes, ctx->E, P.bm_words);
   if (smem > 227 * 1024) return fail(ctx, PIPETTE_E_UNSUPPORTED, "eval shared memory %zu B too large", smem);
+  if (ctx->E >= 32767) return fail(ctx, PIPETTE_E_UNSUPPORTED, "eval supports < 32767 enumerated configurations");
   const void* kern = eval_kernel(mode);
   CU(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   int occ = 0;
   CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, 256, smem));
   occ = std::max(occ, 1);
-  const long long need = (n + 2047) / 2048;   // tiles of 2048 candidates
+  const long long need = (n + eval_tile_size() - 1) / eval_tile_size();   // candidate tiles
   const int grid = (int)std::min<long long>(need, (long long)occ * ctx->n_sms);
   void* args[] = {&P};
   CU(cudaLaunchKernel(kern, dim3(grid), dim3(256), args, smem, s));

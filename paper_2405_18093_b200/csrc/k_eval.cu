@@ -341,8 +341,8 @@ __global__ void __launch_bounds__(kEvalThreads) k_eval_stream(EvalParams P) {
   off += ((size_t)P.E * 8 + 15) & ~(size_t)15;
   uint32_t* bm = reinterpret_cast<uint32_t*>(smem + off);
   off += (size_t)(P.bm_words + (n + 3) / 4) * kEvalThreads * 4;
-  int* tile_e = reinterpret_cast<int*>(smem + off);
-  int* hist = tile_e + kEvalTile;
+  short* tile_e = reinterpret_cast<short*>(smem + off);   // config index per candidate (E < 32767)
+  int* hist = reinterpret_cast<int*>(tile_e + kEvalTile);
   short* order = reinterpret_cast<short*>(hist + ((P.E + 2 + 3) & ~3));
   __shared__ int sh_scan[32];
 
@@ -355,7 +355,7 @@ __global__ void __launch_bounds__(kEvalThreads) k_eval_stream(EvalParams P) {
   __syncthreads();
   const EvalShared S{Rs, bm, bm + P.bm_words * kEvalThreads, n, tid, lane, kEvalThreads};
   const double qnan = __longlong_as_double(0x7ff8000000000000ll);
-  const bool bucket_ok = P.E + 1 <= 32767;
+  const bool bucket_ok = true;   // (E < 32767 is checked by the host)
 
   for (long long base = (long long)blockIdx.x * kEvalTile; base < P.n; base += (long long)gridDim.x * kEvalTile) {
     const int cnt_valid = (int)min((long long)kEvalTile, P.n - base);
@@ -371,7 +371,7 @@ __global__ void __launch_bounds__(kEvalThreads) k_eval_stream(EvalParams P) {
         if (keys[mid] < key) lo = mid + 1; else hi = mid;
       }
       const int e = (lo >= P.E || keys[lo] != key) ? -1 : lo;   // -1: not in the enumeration
-      tile_e[k] = e;
+      tile_e[k] = (short)e;
     }
     __syncthreads();
     for (int k = tid; k < cnt_valid; k += kEvalThreads) mixed |= tile_e[k] != tile_e[0];
@@ -444,12 +444,14 @@ __global__ void __launch_bounds__(kEvalThreads) k_eval_stream(EvalParams P) {
   }
 }
 
+int eval_tile_size() { return kEvalTile; }
+
 // Dynamic shared memory of k_eval_stream (staged: per-warp double-buffered row staging).
 size_t eval_smem_bytes(int mode, int perm_stride, bool staged, int n_nodes, int E, int bm_words) {
   const size_t nn = (size_t)n_nodes * n_nodes;
   const size_t wb = staged ? (size_t)32 * perm_stride * 2 : 0;
   return (size_t)(kEvalThreads / 32) * wb + (mode == 0 ? nn * 16 : nn) * 8 + (((size_t)E * 8 + 15) & ~(size_t)15) +
-         (size_t)(bm_words + (n_nodes + 3) / 4) * kEvalThreads * 4 + (size_t)kEvalTile * sizeof(int) +
+         (size_t)(bm_words + (n_nodes + 3) / 4) * kEvalThreads * 4 + (size_t)kEvalTile * sizeof(short) +
          (size_t)((E + 2 + 3) & ~3) * sizeof(int) + (size_t)kEvalTile * sizeof(short);
 }
 
