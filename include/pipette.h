@@ -198,6 +198,15 @@ pipette_status pipette_search(pipette_ctx* ctx, const pipette_model* model, int6
                               const pipette_sa_opts* opts, pipette_plan* out,
                               pipette_plan* per_config, int32_t per_config_cap);
 
+/* NEXT-4: use the memory estimator MLP of Eq.7 (reading
+ * R23) instead of the analytic estimate (R11) for the memory filter of every later
+ * enumeration, search and eval.  params (HOST, copied): 123023 doubles -- the 10 feature
+ * means and 10 scales of ln(n_gpus, n_layers, hidden, heads, tp, pp, dp, bs_micro,
+ * bs_mini, bs_global), then for each layer 10->200->200->200->200->1 the weights (out x in,
+ * row-major) and biases, then the output's scale and mean (ln GB).  NULL restores the
+ * analytic estimate.  Errors: E_INVALID (count, non-finite values, scale <= 0), E_CUDA. */
+pipette_status pipette_set_memory_model(pipette_ctx* ctx, const double* params, int64_t n_params);
+
 /* NEXT-2: three latency models of n caller candidates (same inputs,
  * layout, ownership and asynchrony as pipette_eval; reading R22 of DESIGN.md):
  *   d_t_pipette[i] : Eq.3-6, bit-identical to pipette_eval's latency

@@ -139,6 +139,12 @@ def lib():
                                       C.c_int32, C.c_int32, C.c_int32, P(Plan), P(C.c_uint16), C.c_int32,
                                       P(C.c_double), P(C.c_int32)]
         L.or_search_moves.restype = C.c_int32
+        L.or_log_det.argtypes = [C.c_double]
+        L.or_log_det.restype = C.c_double
+        L.or_mlp_param_count.restype = C.c_int64
+        L.or_mlp_memory.argtypes = [P(C.c_double), P(C.c_double)]
+        L.or_mlp_memory.restype = C.c_uint64
+        L.or_set_memory_model.argtypes = [P(C.c_double)]
         L.or_des_1f1b.argtypes = [C.c_int32, C.c_int32, C.c_double, C.c_double, P(C.c_double), P(C.c_double)]
         L.or_des_1f1b.restype = C.c_double
         L.or_models.argtypes = [P(Consts), P(C.c_double), P(C.c_uint16), P(C.c_double), P(C.c_double),
@@ -261,6 +267,32 @@ def draw(i, c, e, seed, N):
     p, q, u = C.c_uint32(), C.c_uint32(), C.c_double()
     lib().or_draw(i, c, e, seed, N, C.byref(p), C.byref(q), C.byref(u))
     return p.value, q.value, u.value
+
+
+def log_det(x: float) -> float:
+    return lib().or_log_det(float(x))
+
+
+_mlp_keep = None
+
+
+def set_memory_model(params):
+    """Eq.7's MLP as the memory estimator of enumerate_configs (None: analytic, R11)."""
+    global _mlp_keep
+    if params is None:
+        _mlp_keep = None
+        lib().or_set_memory_model(None)
+        return
+    a = np.ascontiguousarray(np.asarray(params, dtype=np.float64))
+    assert a.size == lib().or_mlp_param_count()
+    _mlp_keep = a
+    lib().or_set_memory_model(_dptr(a))
+
+
+def mlp_memory(params, feat) -> int:
+    a = np.ascontiguousarray(np.asarray(params, dtype=np.float64))
+    f = np.ascontiguousarray(np.asarray(feat, dtype=np.float64))
+    return int(lib().or_mlp_memory(_dptr(a), _dptr(f)))
 
 
 def des_1f1b(pp, n_mb, f, b, hop_f, hop_b=None) -> float:

@@ -38,6 +38,82 @@ static int32_t has_profile(const or_profile* prof, int32_t n_prof, int32_t tp, i
   return 0;
 }
 
+/* ------------------------------------------------------------------------- */
+/* NEXT-4: the memory estimator MLP of Eq.7, reading     */
+/* R23.  Features (Eq.7's order): n_gpus, n_layers, n_hiddens, n_heads, tp, pp, dp,*/
+/* bs_micro, bs_mini, bs_global, each as ln(x) by or_log_det, standardised as      */
+/* (ln x - mean_i) / std_i; layers 10 -> 200 -> 200 -> 200 -> 200 -> 1 (ReLU        */
+/* between); each neuron acc = b_j, then acc = acc + W_ji * in_i for i ascending;  */
+/* z = y * y_std + y_mean = ln(M / 1 GB); M = exp(z) GB = exp_det(min(z,16) - 16) *  */
+/* fl(e^16) * 1e9 bytes, truncated to an integer.                                 */
+/* Parameters, flat: mean[10], std[10], then per layer W (out x in, row-major) and */
+/* b[out], then y_std, y_mean (123023 doubles).                                    */
+/* ------------------------------------------------------------------------- */
+double or_log_det(double x) {   /* ln(x) for x >= 1, only IEEE + - * / on exact parts */
+  uint64_t bits;
+  memcpy(&bits, &x, sizeof bits);
+  int64_t ex = (int64_t)((bits >> 52) & 0x7ff) - 1023;
+  uint64_t mb = (bits & 0x000fffffffffffffull) | 0x3ff0000000000000ull;
+  double m;
+  memcpy(&m, &mb, sizeof m);                    /* x = m * 2^ex, m in [1, 2) exactly */
+  double s = (m - 1.0) / (m + 1.0);             /* ln(m) = 2 atanh(s), s in [0, 1/3) */
+  double s2 = s * s;
+  double p = 1.0 / 31.0;
+  for (int k = 14; k >= 0; --k) p = p * s2 + 1.0 / (double)(2 * k + 1);
+  double lnm = 2.0 * (s * p);
+  double e = (double)ex;
+  return (e * 6.93147180369123816490e-01 + lnm) + e * 1.90821492927058770002e-10;
+}
+
+#define MLP_H 200
+int64_t or_mlp_param_count(void) {
+  return 20 + (int64_t)MLP_H * 10 + MLP_H + 3 * ((int64_t)MLP_H * MLP_H + MLP_H) + MLP_H + 1 + 2;
+}
+
+uint64_t or_mlp_memory(const double* P, const double feat[10]) {
+  double a[MLP_H], b[MLP_H];
+  const double* mean = P;
+  const double* sd = P + 10;
+  const double* w = P + 20;
+  double x[10];
+  for (int i = 0; i < 10; ++i) x[i] = (or_log_det(feat[i]) - mean[i]) / sd[i];
+  const double* in = x;
+  int n_in = 10;
+  double* bufs[2] = {a, b};
+  for (int l = 0; l < 4; ++l) {
+    double* out = bufs[l & 1];
+    const double* W = w;
+    const double* bias = w + (size_t)MLP_H * n_in;
+    for (int j = 0; j < MLP_H; ++j) {
+      double acc = bias[j];
+      for (int i = 0; i < n_in; ++i) acc = acc + W[(size_t)j * n_in + i] * in[i];
+      out[j] = acc > 0.0 ? acc : 0.0;
+    }
+    w = bias + MLP_H;
+    in = out;
+    n_in = MLP_H;
+  }
+  double y = w[MLP_H];                                           /* output bias */
+  for (int i = 0; i < MLP_H; ++i) y = y + w[i] * in[i];
+  const double y_std = w[MLP_H + 1], y_mean = w[MLP_H + 2];
+  double z = y * y_std + y_mean;
+  if (z > 16.0) z = 16.0;
+  double gb = or_exp_det(z - 16.0) * 0x1.0f2ebd0a80020p+23;   /* fl(e^16) */
+  double bytes = gb * 1e9;
+  return bytes > 0.0 ? (uint64_t)bytes : 0u;
+}
+
+static const double* g_mlp = NULL;   /* NULL: analytic estimator (R11) */
+void or_set_memory_model(const double* params) { g_mlp = params; }
+
+static uint64_t config_memory(const or_model* m, int64_t G, int64_t bs_global, int32_t pp, int32_t tp, int32_t dp,
+                              int32_t mb, int32_t n_mb) {
+  if (!g_mlp) return or_memory(m, pp, tp, mb, n_mb);
+  double f[10] = {(double)G, (double)m->n_layers, (double)m->hidden, (double)m->heads, (double)tp, (double)pp,
+                  (double)dp, (double)mb, (double)(bs_global / dp), (double)bs_global};
+  return or_mlp_memory(g_mlp, f);
+}
+
 int32_t or_enumerate(const or_cluster* cl, const or_model* m, int64_t bs_global,
                      const or_profile* prof, int32_t n_prof, or_config* out, int32_t cap) {
   int64_t G = (int64_t)cl->n_nodes * cl->gpus_per_node;
@@ -57,7 +133,7 @@ int32_t or_enumerate(const or_cluster* cl, const or_model* m, int64_t bs_global,
           c->pp = (int32_t)pp; c->tp = (int32_t)tp; c->dp = (int32_t)dp; c->mb = (int32_t)mb;
           c->n_mb = (int32_t)(bs_mini / mb);
           c->e = E;
-          c->mem_bytes = or_memory(m, c->pp, c->tp, c->mb, c->n_mb);
+          c->mem_bytes = config_memory(m, G, bs_global, c->pp, c->tp, c->dp, c->mb, c->n_mb);
           c->feasible = or_feasible(c->mem_bytes, cl->mem_capacity_bytes, cl->mem_margin_permille);
           c->has_profile = has_profile(prof, n_prof, c->tp, c->mb);
         }

@@ -104,6 +104,13 @@ void or_sa_chain(const or_consts* K, const double* R, int32_t iterations, uint64
                  or_chain_result* res, uint16_t* best_perm,
                  or_trace_record* trace, int32_t trace_cap);
 
+/* NEXT-4: Eq.7's memory MLP, reading R23; or_set_memory_model(NULL)
+ * restores the analytic estimator for or_enumerate (process-global, test use only). */
+double or_log_det(double x);
+int64_t or_mlp_param_count(void);
+uint64_t or_mlp_memory(const double* params, const double feat[10]);
+void or_set_memory_model(const double* params);
+
 /* NEXT-2: Eq.1 and a 1F1B discrete-event simulation, reading R22. */
 double or_des_1f1b(int32_t pp, int32_t n_mb, double f, double b, const double* hop_f, const double* hop_b);
 void or_models(const or_consts* K, const double* R, const uint16_t* perm, double* t_pipette, double* t_prev,

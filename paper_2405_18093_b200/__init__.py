@@ -113,6 +113,15 @@ def profile_bandwidth(devices=None, bytes_per_copy: int = 256 << 20, reps: int =
     return bw, ms
 
 
+def load_memory_mlp(path=None) -> dict:
+    """The packaged Eq.7 MLP (data/mem_mlp.json, trained by tools/train_mem_mlp.py)."""
+    import json
+    import os
+    path = path or os.path.join(os.path.dirname(os.path.abspath(__file__)), "data", "mem_mlp.json")
+    with open(path) as f:
+        return json.load(f)
+
+
 class Pipette:
     """A pipette_ctx on one GPU.  For world > 1 pass rank/world/device and the 128-byte
     NCCL id from rank 0 (see `from_torch_distributed`)."""
@@ -230,6 +239,15 @@ class Pipette:
                                          int(perm.shape[1]) if perm.dim() == 2 else 1, lat.data_ptr(),
                                          mem.data_ptr(), status.data_ptr(), C.c_void_p(s.cuda_stream)))
         return lat, mem, status
+
+    def set_memory_model(self, params=None):
+        """NEXT-4: Eq.7's MLP memory estimator (flat float64 parameters, e.g.
+        load_memory_mlp()["params"]) for every later enumeration; None = analytic (R11)."""
+        if params is None:
+            self._check(self._L.pipette_set_memory_model(self._h, None, 0))
+            return
+        a = np.ascontiguousarray(np.asarray(params, dtype=np.float64))
+        self._check(self._L.pipette_set_memory_model(self._h, a.ctypes.data_as(C.POINTER(C.c_double)), a.size))
 
     def eval_models(self, model: Model, bs_global: int, cfg, perm, stream=None):
         """NEXT-2: (T_Pipette Eq.3, T_prev Eq.1, T_DES 1F1B simulation, status) CUDA tensors

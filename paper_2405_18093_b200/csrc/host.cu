@@ -20,6 +20,8 @@ __global__ void k_enumerate_filter(int, int, unsigned long long, int, pipette_mo
                                    const pipette_profile_entry*, int, DevCfg*, unsigned long long*, int, int*,
                                    double*, int, EnumOut*);
 const void* eval_kernel(int mode);
+void launch_mlp_filter(const double* P, int G, int n_nodes, const pipette_model& m, long long bs, unsigned long long cap,
+                       int margin, DevCfg* cfgs, int* feas, EnumOut* out, cudaStream_t s);
 int eval_tile_size();
 pipette_status netprof_run(int n, const int* devs, size_t bytes, int reps, double* bw, double* ms_out, char* err,
                            size_t err_cap);
@@ -132,6 +134,7 @@ struct pipette_ctx {
   DevBuf cfgs, keys, feas, qtab, eout, vin;
   bool vin_valid = false;   // K2 intra-node value table matches the config table and R
   // search buffers
+  DevBuf mlp;   // Eq.7 MLP parameters (NEXT-4), empty = analytic memory (R11)
   DevBuf tasks, chunks, counter, chain_out, best_perm, cfg_slot, cfg_best, gbits, items, gitems, pack, accepted,
       slot_perm_off, slot_lane, trace_slot, trace, task_prof, tin_rank, tin_vs, tl_ac, tl_val, tl_len;
   int64_t n_tasks_last = 0;
@@ -141,6 +144,8 @@ struct pipette_ctx {
 };
 
 namespace {
+
+constexpr int64_t kMlpParams = 20 + 200 * 10 + 200 + 3 * (200 * 200 + 200) + 200 + 1 + 2;   // Eq.7 MLP (R23)
 
 int align16(int x) { return (x + 15) & ~15; }
 thread_local std::string g_init_err;
@@ -263,6 +268,12 @@ pipette_status enumerate(pipette_ctx* ctx, const pipette_model* m, long long bs,
       (EnumOut*)ctx->eout.p);
   ctx->launches++;
   CU(cudaGetLastError());
+  if (ctx->mlp.p) {   // NEXT-4: Eq.7's MLP replaces the analytic memory and the verdicts
+    launch_mlp_filter((const double*)ctx->mlp.p, G, ctx->n_nodes, *m, bs, ctx->cap, ctx->margin, (DevCfg*)ctx->cfgs.p,
+                      (int*)ctx->feas.p, (EnumOut*)ctx->eout.p, ctx->stream);
+    ctx->launches++;
+    CU(cudaGetLastError());
+  }
   if (time_it) CU(cudaEventRecord(ctx->ev[1], ctx->stream));
   // a search re-runs K1 every call (it is step a1-a3 of the path); with the same model and
   // batch its tables are identical, so the host keeps its copy and does not wait for them
@@ -333,6 +344,29 @@ pipette_status pipette_profile_bandwidth(int32_t n_gpus, const int32_t* devices,
     return PIPETTE_E_INVALID;
   }
   return pip::netprof_run(n_gpus, devices, (size_t)bytes, reps, bw_out, ms_out, err, (size_t)err_cap);
+}
+
+pipette_status pipette_set_memory_model(pipette_ctx* ctx, const double* params, int64_t n_params) {
+  if (!ctx) return PIPETTE_E_INVALID;
+  CU(cudaSetDevice(ctx->device));
+  if (!params) {
+    if (ctx->mlp.p) cudaFree(ctx->mlp.p);
+    ctx->mlp.p = nullptr;
+    ctx->mlp.bytes = 0;
+  } else {
+    if (n_params != kMlpParams)
+      return fail(ctx, PIPETTE_E_INVALID, "memory model needs %lld parameters, got %lld", (long long)kMlpParams,
+                  (long long)n_params);
+    for (int64_t i = 0; i < n_params; ++i)
+      if (!std::isfinite(params[i])) return fail(ctx, PIPETTE_E_INVALID, "memory model parameter %lld not finite", (long long)i);
+    for (int i = 10; i < 20; ++i)
+      if (!(params[i] > 0.0)) return fail(ctx, PIPETTE_E_INVALID, "feature scale %d must be > 0", i - 10);
+    CU(ensure(ctx->mlp, sizeof(double) * (size_t)n_params));
+    CU(cudaMemcpy(ctx->mlp.p, params, sizeof(double) * (size_t)n_params, cudaMemcpyHostToDevice));
+  }
+  ctx->enum_valid = false;   // the verdicts change
+  ctx->vin_valid = false;
+  return PIPETTE_OK;
 }
 
 pipette_status pipette_nccl_unique_id(void* id_out) {
@@ -436,7 +470,7 @@ pipette_status pipette_set_stream(pipette_ctx* ctx, void* stream) {
 void pipette_destroy(pipette_ctx* ctx) {
   if (!ctx) return;
   if (ctx->comm) ncclCommDestroy(ctx->comm);
-  DevBuf* bufs[] = {&ctx->cfgs, &ctx->keys, &ctx->feas, &ctx->qtab, &ctx->eout, &ctx->vin, &ctx->tasks, &ctx->chunks, &ctx->counter,
+  DevBuf* bufs[] = {&ctx->cfgs, &ctx->keys, &ctx->feas, &ctx->qtab, &ctx->eout, &ctx->vin, &ctx->mlp, &ctx->tasks, &ctx->chunks, &ctx->counter,
                     &ctx->chain_out, &ctx->best_perm, &ctx->cfg_slot, &ctx->cfg_best, &ctx->gbits, &ctx->items,
                     &ctx->gitems, &ctx->pack, &ctx->accepted, &ctx->slot_perm_off, &ctx->slot_lane,
                     &ctx->trace_slot, &ctx->trace, &ctx->task_prof, &ctx->tin_rank, &ctx->tin_vs, &ctx->tl_ac,

@@ -211,3 +211,105 @@ k_enumerate_filter(int n_nodes, int g, unsigned long long cap, int margin, pipet
 }
 
 }  // namespace pip
+
+namespace pip {
+
+// ------------------------------------------------------------------ NEXT-4: Eq.7's MLP
+// The memory estimator MLP of Eq.7 (reading R23) replacing the analytic
+// estimate of K1 when the context has one (pipette_set_memory_model).  One block; warp w
+// takes configurations w, w + 8, ...; a layer's 200 neurons are split over the lanes, each
+// neuron accumulated in the oracle's order (acc = b, then acc + W_ji * in_i, i ascending),
+// activations in shared memory; lane 0 forms the output sum.  Then the verdicts and the
+// ordered feasible list are rebuilt with a block scan.
+constexpr int kMlpH = 200, kMlpWarps = 8;
+
+// ln(x), x >= 1: exact split x = m 2^e, ln m = 2 atanh((m-1)/(m+1)) by a degree-31 odd
+// series in Horner form with fl(1/(2k+1)) -- the oracle's or_log_det, op for op
+__device__ double log_det(double x) {
+  const unsigned long long bits = (unsigned long long)__double_as_longlong(x);
+  const long long ex = (long long)((bits >> 52) & 0x7ffull) - 1023;
+  const double m = __longlong_as_double((long long)((bits & 0x000fffffffffffffull) | 0x3ff0000000000000ull));
+  const double s = __ddiv_rn(__dadd_rn(m, -1.0), __dadd_rn(m, 1.0));
+  const double s2 = __dmul_rn(s, s);
+  double p = __ddiv_rn(1.0, 31.0);
+  for (int k = 14; k >= 0; --k) p = __dadd_rn(__dmul_rn(p, s2), __ddiv_rn(1.0, (double)(2 * k + 1)));
+  const double lnm = __dmul_rn(2.0, __dmul_rn(s, p));
+  const double e = (double)ex;
+  return __dadd_rn(__dadd_rn(__dmul_rn(e, 6.93147180369123816490e-01), lnm), __dmul_rn(e, 1.90821492927058770002e-10));
+}
+
+__global__ void __launch_bounds__(kMlpWarps * 32)
+k_mlp_filter(const double* __restrict__ P, int G, int n_nodes, pipette_model m, long long bs_global,
+             unsigned long long cap, int margin, DevCfg* __restrict__ cfgs, int* __restrict__ feas,
+             EnumOut* __restrict__ out) {
+  __shared__ double act[kMlpWarps][2][kMlpH];
+  __shared__ int sh_scan[32];
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const int E = out->E;
+  if (out->overflow) return;
+  const unsigned long long keep = (unsigned long long)(1000 - margin);
+  const unsigned long long limit = cap / 1000ull * keep + (cap % 1000ull) * keep / 1000ull;
+  for (int e = wid; e < E; e += kMlpWarps) {
+    const DevCfg c = cfgs[e];
+    const double f[10] = {(double)G, (double)m.n_layers, (double)m.hidden, (double)m.heads, (double)c.tp,
+                          (double)c.pp, (double)c.dp, (double)c.mb, (double)(bs_global / c.dp), (double)bs_global};
+    double x[10];
+#pragma unroll
+    for (int i = 0; i < 10; ++i) x[i] = __ddiv_rn(__dadd_rn(log_det(f[i]), -P[i]), P[10 + i]);
+    const double* w = P + 20;
+    // layer 1: 10 -> 200
+    for (int j = lane; j < kMlpH; j += 32) {
+      double acc = w[kMlpH * 10 + j];
+#pragma unroll
+      for (int i = 0; i < 10; ++i) acc = __dadd_rn(acc, __dmul_rn(w[j * 10 + i], x[i]));
+      act[wid][0][j] = fmax(acc, 0.0);
+    }
+    w += kMlpH * 10 + kMlpH;
+    __syncwarp();
+    // layers 2..4: 200 -> 200
+    for (int l = 1; l < 4; ++l) {
+      const double* in = act[wid][(l - 1) & 1];
+      double* o = act[wid][l & 1];
+      for (int j = lane; j < kMlpH; j += 32) {
+        double acc = w[kMlpH * kMlpH + j];
+        const double* row = w + (size_t)j * kMlpH;
+        for (int i = 0; i < kMlpH; ++i) acc = __dadd_rn(acc, __dmul_rn(row[i], in[i]));
+        o[j] = fmax(acc, 0.0);
+      }
+      w += kMlpH * kMlpH + kMlpH;
+      __syncwarp();
+    }
+    if (lane == 0) {
+      const double* in = act[wid][1];
+      double y = w[kMlpH];
+      for (int i = 0; i < kMlpH; ++i) y = __dadd_rn(y, __dmul_rn(w[i], in[i]));
+      double z = __dadd_rn(__dmul_rn(y, w[kMlpH + 1]), w[kMlpH + 2]);
+      z = fmin(z, 16.0);
+      const double gb = __dmul_rn(exp_det(__dadd_rn(z, -16.0)), 0x1.0f2ebd0a80020p+23);   // fl(e^16)
+      const double bytes = __dmul_rn(gb, 1e9);
+      const unsigned long long mem = bytes > 0.0 ? __double2ull_rz(bytes) : 0ull;
+      cfgs[e].mem = mem;
+      cfgs[e].feasible = mem <= limit;
+    }
+    __syncwarp();
+  }
+  __syncthreads();
+  // ordered feasible list
+  int carry = 0;
+  for (int base = 0; base < E; base += blockDim.x) {
+    const int e = base + tid;
+    const int fe = e < E ? cfgs[e].feasible : 0;
+    int tot;
+    const int o = carry + block_scan_excl(fe, sh_scan, tot);
+    carry += tot;
+    if (fe) feas[o] = e;
+  }
+  if (tid == 0) out->F = carry;
+}
+
+void launch_mlp_filter(const double* P, int G, int n_nodes, const pipette_model& m, long long bs, unsigned long long cap,
+                       int margin, DevCfg* cfgs, int* feas, EnumOut* out, cudaStream_t s) {
+  k_mlp_filter<<<1, kMlpWarps * 32, 0, s>>>(P, G, n_nodes, m, bs, cap, margin, cfgs, feas, out);
+}
+
+}  // namespace pip

@@ -475,3 +475,32 @@ def test_non_power_of_two_eval_stream(w):
     lat, mem, st = _eval_batch(pip, model, w.bs_global, rows, np.stack(perms))
     assert np.all((st == 0) | (st == 1))
     assert _assert_close(lat, want) == 0
+
+
+# ------------------------------------------------------------------ NEXT-4: Eq.7's MLP (R23)
+@pytest.mark.parametrize("name", ["C1", "C2", "C4"])
+def test_memory_mlp_filter_bit_exact(name):
+    from paper_2405_18093_b200 import load_memory_mlp
+    params = np.asarray(load_memory_mlp()["params"], dtype=np.float64)
+    w = W.WORKLOADS[name]
+    pip, B, prof = _ctx(w)
+    model, mo, cl = _models(w)
+    P = O.make_profile(prof)
+    pip.set_memory_model(params)
+    cfgs, nmb, mem, feas = pip.enumerate(model, w.bs_global)
+    O.set_memory_model(params)
+    try:
+        ref = O.enumerate_configs(cl, mo, w.bs_global, P)
+        assert [int(x) for x in mem] == [int(c.mem_bytes) for c in ref]
+        assert feas.tolist() == [bool(c.feasible) for c in ref]
+        if name != "C4":
+            res = pip.search(model, w.bs_global, 2, 300, w.seed)
+            o = O.search(cl, B, P, mo, w.bs_global, 2, 300, w.seed)
+            p = res["plan"]
+            assert (p.latency_s, p.cfg_index, p.chain, p.mem_bytes) == (o.latency, o.cfg_index, o.chain, o.mem_bytes)
+            assert p.configs_rejected_oom == o.E - o.F
+    finally:
+        O.set_memory_model(None)
+    pip.set_memory_model(None)
+    _, _, mem2, _ = pip.enumerate(model, w.bs_global)
+    assert [int(x) for x in mem2] == [int(O.memory(mo, c.pp, c.tp, c.mb, c.n_mb)) for c in ref]
