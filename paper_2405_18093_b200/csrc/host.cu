@@ -104,6 +104,20 @@ struct DevBuf {
   size_t bytes = 0;
 };
 
+struct HostPlanKey {
+  pipette_model model;
+  long long bs;
+  int chains, W, r, dp_cap_env, full_moves;
+};
+struct HostPlan {
+  std::vector<SaTask> sorted;
+  std::vector<int2> chunks;
+  std::vector<int> cfg_slot, slot_perm_off, slot_lane;
+  int slots = 0, perm_words = 0, maxN = 1, mode = 0, r_bytes = 0, dp_cap = 0, warp_bytes = 16, tl_stride = 1, wpb = 1;
+  bool big = false;
+  size_t smem = 0;
+};
+
 struct pipette_ctx {
   int device = 0, rank = 0, world = 1;
   int n_nodes = 0, g = 0, margin = 0;
@@ -138,6 +152,9 @@ struct pipette_ctx {
   DevBuf tasks, chunks, counter, chain_out, best_perm, cfg_slot, cfg_best, gbits, items, gitems, pack, accepted,
       slot_perm_off, slot_lane, trace_slot, trace, task_prof, tin_rank, tin_vs, tl_ac, tl_val, tl_len;
   int64_t n_tasks_last = 0;
+  HostPlanKey plan_key{};
+  HostPlan plan;
+  bool plan_valid = false;
   // host copies of the last uploaded SA work lists (skip identical re-uploads)
   std::vector<unsigned char> up_tasks, up_chunks, up_cfg_slot, up_slot_perm_off, up_slot_lane;
   cudaEvent_t ev[6] = {};
@@ -249,6 +266,121 @@ pipette_status check_model(pipette_ctx* ctx, const pipette_model* m, long long b
 }
 
 // K1 on ctx->stream; synchronous readback of the table (cached per (model, bs)).
+// The host-side work plan of pipette_search (R18 sharding, warp tasks in longest-first
+// order, block chunks of one configuration, kernel variant and shared-memory layout).
+pipette_status build_plan(pipette_ctx* ctx, int chains, int W, int r, const char* cap_env, bool full_moves,
+                          HostPlan& hp) {
+  // ---- shard items j = f*chains + c by j mod world (R18); group 32 local chains per warp task
+  const int F = ctx->F;
+  std::vector<SaTask> tasks;
+  std::vector<int>& cfg_slot = hp.cfg_slot;
+  std::vector<int>& slot_perm_off = hp.slot_perm_off;
+  std::vector<int>& slot_lane = hp.slot_lane;
+  cfg_slot.assign(F + 1, 0);
+  int slots = 0, perm_words = 0, maxN = 1, maxdp2 = 0;
+  for (int f = 0; f < F; ++f) {
+    const DevCfg& c = ctx->hcfg[ctx->hfeas[f]];
+    const long long base = (long long)f * chains;
+    const int c_first = (int)(((r - base) % W + W) % W);
+    const int count = c_first < chains ? (chains - 1 - c_first) / W + 1 : 0;
+    cfg_slot[f] = slots;
+    maxN = std::max(maxN, c.N);
+    if (c.pp >= 2) maxdp2 = std::max(maxdp2, c.dp);
+    for (int k0 = 0; k0 < count; k0 += 32) {
+      SaTask t{};
+      t.cfg = c.e;
+      t.f = f;
+      t.c_first = c_first;
+      t.k0 = k0;
+      t.count = std::min(32, count - k0);
+      t.slot0 = slots;
+      t.perm_off = perm_words;
+      for (int l = 0; l < t.count; ++l) { slot_perm_off.push_back(perm_words); slot_lane.push_back(l); }
+      slots += t.count;
+      perm_words += c.N * 32;
+      tasks.push_back(t);
+    }
+  }
+  cfg_slot[F] = slots;
+  // longest-processing-time-first order of the warp tasks (cost ~ per-step work of the config)
+  std::vector<double> cost(tasks.size());
+  for (size_t i = 0; i < tasks.size(); ++i) {
+    const DevCfg& c = ctx->hcfg[tasks[i].cfg];
+    // per-step work: pipeline re-sums (~pp), plus stage-1 updates with probability
+    // 2(1/pp)(1-1/pp) whose cost grows with the cluster (sorted-list probes)
+    const double pchg = 2.0 * (1.0 / c.pp) * (1.0 - 1.0 / c.pp);
+    cost[i] = c.N < 2 ? 0.0 : (c.pp >= 2 ? 60.0 + 12.0 * (c.pp - 1) + pchg * (40.0 + 4.0 * ctx->n_nodes) : 10.0);
+  }
+  std::vector<int> order(tasks.size());
+  for (size_t i = 0; i < order.size(); ++i) order[i] = (int)i;
+  std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return cost[a] > cost[b]; });
+  std::vector<SaTask>& sorted = hp.sorted;
+  sorted.resize(tasks.size());
+  for (size_t i = 0; i < order.size(); ++i) sorted[i] = tasks[order[i]];
+
+  const int n = ctx->n_nodes;
+  const int nn = n * n;
+  // MODE 0 (n <= 16): packed positions, register stage-1 state, lane-replicated R,
+  // subset-max table.  MODE 1 (N <= 256): packed positions, sorted-table stage-1 state,
+  // R through L1.  MODE 2: 32-bit positions (N > 256).
+  const int mode = (n <= 16 && maxN <= 256 && ctx->g <= 15 && ctx->dTab) ? 0 : (maxN <= 256 ? 1 : 2);
+  // MODE 0: the block's m2*R table, 256 hop codes x 16 lane copies (64-bit loads are served
+  // per half-warp, so 16 copies make every lookup conflict free); MODE 1: the block's
+  // n x n m2*R table (one copy; above 32 KB the block has 8 warps to share it)
+  const int r_bytes = mode == 0 ? 256 * 16 * 8 : (mode == 1 ? align16(nn * 8) : 0);
+  const bool big = mode == 1 && r_bytes > 32 * 1024;
+  if (mode == 2 && full_moves)
+    return fail(ctx, PIPETTE_E_UNSUPPORTED, "the full move set needs N = pp*dp <= 256 (max N here %d)", maxN);
+  const int threads = big ? 256 : kSaThreads;
+  // psum (Eq.5 sums) cached in shared memory for configs with dp <= dp_cap: the largest cap
+  // that still reaches the best achievable number of resident blocks per SM
+  auto warp_bytes_for = [&](int cap, int& tls) {
+    int wb = 16;
+    tls = 1;
+    for (int f = 0; f < F; ++f) {
+      const DevCfg& c = ctx->hcfg[ctx->hfeas[f]];
+      wb = std::max(wb, sa_warp_state_bytes(mode, c.N, c.pp, c.dp, n, cap));
+      tls = std::max(tls, n * (std::min(c.spn, c.dp) - 1));
+    }
+    return wb;
+  };
+  const int reg_blocks = mode == 0 ? 3 : (mode == 1 ? (big ? 1 : 3) : 2);   // the kernels' __launch_bounds__
+  auto blocks_for = [&](int wb) {
+    return std::min(reg_blocks, (227 * 1024) / std::max(1, r_bytes + (threads / 32) * wb));
+  };
+  int dp_cap = 0, warp_bytes = 16, tl_stride = 1, best_blocks = -1;
+  for (int cap : {1024, 64, 32, 16, 8, 4, 2}) {
+    int tls;
+    const int wb = warp_bytes_for(cap, tls);
+    const int b = blocks_for(wb);
+    if (b > best_blocks) { best_blocks = b; dp_cap = cap; warp_bytes = wb; tl_stride = tls; }
+  }
+  if (cap_env) {   // tuning knob
+    dp_cap = atoi(cap_env);
+    warp_bytes = warp_bytes_for(dp_cap, tl_stride);
+  }
+  int wpb = threads / 32;
+  const int smem_max = 227 * 1024;
+  if (r_bytes + warp_bytes > smem_max)
+    return fail(ctx, PIPETTE_E_UNSUPPORTED, "SA state (%d B/warp + %d B) exceeds shared memory", warp_bytes, r_bytes);
+  while (wpb > 1 && r_bytes + wpb * warp_bytes > smem_max) --wpb;
+  const size_t smem = (size_t)r_bytes + (size_t)wpb * warp_bytes;
+  // block work units: up to wpb consecutive tasks of one configuration
+  std::vector<int2>& chunks = hp.chunks;
+  for (size_t i = 0; i < sorted.size();) {
+    size_t j = i + 1;
+    while (j < sorted.size() && (int)(j - i) < wpb && sorted[j].cfg == sorted[i].cfg) ++j;
+    chunks.push_back(make_int2((int)i, (int)(j - i)));
+    i = j;
+  }
+
+  hp.slots = slots; hp.perm_words = perm_words; hp.maxN = maxN; hp.mode = mode; hp.r_bytes = r_bytes;
+  hp.big = big; hp.dp_cap = dp_cap; hp.warp_bytes = warp_bytes; hp.tl_stride = tl_stride; hp.wpb = wpb;
+  hp.smem = smem;
+  (void)maxdp2;
+  return PIPETTE_OK;
+}
+
 pipette_status enumerate(pipette_ctx* ctx, const pipette_model* m, long long bs, bool time_it) {
   const bool cached = ctx->enum_valid && std::memcmp(&ctx->enum_model, m, sizeof *m) == 0 && ctx->enum_bs == bs;
   if (cached && !time_it) return PIPETTE_OK;
@@ -290,6 +422,7 @@ pipette_status enumerate(pipette_ctx* ctx, const pipette_model* m, long long bs,
   if (eo.F) CU(cudaMemcpy(ctx->hfeas.data(), ctx->feas.p, sizeof(int) * eo.F, cudaMemcpyDeviceToHost));
   ctx->enum_valid = true;
   ctx->vin_valid = false;
+  ctx->plan_valid = false;   // the SA work plan is built from this enumeration
   ctx->enum_model = *m;
   ctx->enum_bs = bs;
   return PIPETTE_OK;
@@ -628,108 +761,40 @@ pipette_status pipette_search(pipette_ctx* ctx, const pipette_model* model, int6
       return fail(ctx, PIPETTE_E_PROFILE, "no profile entry for tp=%d mb=%d (feasible config e=%d)", c.tp, c.mb, c.e);
   }
 
-  // ---- shard items j = f*chains + c by j mod world (R18); group 32 local chains per warp task
+  // ---- the host-side work plan (work items, warp tasks, block chunks, kernel variant and
+  //      shared-memory layout) depends only on the enumeration and (chains, world, rank):
+  //      it is rebuilt only when those change
   const int W = ctx->world, r = ctx->rank;
-  std::vector<SaTask> tasks;
-  std::vector<int> cfg_slot(F + 1, 0), slot_perm_off, slot_lane;
-  int slots = 0, perm_words = 0, maxN = 1, maxdp2 = 0;
+  const char* cap_env = getenv("PIPETTE_DP_CAP");
+  HostPlanKey key{};
+  key.model = *model; key.bs = bs_global; key.chains = chains; key.W = W; key.r = r;
+  key.dp_cap_env = cap_env ? atoi(cap_env) : -1;
+  key.full_moves = (o.w_migrate || o.w_reverse) ? 1 : 0;
+  if (!(ctx->plan_valid && std::memcmp(&ctx->plan_key, &key, sizeof key) == 0)) {
+    ctx->plan_valid = false;
+    HostPlan& np_ = ctx->plan;
+    np_ = HostPlan{};
+    pipette_status pst = build_plan(ctx, chains, W, r, cap_env, key.full_moves != 0, np_);
+    if (pst != PIPETTE_OK) return pst;
+    ctx->plan_key = key;
+    ctx->plan_valid = true;
+  }
+  const HostPlan& pl = ctx->plan;
+  const std::vector<SaTask>& sorted = pl.sorted;
+  const std::vector<int2>& chunks = pl.chunks;
+  const std::vector<int>& cfg_slot = pl.cfg_slot;
+  const std::vector<int>& slot_perm_off = pl.slot_perm_off;
+  const std::vector<int>& slot_lane = pl.slot_lane;
+  const int slots = pl.slots, perm_words = pl.perm_words, maxN = pl.maxN, mode = pl.mode, n = ctx->n_nodes;
+  const int r_bytes = pl.r_bytes, dp_cap = pl.dp_cap, warp_bytes = pl.warp_bytes, tl_stride = pl.tl_stride;
+  const int wpb = pl.wpb;
+  const bool big = pl.big;
+  const size_t smem = pl.smem;
+  (void)maxN;
   uint64_t steps = 0;
-  for (int f = 0; f < F; ++f) {
-    const DevCfg& c = ctx->hcfg[ctx->hfeas[f]];
-    if (c.N >= 2) steps += (uint64_t)chains * (uint64_t)iterations;
-    const long long base = (long long)f * chains;
-    const int c_first = (int)(((r - base) % W + W) % W);
-    const int count = c_first < chains ? (chains - 1 - c_first) / W + 1 : 0;
-    cfg_slot[f] = slots;
-    maxN = std::max(maxN, c.N);
-    if (c.pp >= 2) maxdp2 = std::max(maxdp2, c.dp);
-    for (int k0 = 0; k0 < count; k0 += 32) {
-      SaTask t{};
-      t.cfg = c.e;
-      t.f = f;
-      t.c_first = c_first;
-      t.k0 = k0;
-      t.count = std::min(32, count - k0);
-      t.slot0 = slots;
-      t.perm_off = perm_words;
-      for (int l = 0; l < t.count; ++l) { slot_perm_off.push_back(perm_words); slot_lane.push_back(l); }
-      slots += t.count;
-      perm_words += c.N * 32;
-      tasks.push_back(t);
-    }
-  }
-  cfg_slot[F] = slots;
+  for (int f = 0; f < F; ++f)
+    if (ctx->hcfg[ctx->hfeas[f]].N >= 2) steps += (uint64_t)chains * (uint64_t)iterations;
   out->sa_steps = steps;
-  // longest-processing-time-first order of the warp tasks (cost ~ per-step work of the config)
-  std::vector<double> cost(tasks.size());
-  for (size_t i = 0; i < tasks.size(); ++i) {
-    const DevCfg& c = ctx->hcfg[tasks[i].cfg];
-    // per-step work: pipeline re-sums (~pp), plus stage-1 updates with probability
-    // 2(1/pp)(1-1/pp) whose cost grows with the cluster (sorted-list probes)
-    const double pchg = 2.0 * (1.0 / c.pp) * (1.0 - 1.0 / c.pp);
-    cost[i] = c.N < 2 ? 0.0 : (c.pp >= 2 ? 60.0 + 12.0 * (c.pp - 1) + pchg * (40.0 + 4.0 * ctx->n_nodes) : 10.0);
-  }
-  std::vector<int> order(tasks.size());
-  for (size_t i = 0; i < order.size(); ++i) order[i] = (int)i;
-  std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return cost[a] > cost[b]; });
-  std::vector<SaTask> sorted(tasks.size());
-  for (size_t i = 0; i < order.size(); ++i) sorted[i] = tasks[order[i]];
-
-  const int n = ctx->n_nodes;
-  const int nn = n * n;
-  // MODE 0 (n <= 16): packed positions, register stage-1 state, lane-replicated R,
-  // subset-max table.  MODE 1 (N <= 256): packed positions, sorted-table stage-1 state,
-  // R through L1.  MODE 2: 32-bit positions (N > 256).
-  const int mode = (n <= 16 && maxN <= 256 && ctx->g <= 15 && ctx->dTab) ? 0 : (maxN <= 256 ? 1 : 2);
-  // MODE 0: the block's m2*R table, 256 hop codes x 16 lane copies (64-bit loads are served
-  // per half-warp, so 16 copies make every lookup conflict free); MODE 1: the block's
-  // n x n m2*R table (one copy; above 32 KB the block has 8 warps to share it)
-  const int r_bytes = mode == 0 ? 256 * 16 * 8 : (mode == 1 ? align16(nn * 8) : 0);
-  const bool big = mode == 1 && r_bytes > 32 * 1024;
-  if (mode == 2 && (o.w_migrate || o.w_reverse))
-    return fail(ctx, PIPETTE_E_UNSUPPORTED, "the full move set needs N = pp*dp <= 256 (max N here %d)", maxN);
-  const int threads = big ? 256 : kSaThreads;
-  // psum (Eq.5 sums) cached in shared memory for configs with dp <= dp_cap: the largest cap
-  // that still reaches the best achievable number of resident blocks per SM
-  auto warp_bytes_for = [&](int cap, int& tls) {
-    int wb = 16;
-    tls = 1;
-    for (int f = 0; f < F; ++f) {
-      const DevCfg& c = ctx->hcfg[ctx->hfeas[f]];
-      wb = std::max(wb, sa_warp_state_bytes(mode, c.N, c.pp, c.dp, n, cap));
-      tls = std::max(tls, n * (std::min(c.spn, c.dp) - 1));
-    }
-    return wb;
-  };
-  const int reg_blocks = mode == 0 ? 3 : (mode == 1 ? (big ? 1 : 3) : 2);   // the kernels' __launch_bounds__
-  auto blocks_for = [&](int wb) {
-    return std::min(reg_blocks, (227 * 1024) / std::max(1, r_bytes + (threads / 32) * wb));
-  };
-  int dp_cap = 0, warp_bytes = 16, tl_stride = 1, best_blocks = -1;
-  for (int cap : {1024, 64, 32, 16, 8, 4, 2}) {
-    int tls;
-    const int wb = warp_bytes_for(cap, tls);
-    const int b = blocks_for(wb);
-    if (b > best_blocks) { best_blocks = b; dp_cap = cap; warp_bytes = wb; tl_stride = tls; }
-  }
-  if (const char* e = getenv("PIPETTE_DP_CAP")) {   // tuning knob
-    dp_cap = atoi(e);
-    warp_bytes = warp_bytes_for(dp_cap, tl_stride);
-  }
-  int wpb = threads / 32;
-  const int smem_max = 227 * 1024;
-  if (r_bytes + warp_bytes > smem_max)
-    return fail(ctx, PIPETTE_E_UNSUPPORTED, "SA state (%d B/warp + %d B) exceeds shared memory", warp_bytes, r_bytes);
-  while (wpb > 1 && r_bytes + wpb * warp_bytes > smem_max) --wpb;
-  const size_t smem = (size_t)r_bytes + (size_t)wpb * warp_bytes;
-  // block work units: up to wpb consecutive tasks of one configuration
-  std::vector<int2> chunks;
-  for (size_t i = 0; i < sorted.size();) {
-    size_t j = i + 1;
-    while (j < sorted.size() && (int)(j - i) < wpb && sorted[j].cfg == sorted[i].cfg) ++j;
-    chunks.push_back(make_int2((int)i, (int)(j - i)));
-    i = j;
-  }
 
   const bool tracing = o.trace && o.trace_items && o.n_trace > 0 && o.trace_cap > 0;
   std::vector<int> trace_slot;
