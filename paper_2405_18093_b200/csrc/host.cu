@@ -327,7 +327,9 @@ pipette_status build_plan(pipette_ctx* ctx, int chains, int W, int r, const char
   // MODE 0: the block's m2*R table, 256 hop codes x 16 lane copies (64-bit loads are served
   // per half-warp, so 16 copies make every lookup conflict free); MODE 1: the block's
   // n x n m2*R table (one copy; above 32 KB the block has 8 warps to share it)
-  const int r_bytes = mode == 0 ? 256 * 16 * 8 : (mode == 1 ? align16(nn * 8) : 0);
+  // (+ MODE 0's shared stage-1 tables: vs 256, qe 32 and tab 256 doubles, rank 256 bytes)
+  const int r_bytes = mode == 0 ? 256 * 16 * 8 + (n <= 8 ? (256 + 32 + 256) * 8 + 256 : 0)
+                                : (mode == 1 ? align16(nn * 8) : 0);
   const bool big = mode == 1 && r_bytes > 32 * 1024;
   if (mode == 2 && full_moves)
     return fail(ctx, PIPETTE_E_UNSUPPORTED, "the full move set needs N = pp*dp <= 256 (max N here %d)", maxN);

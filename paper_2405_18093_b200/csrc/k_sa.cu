@@ -159,10 +159,10 @@ struct S1Reg {
     uint32_t m = NW == 4 ? __vminu4(__vminu4(r0, r1), __vminu4(r2, r3)) : __vminu4(r0, r1);
     m = __vminu4(m, m >> 16);
     m = __vminu4(m, m >> 8) & 0xffu;
-    return m == 0xffu ? 0.0 : __ldg(X.vs + m);
+    return m == 0xffu ? 0.0 : X.vs[m];
   }
   __device__ __forceinline__ double tex_of(uint32_t m, int kk, const S1Ctx& X) const {
-    return kk >= 2 ? __dmul_rn(__ldg(X.qe + kk), __ldg(X.tab + m)) : 0.0;
+    return kk >= 2 ? __dmul_rn(X.qe[kk], X.tab[m]) : 0.0;
   }
   __device__ __forceinline__ void clear() { cnt = 0; mask = 0u; }
   __device__ __forceinline__ void add_init(uint32_t a) { cnt += (CT)1 << (4u * a); mask |= 1u << a; }
@@ -700,18 +700,32 @@ __host__ __device__ inline int hc_warp_state_bytes(int N, int pp, int dp, int dp
 // One warp task of MODE 0.  Every lane runs the same instruction stream whatever its
 // proposal (the swap is always applied tentatively, both touched pipelines are always
 // re-summed), so the only divergent paths are the rare rescans and best-mapping writes.
+// The block's shared copies of the configuration's stage-1 tables (MODE 0): ranks and
+// values of T_in, qe(k), and the subset-max table when n <= 8 (2^n entries).
+struct S1Shared {
+  const uint8_t* rank;
+  const double* vs;
+  const double* qe;
+  const double* tab;
+};
+
 template <bool TRACE, int PP, int NW>
 __device__ __forceinline__ void run_task_hc(const SaParams& P, const SaTask T, const DevCfg C, const double* Tl,
-                                            unsigned char* ws, int lane) {
+                                            const S1Shared& SS, unsigned char* ws, int lane) {
   using RT = RGlob;   // (S1Reg takes no R)
   const bool active = lane < T.count;
   const int N = C.N, pp = PP > 0 ? PP : C.pp, dp = C.dp, n = P.n_nodes;
   const uint32_t chain = (uint32_t)(T.c_first + (T.k0 + lane) * P.world);
   const int slot = T.slot0 + lane;
   S1Ctx X;
-  X.qi = P.qtab + C.qi_off; X.qe = P.qtab + C.qe_off; X.tab = P.subset_max;
-  X.rank = P.tin_rank + (size_t)T.f * 256;
-  X.vs = P.tin_vs + (size_t)T.f * 256;
+  X.qi = P.qtab + C.qi_off;
+  if (NW == 2) {   // the block's shared copies
+    X.qe = SS.qe; X.tab = SS.tab; X.rank = SS.rank; X.vs = SS.vs;
+  } else {
+    X.qe = P.qtab + C.qe_off; X.tab = P.subset_max;
+    X.rank = P.tin_rank + (size_t)T.f * 256;
+    X.vs = P.tin_vs + (size_t)T.f * 256;
+  }
   X.n = n;
   const RT Rdummy{nullptr, n, 0};
 
@@ -1417,6 +1431,13 @@ __global__ void __launch_bounds__(SaLB<MODE, BIG>::threads, SaLB<MODE, BIG>::blo
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   RT R{P.R, n, lane};
   const double* Tl = Rs + (lane & 15);   // MODE 0: this lane's copy of the block's m2*R table
+  // MODE 0: the block's stage-1 tables after the m2*R table (kS1SharedBytes)
+  double* s1_vs = Rs + 256 * 16;
+  double* s1_qe = s1_vs + 256;
+  double* s1_tab = s1_qe + 32;
+  uint8_t* s1_rank = reinterpret_cast<uint8_t*>(s1_tab + 256);
+  // (n <= 8 only: at n <= 16 the extra shared memory costs more than the loads save)
+  const S1Shared SS{s1_rank, s1_vs, s1_qe, s1_tab};
   unsigned char* ws = smem + P.r_smem_bytes + wid * P.warp_smem_bytes;
   __shared__ int s_chunk;
   int table_cfg = -1;
@@ -1438,6 +1459,17 @@ __global__ void __launch_bounds__(SaLB<MODE, BIG>::threads, SaLB<MODE, BIG>::blo
           for (int i = threadIdx.x; i < 256 * 16; i += blockDim.x) {
             const int code = i >> 4, a = code & 15, b = code >> 4;
             Rs[i] = (a < n && b < n) ? __dmul_rn(m2, P.R[a * n + b]) : 0.0;
+          }
+          // the configuration's stage-1 tables (all chunks of a configuration share f)
+          if (NW == 2) {
+          const int f0 = P.tasks[chunk.x].f;
+          const DevCfg& C0 = P.cfgs[cfg0];
+          for (int i = threadIdx.x; i < 256; i += blockDim.x) {
+            s1_rank[i] = P.tin_rank[(size_t)f0 * 256 + i];
+            s1_vs[i] = P.tin_vs[(size_t)f0 * 256 + i];
+          }
+          for (int i = threadIdx.x; i < 32; i += blockDim.x) s1_qe[i] = i <= min(C0.dp, n) ? P.qtab[C0.qe_off + i] : 0.0;
+          for (int i = threadIdx.x; i < (1 << n); i += blockDim.x) s1_tab[i] = P.subset_max[i];
           }
         } else {
           for (int i = threadIdx.x; i < nn; i += blockDim.x) Rs[i] = __dmul_rn(m2, P.R[i]);
@@ -1467,13 +1499,13 @@ __global__ void __launch_bounds__(SaLB<MODE, BIG>::threads, SaLB<MODE, BIG>::blo
     if (full) {
     } else if constexpr (MODE == 0) {
       switch (C.pp) {   // compile-time pipeline depth for the common power-of-two depths
-        case 1: run_task_hc<TRACE, 1, NW>(P, T, C, Tl, ws, lane); break;
-        case 2: run_task_hc<TRACE, 2, NW>(P, T, C, Tl, ws, lane); break;
-        case 4: run_task_hc<TRACE, 4, NW>(P, T, C, Tl, ws, lane); break;
-        case 8: run_task_hc<TRACE, 8, NW>(P, T, C, Tl, ws, lane); break;
-        case 16: run_task_hc<TRACE, 16, NW>(P, T, C, Tl, ws, lane); break;
-        case 32: run_task_hc<TRACE, 32, NW>(P, T, C, Tl, ws, lane); break;
-        default: run_task_hc<TRACE, 0, NW>(P, T, C, Tl, ws, lane); break;
+        case 1: run_task_hc<TRACE, 1, NW>(P, T, C, Tl, SS, ws, lane); break;
+        case 2: run_task_hc<TRACE, 2, NW>(P, T, C, Tl, SS, ws, lane); break;
+        case 4: run_task_hc<TRACE, 4, NW>(P, T, C, Tl, SS, ws, lane); break;
+        case 8: run_task_hc<TRACE, 8, NW>(P, T, C, Tl, SS, ws, lane); break;
+        case 16: run_task_hc<TRACE, 16, NW>(P, T, C, Tl, SS, ws, lane); break;
+        case 32: run_task_hc<TRACE, 32, NW>(P, T, C, Tl, SS, ws, lane); break;
+        default: run_task_hc<TRACE, 0, NW>(P, T, C, Tl, SS, ws, lane); break;
       }
     } else if constexpr (MODE == 1) {
       switch (C.pp) {
