@@ -1,5 +1,5 @@
 """torchrun worker: pipette_search over NCCL on W GPUs; rank 0 writes the plan as JSON.
-Usage: torchrun --nproc-per-node W tests/helpers/mp_search.py OUT.json WORKLOAD CHAINS ITERS"""
+Usage: torchrun --nproc-per-node W tests/helpers/mp_search.py OUT.json WORKLOAD CHAINS ITERS [W_MIGRATE W_REVERSE]"""
 import json
 import os
 import sys
@@ -14,7 +14,7 @@ import workloads as W  # noqa: E402
 from paper_2405_18093_b200 import Model, Pipette  # noqa: E402
 
 
-def main(out, name, chains, iters):
+def main(out, name, chains, iters, w_migrate=0, w_reverse=0):
     local = int(os.environ["LOCAL_RANK"])
     torch.cuda.set_device(local)
     dist.init_process_group("nccl", device_id=torch.device("cuda", local))
@@ -24,7 +24,7 @@ def main(out, name, chains, iters):
     pip = Pipette.from_torch_distributed(w.n_nodes, w.gpus_per_node, B, prof, device=local,
                                          mem_capacity_bytes=w.cap_bytes, mem_margin_permille=w.margin_permille)
     res = pip.search(Model(m.n_layers, m.hidden, m.heads, m.seq_len, m.vocab), w.bs_global, chains, iters, w.seed,
-                     per_config=True)
+                     per_config=True, w_migrate=w_migrate, w_reverse=w_reverse)
     p = res["plan"]
     rec = {"rank": dist.get_rank(), "world": dist.get_world_size(), "latency": p.latency_s.hex(),
            "cfg_index": p.cfg_index, "chain": p.chain, "best_step": p.best_step, "perm": p.perm.tolist(),
@@ -38,4 +38,4 @@ def main(out, name, chains, iters):
 
 
 if __name__ == "__main__":
-    main(sys.argv[1], sys.argv[2], int(sys.argv[3]), int(sys.argv[4]))
+    main(sys.argv[1], sys.argv[2], int(sys.argv[3]), int(sys.argv[4]), *[int(x) for x in sys.argv[5:7]])

@@ -20,15 +20,16 @@ def _ngpu():
     return torch.cuda.device_count()
 
 
-@pytest.mark.parametrize("world,chains", [(2, 8), (2, 7), (4, 8), (4, 5), (8, 8)])
-def test_multi_gpu_plan_bit_identical(world, chains, tmp_path):
+@pytest.mark.parametrize("world,chains,moves", [(2, 8, (0, 0)), (2, 7, (0, 0)), (4, 8, (0, 0)), (4, 5, (0, 0)),
+                                               (8, 8, (0, 0)), (2, 6, (683, 682)), (4, 5, (683, 682))])
+def test_multi_gpu_plan_bit_identical(world, chains, moves, tmp_path):
     if _ngpu() < world:
         pytest.skip(f"needs {world} GPUs")
     name, iters = "C1", 1000
     out = tmp_path / "plan.json"
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={world}",
            "--master-addr=127.0.0.1", "--master-port=29533", os.path.join(HERE, "helpers", "mp_search.py"),
-           str(out), name, str(chains), str(iters)]
+           str(out), name, str(chains), str(iters), str(moves[0]), str(moves[1])]
     subprocess.run(cmd, check=True, timeout=600)
     recs = json.load(open(out))
     w = W.WORKLOADS[name]
@@ -36,7 +37,8 @@ def test_multi_gpu_plan_bit_identical(world, chains, tmp_path):
     m = w.model
     cl = O.make_cluster(w.n_nodes, w.gpus_per_node, w.cap_bytes, w.margin_permille)
     mo = O.make_model(m.n_layers, m.hidden, m.heads, m.seq_len, m.vocab)
-    ref = O.search(cl, B, O.make_profile(prof), mo, w.bs_global, chains, iters, w.seed)
+    ref = O.search(cl, B, O.make_profile(prof), mo, w.bs_global, chains, iters, w.seed,
+                   w_migrate=moves[0], w_reverse=moves[1])
     assert len(recs) == world
     for r in recs:
         assert r == {**recs[0], "rank": r["rank"]}                      # identical on every rank
