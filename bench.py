@@ -98,14 +98,14 @@ class ClockSampler:
             time.sleep(0.02)
 
     def __enter__(self):
-        if self.nv:
+        if self.nv and os.environ.get("PIPETTE_BENCH_NO_CLOCKS") != "1":
             self.t = threading.Thread(target=self._run, daemon=True)
             self.t.start()
         return self
 
     def __exit__(self, *a):
         self._stop.set()
-        if self.nv:
+        if self.nv and hasattr(self, "t"):
             self.t.join()
 
     def summary(self):
@@ -219,7 +219,8 @@ def run_ours(args):
     barrier()
     with ClockSampler(local) as clk:
         for k in range(args.steps):
-            flush.fill_(k & 0xFF)
+            if os.environ.get("PIPETTE_BENCH_NO_FLUSH") != "1":   # (diagnostics only)
+                flush.fill_(k & 0xFF)
             evs[k][0].record(stream)
             res = pip.search(model, w.bs_global, chains, w.iterations, w.seed)
             evs[k][1].record(stream)
@@ -246,13 +247,24 @@ def run_ours(args):
     sa_avg_s = (sa_max / args.steps) / 1000.0
     pk = peaks()
     clocks = clk.summary()
-    fp64_peak = N_SMS * FP64_LANES_PER_SM * (pk.get("sm_max_mhz", 1965.0) * 1e6) / 1e12
+    fp64_nominal = N_SMS * FP64_LANES_PER_SM * (pk.get("sm_max_mhz", 1965.0) * 1e6) / 1e12
+    fp64_peak, peak_source = fp64_nominal, "148 SMs x 64 FP64 lanes x sm_max_mhz (MEASURED_PEAKS.json), DESIGN.md 8"
+    measured = None
+    try:   # the DADD/DMUL rate measured on this GPU at this clock (pipette_measure_peaks)
+        from paper_2405_18093_b200 import measure_peaks
+        measured = measure_peaks(local)
+        fp64_peak = measured["fp64_ops_per_s"] / 1e12
+        peak_source = ("measured: independent DADD+DMUL chains at full occupancy (pipette_measure_peaks), "
+                       f"nominal {fp64_nominal:.2f}")
+    except Exception:
+        pass
     achieved = ops_local / sa_avg_s / 1e12
     roofline = {"kernel": "k_sa_chains", "bound": "alu", "achieved": achieved, "peak": fp64_peak,
                 "unit": "TFLOP/s (fp64 DADD/DMUL ops)", "frac": achieved / fp64_peak,
+                "alu_peak_measured_tops": (measured["alu_ops_per_s"] / 1e12) if measured else None,
                 "traffic": ncu_traffic("k_sa_chains") if args.workload == "C2" else None,
                 "traffic_note": "DRAM bytes per launch (ncu): chain state lives in shared memory, R/tables in L2",
-                "peak_source": "148 SMs x 64 FP64 lanes x sm_max_mhz (MEASURED_PEAKS.json), DESIGN.md 8",
+                "peak_source": peak_source,
                 "sa_kernel_ms": sa_avg_s * 1000.0, "sa_share_of_step": (sa_max / t_max) if t_max else None,
                 "pipes": ncu_pipes("r01c_sa_ncu_summary.txt") if args.workload == "C2" else None,
                 "note": "issue/ALU-bound, not FP64-bound: the FP64 fraction is small by construction (DESIGN.md 8)"}
@@ -304,7 +316,7 @@ def run_ours(args):
                            "l2": "flushed between timed steps (256 MiB write)", "parallelism": f"chains sharded x{world}"},
                 "plan": {"cfg": list(plan.cfg), "latency_s": plan.latency_s, "cfg_index": plan.cfg_index,
                          "chain": plan.chain, "best_step": plan.best_step},
-                "phase_ms": plan.timings_ms,
+                "phase_ms": plan.timings_ms, "step_ms": [round(x, 3) for x in step_ms],
                 "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
                 "clocks": clocks, "eval_stream": eval_stream}
         print(json.dumps(line))

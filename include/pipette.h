@@ -236,6 +236,12 @@ pipette_status pipette_eval_models(pipette_ctx* ctx, const pipette_model* model,
 pipette_status pipette_profile_bandwidth(int32_t n_gpus, const int32_t* devices, uint64_t bytes, int32_t reps,
                                          double* bw_out, double* ms_out, char* err, int32_t err_cap);
 
+/* Measured roofline denominators on `device`: sustained FP64 DADD+DMUL
+ * instructions per second (counted per thread op) and 32-bit ALU (LOP3 + SHF) ops per
+ * second, from independent chains at full occupancy.  Outputs HOST (either may be NULL).
+ * Errors: E_CUDA. */
+pipette_status pipette_measure_peaks(int32_t device, double* fp64_ops_per_s, double* alu_ops_per_s);
+
 /* Host-only helper (no GPU needed): the items j in [0, n_items) that `rank` of `world`
  * runs (R18), written to items (capacity cap).  Returns the count (may exceed cap). */
 int64_t pipette_shard_items(int64_t n_items, int32_t rank, int32_t world, int64_t* items, int64_t cap);

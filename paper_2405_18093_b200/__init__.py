@@ -113,6 +113,15 @@ def profile_bandwidth(devices=None, bytes_per_copy: int = 256 << 20, reps: int =
     return bw, ms
 
 
+def measure_peaks(device: int = 0) -> dict:
+    """Measured FP64 (DADD + DMUL) and 32-bit ALU op rates of this GPU (roofline denominators)."""
+    f, a = C.c_double(), C.c_double()
+    st = _abi.lib().pipette_measure_peaks(device, C.byref(f), C.byref(a))
+    if st != 0:
+        raise PipetteError(st, "pipette_measure_peaks failed")
+    return {"fp64_ops_per_s": f.value, "alu_ops_per_s": a.value}
+
+
 def load_memory_mlp(path=None) -> dict:
     """The packaged Eq.7 MLP (data/mem_mlp.json, trained by tools/train_mem_mlp.py)."""
     import json

@@ -31,7 +31,7 @@ pipette_status models_launch(const DevCfg* cfgs, const unsigned long long* keys,
                              uint8_t* status, void* stream);
 size_t eval_smem_bytes(int mode, int perm_stride, bool staged, int n_nodes, int E, int bm_words);
 __global__ void k_tin_values(const DevCfg*, const double*, const double*, int, double*);
-const void* sa_kernel(int mode, bool trace, int n_nodes);
+const void* sa_kernel(int mode, bool trace, int n_nodes, bool full);
 int sa_warp_state_bytes(int mode, int N, int pp, int dp, int n, int dp_cap);
 __global__ void k_node_lists(const double*, int, uint8_t*, double*);
 __global__ void k_pair_list(const double*, int, uint16_t*, double*);
@@ -897,7 +897,7 @@ pipette_status pipette_search(pipette_ctx* ctx, const pipette_model* model, int6
   P.w_migrate = o.w_migrate;
   P.w_reverse = o.w_reverse;
 
-  const void* kern = sa_kernel(big ? 3 : mode, tracing, n);
+  const void* kern = sa_kernel(big ? 3 : mode, tracing, n, o.w_migrate || o.w_reverse);
   CU(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   int occ = 0;
   CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, wpb * 32, smem));

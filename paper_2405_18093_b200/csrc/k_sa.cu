@@ -1420,7 +1420,9 @@ struct SaLB {
   static constexpr int blocks = MODE == 0 ? 3 : (MODE == 1 ? (BIG ? 1 : 3) : 2);
 };
 
-template <int MODE, bool TRACE, int NW = 4, bool BIG = false>
+// FULL: the full move set (run_task_full) -- a separate instantiation, so the swap kernel's
+// instruction footprint stays small (its cold start after an L2 flush refetches the code).
+template <int MODE, bool TRACE, int NW = 4, bool BIG = false, bool FULL = false>
 __global__ void __launch_bounds__(SaLB<MODE, BIG>::threads, SaLB<MODE, BIG>::blocks) k_sa_chains(SaParams P) {
   using POS = PosWide;
   using RT = RGlob;
@@ -1484,19 +1486,13 @@ __global__ void __launch_bounds__(SaLB<MODE, BIG>::threads, SaLB<MODE, BIG>::blo
     const DevCfg C = P.cfgs[T.cfg];
     unsigned long long t_start = 0;
     if (lane == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_start));
-    bool full = false;
-    if constexpr (MODE == 0 || MODE == 1) {
-      if (P.w_migrate | P.w_reverse) {   // the full move set (launch-uniform)
-        switch (C.pp) {
-          case 4: run_task_full<MODE, TRACE, 4, NW>(P, T, C, Rs, ws, lane); break;
-          case 8: run_task_full<MODE, TRACE, 8, NW>(P, T, C, Rs, ws, lane); break;
-          case 16: run_task_full<MODE, TRACE, 16, NW>(P, T, C, Rs, ws, lane); break;
-          default: run_task_full<MODE, TRACE, 0, NW>(P, T, C, Rs, ws, lane); break;
-        }
-        full = true;
+    if constexpr (FULL && (MODE == 0 || MODE == 1)) {   // the full move set
+      switch (C.pp) {
+        case 4: run_task_full<MODE, TRACE, 4, NW>(P, T, C, Rs, ws, lane); break;
+        case 8: run_task_full<MODE, TRACE, 8, NW>(P, T, C, Rs, ws, lane); break;
+        case 16: run_task_full<MODE, TRACE, 16, NW>(P, T, C, Rs, ws, lane); break;
+        default: run_task_full<MODE, TRACE, 0, NW>(P, T, C, Rs, ws, lane); break;
       }
-    }
-    if (full) {
     } else if constexpr (MODE == 0) {
       switch (C.pp) {   // compile-time pipeline depth for the common power-of-two depths
         case 1: run_task_hc<TRACE, 1, NW>(P, T, C, Tl, SS, ws, lane); break;
@@ -1693,7 +1689,18 @@ __global__ void __launch_bounds__(256) k_argmin(const ChainOut* __restrict__ out
 }
 
 // Host-side handles of the K3 variants (MODE 0/1/2 as above; TRACE records).
-const void* sa_kernel(int mode, bool trace, int n_nodes) {
+const void* sa_kernel(int mode, bool trace, int n_nodes, bool full) {
+  if (full) {
+    if (mode == 0 && n_nodes <= 8)
+      return trace ? (const void*)k_sa_chains<0, true, 2, false, true> : (const void*)k_sa_chains<0, false, 2, false, true>;
+    if (mode == 0)
+      return trace ? (const void*)k_sa_chains<0, true, 4, false, true> : (const void*)k_sa_chains<0, false, 4, false, true>;
+    if (mode == 1)
+      return trace ? (const void*)k_sa_chains<1, true, 4, false, true> : (const void*)k_sa_chains<1, false, 4, false, true>;
+    if (mode == 3)
+      return trace ? (const void*)k_sa_chains<1, true, 4, true, true> : (const void*)k_sa_chains<1, false, 4, true, true>;
+    return nullptr;   // (MODE 2: rejected by the host)
+  }
   if (mode == 0 && n_nodes <= 8) return trace ? (const void*)k_sa_chains<0, true, 2> : (const void*)k_sa_chains<0, false, 2>;
   if (mode == 0) return trace ? (const void*)k_sa_chains<0, true, 4> : (const void*)k_sa_chains<0, false, 4>;
   if (mode == 1) return trace ? (const void*)k_sa_chains<1, true> : (const void*)k_sa_chains<1, false>;
