@@ -149,6 +149,7 @@ struct pipette_ctx {
   bool vin_valid = false;   // K2 intra-node value table matches the config table and R
   // search buffers
   DevBuf mlp;   // Eq.7 MLP parameters (NEXT-4), empty = analytic memory (R11)
+  DevBuf claimed;   // SA chunk claim flags + per-SM first-fetch slots
   DevBuf tasks, chunks, counter, chain_out, best_perm, cfg_slot, cfg_best, gbits, items, gitems, pack, accepted,
       slot_perm_off, slot_lane, trace_slot, trace, task_prof, tin_rank, tin_vs, tl_ac, tl_val, tl_len;
   int64_t n_tasks_last = 0;
@@ -605,7 +606,7 @@ pipette_status pipette_set_stream(pipette_ctx* ctx, void* stream) {
 void pipette_destroy(pipette_ctx* ctx) {
   if (!ctx) return;
   if (ctx->comm) ncclCommDestroy(ctx->comm);
-  DevBuf* bufs[] = {&ctx->cfgs, &ctx->keys, &ctx->feas, &ctx->qtab, &ctx->eout, &ctx->vin, &ctx->mlp, &ctx->tasks, &ctx->chunks, &ctx->counter,
+  DevBuf* bufs[] = {&ctx->cfgs, &ctx->keys, &ctx->feas, &ctx->qtab, &ctx->eout, &ctx->vin, &ctx->mlp, &ctx->claimed, &ctx->tasks, &ctx->chunks, &ctx->counter,
                     &ctx->chain_out, &ctx->best_perm, &ctx->cfg_slot, &ctx->cfg_best, &ctx->gbits, &ctx->items,
                     &ctx->gitems, &ctx->pack, &ctx->accepted, &ctx->slot_perm_off, &ctx->slot_lane,
                     &ctx->trace_slot, &ctx->trace, &ctx->task_prof, &ctx->tin_rank, &ctx->tin_vs, &ctx->tl_ac,
@@ -841,6 +842,8 @@ pipette_status pipette_search(pipette_ctx* ctx, const pipette_model* model, int6
   CU(upload(ctx->up_slot_perm_off, ctx->slot_perm_off, slot_perm_off.data(), sizeof(int) * slots));
   CU(upload(ctx->up_slot_lane, ctx->slot_lane, slot_lane.data(), sizeof(int) * slots));
   CU(cudaMemsetAsync(ctx->counter.p, 0, sizeof(int), s));
+  CU(ensure(ctx->claimed, sizeof(int) * (std::max<size_t>(1, chunks.size()) + 1024)));
+  CU(cudaMemsetAsync(ctx->claimed.p, 0, sizeof(int) * (std::max<size_t>(1, chunks.size()) + 1024), s));
   if (tracing) {
     CU(ensure(ctx->trace_slot, sizeof(int) * trace_slot.size()));
     CU(ensure(ctx->trace, sizeof(pipette_trace_record) * (size_t)o.n_trace * o.trace_cap));
@@ -877,6 +880,9 @@ pipette_status pipette_search(pipette_ctx* ctx, const pipette_model* model, int6
   P.chunks = (const int2*)ctx->chunks.p;
   P.n_chunks = (int)chunks.size();
   P.task_counter = (int*)ctx->counter.p;
+  P.claimed = (int*)ctx->claimed.p;
+  P.sm_slot = (int*)ctx->claimed.p + std::max<size_t>(1, chunks.size());   // 1024 per-SM slots after the flags
+  P.n_sms = ctx->n_sms;
   P.n_nodes = n;
   P.iterations = iterations;
   P.key = make_uint2((uint32_t)seed, (uint32_t)(seed >> 32));

@@ -1443,12 +1443,36 @@ __global__ void __launch_bounds__(SaLB<MODE, BIG>::threads, SaLB<MODE, BIG>::blo
   unsigned char* ws = smem + P.r_smem_bytes + wid * P.warp_smem_bytes;
   __shared__ int s_chunk;
   int table_cfg = -1;
+  bool first_fetch = true;
   for (;;) {
     // a block takes one chunk: up to warps-per-block consecutive tasks of ONE configuration
     // (host-built), so the block runs one code path (I-cache locality), shares the
     // configuration's m2*R table (MODE 0/1), and its warps finish together
+    // The first chunk of a block is the one its SM slot points at (chunk slot*SMs + smid,
+    // snaking: reversed on odd slots): the chunk list is longest first, so the first wave
+    // puts one of the heaviest chunks on every SM with the lightest of the next group beside
+    // it, whatever order the blocks start in.
+    // Later chunks come from the global counter; a claim flag per chunk makes every chunk
+    // run exactly once either way.
     __syncthreads();
-    if (threadIdx.x == 0) s_chunk = atomicAdd(P.task_counter, 1);
+    if (threadIdx.x == 0) {
+      int c = -1;
+      if (first_fetch) {
+        uint32_t smid;
+        asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+        const int slot = atomicAdd(P.sm_slot + (smid % (uint32_t)P.n_sms), 1);
+        const int sm = (int)(smid % (uint32_t)P.n_sms);
+        const int pref = slot * P.n_sms + ((slot & 1) ? P.n_sms - 1 - sm : sm);   // snake: heavy beside light
+        if (pref < P.n_chunks && atomicExch(P.claimed + pref, 1) == 0) c = pref;
+      }
+      while (c < 0) {
+        const int g = atomicAdd(P.task_counter, 1);
+        if (g >= P.n_chunks) { c = P.n_chunks; break; }
+        if (atomicExch(P.claimed + g, 1) == 0) c = g;
+      }
+      s_chunk = c;
+    }
+    first_fetch = false;
     __syncthreads();
     const int ch = s_chunk;
     if (ch >= P.n_chunks) break;

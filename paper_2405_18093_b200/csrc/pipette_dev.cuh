@@ -77,6 +77,9 @@ struct SaParams {
   const int2* chunks;        // block work units: (first task, task count <= warps per block), one config each
   int32_t n_chunks;
   int32_t* task_counter;
+  int32_t* claimed;          // per chunk: taken (zeroed per launch)
+  int32_t* sm_slot;          // per SM: blocks that made their first fetch (zeroed per launch)
+  int32_t n_sms;
   int32_t n_nodes;
   int32_t iterations;
   uint2 key;                 // Philox key (seed lo, seed hi)
