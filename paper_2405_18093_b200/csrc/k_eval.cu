@@ -81,11 +81,18 @@ struct EvalShared {
   uint32_t* bm;     // [bm_words][T]
   uint32_t* cnt;    // [ceil(n/4)][T]
   int n, tid, lane, T;
+  uint32_t lgn;     // MODE 0: log2 of the padded table side
+  const unsigned char* Rl;   // MODE 0: this lane's copy, &Rs[lane & 15]
+  uint32_t row_bytes;        // MODE 0: 2^lgn * 16 copies * 8 B
 };
 
+// MODE 0: R padded to npad x npad (npad = 2^lgn >= n; zeros outside n x n) with 16 lane
+// copies, so any masked node pair (a, b < npad) is in range and conflict free.
+// (MODE 0 address: two integer multiply-adds, which issue on the FMA pipe and leave the
+// ALU pipe -- K2's limiter -- to the bijection test)
 template <bool REP>
 __device__ __forceinline__ double r_at(const EvalShared& S, uint32_t a, uint32_t b) {
-  return REP ? S.Rs[((int)a * S.n + (int)b) * 16 + (S.lane & 15)] : S.Rs[(int)a * S.n + (int)b];
+  return REP ? *reinterpret_cast<const double*>(S.Rl + a * S.row_bytes + b * 128u) : S.Rs[(int)a * S.n + (int)b];
 }
 
 // MODE 0 evaluation of one candidate with compile-time pipeline depth PP (0: runtime).
@@ -95,6 +102,7 @@ __device__ __forceinline__ void eval_small(const EvalParams& P, const EvalShared
   const int N = C.N;
   const int pp = PP > 0 ? PP : C.pp;
   const uint32_t spn = (uint32_t)C.spn;
+  const uint32_t nmask = (1u << S.lgn) - 1u;
   constexpr bool regbm = RB;   // N <= 64: bitmap in a register pair
   if (!regbm)
     for (int w = 0; w < (N + 31) / 32; ++w) S.bm[w * S.T + S.tid] = 0u;
@@ -111,15 +119,16 @@ __device__ __forceinline__ void eval_small(const EvalParams& P, const EvalShared
   auto visit = [&](uint32_t v, bool stage1, bool last) {
     if (regbm) {
       seen_lo |= shl_clamp(1u, v);
-      seen_hi |= shl_clamp(1u, v - 32u);
-      v = min(v, (uint32_t)N - 1u);                 // keeps node ids in range (the row is invalid)
+      seen_hi |= shl_clamp(1u, v ^ 32u);
     } else {
       bad |= v >= (uint32_t)N;
-      v = min(v, (uint32_t)N - 1u);
-      uint32_t& bw = S.bm[(v >> 5) * S.T + S.tid];
-      bw |= 1u << (v & 31);
+      const uint32_t vc = min(v, (uint32_t)N - 1u);
+      uint32_t& bw = S.bm[(vc >> 5) * S.T + S.tid];
+      bw |= 1u << (vc & 31);
     }
-    const uint32_t nd = div_small(v, C.spn_magic, spn);
+    // node of the slot; an id >= N (invalid row, flagged above) is masked into the padded
+    // table instead of clamped
+    const uint32_t nd = div_small(v, C.spn_magic, spn) & nmask;
     if (stage1) {                                    // stage-1 worker of pipeline z (Eq.6)
       c_lo += shl_clamp(1u, 4u * nd);
       c_hi += shl_clamp(1u, 4u * nd - 32u);
@@ -184,7 +193,6 @@ __device__ __forceinline__ void eval_small(const EvalParams& P, const EvalShared
     ok = ok && c == N;
   }
   // stage-1 node set N1 from the nibble counts: bit a set iff nibble a is non-zero
-  const unsigned long long c64 = ((unsigned long long)c_hi << 32) | c_lo;
   uint32_t lo = c_lo | (c_lo >> 1), hi = c_hi | (c_hi >> 1);
   lo = (lo | (lo >> 2)) & 0x11111111u; hi = (hi | (hi >> 2)) & 0x11111111u;
   lo = (lo | (lo >> 3)) & 0x03030303u; hi = (hi | (hi >> 3)) & 0x03030303u;
@@ -198,13 +206,17 @@ __device__ __forceinline__ void eval_small(const EvalParams& P, const EvalShared
   // Eq.6: per-node intra ring over nodes with >= 2 stage-1 members (value table
   // vin[e][a*16 + c] = qi(c) R[a][a], 0 for c < 2), slowest inter link
   const double* vin = P.vin + (size_t)e * 256;
+  // only nodes with c >= 2 members contribute (a nibble with bit 1, 2 or 3 set)
   double t_in = 0.0;
-  uint32_t bits = mask;
-  while (bits) {
-    const uint32_t a = __ffs(bits) - 1;
-    bits &= bits - 1;
-    const uint32_t c = (uint32_t)(c64 >> (4u * a)) & 15u;
-    t_in = fmax(t_in, __ldg(vin + a * 16 + c));
+#pragma unroll
+  for (int hw = 0; hw < 2; ++hw) {
+    const uint32_t h = hw ? c_hi : c_lo;
+    uint32_t b = h & 0xeeeeeeeeu;
+    while (b) {
+      const uint32_t sh = (uint32_t)(__ffs(b) - 1) & ~3u;
+      b &= ~(15u << sh);
+      t_in = fmax(t_in, __ldg(vin + (hw * 8 + (sh >> 2)) * 16 + ((h >> sh) & 15u)));
+    }
   }
   const int k = __popc(mask);
   const double t_ex = k >= 2 ? __dmul_rn(__ldg(P.qtab + C.qe_off + k), __ldg(P.subset_max + mask)) : 0.0;
@@ -322,8 +334,20 @@ __device__ __forceinline__ void gather_rows(const EvalParams& P, unsigned char* 
   asm volatile("cp.async.commit_group;\n" ::: "memory");
 }
 
+// The same for 32 consecutive candidates (a tile of one configuration): their rows are one
+// contiguous range of rows * rb bytes, so piece pc sits at byte pc * 16 on both sides.
+__device__ __forceinline__ void gather_contig(const EvalParams& P, unsigned char* wbuf, long long first, int rows,
+                                              uint32_t rb, int lane) {
+  const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(wbuf);
+  const unsigned char* src = reinterpret_cast<const unsigned char*>(P.perm) + (size_t)first * rb;
+  const uint32_t bytes = (uint32_t)rows * rb;
+  for (uint32_t b = (uint32_t)lane * 16u; b < bytes; b += 512u)
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sbase + swz(b)), "l"(src + b) : "memory");
+  asm volatile("cp.async.commit_group;\n" ::: "memory");
+}
+
 template <int MODE>
-__global__ void __launch_bounds__(kEvalThreads) k_eval_stream(EvalParams P) {
+__global__ void __launch_bounds__(kEvalThreads, 4) k_eval_stream(EvalParams P) {
   constexpr bool REP = MODE == 0;
   extern __shared__ __align__(128) unsigned char smem[];
   const int n = P.n_nodes, nn = n * n;
@@ -336,7 +360,9 @@ __global__ void __launch_bounds__(kEvalThreads) k_eval_stream(EvalParams P) {
   unsigned char* wbuf = smem + (size_t)wid * wb_bytes;
   size_t off = (size_t)nwarps * wb_bytes;
   double* Rs = reinterpret_cast<double*>(smem + off);
-  off += (size_t)(REP ? nn * 16 : nn) * 8;
+  const uint32_t lgn = n <= 1 ? 0u : 32u - __clz(n - 1);   // MODE 0 padded side 2^lgn >= n
+  const int np = 1 << lgn;
+  off += (size_t)(REP ? np * np * 16 : nn) * 8;
   unsigned long long* keys = reinterpret_cast<unsigned long long*>(smem + off);
   off += ((size_t)P.E * 8 + 15) & ~(size_t)15;
   uint32_t* bm = reinterpret_cast<uint32_t*>(smem + off);
@@ -347,31 +373,43 @@ __global__ void __launch_bounds__(kEvalThreads) k_eval_stream(EvalParams P) {
   __shared__ int sh_scan[32];
 
   if (REP) {
-    for (int i = tid; i < nn * 16; i += kEvalThreads) Rs[i] = P.R[i >> 4];
+    for (int i = tid; i < np * np * 16; i += kEvalThreads) {
+      const int a = i >> (4 + lgn), b = (i >> 4) & (np - 1);
+      Rs[i] = (a < n && b < n) ? P.R[a * n + b] : 0.0;
+    }
   } else {
     for (int i = tid; i < nn; i += kEvalThreads) Rs[i] = P.R[i];
   }
   for (int i = tid; i < P.E; i += kEvalThreads) keys[i] = P.keys[i];
   __syncthreads();
-  const EvalShared S{Rs, bm, bm + P.bm_words * kEvalThreads, n, tid, lane, kEvalThreads};
+  const EvalShared S{Rs, bm, bm + P.bm_words * kEvalThreads, n, tid, lane, kEvalThreads, lgn,
+                     reinterpret_cast<const unsigned char*>(Rs + (lane & 15)), (uint32_t)np * 128u};
   const double qnan = __longlong_as_double(0x7ff8000000000000ll);
   const bool bucket_ok = true;   // (E < 32767 is checked by the host)
+  unsigned long long last_raw = ~0ull;   // (pp = 0xffff is never a valid record)
+  int last_e = -1;
 
   for (long long base = (long long)blockIdx.x * kEvalTile; base < P.n; base += (long long)gridDim.x * kEvalTile) {
     const int cnt_valid = (int)min((long long)kEvalTile, P.n - base);
     // configuration lookup (Alg.1 l.3-5 membership) of every candidate of the tile
+    // (a thread's previous candidate usually has the same configuration: the binary search
+    // runs only when the raw 8-byte record changes)
     bool mixed = false;
     for (int k = tid; k < cnt_valid; k += kEvalThreads) {
-      const pipette_config cf = P.cand[base + k];
-      const unsigned long long key = ((unsigned long long)cf.pp << 48) | ((unsigned long long)cf.tp << 32) |
-                                     ((unsigned long long)cf.dp << 16) | (unsigned long long)cf.mb;
-      int lo = 0, hi = P.E;   // first index with keys[idx] >= key
-      while (lo < hi) {
-        const int mid = (lo + hi) >> 1;
-        if (keys[mid] < key) lo = mid + 1; else hi = mid;
+      const unsigned long long raw = __ldg(reinterpret_cast<const unsigned long long*>(P.cand) + base + k);
+      if (raw != last_raw) {
+        const pipette_config cf = *reinterpret_cast<const pipette_config*>(&raw);
+        const unsigned long long key = ((unsigned long long)cf.pp << 48) | ((unsigned long long)cf.tp << 32) |
+                                       ((unsigned long long)cf.dp << 16) | (unsigned long long)cf.mb;
+        int lo = 0, hi = P.E;   // first index with keys[idx] >= key
+        while (lo < hi) {
+          const int mid = (lo + hi) >> 1;
+          if (keys[mid] < key) lo = mid + 1; else hi = mid;
+        }
+        last_e = (lo >= P.E || keys[lo] != key) ? -1 : lo;   // -1: not in the enumeration
+        last_raw = raw;
       }
-      const int e = (lo >= P.E || keys[lo] != key) ? -1 : lo;   // -1: not in the enumeration
-      tile_e[k] = (short)e;
+      tile_e[k] = (short)last_e;
     }
     __syncthreads();
     for (int k = tid; k < cnt_valid; k += kEvalThreads) mixed |= tile_e[k] != tile_e[0];
@@ -407,7 +445,8 @@ __global__ void __launch_bounds__(kEvalThreads) k_eval_stream(EvalParams P) {
     for (int g = wid; g < groups; g += nwarps) {
       unsigned char* cur = wbuf;
       if (staged) {   // (one buffer per warp: the other resident warps hide the gather)
-        gather_rows(P, wbuf, order + g * 32, base, rb, lane);
+        if (mixed) gather_rows(P, wbuf, order + g * 32, base, rb, lane);
+        else gather_contig(P, wbuf, base + (long long)g * 32, min(32, cnt_valid - g * 32), rb, lane);
         asm volatile("cp.async.wait_group 0;\n" ::: "memory");
         __syncwarp();
       }
@@ -450,7 +489,9 @@ int eval_tile_size() { return kEvalTile; }
 size_t eval_smem_bytes(int mode, int perm_stride, bool staged, int n_nodes, int E, int bm_words) {
   const size_t nn = (size_t)n_nodes * n_nodes;
   const size_t wb = staged ? (size_t)32 * perm_stride * 2 : 0;
-  return (size_t)(kEvalThreads / 32) * wb + (mode == 0 ? nn * 16 : nn) * 8 + (((size_t)E * 8 + 15) & ~(size_t)15) +
+  size_t np = 1;
+  while (np < (size_t)n_nodes) np <<= 1;
+  return (size_t)(kEvalThreads / 32) * wb + (mode == 0 ? np * np * 16 : nn) * 8 + (((size_t)E * 8 + 15) & ~(size_t)15) +
          (size_t)(bm_words + (n_nodes + 3) / 4) * kEvalThreads * 4 + (size_t)kEvalTile * sizeof(short) +
          (size_t)((E + 2 + 3) & ~3) * sizeof(int) + (size_t)kEvalTile * sizeof(short);
 }

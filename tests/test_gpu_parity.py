@@ -135,6 +135,42 @@ def test_eval_stream_edge_cases():
     assert mem[3] == 0 and mem[1] == ref[(4, 2, 2, 1)].mem_bytes
 
 
+@pytest.mark.parametrize("name,n_cand", [("C1", 4099), ("C2", 6001), ("C3", 5003), ("C4", 2085)])
+def test_eval_stream_homogeneous_tiles(name, n_cand):
+    """Batches of ONE configuration (the bench's homogeneous stream): whole tiles of one
+    config take the contiguous staging path.  Invalid rows (duplicates, ids >= N, 0xffff)
+    sit inside those tiles; the batch ends in a ragged tail.  Every latency is compared."""
+    w = W.WORKLOADS[name]
+    pip, B, prof = _ctx(w)
+    model, mo, cl = _models(w)
+    P = O.make_profile(prof)
+    R = O.inverse_bandwidth(B)
+    feas = [c for c in O.enumerate_configs(cl, mo, w.bs_global, P) if c.feasible]
+    for c in (max(feas, key=lambda c: (c.pp * c.dp, -c.e)), feas[len(feas) // 2]):
+        K = O.constants(cl, mo, c, P)
+        stride = ((K.N + 7) // 8) * 8
+        rng = np.random.default_rng(K.N * 7 + n_cand)
+        ps = W.random_perms(K.N, n_cand, int(rng.integers(1 << 30)))
+        rows = np.zeros((n_cand, stride), dtype=np.uint16)
+        rows[:, :K.N] = ps
+        bad = rng.choice(n_cand, size=min(60, n_cand // 20), replace=False)
+        for j, i in enumerate(bad):
+            if K.N < 2:
+                rows[i, 0] = [1, 0xFFFF, K.N][j % 3]
+                continue
+            a, b = rng.choice(K.N, size=2, replace=False)
+            rows[i, a] = [rows[i, b], K.N, 0xFFFF, min(K.N + 64, 0xFFFF)][j % 4]
+        lat, mem, st = _eval_batch(pip, model, w.bs_global, [(c.pp, c.tp, c.dp, c.mb)] * n_cand, rows)
+        want_st = np.full(n_cand, 0 if c.feasible else 1)
+        want_st[bad] = 3
+        assert st.tolist() == want_st.tolist()
+        assert np.all(mem == c.mem_bytes)
+        ok = want_st != 3
+        assert np.all(np.isnan(lat[~ok]))
+        want = [O.latency(K, R, rows[i, :K.N]).T for i in np.flatnonzero(ok)]
+        assert _assert_close(lat[ok], want) == 0
+
+
 def test_eval_single_gpu_cluster_and_empty_batch():
     import torch
     from paper_2405_18093_b200 import Model, Pipette
