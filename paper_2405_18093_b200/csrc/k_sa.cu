@@ -161,7 +161,10 @@ struct S1Reg {
     m = __vminu4(m, m >> 8) & 0xffu;
     return m == 0xffu ? 0.0 : X.vs[m];
   }
+  // NW = 2: X.tab is the block's table of the whole term, tab[m] = fl(qe(|m|) * maxR(m))
+  // (0 for |m| < 2), so T_ex is one load
   __device__ __forceinline__ double tex_of(uint32_t m, int kk, const S1Ctx& X) const {
+    if constexpr (NW == 2) return X.tab[m];
     return kk >= 2 ? __dmul_rn(X.qe[kk], X.tab[m]) : 0.0;
   }
   __device__ __forceinline__ void clear() { cnt = 0; mask = 0u; }
@@ -891,8 +894,13 @@ __device__ __forceinline__ void run_task_hc(const SaParams& P, const SaTask T, c
         *sq_ = (uint8_t)sp;
         ++accepted;
       }
-      if (improved)
-        for (int w = 0; w < N; ++w) bperm[w * 32 + lane] = (uint16_t)st.sb[HcState::off((uint32_t)w)];
+      // best-mapping copy, warp-cooperative (the warp is converged here): the lanes copy
+      // the slot plane of each improved lane together, 32 positions per instruction
+      for (uint32_t imp = __ballot_sync(0xffffffffu, improved); imp; imp &= imp - 1u) {
+        const int L = __ffs(imp) - 1;
+        const uint8_t* sbL = ws + plane + L * 4;
+        for (int w = lane; w < N; w += 32) bperm[w * 32 + L] = (uint16_t)sbL[HcState::off((uint32_t)w)];
+      }
       if (TRACE && trow >= 0 && i < P.trace_cap) {
         pipette_trace_record rec;
         rec.i = (uint32_t)i; rec.p = (uint16_t)d.p; rec.q = (uint16_t)d.q;
@@ -1163,8 +1171,11 @@ __device__ __forceinline__ void run_task_sb(const SaParams& P, const SaTask T, c
         *bq = (uint8_t)sp;
       }
       if (acc) ++accepted;
-      if (improved)
-        for (int w = 0; w < N; ++w) bperm[w * 32 + lane] = (uint16_t)st.hb[HcState::off((uint32_t)w)];
+      for (uint32_t imp = __ballot_sync(0xffffffffu, improved); imp; imp &= imp - 1u) {   // (as in MODE 0)
+        const int L = __ffs(imp) - 1;
+        const uint8_t* sbL = ws + L * 4;
+        for (int w = lane; w < N; w += 32) bperm[w * 32 + L] = (uint16_t)sbL[HcState::off((uint32_t)w)];
+      }
       if (TRACE && trow >= 0 && i < P.trace_cap) {
         pipette_trace_record rec;
         rec.i = (uint32_t)i; rec.p = (uint16_t)d.p; rec.q = (uint16_t)d.q;
@@ -1495,7 +1506,10 @@ __global__ void __launch_bounds__(SaLB<MODE, BIG>::threads, SaLB<MODE, BIG>::blo
             s1_vs[i] = P.tin_vs[(size_t)f0 * 256 + i];
           }
           for (int i = threadIdx.x; i < 32; i += blockDim.x) s1_qe[i] = i <= min(C0.dp, n) ? P.qtab[C0.qe_off + i] : 0.0;
-          for (int i = threadIdx.x; i < (1 << n); i += blockDim.x) s1_tab[i] = P.subset_max[i];
+          for (int i = threadIdx.x; i < (1 << n); i += blockDim.x) {
+            const int k = __popc(i);
+            s1_tab[i] = (k >= 2 && k <= min(C0.dp, n)) ? __dmul_rn(P.qtab[C0.qe_off + k], P.subset_max[i]) : 0.0;
+          }
           }
         } else {
           for (int i = threadIdx.x; i < nn; i += blockDim.x) Rs[i] = __dmul_rn(m2, P.R[i]);
