@@ -329,7 +329,7 @@ pipette_status build_plan(pipette_ctx* ctx, int chains, int W, int r, const char
   // per half-warp, so 16 copies make every lookup conflict free); MODE 1: the block's
   // n x n m2*R table (one copy; above 32 KB the block has 8 warps to share it)
   // (+ MODE 0's shared stage-1 tables: vs 256, qe 32 and tab 256 doubles, rank 256 bytes)
-  const int r_bytes = mode == 0 ? 256 * 16 * 8 + (n <= 8 ? (256 + 32 + 256) * 8 + 256 : 0)
+  const int r_bytes = mode == 0 ? (n <= 8 ? kSaCodesN8 : 256) * 16 * 8 + (n <= 8 ? (256 + 32 + 256) * 8 + 256 : 0)
                                 : (mode == 1 ? align16(nn * 8) : 0);
   const bool big = mode == 1 && r_bytes > 32 * 1024;
   if (mode == 2 && full_moves)
@@ -347,7 +347,7 @@ pipette_status build_plan(pipette_ctx* ctx, int chains, int W, int r, const char
     }
     return wb;
   };
-  const int reg_blocks = mode == 0 ? 3 : (mode == 1 ? (big ? 1 : 3) : 2);   // the kernels' __launch_bounds__
+  const int reg_blocks = mode == 0 ? (n <= 8 ? kSaBlocksN8 : 3) : (mode == 1 ? (big ? 1 : 3) : 2);   // __launch_bounds__
   auto blocks_for = [&](int wb) {
     return std::min(reg_blocks, (227 * 1024) / std::max(1, r_bytes + (threads / 32) * wb));
   };

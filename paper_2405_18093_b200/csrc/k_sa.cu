@@ -297,6 +297,10 @@ struct S1Large {
     }
     return -1;
   }
+  // PAIRS: the witness recompute for small k splits the member PAIRS over the lanes (the
+  // BIG kernel, where R comes from L2 and a serial per-lane scan is latency-bound);
+  // otherwise the member ROWS are split (fewer registers: the small-table kernel spills)
+  template <bool PAIRS = false>
   __device__ __forceinline__ void coop(const S1Ctx& X, const RT& R) {
     const unsigned full = 0xffffffffu;
     // T_in: first (a, c) entry (by value) whose node has c members after the move
@@ -346,7 +350,7 @@ struct S1Large {
       const int kL = __shfl_sync(full, k2, L);
       double mx = 0.0;
       int a_ = -1, b_ = -1;
-      if (kL * kL * kL * kL <= 4 * X.n * X.n) {
+      if (!PAIRS && kL * kL * kL * kL <= 4 * X.n * X.n) {
         // member rows split over the lanes: lane j takes nodes j, j+32, ... in N1
         for (int a = lane; a < X.n; a += 32) {
           if (!in(m, (uint32_t)a)) continue;
@@ -361,6 +365,42 @@ struct S1Large {
               if (v > mx) { mx = v; a_ = a; b_ = b; }
             }
           }
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {   // max-reduce (any witness of an equal max is fine)
+          const double v2 = __shfl_xor_sync(full, mx, o);
+          const int a2 = __shfl_xor_sync(full, a_, o), b2 = __shfl_xor_sync(full, b_, o);
+          if (v2 > mx) { mx = v2; a_ = a2; b_ = b2; }
+        }
+      } else if (PAIRS && kL * kL * kL * kL <= 4 * X.n * X.n) {
+        // the k^2 ordered member pairs split over the lanes (k <= 16 here): lane i holds
+        // the i-th member node, pair j = (j / k, j % k) is fetched by shuffles, and the R
+        // loads of four pairs per lane are in flight together (independent, unrolled)
+        uint32_t memv = 0u;
+        {
+          const uint32_t c0 = __popc(m.w0), c1 = c0 + __popc(m.w1), c2 = c1 + __popc(m.w2);
+          const uint32_t i = (uint32_t)lane;
+          const uint32_t wd = i < c0 ? 0u : (i < c1 ? 1u : (i < c2 ? 2u : 3u));
+          const uint32_t r = i - (wd == 0u ? 0u : (wd == 1u ? c0 : (wd == 2u ? c1 : c2)));
+          const uint32_t bits = m.word((int)wd);
+          if (i < (uint32_t)kL) memv = wd * 32u + (uint32_t)__fns(bits, 0u, (int)r + 1);
+        }
+        const uint32_t kk = (uint32_t)kL, npair = kk * kk;
+        const uint32_t mg = (uint32_t)((0x100000000ull + kk - 1u) / kk);   // j / k = umulhi(j, mg), j < 2^16
+        for (uint32_t base = 0; base < npair; base += 128u) {
+          double v[4];
+          uint32_t ja[4], jb[4];
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const uint32_t j = base + (uint32_t)u * 32u + (uint32_t)lane;
+            const uint32_t ia = __umulhi(j, mg), ib = j - ia * kk;
+            ja[u] = __shfl_sync(full, memv, (int)(ia & 31u));
+            jb[u] = __shfl_sync(full, memv, (int)(ib & 31u));
+            v[u] = (j < npair && ia != ib) ? R(ja[u], jb[u]) : 0.0;
+          }
+#pragma unroll
+          for (int u = 0; u < 4; ++u)
+            if (v[u] > mx) { mx = v[u]; a_ = (int)ja[u]; b_ = (int)jb[u]; }
         }
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) {   // max-reduce (any witness of an equal max is fine)
@@ -1024,7 +1064,7 @@ __host__ __device__ inline int sb_warp_state_bytes(int N, int pp, int dp, int n,
 }
 
 // One warp task of MODE 1 (same step structure as run_task_hc).
-template <bool TRACE, int PP>
+template <bool TRACE, int PP, bool BIG>
 __device__ __forceinline__ void run_task_sb(const SaParams& P, const SaTask T, const DevCfg C, const double* Tt,
                                             unsigned char* ws, int lane) {
   const bool active = lane < T.count;
@@ -1140,7 +1180,7 @@ __device__ __forceinline__ void run_task_sb(const SaParams& P, const SaTask T, c
           const uint32_t up = xp == 0u ? nq : np;
           s1.propose(dn, up, X, Rg);
         }
-        s1.coop(X, Rg);   // converged: all lanes' flagged searches
+        s1.template coop<BIG>(X, Rg);   // converged: all lanes' flagged searches
         double tin2 = s1.tin, tex2 = s1.tex;
         if (dpchg) {
           s1.finish(X);
@@ -1425,16 +1465,17 @@ __device__ __forceinline__ void run_task_full(const SaParams& P, const SaTask T,
 // MODE 2: general (N <= 1024): 32-bit positions, S1Large, R through L1.
 // launch bounds per mode: MODE 0 4 warps x 3 blocks; MODE 1 4 warps x 3 blocks (small
 // table) or 8 warps x 1 block (BIG: a table of up to 128 KB shared by more warps); MODE 2.
-template <int MODE, bool BIG>
+// MODE 0 with n <= 8 (NW = 2): the m2*R table has 120 codes (15 KB), so 4 blocks fit.
+template <int MODE, bool BIG, int NW = 4>
 struct SaLB {
   static constexpr int threads = (MODE == 1 && BIG) ? 256 : 128;
-  static constexpr int blocks = MODE == 0 ? 3 : (MODE == 1 ? (BIG ? 1 : 3) : 2);
+  static constexpr int blocks = MODE == 0 ? (NW == 2 ? kSaBlocksN8 : 3) : (MODE == 1 ? (BIG ? 1 : 3) : 2);
 };
 
 // FULL: the full move set (run_task_full) -- a separate instantiation, so the swap kernel's
 // instruction footprint stays small (its cold start after an L2 flush refetches the code).
 template <int MODE, bool TRACE, int NW = 4, bool BIG = false, bool FULL = false>
-__global__ void __launch_bounds__(SaLB<MODE, BIG>::threads, SaLB<MODE, BIG>::blocks) k_sa_chains(SaParams P) {
+__global__ void __launch_bounds__(SaLB<MODE, BIG, NW>::threads, SaLB<MODE, BIG, NW>::blocks) k_sa_chains(SaParams P) {
   using POS = PosWide;
   using RT = RGlob;
   using S1 = S1Large<RT>;
@@ -1445,7 +1486,8 @@ __global__ void __launch_bounds__(SaLB<MODE, BIG>::threads, SaLB<MODE, BIG>::blo
   RT R{P.R, n, lane};
   const double* Tl = Rs + (lane & 15);   // MODE 0: this lane's copy of the block's m2*R table
   // MODE 0: the block's stage-1 tables after the m2*R table (kS1SharedBytes)
-  double* s1_vs = Rs + 256 * 16;
+  constexpr int kCodes = NW == 2 ? kSaCodesN8 : 256;   // hop codes a | b << 4 in the table
+  double* s1_vs = Rs + kCodes * 16;
   double* s1_qe = s1_vs + 256;
   double* s1_tab = s1_qe + 32;
   uint8_t* s1_rank = reinterpret_cast<uint8_t*>(s1_tab + 256);
@@ -1493,7 +1535,7 @@ __global__ void __launch_bounds__(SaLB<MODE, BIG>::threads, SaLB<MODE, BIG>::blo
       if (cfg0 != table_cfg) {   // block-uniform: rebuild the table for this configuration
         const double m2 = P.cfgs[cfg0].m2;
         if constexpr (MODE == 0) {
-          for (int i = threadIdx.x; i < 256 * 16; i += blockDim.x) {
+          for (int i = threadIdx.x; i < kCodes * 16; i += blockDim.x) {
             const int code = i >> 4, a = code & 15, b = code >> 4;
             Rs[i] = (a < n && b < n) ? __dmul_rn(m2, P.R[a * n + b]) : 0.0;
           }
@@ -1543,13 +1585,13 @@ __global__ void __launch_bounds__(SaLB<MODE, BIG>::threads, SaLB<MODE, BIG>::blo
       }
     } else if constexpr (MODE == 1) {
       switch (C.pp) {
-        case 1: run_task_sb<TRACE, 1>(P, T, C, Rs, ws, lane); break;
-        case 2: run_task_sb<TRACE, 2>(P, T, C, Rs, ws, lane); break;
-        case 4: run_task_sb<TRACE, 4>(P, T, C, Rs, ws, lane); break;
-        case 8: run_task_sb<TRACE, 8>(P, T, C, Rs, ws, lane); break;
-        case 16: run_task_sb<TRACE, 16>(P, T, C, Rs, ws, lane); break;
-        case 32: run_task_sb<TRACE, 32>(P, T, C, Rs, ws, lane); break;
-        default: run_task_sb<TRACE, 0>(P, T, C, Rs, ws, lane); break;
+        case 1: run_task_sb<TRACE, 1, BIG>(P, T, C, Rs, ws, lane); break;
+        case 2: run_task_sb<TRACE, 2, BIG>(P, T, C, Rs, ws, lane); break;
+        case 4: run_task_sb<TRACE, 4, BIG>(P, T, C, Rs, ws, lane); break;
+        case 8: run_task_sb<TRACE, 8, BIG>(P, T, C, Rs, ws, lane); break;
+        case 16: run_task_sb<TRACE, 16, BIG>(P, T, C, Rs, ws, lane); break;
+        case 32: run_task_sb<TRACE, 32, BIG>(P, T, C, Rs, ws, lane); break;
+        default: run_task_sb<TRACE, 0, BIG>(P, T, C, Rs, ws, lane); break;
       }
     } else {
       switch (C.pp) {

@@ -14,6 +14,11 @@ constexpr int kMaxGpus = 1024;      // v1 limit (G); N = G/tp <= 1024 slots
 // One enumerated configuration (Alg.1 l.3-5) with its memory verdict (l.7) and the
 // per-config model constants of DESIGN.md section 3.  Built on the device by
 // k_enumerate_filter; read by k_eval_stream and k_sa_chains.
+// K3 MODE 0 with n <= 8 nodes: hop codes a | b << 4 stay below 0x78, so the block's m2*R
+// table has kSaCodesN8 codes (x 16 lane copies x 8 B = 15 KB instead of 32 KB).
+constexpr int kSaCodesN8 = 120;
+constexpr int kSaBlocksN8 = 3;   // (4 blocks = 128 registers: spills, measured 30% slower on C2)
+
 struct DevCfg {
   int32_t pp, tp, dp, mb;
   int32_t n_mb, e, N, spn;
