@@ -300,6 +300,29 @@ struct S1Large {
   // PAIRS: the witness recompute for small k splits the member PAIRS over the lanes (the
   // BIG kernel, where R comes from L2 and a serial per-lane scan is latency-bound);
   // otherwise the member ROWS are split (fewer registers: the small-table kernel spills)
+  // The same, also returning the hit entry's value and key: every probe loads its value
+  // beside its key, and the hit lane's pair is shuffled out (no dependent round trip to L2
+  // after the search).  hit(i, key) sets the key it read.
+  template <class F, class G>
+  static __device__ __forceinline__ int coop_first_v(int len, F hit, G val, double& v_out, uint32_t& key_out) {
+    const int ln = threadIdx.x & 31;
+    for (int base = 0; base < len; base += 32) {
+      const int i = base + ln;
+      const bool ok = i < len;
+      const double v = ok ? val(i) : 0.0;
+      uint32_t key = 0u;
+      const unsigned b = __ballot_sync(0xffffffffu, ok && hit(i, key));
+      if (b) {
+        const int f = __ffs(b) - 1;
+        v_out = __shfl_sync(0xffffffffu, v, f);
+        key_out = __shfl_sync(0xffffffffu, key, f);
+        return base + f;
+      }
+    }
+    v_out = 0.0;
+    key_out = 0u;
+    return -1;
+  }
   template <bool PAIRS = false>
   __device__ __forceinline__ void coop(const S1Ctx& X, const RT& R) {
     const unsigned full = 0xffffffffu;
@@ -310,14 +333,17 @@ struct S1Large {
       todo &= todo - 1;
       const uint32_t dnL = __shfl_sync(full, dn_, L), upL = __shfl_sync(full, up_, L);
       const uint32_t cdL = __shfl_sync(full, c_dn_, L), cuL = __shfl_sync(full, c_up_, L);
-      const int i = coop_first(X.tl_len, [&](int j) {
-        const uint32_t ac = X.tl_ac[j], a = ac & 0xffu;
+      double v;
+      uint32_t acv;
+      const int i = coop_first_v(X.tl_len, [&](int j, uint32_t& ac) {
+        ac = X.tl_ac[j];
+        const uint32_t a = ac & 0xffu;
         const uint32_t cnt = a == dnL ? cdL : (a == upL ? cuL : get_of(a, L));
         return cnt == (ac >> 8);
-      });
+      }, [&](int j) { return X.tl_val[j]; }, v, acv);
       if (lane == L) {
         need_tin = false;
-        if (i >= 0) { tin2 = X.tl_val[i]; win2 = (int)(X.tl_ac[i] & 0xffu); } else { tin2 = 0.0; win2 = -1; }
+        if (i >= 0) { tin2 = v; win2 = (int)(acv & 0xffu); } else { tin2 = 0.0; win2 = -1; }
       }
     }
     // T_ex, join: first partner (by R) of the joining node inside N1
@@ -330,13 +356,14 @@ struct S1Large {
       m.w0 = __shfl_sync(full, mask2.w0, L); m.w1 = __shfl_sync(full, mask2.w1, L);
       m.w2 = __shfl_sync(full, mask2.w2, L); m.w3 = __shfl_sync(full, mask2.w3, L);
       const uint8_t* nl = X.nl_node + (size_t)upL * X.nl_len;
-      const int i = coop_first(X.nl_len, [&](int j) { return in(m, nl[j]); });
+      const double* nv = X.nl_val + (size_t)upL * X.nl_len;
+      double v;
+      uint32_t bn;
+      const int i = coop_first_v(X.nl_len, [&](int j, uint32_t& b) { b = nl[j]; return in(m, b); },
+                                 [&](int j) { return nv[j]; }, v, bn);
       if (lane == L) {
         need_join = false;
-        if (i >= 0) {
-          const double v = X.nl_val[(size_t)upL * X.nl_len + i];
-          if (v > maxR2) { maxR2 = v; wa2 = (int)upL; wb2 = (int)nl[i]; }
-        }
+        if (i >= 0 && v > maxR2) { maxR2 = v; wa2 = (int)upL; wb2 = (int)bn; }
       }
     }
     // T_ex, the witness left: recompute the slowest link of N1
@@ -409,11 +436,13 @@ struct S1Large {
           if (v2 > mx) { mx = v2; a_ = a2; b_ = b2; }
         }
       } else {
-        const int i = coop_first(X.gl_len, [&](int j) {
-          const uint32_t ab = X.gl_ab[j];
+        uint32_t abv;
+        double v;
+        const int i = coop_first_v(X.gl_len, [&](int j, uint32_t& ab) {
+          ab = X.gl_ab[j];
           return in(m, ab & 0xffu) && in(m, ab >> 8);
-        });
-        if (i >= 0) { mx = X.gl_val[i]; a_ = X.gl_ab[i] & 0xff; b_ = X.gl_ab[i] >> 8; }
+        }, [&](int j) { return X.gl_val[j]; }, v, abv);
+        if (i >= 0) { mx = v; a_ = (int)(abv & 0xffu); b_ = (int)(abv >> 8); }
       }
       if (lane == L) { need_maxr = false; maxR2 = mx; wa2 = a_; wb2 = b_; }
     }
@@ -967,9 +996,10 @@ struct SbCtx {
   const double* T;   // block table, n x n
   int n;
   uint32_t spn, spn_magic, spn_sh;   // spn_sh < 32: spn is a power of two
-  __device__ __forceinline__ uint32_t node(uint32_t slot) const {
-    return spn_sh < 32u ? slot >> spn_sh : div_small(slot, spn_magic, spn);
-  }
+  uint32_t m16;                      // ceil(2^16 / spn)
+  // node = floor(slot / spn) as (slot * m16) >> 16: exact for slot < 256 and spn < 256
+  // (the error slot * (m16 - 2^16/spn) / 2^16 < 1/256 never crosses an integer)
+  __device__ __forceinline__ uint32_t node(uint32_t slot) const { return (slot * m16) >> 16; }
 };
 
 template <int PP>
@@ -1081,6 +1111,7 @@ __device__ __forceinline__ void run_task_sb(const SaParams& P, const SaTask T, c
   SbCtx K;
   K.T = Tt; K.n = n; K.spn = (uint32_t)C.spn; K.spn_magic = C.spn_magic;
   K.spn_sh = (C.spn & (C.spn - 1)) == 0 ? (uint32_t)(31 - __clz(C.spn)) : 32u;
+  K.m16 = (uint32_t)((65536u + (uint32_t)C.spn - 1u) / (uint32_t)C.spn);
 
   const bool cache = pp >= 4 && dp <= P.psum_dp_cap;
   const int plane = align16(((N + 3) / 4) * 128);
@@ -1401,6 +1432,7 @@ __device__ __forceinline__ void run_task_full(const SaParams& P, const SaTask T,
   SbCtx K;
   K.T = MODE == 0 ? Tt + (lane & 15) : Tt; K.n = n; K.spn = (uint32_t)C.spn; K.spn_magic = C.spn_magic;
   K.spn_sh = (C.spn & (C.spn - 1)) == 0 ? (uint32_t)(31 - __clz(C.spn)) : 32u;
+  K.m16 = (uint32_t)((65536u + (uint32_t)C.spn - 1u) / (uint32_t)C.spn);
   const int plane = align16(((N + 3) / 4) * 128);
   // MODE 0 layout: [hop-code plane (unused)][slot plane]; MODE 1: [slot plane][counts]
   unsigned char* splane = MODE == 0 ? ws + plane : ws;
