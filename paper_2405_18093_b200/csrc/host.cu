@@ -32,7 +32,7 @@ pipette_status models_launch(const DevCfg* cfgs, const unsigned long long* keys,
 size_t eval_smem_bytes(int mode, int perm_stride, bool staged, int n_nodes, int E, int bm_words);
 __global__ void k_tin_values(const DevCfg*, const double*, const double*, int, double*);
 const void* sa_kernel(int mode, bool trace, int n_nodes, bool full);
-int sa_warp_state_bytes(int mode, int N, int pp, int dp, int n, int dp_cap);
+int sa_warp_state_bytes(int mode, int N, int pp, int dp, int n, int dp_cap, bool nib);
 __global__ void k_node_lists(const double*, int, uint8_t*, double*);
 __global__ void k_pair_list(const double*, int, uint16_t*, double*);
 __global__ void k_tin_list(const DevCfg*, const int*, const double*, const double*, int, int, uint16_t*, double*, int*);
@@ -114,7 +114,7 @@ struct HostPlan {
   std::vector<int2> chunks;
   std::vector<int> cfg_slot, slot_perm_off, slot_lane;
   int slots = 0, perm_words = 0, maxN = 1, mode = 0, r_bytes = 0, dp_cap = 0, warp_bytes = 16, tl_stride = 1, wpb = 1;
-  bool big = false;
+  bool big = false, nib = false;
   size_t smem = 0;
 };
 
@@ -337,12 +337,20 @@ pipette_status build_plan(pipette_ctx* ctx, int chains, int W, int r, const char
   const int threads = big ? 256 : kSaThreads;
   // psum (Eq.5 sums) cached in shared memory for configs with dp <= dp_cap: the largest cap
   // that still reaches the best achievable number of resident blocks per SM
+  // MODE 1 swap kernels keep the stage-1 counts as nibbles when no count can exceed 15
+  // (c_n <= min(spn, dp)): half the count plane, so the psum cache fits beside the 128 KB
+  // table at n = 128
+  bool nib = mode == 1 && !full_moves;
+  for (int f = 0; f < F; ++f) {
+    const DevCfg& c = ctx->hcfg[ctx->hfeas[f]];
+    nib = nib && std::min(c.spn, c.dp) <= 15;
+  }
   auto warp_bytes_for = [&](int cap, int& tls) {
     int wb = 16;
     tls = 1;
     for (int f = 0; f < F; ++f) {
       const DevCfg& c = ctx->hcfg[ctx->hfeas[f]];
-      wb = std::max(wb, sa_warp_state_bytes(mode, c.N, c.pp, c.dp, n, cap));
+      wb = std::max(wb, sa_warp_state_bytes(mode, c.N, c.pp, c.dp, n, cap, nib));
       tls = std::max(tls, n * (std::min(c.spn, c.dp) - 1));
     }
     return wb;
@@ -378,7 +386,7 @@ pipette_status build_plan(pipette_ctx* ctx, int chains, int W, int r, const char
   }
 
   hp.slots = slots; hp.perm_words = perm_words; hp.maxN = maxN; hp.mode = mode; hp.r_bytes = r_bytes;
-  hp.big = big; hp.dp_cap = dp_cap; hp.warp_bytes = warp_bytes; hp.tl_stride = tl_stride; hp.wpb = wpb;
+  hp.big = big; hp.nib = nib; hp.dp_cap = dp_cap; hp.warp_bytes = warp_bytes; hp.tl_stride = tl_stride; hp.wpb = wpb;
   hp.smem = smem;
   (void)maxdp2;
   return PIPETTE_OK;
@@ -902,6 +910,7 @@ pipette_status pipette_search(pipette_ctx* ctx, const pipette_model* model, int6
   P.trace = tracing ? (pipette_trace_record*)ctx->trace.p : nullptr;
   P.w_migrate = o.w_migrate;
   P.w_reverse = o.w_reverse;
+  P.s1_nib = pl.nib ? 1 : 0;
 
   const void* kern = sa_kernel(big ? 3 : mode, tracing, n, o.w_migrate || o.w_reverse);
   CU(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));

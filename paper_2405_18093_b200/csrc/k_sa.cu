@@ -211,19 +211,25 @@ struct S1Reg {
 // splitting the member rows over the lanes (shuffle max-reduction).
 template <class RT>
 struct S1Large {
-  uint32_t* c;   // [ceil(n/4)][32] words
+  uint32_t* c;   // [ceil(n/4)][32] words of byte counts, or [ceil(n/8)][32] of nibbles
   int lane;
+  uint32_t lgw = 2u, bw = 8u, cm = 0xffu;   // log2 counts per word, bits per count, count mask
+  __device__ __forceinline__ void set_nibbles(bool nib) {   // (nibbles: every count <= 15)
+    lgw = nib ? 3u : 2u; bw = nib ? 4u : 8u; cm = nib ? 0xfu : 0xffu;
+  }
   Mask4 mask, mask2;
   int k, k2, win, win2, wa, wb, wa2, wb2;
   uint32_t dn_, up_, c_dn_, c_up_;
   bool need_tin, need_maxr, need_join;
   double tin, tex, maxR, tin2, tex2, maxR2;
 
-  __device__ __forceinline__ uint32_t get(uint32_t a) const { return (c[(a >> 2) * 32 + lane] >> ((a & 3) * 8)) & 0xffu; }
-  __device__ __forceinline__ uint32_t get_of(uint32_t a, int L) const { return (c[(a >> 2) * 32 + L] >> ((a & 3) * 8)) & 0xffu; }
+  __device__ __forceinline__ uint32_t get(uint32_t a) const { return get_of(a, lane); }
+  __device__ __forceinline__ uint32_t get_of(uint32_t a, int L) const {
+    return (c[(a >> lgw) * 32 + L] >> ((a & ((1u << lgw) - 1u)) * bw)) & cm;
+  }
   __device__ __forceinline__ void add(uint32_t a, int delta) {
-    uint32_t& w = c[(a >> 2) * 32 + lane];
-    const uint32_t sh = (a & 3) * 8;
+    uint32_t& w = c[(a >> lgw) * 32 + lane];
+    const uint32_t sh = (a & ((1u << lgw) - 1u)) * bw;
     w = delta > 0 ? w + (1u << sh) : w - (1u << sh);
   }
   static __device__ __forceinline__ bool in(const Mask4& m, uint32_t a) { return m.test(a); }
@@ -247,7 +253,7 @@ struct S1Large {
   }
 
   __device__ __forceinline__ void clear(int n) {
-    for (int wd = 0; wd < (n + 3) / 4; ++wd) c[wd * 32 + lane] = 0u;
+    for (int wd = 0; wd < ((n - 1) >> lgw) + 1; ++wd) c[wd * 32 + lane] = 0u;
     mask.clear();
   }
   __device__ __forceinline__ void add_init(uint32_t a) { add(a, +1); mask.set(a); }
@@ -1089,8 +1095,10 @@ __device__ __forceinline__ void sb_rescan(const HcState& st, int dp, int pp_rt, 
   cnt = (m0 == mx ? c0 : 0) + (m1 == mx ? c1 : 0);
 }
 
-__host__ __device__ inline int sb_warp_state_bytes(int N, int pp, int dp, int n, int dp_cap) {
-  return align16(((N + 3) / 4) * 128) + align16(((n + 3) / 4) * 128) + ((pp >= 4 && dp <= dp_cap) ? align16(dp * 256) : 0);
+// [slot plane][stage-1 counts: bytes, or nibbles when nib][psum]
+__host__ __device__ inline int sb_count_bytes(int n, bool nib) { return align16((nib ? (n + 7) / 8 : (n + 3) / 4) * 128); }
+__host__ __device__ inline int sb_warp_state_bytes(int N, int pp, int dp, int n, int dp_cap, bool nib) {
+  return align16(((N + 3) / 4) * 128) + sb_count_bytes(n, nib) + ((pp >= 4 && dp <= dp_cap) ? align16(dp * 256) : 0);
 }
 
 // One warp task of MODE 1 (same step structure as run_task_hc).
@@ -1126,7 +1134,8 @@ __device__ __forceinline__ void run_task_sb(const SaParams& P, const SaTask T, c
   const RGlob Rg{P.R, n, lane};
   s1.c = reinterpret_cast<uint32_t*>(ws + plane);
   s1.lane = lane;
-  double* psum = reinterpret_cast<double*>(ws + plane + align16(((n + 3) / 4) * 128));
+  s1.set_nibbles(P.s1_nib != 0);
+  double* psum = reinterpret_cast<double*>(ws + plane + sb_count_bytes(n, P.s1_nib != 0));
   uint16_t* bperm = P.best_perm + T.perm_off;
   s1.clear(n);
 
@@ -1820,9 +1829,9 @@ const void* sa_kernel(int mode, bool trace, int n_nodes, bool full) {
   return trace ? (const void*)k_sa_chains<2, true> : (const void*)k_sa_chains<2, false>;
 }
 
-int sa_warp_state_bytes(int mode, int N, int pp, int dp, int n, int dp_cap) {
+int sa_warp_state_bytes(int mode, int N, int pp, int dp, int n, int dp_cap, bool nib) {
   if (mode == 0) return hc_warp_state_bytes(N, pp, dp, dp_cap);
-  if (mode == 1 || mode == 3) return sb_warp_state_bytes(N, pp, dp, n, dp_cap);
+  if (mode == 1 || mode == 3) return sb_warp_state_bytes(N, pp, dp, n, dp_cap, nib);
   return warp_state_bytes<PosWide>(N, pp, dp, n, true, dp_cap);
 }
 

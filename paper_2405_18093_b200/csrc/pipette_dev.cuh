@@ -102,6 +102,7 @@ struct SaParams {
   int32_t trace_cap;
   pipette_trace_record* trace;
   int32_t w_migrate, w_reverse;   // full move set (R21); both 0: swap only
+  int32_t s1_nib;                 // MODE 1 swap kernels: stage-1 counts as nibbles (all <= 15)
 };
 
 struct EvalParams {
