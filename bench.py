@@ -124,6 +124,19 @@ def fp64_ops_per_step(pp: int, dp: int) -> int:
     return (4 * (pp - 1) if pp >= 2 and dp >= 2 else 2 * (pp - 1)) + 7
 
 
+INT_OPS_PER_STEP = 60   # Philox4x32-10 (10 x (2 IMAD.WIDE + 2 LOP3)) 40 + draw 8 + stage/pipeline of p, q and 4 hop codes 12
+
+
+def smem_bytes_per_step(pp: int, dp: int) -> int:
+    """Algorithmic shared-memory bytes of one SA proposal: the slot and hop-code
+    bytes of p and q read and written (12), the m2*R term of every hop of the re-summed
+    pipelines (8 B each), and the two cached pipeline sums read and written (32, pp >= 4)."""
+    if pp < 2:
+        return 4
+    a = 2 if dp >= 2 else 1
+    return 12 + 8 * a * (pp - 1) + (32 if pp >= 4 else 0)
+
+
 def setup(name: str):
     w = W.WORKLOADS[name]
     B, prof = W.workload_inputs(w)
@@ -239,10 +252,13 @@ def run_ours(args):
 
     # ---------------- roofline of the dominant kernel (k_sa_chains), achieved = algorithmic
     cfgs, nmb, mem, feas = pip.enumerate(model, w.bs_global)
-    ops = 0
+    ops = iops = sbytes = props = 0
     for (pp, tp, dp, mb), f in zip(cfgs.tolist(), feas.tolist()):
         if f and pp * dp >= 2:
             ops += fp64_ops_per_step(pp, dp) * chains * w.iterations
+            iops += INT_OPS_PER_STEP * chains * w.iterations
+            sbytes += smem_bytes_per_step(pp, dp) * chains * w.iterations
+            props += chains * w.iterations
     ops_local = ops / world
     sa_avg_s = (sa_max / args.steps) / 1000.0
     pk = peaks()
@@ -259,15 +275,36 @@ def run_ours(args):
     except Exception:
         pass
     achieved = ops_local / sa_avg_s / 1e12
-    roofline = {"kernel": "k_sa_chains", "bound": "alu", "achieved": achieved, "peak": fp64_peak,
-                "unit": "TFLOP/s (fp64 DADD/DMUL ops)", "frac": achieved / fp64_peak,
+    # the fraction against the tightest of the FP64, INT and SMEM ceilings, each
+    # from algorithmic counts per proposal and a measured peak: the roofline time of one
+    # launch is max_i(work_i / peak_i); frac = roofline time / measured kernel time
+    int_peak = measured["alu_ops_per_s"] if measured else N_SMS * 64 * pk.get("sm_max_mhz", 1965.0) * 1e6
+    smem_peak = (measured or {}).get("smem_bytes_per_s") or N_SMS * 128 * pk.get("sm_max_mhz", 1965.0) * 1e6
+    t_fp64 = ops_local / (fp64_peak * 1e12)
+    t_int = (iops / world) / int_peak
+    t_smem = (sbytes / world) / smem_peak
+    t_roof = max(t_fp64, t_int, t_smem)
+    props_local = props / world
+    ceil = {
+        "fp64": {"work_per_proposal": ops / max(props, 1), "peak": fp64_peak * 1e12, "unit": "DADD/DMUL per s",
+                 "bound_proposals_per_s": props_local / t_fp64, "frac": t_fp64 / sa_avg_s},
+        "int": {"work_per_proposal": INT_OPS_PER_STEP, "peak": int_peak, "unit": "int32 ALU ops per s",
+                "bound_proposals_per_s": props_local / t_int, "frac": t_int / sa_avg_s},
+        "smem": {"work_per_proposal": sbytes / max(props, 1), "peak": smem_peak, "unit": "shared-memory B/s",
+                 "bound_proposals_per_s": props_local / t_smem, "frac": t_smem / sa_avg_s},
+    }
+    binding = max(ceil, key=lambda k: ceil[k]["frac"])
+    roofline = {"kernel": "k_sa_chains", "bound": "alu", "achieved": props_local / sa_avg_s / 1e9,
+                "peak": props_local / t_roof / 1e9, "unit": "G proposals/s (min of FP64, INT, SMEM ceilings)",
+                "frac": t_roof / sa_avg_s, "binding_ceiling": binding, "ceilings": ceil,
+                "fp64_achieved_tflops": achieved, "fp64_peak_tflops": fp64_peak,
                 "alu_peak_measured_tops": (measured["alu_ops_per_s"] / 1e12) if measured else None,
                 "traffic": ncu_traffic("k_sa_chains") if args.workload == "C2" else None,
                 "traffic_note": "DRAM bytes per launch (ncu): chain state lives in shared memory, R/tables in L2",
                 "peak_source": peak_source,
                 "sa_kernel_ms": sa_avg_s * 1000.0, "sa_share_of_step": (sa_max / t_max) if t_max else None,
                 "pipes": ncu_pipes("r01d_sa_ncu_summary.txt") if args.workload == "C2" else None,
-                "note": "issue/ALU-bound, not FP64-bound: the FP64 fraction is small by construction (DESIGN.md 8)"}
+                "note": "latency/issue-bound below every ceiling (ncu pipes); ceilings and counts in DESIGN.md 8"}
 
     # ---------------- e2e through the public API: host bandwidth matrix in, plan out
     e2e = None

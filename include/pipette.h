@@ -242,6 +242,12 @@ pipette_status pipette_profile_bandwidth(int32_t n_gpus, const int32_t* devices,
  * Errors: E_CUDA. */
 pipette_status pipette_measure_peaks(int32_t device, double* fp64_ops_per_s, double* alu_ops_per_s);
 
+/* Measured shared-memory load bandwidth of this GPU in bytes per second (the SMEM
+ * ceiling of SURVEY 8(d)'s min(FP64, INT, SMEM) roofline of the SA kernel): conflict-free
+ * 64-bit loads from every warp at 64 warps per SM, CUDA-event timed, best of 3.
+ * Output HOST (may be NULL).  Errors: E_CUDA. */
+pipette_status pipette_measure_smem_bw(int32_t device, double* bytes_per_s);
+
 /* Host-only helper (no GPU needed): the items j in [0, n_items) that `rank` of `world`
  * runs (R18), written to items (capacity cap).  Returns the count (may exceed cap). */
 int64_t pipette_shard_items(int64_t n_items, int32_t rank, int32_t world, int64_t* items, int64_t cap);

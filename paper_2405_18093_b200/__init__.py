@@ -119,7 +119,11 @@ def measure_peaks(device: int = 0) -> dict:
     st = _abi.lib().pipette_measure_peaks(device, C.byref(f), C.byref(a))
     if st != 0:
         raise PipetteError(st, "pipette_measure_peaks failed")
-    return {"fp64_ops_per_s": f.value, "alu_ops_per_s": a.value}
+    sm = C.c_double()
+    st = _abi.lib().pipette_measure_smem_bw(device, C.byref(sm))
+    if st != 0:
+        raise PipetteError(st, "pipette_measure_smem_bw failed")
+    return {"fp64_ops_per_s": f.value, "alu_ops_per_s": a.value, "smem_bytes_per_s": sm.value}
 
 
 def load_memory_mlp(path=None) -> dict:

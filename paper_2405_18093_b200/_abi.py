@@ -66,7 +66,7 @@ class Plan(C.Structure):
                 ("sa_ms", C.c_double), ("argmin_ms", C.c_double), ("combine_ms", C.c_double)]
 
 
-EXPORTS = ("pipette_init", "pipette_enumerate", "pipette_set_bandwidth", "pipette_set_stream", "pipette_eval", "pipette_eval_models", "pipette_profile_bandwidth", "pipette_set_memory_model", "pipette_measure_peaks", "pipette_search",
+EXPORTS = ("pipette_init", "pipette_enumerate", "pipette_set_bandwidth", "pipette_set_stream", "pipette_eval", "pipette_eval_models", "pipette_profile_bandwidth", "pipette_set_memory_model", "pipette_measure_peaks", "pipette_measure_smem_bw", "pipette_search",
            "pipette_shard_items", "pipette_nccl_unique_id", "pipette_last_launch_count", "pipette_last_task_profile", "pipette_destroy",
            "pipette_last_error", "pipette_strerror")
 
@@ -103,6 +103,8 @@ def lib() -> C.CDLL:
     L.pipette_set_memory_model.argtypes = [vp, P(C.c_double), C.c_int64]
     L.pipette_set_memory_model.restype = C.c_int
     L.pipette_measure_peaks.argtypes = [C.c_int32, P(C.c_double), P(C.c_double)]
+    L.pipette_measure_smem_bw.argtypes = [C.c_int32, P(C.c_double)]
+    L.pipette_measure_smem_bw.restype = C.c_int
     L.pipette_measure_peaks.restype = C.c_int
     L.pipette_search.argtypes = [vp, P(Model), C.c_int64, C.c_int32, C.c_int32, C.c_uint64, P(SaOpts),
                                  P(Plan), P(Plan), C.c_int32]
