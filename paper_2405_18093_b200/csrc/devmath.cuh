@@ -177,6 +177,12 @@ struct Mask {
 #pragma unroll
     for (int i = 0; i < MW; ++i) w[i] &= ((a >> 5) == (uint32_t)i) ? ~(1u << (a & 31)) : 0xffffffffu;
   }
+  __device__ __forceinline__ bool test(uint32_t a) const {
+    uint32_t x = 0u;
+#pragma unroll
+    for (int i = 0; i < MW; ++i) x |= ((a >> 5) == (uint32_t)i) ? w[i] : 0u;
+    return (x >> (a & 31)) & 1u;
+  }
   __device__ __forceinline__ int count() const {
     int c = 0;
 #pragma unroll

@@ -687,6 +687,8 @@ pipette_status pipette_eval(pipette_ctx* ctx, const pipette_model* model, int64_
     ctx->vin_valid = true;
   }
   P.vin = (const double*)ctx->vin.p;
+  P.gl_ab = ctx->dGlAb;
+  P.gl_val = ctx->dGlVal;
   P.n_nodes = ctx->n_nodes;
   P.n = n;
   P.cand = d_cfg;

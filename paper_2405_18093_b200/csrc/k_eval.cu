@@ -285,6 +285,11 @@ __device__ __forceinline__ void eval_general(const EvalParams& P, const EvalShar
   if (!C.has_profile) { P.latency[i] = qnan; P.status[i] = 4; return; }
   const double* qi = P.qtab + C.qi_off;
   double t_in = 0.0, mx = 0.0;
+  const int k = mask.count();
+  // slowest link of N1: the k(k-1) member pairs when k^2 <= n, else the first pair inside N1
+  // of the R-descending pair list (expected ~(n/k)^2 probes; every thread scans the same
+  // prefix, so it stays in L1).  Both give the exact max.
+  const bool pairs = k * k <= S.n;
 #pragma unroll
   for (int wd = 0; wd < 4; ++wd) {
     uint32_t bits = mask.w[wd];
@@ -293,18 +298,26 @@ __device__ __forceinline__ void eval_general(const EvalParams& P, const EvalShar
       bits &= bits - 1;
       const uint32_t c = (S.cnt[(a >> 2) * S.T + S.tid] >> ((a & 3) * 8)) & 0xffu;
       if (c >= 2) t_in = fmax(t_in, __dmul_rn(__ldg(qi + c), r_at<false>(S, a, a)));
+      if (pairs) {
 #pragma unroll
-      for (int wd2 = 0; wd2 < 4; ++wd2) {
-        uint32_t bits2 = mask.w[wd2];
-        while (bits2) {
-          const uint32_t b = wd2 * 32 + __ffs(bits2) - 1;
-          bits2 &= bits2 - 1;
-          if (a != b) mx = fmax(mx, r_at<false>(S, a, b));
+        for (int wd2 = 0; wd2 < 4; ++wd2) {
+          uint32_t bits2 = mask.w[wd2];
+          while (bits2) {
+            const uint32_t b = wd2 * 32 + __ffs(bits2) - 1;
+            bits2 &= bits2 - 1;
+            if (a != b) mx = fmax(mx, r_at<false>(S, a, b));
+          }
         }
       }
     }
   }
-  const int k = mask.count();
+  if (!pairs && k >= 2) {
+    const int len = S.n * (S.n - 1);
+    for (int j = 0; j < len; ++j) {
+      const uint32_t ab = __ldg(P.gl_ab + j);
+      if (mask.test(ab & 0xffu) && mask.test(ab >> 8)) { mx = __ldg(P.gl_val + j); break; }
+    }
+  }
   const double t_ex = k >= 2 ? __dmul_rn(__ldg(P.qtab + C.qe_off + k), mx) : 0.0;
   P.latency[i] = compose(C.Sb, C.r, C.Ss, tpp, t_in, t_ex);
   P.status[i] = C.feasible ? 0 : 1;

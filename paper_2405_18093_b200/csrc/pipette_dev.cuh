@@ -113,6 +113,8 @@ struct EvalParams {
   const double* R;
   const double* subset_max;  // 2^n table (MODE 0)
   const double* vin;         // [E][256] qi(c) R[a][a] values (MODE 0)
+  const uint16_t* gl_ab;     // all ordered node pairs (a | b << 8) by R descending (MODE 1)
+  const double* gl_val;      // their R values
   int32_t n_nodes;
   int64_t n;
   const pipette_config* cand;
