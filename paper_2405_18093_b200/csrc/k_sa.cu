@@ -1311,7 +1311,7 @@ __device__ __forceinline__ void unmove_bytes(uint8_t* sb, int kind, uint32_t p, 
 __device__ __forceinline__ double pair_max_lane(const Mask4& m, int kk, const S1Ctx& X, const double* R) {
   const int n = X.n;
   double mx = 0.0;
-  if (kk * kk * kk * kk <= 4 * n * n) {
+  if (kk * kk <= max(n, 64)) {   // (k^2 pair loads against ~(n/k)^2 list probes; measured on C4, C5)
 #pragma unroll
     for (int wd = 0; wd < 4; ++wd) {
       uint32_t ba = m.word(wd);
@@ -1331,7 +1331,16 @@ __device__ __forceinline__ double pair_max_lane(const Mask4& m, int kk, const S1
     }
     return mx;
   }
-  for (int i = 0; i < X.gl_len; ++i) {
+  // every lane scans the same list prefix (L1-resident); four probes per round in flight
+  int i = 0;
+  for (; i + 4 <= X.gl_len; i += 4) {
+    const uint2 ab4 = __ldg(reinterpret_cast<const uint2*>(X.gl_ab + i));   // (i is a multiple of 4)
+    const uint32_t e0 = ab4.x & 0xffffu, e1 = ab4.x >> 16, e2 = ab4.y & 0xffffu, e3 = ab4.y >> 16;
+    const bool h0 = m.test(e0 & 0xffu) && m.test(e0 >> 8), h1 = m.test(e1 & 0xffu) && m.test(e1 >> 8);
+    const bool h2 = m.test(e2 & 0xffu) && m.test(e2 >> 8), h3 = m.test(e3 & 0xffu) && m.test(e3 >> 8);
+    if (h0 | h1 | h2 | h3) return __ldg(X.gl_val + i + (h0 ? 0 : (h1 ? 1 : (h2 ? 2 : 3))));
+  }
+  for (; i < X.gl_len; ++i) {
     const uint32_t ab = __ldg(X.gl_ab + i);
     if (m.test(ab & 0xffu) && m.test(ab >> 8)) return __ldg(X.gl_val + i);
   }
@@ -1473,15 +1482,22 @@ __device__ __forceinline__ void run_task_full(const SaParams& P, const SaTask T,
       double tpp2, tdp2;
       const double Lp = full_eval<MODE, PP, NW>(sb, sw, cb, C, K, X, P.R, tpp2, tdp2);
       const bool acc = metropolis_fast(__dadd_rn(Lp, -cur), beta, m.d.u);
+      bool improved = false;
       if (acc) {
         cur = Lp;
         ++accepted;
         if (Lp < best) {
           best = Lp; best_step = i; best_tpp = tpp2; best_tdp = tdp2;
-          for (int w = 0; w < N; ++w) bperm[w * 32 + lane] = (uint16_t)sb[HcState::off((uint32_t)w)];
+          improved = true;
         }
       } else {
         unmove_bytes(sb, kind, m.d.p, m.d.q);
+      }
+      __syncwarp();
+      for (uint32_t imp = __ballot_sync(0xffffffffu, improved); imp; imp &= imp - 1u) {   // (as in run_task_hc)
+        const int L = __ffs(imp) - 1;
+        const uint8_t* sbL = splane + L * 4;
+        for (int w = lane; w < N; w += 32) bperm[w * 32 + L] = (uint16_t)sbL[HcState::off((uint32_t)w)];
       }
       if (TRACE && trow >= 0 && i < P.trace_cap) {
         pipette_trace_record rec;
