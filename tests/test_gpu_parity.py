@@ -350,6 +350,14 @@ def test_search_mode1_c5_sampled_chains_and_traces():
     _sampled_chain_parity(W.WORKLOADS["C5"], chains=32, iters=1000, n_sample=24, trace_n=2)
 
 
+def test_search_mode1_byte_counts_16_gpus_per_node():
+    # 16 nodes x 16 GPUs: g > 15 takes MODE 1; with tp = 1 a node holds 16 slots, so a
+    # stage-1 count can reach 16 and the counts stay bytes (no nibble plane)
+    w = W.Workload("C0", 16, 16, W.GPT_345M, 256, 80_000_000_000, 100, 4, 400, 0.2, 0.2, 13)
+    res = _sampled_chain_parity(w, chains=4, iters=400, n_sample=40, trace_n=3)
+    assert any(p.cfg[1] == 1 and p.cfg[2] >= 16 for p in res["per_config"])
+
+
 def test_search_mode2_wide_positions():
     # N > 256 (tp = 1 on 40 nodes x 8 GPUs) takes the 32-bit position layout
     w = W.Workload("C0", 40, 8, W.GPT_345M, 320, 80_000_000_000, 100, 8, 600, 0.2, 0.2, 11)

@@ -1,9 +1,7 @@
 A=${1:-paper_2405_18093_b200/lib/ab/libpipette_HEAD.so}
 mkdir -p gpurun_out
-timeout 900 python -m pytest tests/test_gpu_parity.py -x -q -k "full_moves or non_power" > gpurun_out/fm_pytest.log 2>&1; echo "rc=$?" >> gpurun_out/fm_pytest.log
-for wl in C2 C4; do
+timeout 900 python -m pytest tests/test_gpu_parity.py -x -q -k "full_moves or non_power or byte_counts" > gpurun_out/fm_pytest.log 2>&1; echo "rc=$?" >> gpurun_out/fm_pytest.log
+for wl in ${WLS:-C2 C3 C1}; do
   echo "A $wl $(PIPETTE_LIB=$A python tools/search_probe.py $wl - - full)"
   echo "B $wl $(python tools/search_probe.py $wl - - full)"
 done > gpurun_out/fm_ab.log 2>&1
-echo "A C5 $(PIPETTE_LIB=$A python tools/search_probe.py C5 8192 - full)" >> gpurun_out/fm_ab.log 2>&1
-echo "B C5 $(python tools/search_probe.py C5 8192 - full)" >> gpurun_out/fm_ab.log 2>&1
