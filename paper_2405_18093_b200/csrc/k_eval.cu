@@ -55,6 +55,14 @@ __device__ int block_scan_excl_eval(int v, int* sh, int& total) {
 // 128-byte XOR swizzle of a byte offset inside a staging buffer (16-byte granules).
 __device__ __forceinline__ uint32_t swz(uint32_t x) { return x ^ (((x >> 7) & 7u) << 4); }
 
+// PTX shl.b64: shift amounts >= 64 give 0; two SASS funnel shifts (SHF.L.U32 for the low
+// word, SHF.L.U64.HI for the high word), no range fix-up.
+__device__ __forceinline__ unsigned long long shl64_clamp(uint32_t sh) {
+  unsigned long long r;
+  asm("shl.b64 %0, %1, %2;" : "=l"(r) : "l"(1ull), "r"(sh));
+  return r;
+}
+
 // PTX shl.b32: shift amounts >= 32 give 0 (C's << is undefined there).
 __device__ __forceinline__ uint32_t shl_clamp(uint32_t x, uint32_t sh) {
   uint32_t r;
@@ -110,7 +118,7 @@ __device__ __forceinline__ void eval_small(const EvalParams& P, const EvalShared
   // pair; shl clamps, so ids >= 64 set nothing).  The row is a permutation of [0, N) iff
   // exactly the N low bits end up set: an id >= N sets a bit above N or none, and a
   // duplicate leaves one of the N bits unset.  Larger N: bitmap in shared memory.
-  uint32_t seen_lo = 0u, seen_hi = 0u;
+  unsigned long long seen = 0ull;
   uint32_t c_lo = 0u, c_hi = 0u;        // stage-1 counts, nibble a of (c_hi:c_lo) = node a
   bool bad = false;
   double tpp = 0.0, s = 0.0;
@@ -118,8 +126,7 @@ __device__ __forceinline__ void eval_small(const EvalParams& P, const EvalShared
   int x = 0;   // runtime stage counter (PP == 0 only)
   auto visit = [&](uint32_t v, bool stage1, bool last) {
     if (regbm) {
-      seen_lo |= shl_clamp(1u, v);
-      seen_hi |= shl_clamp(1u, v ^ 32u);
+      seen |= shl64_clamp(v);
     } else {
       bad |= v >= (uint32_t)N;
       const uint32_t vc = min(v, (uint32_t)N - 1u);
@@ -184,9 +191,7 @@ __device__ __forceinline__ void eval_small(const EvalParams& P, const EvalShared
   }
   bool ok = !bad;
   if (regbm) {
-    const uint32_t want_lo = N >= 32 ? 0xffffffffu : ((1u << N) - 1u);
-    const uint32_t want_hi = N >= 64 ? 0xffffffffu : (N > 32 ? ((1u << (N - 32)) - 1u) : 0u);
-    ok = seen_lo == want_lo && seen_hi == want_hi;
+    ok = seen == (N >= 64 ? ~0ull : ((1ull << N) - 1ull));
   } else {
     int c = 0;
     for (int w = 0; w < (N + 31) / 32; ++w) c += __popc(S.bm[w * S.T + S.tid]);
