@@ -58,7 +58,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
     objs = []
     for src in sources():
         obj = os.path.join(LIBDIR, os.path.basename(src) + ".o")
-        cmd = [NVCC, *NVCC_FLAGS, "-I", os.path.join(ROOT, "include"), "-I", inc, "-c", src, "-o", obj]
+        extra = os.environ.get("PIPETTE_NVCC_EXTRA", "").split()   # A/B build knobs (-D...)
+        cmd = [NVCC, *NVCC_FLAGS, *extra, "-I", os.path.join(ROOT, "include"), "-I", inc, "-c", src, "-o", obj]
         if verbose:
             cmd.insert(1, "-Xptxas=-v")
             print(" ".join(cmd), file=sys.stderr)

@@ -334,7 +334,7 @@ pipette_status build_plan(pipette_ctx* ctx, int chains, int W, int r, const char
   const bool big = mode == 1 && r_bytes > 32 * 1024;
   if (mode == 2 && full_moves)
     return fail(ctx, PIPETTE_E_UNSUPPORTED, "the full move set needs N = pp*dp <= 256 (max N here %d)", maxN);
-  const int threads = big ? 256 : kSaThreads;
+  const int threads = big ? 256 : ((mode == 0 && n <= 8) ? kSaThreadsN8 : kSaThreads);
   // psum (Eq.5 sums) cached in shared memory for configs with dp <= dp_cap: the largest cap
   // that still reaches the best achievable number of resident blocks per SM
   // MODE 1 swap kernels keep the stage-1 counts as nibbles when no count can exceed 15

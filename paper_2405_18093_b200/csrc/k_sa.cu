@@ -1525,7 +1525,7 @@ __device__ __forceinline__ void run_task_full(const SaParams& P, const SaTask T,
 // MODE 0 with n <= 8 (NW = 2): the m2*R table has 120 codes (15 KB), so 4 blocks fit.
 template <int MODE, bool BIG, int NW = 4>
 struct SaLB {
-  static constexpr int threads = (MODE == 1 && BIG) ? 256 : 128;
+  static constexpr int threads = (MODE == 1 && BIG) ? 256 : ((MODE == 0 && NW == 2) ? kSaThreadsN8 : 128);
   static constexpr int blocks = MODE == 0 ? (NW == 2 ? kSaBlocksN8 : 3) : (MODE == 1 ? (BIG ? 1 : 3) : 2);
 };
 

@@ -17,7 +17,16 @@ constexpr int kMaxGpus = 1024;      // v1 limit (G); N = G/tp <= 1024 slots
 // K3 MODE 0 with n <= 8 nodes: hop codes a | b << 4 stay below 0x78, so the block's m2*R
 // table has kSaCodesN8 codes (x 16 lane copies x 8 B = 15 KB instead of 32 KB).
 constexpr int kSaCodesN8 = 120;
-constexpr int kSaBlocksN8 = 3;   // (4 blocks = 128 registers: spills, measured 30% slower on C2)
+// Block shape of that variant: threads per block and resident blocks per SM (the
+// __launch_bounds__ pair, hence the register cap); build-time knobs for A/B runs.
+#ifndef PIPETTE_N8_THREADS
+#define PIPETTE_N8_THREADS 128
+#endif
+#ifndef PIPETTE_N8_BLOCKS
+#define PIPETTE_N8_BLOCKS 3   // (4 blocks of 128 = 128 registers: spills, measured 30% slower on C2)
+#endif
+constexpr int kSaThreadsN8 = PIPETTE_N8_THREADS;
+constexpr int kSaBlocksN8 = PIPETTE_N8_BLOCKS;
 
 struct DevCfg {
   int32_t pp, tp, dp, mb;
