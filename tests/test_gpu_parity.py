@@ -340,6 +340,18 @@ def _sampled_chain_parity(w, chains, iters, n_sample, seed=2, trace_n=3, **moves
     return res
 
 
+def test_search_mode0_c3_sixteen_nodes_sampled_chains_and_traces():
+    # 16 nodes: MODE 0 with the 256-code m2*R table and four rank words (the n <= 16 kernel
+    # instantiation, not C2's n <= 8 one), every pipeline depth of C3 (pp = 1 .. 32)
+    res = _sampled_chain_parity(W.WORKLOADS["C3"], chains=64, iters=2000, n_sample=48)
+    assert {p.cfg[0] for p in res["per_config"]} >= {1, 2, 4, 8, 16, 32}
+
+
+def test_full_moves_mode0_c3_sixteen_nodes():
+    _sampled_chain_parity(W.WORKLOADS["C3"], chains=32, iters=1000, n_sample=32, trace_n=2,
+                          w_migrate=683, w_reverse=682)
+
+
 def test_search_mode1_c4_sampled_chains_and_traces():
     # 32 nodes: packed positions, sorted-table stage-1 state (S1Large), R through L1
     _sampled_chain_parity(W.WORKLOADS["C4"], chains=64, iters=2000, n_sample=40)
