@@ -303,14 +303,26 @@ pipette_status build_plan(pipette_ctx* ctx, int chains, int W, int r, const char
     }
   }
   cfg_slot[F] = slots;
-  // longest-processing-time-first order of the warp tasks (cost ~ per-step work of the config)
+  // longest-processing-time-first order of the warp tasks.  The cost of a task is its
+  // expected duration, fitted (least squares) to the per-task timings of tools/task_profile.py
+  // on B200 (profiles/r01i_task_profile_c*.log): MODE 0 with n <= 8 on C2; MODE 1 on C4/C5,
+  // where the stage-1 updates (probability pchg = 2(1/pp)(1-1/pp)) dominate and grow with n;
+  // MODE 0 with 8 < n <= 16 keeps the earlier pp-driven estimate (the C2 fit measured 6%
+  // slower on the multi-wave C3).  PIPETTE_COST_FIT=0 selects the earlier estimate everywhere.
   std::vector<double> cost(tasks.size());
+  const char* cf_env = getenv("PIPETTE_COST_FIT");
+  const bool cost_fit = !(cf_env && atoi(cf_env) == 0);
+  const int n_nodes = ctx->n_nodes;
+  const bool mode0 = n_nodes <= 16 && maxN <= 256 && ctx->g <= 15 && ctx->dTab;
   for (size_t i = 0; i < tasks.size(); ++i) {
     const DevCfg& c = ctx->hcfg[tasks[i].cfg];
-    // per-step work: pipeline re-sums (~pp), plus stage-1 updates with probability
-    // 2(1/pp)(1-1/pp) whose cost grows with the cluster (sorted-list probes)
     const double pchg = 2.0 * (1.0 / c.pp) * (1.0 - 1.0 / c.pp);
-    cost[i] = c.N < 2 ? 0.0 : (c.pp >= 2 ? 60.0 + 12.0 * (c.pp - 1) + pchg * (40.0 + 4.0 * ctx->n_nodes) : 10.0);
+    double v = c.pp >= 2 ? 60.0 + 12.0 * (c.pp - 1) + pchg * (40.0 + 4.0 * n_nodes) : 10.0;
+    if (cost_fit && mode0 && n_nodes <= 8)
+      v = c.pp >= 2 ? 10.3 + 0.079 * c.pp + 0.037 * c.N + 0.067 * c.dp + 3.06 * pchg : 1.8;
+    else if (cost_fit && !mode0)
+      v = c.pp >= 2 ? 1.0 - 0.0135 * c.pp + 0.0026 * c.N - 0.02 * c.dp + pchg * (0.9 + 0.028 * n_nodes) : 0.05;
+    cost[i] = c.N < 2 ? 0.0 : v;
   }
   std::vector<int> order(tasks.size());
   for (size_t i = 0; i < order.size(); ++i) order[i] = (int)i;
