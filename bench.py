@@ -303,7 +303,7 @@ def run_ours(args):
                 "traffic_note": "DRAM bytes per launch (ncu): chain state lives in shared memory, R/tables in L2",
                 "peak_source": peak_source,
                 "sa_kernel_ms": sa_avg_s * 1000.0, "sa_share_of_step": (sa_max / t_max) if t_max else None,
-                "pipes": ncu_pipes("r01i_sa_ncu_summary.txt") if args.workload == "C2" else None,
+                "pipes": ncu_pipes("r01j_sa_ncu_summary.txt") if args.workload == "C2" else None,
                 "note": "latency/issue-bound below every ceiling (ncu pipes); ceilings and counts in DESIGN.md 8"}
 
     # ---------------- e2e through the public API: host bandwidth matrix in, plan out
