@@ -188,8 +188,8 @@ def run_reference(args):
                                    f"{w.chains} chains x {w.iterations} swaps per config",
                        "l2": "n/a (host)"},
             "cpu_baseline": {"value": value, "unit": "evals/s", "cores": 1, "kind": "oracle",
-                             "sample": f"{nch} full-length SA chains round-robin over the feasible configs, "
-                                       f"{args.ref_seconds:.0f} s per step"},
+                             "sample": f"{nch} full-length SA chains in total, round-robin over the feasible configs, "
+                                       f"{args.ref_seconds:.0f} s per step x {args.steps} steps"},
             "e2e": {"value": value, "unit": "evals/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line))
 
