@@ -205,6 +205,11 @@ def run_ours(args):
     local = int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(local)
     if world > 1:
+        # stdout carries one JSON line: NCCL_DEBUG=VERSION makes NCCL printf its version banner
+        # to stdout, so that level is lifted to WARN, and NCCL's log lines go to stderr.
+        if os.environ.get("NCCL_DEBUG", "").upper() == "VERSION":
+            os.environ["NCCL_DEBUG"] = "WARN"
+        os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     w, B, prof = setup(args.workload)
     m = w.model
