@@ -128,6 +128,11 @@ def lib():
         L.or_draw_move.argtypes = [C.c_uint32, C.c_uint32, C.c_uint32, C.c_uint64, C.c_int32,
                                    P(C.c_uint32), P(C.c_uint32), P(C.c_double), P(C.c_uint32)]
         L.or_move_kind.argtypes = [C.c_uint32, C.c_int32, C.c_int32]
+        L.or_draw_ctr.argtypes = [C.c_uint32, C.c_uint32, C.c_uint32, C.c_uint32, C.c_uint64, C.c_int32,
+                                  P(C.c_uint32), P(C.c_uint32), P(C.c_uint32)]
+        L.or_calibrate_beta.argtypes = [P(Consts), P(C.c_double), C.c_uint64, C.c_uint32, C.c_int32, C.c_int32,
+                                        C.c_double]
+        L.or_calibrate_beta.restype = C.c_double
         L.or_move_kind.restype = C.c_int32
         L.or_apply_move.argtypes = [P(C.c_uint16), C.c_int32, C.c_uint32, C.c_uint32]
         L.or_undo_move.argtypes = [P(C.c_uint16), C.c_int32, C.c_uint32, C.c_uint32]
@@ -341,6 +346,21 @@ class ChainOut:
     accepted: int
     best_perm: np.ndarray
     trace: list | None
+
+
+def draw_ctr(i: int, c: int, e: int, d: int, seed: int, N: int):
+    """One Philox draw of counter (i, c, e, d) as (p, q, t) (R14, R21; d = 1: R24's stream)."""
+    p, q, t = C.c_uint32(), C.c_uint32(), C.c_uint32()
+    lib().or_draw_ctr(i, c, e, d, seed, N, C.byref(p), C.byref(q), C.byref(t))
+    return p.value, q.value, t.value
+
+
+def calibrate_beta(K: Consts, R: np.ndarray, seed: int, e: int, w_migrate=0, w_reverse=0, tau=0.05) -> float:
+    """SPEC S:448 (R24): 1/T0 with exp(-median|Delta| / T0) = 0.8 over 100 seeded moves of
+    the identity mapping (counter (i, 0, e, 1)); 1/(tau L0) when the median is 0.  The SA
+    chains use it when t0 < 0."""
+    R = np.ascontiguousarray(R, dtype=np.float64)
+    return float(lib().or_calibrate_beta(C.byref(K), _dptr(R), seed, e, w_migrate, w_reverse, tau))
 
 
 def sa_chain(K: Consts, R: np.ndarray, iterations: int, seed: int, chain: int, e: int,

@@ -494,6 +494,65 @@ void or_undo_move(uint16_t* perm, int32_t kind, uint32_t p, uint32_t q) {
 }
 
 /* ------------------------------------------------------------------------- */
+/* Initial temperature by self-calibration (reading R24; NEXT-1): the  */
+/* paper fixes only alpha.  T0 is chosen "so the median |Delta| of 100     */
+/* seeded random moves is accepted with probability 0.8": exp(-median / T0) = 0.8, */
+/* i.e. beta0 = 1/T0 = ln(1.25) / median.                                          */
+/*   move i = 0..99: the Philox block of counter (i, 0, e, 1) -- fourth word 1, so  */
+/*     the stream is disjoint from every SA proposal (fourth word 0) -- drawn and   */
+/*     selected exactly like an SA proposal (R14, R21), applied to the identity     */
+/*     mapping (the chains' start, R16);                                            */
+/*   |Delta_i| = |L(move_i(identity)) - L0|, both from the definition (or_latency); */
+/*   median = (s[49] + s[50]) * 0.5 of the |Delta| sorted ascending;                */
+/*   beta0 = 0.22314355131420976 / median (the double nearest ln 1.25).            */
+/* One value per configuration and seed (independent of the chain).  If median is  */
+/* 0 (every move keeps the latency, e.g. pp = 1) or N < 2, beta0 = 1/(tau * L0).    */
+/* ------------------------------------------------------------------------- */
+void or_draw_ctr(uint32_t i, uint32_t c, uint32_t e, uint32_t d, uint64_t seed, int32_t N,
+                 uint32_t* p, uint32_t* q, uint32_t* t) {
+  uint32_t ctr[4] = {i, c, e, d};
+  uint32_t key[2] = {(uint32_t)seed, (uint32_t)(seed >> 32)};
+  uint32_t w[4];
+  or_philox4x32_10(ctr, key, w);
+  uint32_t pp_ = (uint32_t)(((uint64_t)w[0] * (uint64_t)N) >> 32);
+  uint32_t off = (uint32_t)(((uint64_t)w[1] * (uint64_t)(N - 1)) >> 32);
+  *p = pp_;
+  *q = (pp_ + 1u + off) % (uint32_t)N;
+  *t = ((w[2] & 31u) << 6) | (w[3] & 63u);
+}
+
+static int cmp_double(const void* a, const void* b) {
+  double x = *(const double*)a, y = *(const double*)b;
+  return (x > y) - (x < y);
+}
+
+double or_calibrate_beta(const or_consts* K, const double* R, uint64_t seed, uint32_t e,
+                         int32_t w_migrate, int32_t w_reverse, double tau) {
+  const int32_t N = K->N;
+  uint16_t* perm = (uint16_t*)malloc(sizeof(uint16_t) * (size_t)(N > 0 ? N : 1));
+  for (int32_t w = 0; w < N; ++w) perm[w] = (uint16_t)w;
+  or_breakdown bd;
+  const double L0 = or_latency(K, R, perm, &bd);
+  double beta = 1.0 / (tau * L0);
+  if (N >= 2) {
+    double d[100];
+    for (int32_t i = 0; i < 100; ++i) {
+      uint32_t p, q, t;
+      or_draw_ctr((uint32_t)i, 0u, e, 1u, seed, N, &p, &q, &t);
+      const int32_t kind = or_move_kind(t, w_migrate, w_reverse);
+      for (int32_t w = 0; w < N; ++w) perm[w] = (uint16_t)w;
+      or_apply_move(perm, kind, p, q);
+      d[i] = fabs(or_latency(K, R, perm, &bd) - L0);
+    }
+    qsort(d, 100, sizeof(double), cmp_double);
+    const double median = (d[49] + d[50]) * 0.5;
+    if (median > 0.0) beta = 0.22314355131420976 / median;
+  }
+  free(perm);
+  return beta;
+}
+
+/* ------------------------------------------------------------------------- */
 /* One SA chain of fine-grained worker dedication (Alg.1 l.9-15) on   */
 /* configuration e: Metropolis acceptance (R13, R16), every proposal evaluated   */
 /* from scratch by or_latency.  w_migrate = w_reverse = 0 is the swap-only chain. */
@@ -513,7 +572,9 @@ void or_sa_chain_moves(const or_consts* K, const double* R, int32_t iterations, 
   int32_t best_step = -1;
   uint32_t accepted = 0;
   if (best_perm) memcpy(best_perm, perm, sizeof(uint16_t) * (size_t)N);
-  double beta = (t0 > 0.0) ? 1.0 / t0 : 1.0 / (tau * L0);
+  /* R13: beta0 = 1/t0 (t0 > 0), the self-calibration of R24 (t0 < 0), else 1/(tau L0) */
+  double beta = (t0 > 0.0) ? 1.0 / t0
+              : (t0 < 0.0 ? or_calibrate_beta(K, R, seed, e, w_migrate, w_reverse, tau) : 1.0 / (tau * L0));
   double ia = 1.0 / alpha;
   if (N >= 2) {
     for (int32_t i = 0; i < iterations; ++i) {

@@ -117,6 +117,14 @@ void or_models(const or_consts* K, const double* R, const uint16_t* perm, double
                double* t_des);
 
 /* NEXT-1: the paper's three SA movements, reading R21. */
+/* R24: one Philox draw of counter (i, c, e, d) as (p, q, t), and the
+ * calibrated inverse initial temperature of configuration e: ln(1.25) / median |Delta| of
+ * 100 seeded moves of the identity mapping (fallback 1/(tau L0)).  or_sa_chain[_moves]
+ * use it when t0 < 0. */
+void or_draw_ctr(uint32_t i, uint32_t c, uint32_t e, uint32_t d, uint64_t seed, int32_t N,
+                 uint32_t* p, uint32_t* q, uint32_t* t);
+double or_calibrate_beta(const or_consts* K, const double* R, uint64_t seed, uint32_t e,
+                         int32_t w_migrate, int32_t w_reverse, double tau);
 void or_draw_move(uint32_t i, uint32_t c, uint32_t e, uint64_t seed, int32_t N,
                   uint32_t* p, uint32_t* q, double* u, uint32_t* t);
 int32_t or_move_kind(uint32_t t, int32_t w_migrate, int32_t w_reverse);   /* 0 swap, 1 migrate, 2 reverse */
