@@ -31,7 +31,7 @@ typedef enum {
   PIPETTE_E_PROFILE = 3,     /* a feasible (tp, mb) has no profile entry (R3) */
   PIPETTE_E_CUDA = 4,        /* a CUDA runtime call failed */
   PIPETTE_E_NCCL = 5,        /* an NCCL call failed */
-  PIPETTE_E_UNSUPPORTED = 6  /* outside v1 limits (G > 1024 GPUs, n_nodes > 128) */
+  PIPETTE_E_UNSUPPORTED = 6  /* outside v1 limits (G > 1024 GPUs, n_nodes > 128, gpus_per_node > 255) */
 } pipette_status;
 
 /* Cluster shape (Alg.1 inputs G and M_limit). G = n_nodes * gpus_per_node.
@@ -92,13 +92,19 @@ typedef struct {
 } pipette_chain_result;
 
 /* Simulated-annealing options (R13).  NULL means: alpha = 0.999, tau = 0.05,
- * t0 = 0 (T0 = tau * L(identity)), no diagnostics.  Diagnostic outputs are HOST buffers
+ * t0 = 0 (T0 = tau * L(identity)), no diagnostics.  t0 < 0 selects SPEC's self-calibration
+ * (reading R24): per feasible configuration, T0 such that the median |Delta| of 100
+ * seeded moves of the identity mapping (Philox counter (i, 0, e, 1), i < 100, drawn and
+ * selected like SA proposals) is accepted with probability 0.8, i.e. 1/T0 = ln(1.25) /
+ * median; a zero median (e.g. pp = 1) falls back to tau * L(identity).  Note the defaults
+ * differ from SPEC's CLI defaults: swap moves only (north_star) and T0 = tau * L0;
+ * SPEC's behaviour is w_migrate = 683, w_reverse = 682 and t0 < 0.  Diagnostic outputs are HOST buffers
  * owned by the caller; items are numbered j = f*chains_per_config + c (f = index among
  * feasible configs), as in R18. */
 typedef struct {
   double alpha;             /* temperature reduction per iteration, (0, 1] */
   double tau;               /* T0 = tau * L(identity) when t0 <= 0 */
-  double t0;                /* explicit initial temperature (s) if > 0 */
+  double t0;                /* explicit initial temperature (s) if > 0; < 0: self-calibrated (R24) */
   pipette_chain_result* chains;   /* chains_cap entries indexed by j, or NULL */
   uint16_t* chain_perms;          /* chains_cap x chain_perm_stride best mappings, or NULL */
   int32_t chain_perm_stride;
@@ -140,7 +146,8 @@ typedef struct {
  *     P:295 "B(g1,g2)"); finite and > 0.  Copied; the caller may free it on return.
  *   profile: n_profile entries, copied.
  * Errors: E_INVALID (shapes, non-finite or non-positive values, margin outside
- * [0,500], hidden % heads checked later), E_UNSUPPORTED (n_nodes > 128 or G > 1024),
+ * [0,500], hidden % heads checked later), E_UNSUPPORTED (n_nodes > 128, G > 1024 or
+ * gpus_per_node > 255: per-node stage-1 member counts are bytes on the device),
  * E_CUDA, E_NCCL.  On error *out is NULL. */
 pipette_status pipette_init(pipette_ctx** out, const pipette_cluster* cluster,
                             const double* bw_bytes_per_s,
@@ -170,12 +177,14 @@ pipette_status pipette_enumerate(pipette_ctx* ctx, const pipette_model* model, i
  * the buffers must stay alive until the stream is synchronised.
  *   d_cfg[i]        : configuration of candidate i
  *   d_perm          : candidate i's mapping at d_perm + i*perm_stride, N = pp*dp slots
- *                     (uint16, slot ids in [0,N)); perm_stride >= max N
+ *                     (uint16, slot ids in [0,N)); perm_stride >= N of every candidate
+ *                     (a shorter row gets status 3)
  *   d_latency[i]    : T_Pipette in seconds, NaN when status is 2, 3 or 4
  *   d_mem[i]        : per-GPU memory in bytes (0 when status is 2)
  *   d_status[i]     : 0 feasible, 1 over the memory limit (latency still computed),
  *                     2 configuration not in the enumeration of Alg.1 l.3-5,
- *                     3 mapping not a bijection on [0,N), 4 profile entry missing.
+ *                     3 mapping not a bijection on [0,N) (also when perm_stride < N: the
+ *                       row is never read past perm_stride), 4 profile entry missing.
  * Errors: E_INVALID (n < 0, null pointers with n > 0, perm_stride < 1, bad model). */
 pipette_status pipette_eval(pipette_ctx* ctx, const pipette_model* model, int64_t bs_global,
                             int64_t n, const pipette_config* d_cfg, const uint16_t* d_perm,

@@ -323,17 +323,17 @@ class Pipette:
         pbuf = np.zeros(cap, dtype=np.uint16)
         plan.perm = pbuf.ctypes.data_as(C.POINTER(C.c_uint16))
         plan.perm_cap = cap
-        pcs, pbufs = None, []
+        pcs, pbufs, n_pc = None, [], 0
         if per_config:
-            pcs = (_abi.Plan * 4096)()
-            for i in range(4096):
+            n_pc = max(1, int(self.enumerate(model, bs_global)[3].sum()))   # one plan per feasible config
+            pcs = (_abi.Plan * n_pc)()
+            for i in range(n_pc):
                 b = np.zeros(cap, dtype=np.uint16)
                 pbufs.append(b)
                 pcs[i].perm = b.ctypes.data_as(C.POINTER(C.c_uint16))
                 pcs[i].perm_cap = cap
         st = self._L.pipette_search(self._h, C.byref(m), int(bs_global), int(chains), int(iterations),
-                                    int(seed) & 0xFFFFFFFFFFFFFFFF, C.byref(opts), C.byref(plan), pcs,
-                                    4096 if per_config else 0)
+                                    int(seed) & 0xFFFFFFFFFFFFFFFF, C.byref(opts), C.byref(plan), pcs, n_pc)
         if st == _abi.NO_FEASIBLE:
             raise PipetteError(st, self._L.pipette_last_error(self._h).decode())
         self._check(st)
@@ -341,7 +341,7 @@ class Pipette:
         result = {"plan": best}
         if per_config:
             F = int(plan.configs_enumerated - plan.configs_rejected_oom)
-            result["per_config"] = [_plan(pcs[i], pbufs[i]) for i in range(F)]
+            result["per_config"] = [_plan(pcs[i], pbufs[i]) for i in range(min(F, n_pc))]
         if chain_results:
             rows = []
             for j in range(n_items):

@@ -33,6 +33,11 @@ size_t eval_smem_bytes(int mode, int perm_stride, bool staged, int n_nodes, int 
 __global__ void k_tin_values(const DevCfg*, const double*, const double*, int, double*);
 const void* sa_kernel(int mode, bool trace, int n_nodes, bool full);
 int sa_warp_state_bytes(int mode, int N, int pp, int dp, int n, int dp_cap, bool nib);
+int sa_m1_warp_state_bytes(int N, int dp, int n, bool counts, bool cache, bool nib);
+int sa_m1_count_bytes(int n, bool nib);
+void launch_t0_calibrate(const DevCfg*, const int*, int, const double*, const double*, int, const RoundKeys&, int, int,
+                         double, double*, cudaStream_t);
+__global__ void k_partner_lists(const uint16_t*, int, uint32_t*, int);
 __global__ void k_node_lists(const double*, int, uint8_t*, double*);
 __global__ void k_pair_list(const double*, int, uint16_t*, double*);
 __global__ void k_tin_list(const DevCfg*, const int*, const double*, const double*, int, int, uint16_t*, double*, int*);
@@ -114,6 +119,7 @@ struct HostPlan {
   std::vector<int2> chunks;
   std::vector<int> cfg_slot, slot_perm_off, slot_lane;
   int slots = 0, perm_words = 0, maxN = 1, mode = 0, r_bytes = 0, dp_cap = 0, warp_bytes = 16, tl_stride = 1, wpb = 1;
+  int r_lg = 0, plen = 0;   // MODE 1: R row stride 2^r_lg, pair-list prefix entries
   bool big = false, nib = false;
   size_t smem = 0;
 };
@@ -135,6 +141,8 @@ struct pipette_ctx {
   double* dNlVal = nullptr;
   uint16_t* dGlAb = nullptr;
   double* dGlVal = nullptr;
+  uint32_t* dPt = nullptr;   // MODE 1 per-node pair rows (k_partner_lists)
+  int pt_stride = 0;
   pipette_profile_entry* dProf = nullptr;
   int n_prof = 0;
   std::vector<pipette_profile_entry> prof;
@@ -151,7 +159,7 @@ struct pipette_ctx {
   DevBuf mlp;   // Eq.7 MLP parameters (NEXT-4), empty = analytic memory (R11)
   DevBuf claimed;   // SA chunk claim flags + per-SM first-fetch slots
   DevBuf tasks, chunks, counter, chain_out, best_perm, cfg_slot, cfg_best, gbits, items, gitems, pack, accepted,
-      slot_perm_off, slot_lane, trace_slot, trace, task_prof, tin_rank, tin_vs, tl_ac, tl_val, tl_len;
+      slot_perm_off, slot_lane, trace_slot, trace, task_prof, tin_rank, tin_vs, tl_ac, tl_val, tl_len, beta0;
   int64_t n_tasks_last = 0;
   HostPlanKey plan_key{};
   HostPlan plan;
@@ -248,8 +256,11 @@ pipette_status upload_bw(pipette_ctx* ctx, const double* bw) {
       CU(cudaMalloc(&ctx->dGlAb, sizeof(uint16_t) * L2));
       CU(cudaMalloc(&ctx->dGlVal, sizeof(double) * L2));
     }
+    ctx->pt_stride = ((2 * (n - 1)) + 3) & ~3;
+    if (!ctx->dPt) CU(cudaMalloc(&ctx->dPt, sizeof(uint32_t) * (size_t)n * ctx->pt_stride));
     k_node_lists<<<n, 256>>>(ctx->dR, n, ctx->dNlNode, ctx->dNlVal);
     k_pair_list<<<(unsigned)((L2 + 255) / 256), 256>>>(ctx->dR, n, ctx->dGlAb, ctx->dGlVal);
+    k_partner_lists<<<n, 32>>>(ctx->dGlAb, n, ctx->dPt, ctx->pt_stride);
     CU(cudaGetLastError());
     CU(cudaDeviceSynchronize());
   }
@@ -332,31 +343,83 @@ pipette_status build_plan(pipette_ctx* ctx, int chains, int W, int r, const char
   for (size_t i = 0; i < order.size(); ++i) sorted[i] = tasks[order[i]];
 
   const int n = ctx->n_nodes;
-  const int nn = n * n;
   // MODE 0 (n <= 16): packed positions, register stage-1 state, lane-replicated R,
-  // subset-max table.  MODE 1 (N <= 256): packed positions, sorted-table stage-1 state,
-  // R through L1.  MODE 2: 32-bit positions (N > 256).
+  // subset-max table.  MODE 1 (N <= 256): slot bytes, the block's shared R table, S1M
+  // stage-1 state.  MODE 2: 32-bit positions (N > 256).
   const int mode = (n <= 16 && maxN <= 256 && ctx->g <= 15 && ctx->dTab) ? 0 : (maxN <= 256 ? 1 : 2);
-  // MODE 0: the block's m2*R table, 256 hop codes x 16 lane copies (64-bit loads are served
-  // per half-warp, so 16 copies make every lookup conflict free); MODE 1: the block's
-  // n x n m2*R table (one copy; above 32 KB the block has 8 warps to share it)
-  // (+ MODE 0's shared stage-1 tables: vs 256, qe 32 and tab 256 doubles, rank 256 bytes)
-  const int r_bytes = mode == 0 ? (n <= 8 ? kSaCodesN8 : 256) * 16 * 8 + (n <= 8 ? (256 + 32 + 256) * 8 + 256 : 0)
-                                : (mode == 1 ? align16(nn * 8) : 0);
-  const bool big = mode == 1 && r_bytes > 32 * 1024;
   if (mode == 2 && full_moves)
     return fail(ctx, PIPETTE_E_UNSUPPORTED, "the full move set needs N = pp*dp <= 256 (max N here %d)", maxN);
-  const int threads = big ? 256 : ((mode == 0 && n <= 8) ? kSaThreadsN8 : kSaThreads);
+  if (mode == 1) {
+    // MODE 1: one block of kSaM1Warps warps per SM; the block holds R (row stride 2^lg) and
+    // the pair-list prefix; a chunk of a configuration runs as many warps as that
+    // configuration's chain state fits in the rest of shared memory.  Per configuration:
+    // stage-1 counts when some node can hold >= 2 members, T_ex by member pairs when N1
+    // never exceeds 8 nodes, and the pipeline-sum cache unless it costs more than a few
+    // resident warps (PIPETTE_M1_CACHE_MIN).
+    int lg = 0;
+    while ((1 << lg) < n) ++lg;
+    const int plen = std::min(n * (n - 1), kSaM1PairPrefix);
+    const int r_bytes = align16(8 << (2 * lg)) + align16(plen * 2);
+    const int avail = 227 * 1024 - 64 - r_bytes;
+    bool nib = !full_moves;
+    for (int f = 0; f < F; ++f) {
+      const DevCfg& c = ctx->hcfg[ctx->hfeas[f]];
+      nib = nib && std::min(c.spn, c.dp) <= 15;
+    }
+    const char* cm_env = getenv("PIPETTE_M1_CACHE_MIN");
+    const int cache_min = cm_env ? atoi(cm_env) : 6;
+    std::vector<int> fbytes(F), fwarps(F);
+    std::vector<uint32_t> fflags(F);
+    for (int f = 0; f < F; ++f) {
+      const DevCfg& c = ctx->hcfg[ctx->hfeas[f]];
+      const bool counts = full_moves || std::min(c.spn, c.dp) >= 2;
+      const bool direct = std::min(c.dp, n) <= 8;
+      const int base = full_moves ? align16(((c.N + 3) / 4) * 128) + sa_m1_count_bytes(n, false)
+                                  : sa_m1_warp_state_bytes(c.N, c.dp, n, counts, false, nib);
+      const int with = sa_m1_warp_state_bytes(c.N, c.dp, n, counts, true, nib);
+      const int w_nc = std::min(kSaM1Warps, avail / base), w_c = std::min(kSaM1Warps, avail / with);
+      const bool cache = !full_moves && c.pp >= 2 && w_c >= 1 && w_c >= std::min(w_nc, cache_min);
+      fbytes[f] = cache ? with : base;
+      fwarps[f] = cache ? w_c : w_nc;
+      if (fwarps[f] < 1)
+        return fail(ctx, PIPETTE_E_UNSUPPORTED, "SA state of config e=%d (%d B/warp) exceeds shared memory", c.e, base);
+      fflags[f] = (uint32_t)(fbytes[f] / 16) | (cache ? kTfCache : 0u) | (counts ? kTfCounts : 0u) |
+                  (direct ? kTfDirect : 0u);
+    }
+    for (SaTask& t : sorted) t.pad = (int32_t)fflags[t.f];
+    // block work units: up to the configuration's warp count of consecutive tasks of one
+    // configuration, and no more than an even share of the tasks per SM (a small search
+    // spreads over every SM)
+    const int share = std::max(1, (int)((sorted.size() + ctx->n_sms - 1) / ctx->n_sms));
+    std::vector<int2>& chunks = hp.chunks;
+    size_t smem = (size_t)r_bytes;
+    for (size_t i = 0; i < sorted.size();) {
+      const int f = sorted[i].f;
+      const int cap = std::min(fwarps[f], share);
+      size_t j = i + 1;
+      while (j < sorted.size() && (int)(j - i) < cap && sorted[j].cfg == sorted[i].cfg) ++j;
+      chunks.push_back(make_int2((int)i, (int)(j - i)));
+      smem = std::max(smem, (size_t)r_bytes + (size_t)(j - i) * fbytes[f]);
+      i = j;
+    }
+    int tls = 1;
+    for (int f = 0; f < F; ++f) {
+      const DevCfg& c = ctx->hcfg[ctx->hfeas[f]];
+      tls = std::max(tls, n * (std::min(c.spn, c.dp) - 1));
+    }
+    hp.slots = slots; hp.perm_words = perm_words; hp.maxN = maxN; hp.mode = 1; hp.r_bytes = r_bytes;
+    hp.big = false; hp.nib = nib; hp.dp_cap = 0; hp.warp_bytes = 0; hp.tl_stride = tls; hp.wpb = kSaM1Warps;
+    hp.smem = smem; hp.r_lg = lg; hp.plen = plen;
+    return PIPETTE_OK;
+  }
+  // MODE 0: the block's m2*R table, 256 hop codes x 16 lane copies (64-bit loads are served
+  // per half-warp, so 16 copies make every lookup conflict free)
+  // (+ MODE 0's shared stage-1 tables: vs 256, qe 32 and tab 256 doubles, rank 256 bytes)
+  const int r_bytes = mode == 0 ? (n <= 8 ? kSaCodesN8 : 256) * 16 * 8 + (n <= 8 ? (256 + 32 + 256) * 8 + 256 : 0) : 0;
+  const int threads = (mode == 0 && n <= 8) ? kSaThreadsN8 : kSaThreads;
   // psum (Eq.5 sums) cached in shared memory for configs with dp <= dp_cap: the largest cap
   // that still reaches the best achievable number of resident blocks per SM
-  // MODE 1 swap kernels keep the stage-1 counts as nibbles when no count can exceed 15
-  // (c_n <= min(spn, dp)): half the count plane, so the psum cache fits beside the 128 KB
-  // table at n = 128
-  bool nib = mode == 1 && !full_moves;
-  for (int f = 0; f < F; ++f) {
-    const DevCfg& c = ctx->hcfg[ctx->hfeas[f]];
-    nib = nib && std::min(c.spn, c.dp) <= 15;
-  }
+  const bool nib = false;
   auto warp_bytes_for = [&](int cap, int& tls) {
     int wb = 16;
     tls = 1;
@@ -367,7 +430,7 @@ pipette_status build_plan(pipette_ctx* ctx, int chains, int W, int r, const char
     }
     return wb;
   };
-  const int reg_blocks = mode == 0 ? (n <= 8 ? kSaBlocksN8 : 3) : (mode == 1 ? (big ? 1 : 3) : 2);   // __launch_bounds__
+  const int reg_blocks = mode == 0 ? (n <= 8 ? kSaBlocksN8 : 3) : 2;   // __launch_bounds__
   auto blocks_for = [&](int wb) {
     return std::min(reg_blocks, (227 * 1024) / std::max(1, r_bytes + (threads / 32) * wb));
   };
@@ -398,7 +461,7 @@ pipette_status build_plan(pipette_ctx* ctx, int chains, int W, int r, const char
   }
 
   hp.slots = slots; hp.perm_words = perm_words; hp.maxN = maxN; hp.mode = mode; hp.r_bytes = r_bytes;
-  hp.big = big; hp.nib = nib; hp.dp_cap = dp_cap; hp.warp_bytes = warp_bytes; hp.tl_stride = tl_stride; hp.wpb = wpb;
+  hp.big = false; hp.nib = nib; hp.dp_cap = dp_cap; hp.warp_bytes = warp_bytes; hp.tl_stride = tl_stride; hp.wpb = wpb;
   hp.smem = smem;
   (void)maxdp2;
   return PIPETTE_OK;
@@ -545,8 +608,12 @@ pipette_status pipette_init(pipette_ctx** out, const pipette_cluster* cl, const 
   };
   if (!cl) { fail(ctx, PIPETTE_E_INVALID, "cluster is NULL"); return bail(PIPETTE_E_INVALID); }
   if (cl->n_nodes < 1 || cl->gpus_per_node < 1) { fail(ctx, PIPETTE_E_INVALID, "cluster shape must be >= 1"); return bail(PIPETTE_E_INVALID); }
-  if (cl->n_nodes > kMaxNodes || (long long)cl->n_nodes * cl->gpus_per_node > kMaxGpus) {
-    fail(ctx, PIPETTE_E_UNSUPPORTED, "v1 supports n_nodes <= %d and G <= %d", kMaxNodes, kMaxGpus);
+  // per-node stage-1 member counts are bytes on the device (c_n <= gpus_per_node), so
+  // gpus_per_node is limited to 255
+  if (cl->n_nodes > kMaxNodes || (long long)cl->n_nodes * cl->gpus_per_node > kMaxGpus ||
+      cl->gpus_per_node > kMaxGpusPerNode) {
+    fail(ctx, PIPETTE_E_UNSUPPORTED, "v1 supports n_nodes <= %d, gpus_per_node <= %d and G <= %d", kMaxNodes,
+         kMaxGpusPerNode, kMaxGpus);
     return bail(PIPETTE_E_UNSUPPORTED);
   }
   if (cl->mem_margin_permille < 0 || cl->mem_margin_permille > 500) { fail(ctx, PIPETTE_E_INVALID, "margin must be in [0, 500] permille"); return bail(PIPETTE_E_INVALID); }
@@ -630,7 +697,7 @@ void pipette_destroy(pipette_ctx* ctx) {
                     &ctx->chain_out, &ctx->best_perm, &ctx->cfg_slot, &ctx->cfg_best, &ctx->gbits, &ctx->items,
                     &ctx->gitems, &ctx->pack, &ctx->accepted, &ctx->slot_perm_off, &ctx->slot_lane,
                     &ctx->trace_slot, &ctx->trace, &ctx->task_prof, &ctx->tin_rank, &ctx->tin_vs, &ctx->tl_ac,
-                    &ctx->tl_val, &ctx->tl_len};
+                    &ctx->tl_val, &ctx->tl_len, &ctx->beta0};
   for (DevBuf* b : bufs)
     if (b->p) cudaFree(b->p);
   if (ctx->dR) cudaFree(ctx->dR);
@@ -639,6 +706,7 @@ void pipette_destroy(pipette_ctx* ctx) {
   if (ctx->dNlVal) cudaFree(ctx->dNlVal);
   if (ctx->dGlAb) cudaFree(ctx->dGlAb);
   if (ctx->dGlVal) cudaFree(ctx->dGlVal);
+  if (ctx->dPt) cudaFree(ctx->dPt);
   if (ctx->dProf) cudaFree(ctx->dProf);
   for (auto& e : ctx->ev)
     if (e) cudaEventDestroy(e);
@@ -813,7 +881,6 @@ pipette_status pipette_search(pipette_ctx* ctx, const pipette_model* model, int6
   const int slots = pl.slots, perm_words = pl.perm_words, maxN = pl.maxN, mode = pl.mode, n = ctx->n_nodes;
   const int r_bytes = pl.r_bytes, dp_cap = pl.dp_cap, warp_bytes = pl.warp_bytes, tl_stride = pl.tl_stride;
   const int wpb = pl.wpb;
-  const bool big = pl.big;
   const size_t smem = pl.smem;
   (void)maxN;
   uint64_t steps = 0;
@@ -925,8 +992,12 @@ pipette_status pipette_search(pipette_ctx* ctx, const pipette_model* model, int6
   P.w_migrate = o.w_migrate;
   P.w_reverse = o.w_reverse;
   P.s1_nib = pl.nib ? 1 : 0;
+  P.r_lg = pl.r_lg;
+  P.pt = ctx->dPt;
+  P.pt_stride = ctx->pt_stride;
+  P.plen = pl.plen;
 
-  const void* kern = sa_kernel(big ? 3 : mode, tracing, n, o.w_migrate || o.w_reverse);
+  const void* kern = sa_kernel(mode, tracing, n, o.w_migrate || o.w_reverse);
   CU(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   int occ = 0;
   CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, wpb * 32, smem));
@@ -943,6 +1014,14 @@ pipette_status pipette_search(pipette_ctx* ctx, const pipette_model* model, int6
   }
   ctx->launches++;
   CU(cudaGetLastError());
+  if (o.t0 < 0.0) {   // R24: self-calibrated 1/T0 per feasible configuration
+    CU(ensure(ctx->beta0, sizeof(double) * (size_t)F));
+    launch_t0_calibrate((const DevCfg*)ctx->cfgs.p, (const int*)ctx->feas.p, F, (const double*)ctx->qtab.p, ctx->dR, n,
+                        P.rk, o.w_migrate, o.w_reverse, o.tau, (double*)ctx->beta0.p, s);
+    ctx->launches++;
+    CU(cudaGetLastError());
+    P.beta0 = (const double*)ctx->beta0.p;
+  }
   if (!sorted.empty()) {
     void* args[] = {&P};
     CU(cudaLaunchKernel(kern, dim3(grid), dim3(wpb * 32), args, smem, s));

@@ -477,6 +477,9 @@ __global__ void __launch_bounds__(kEvalThreads, 4) k_eval_stream(EvalParams P) {
           P.latency[i] = qnan; P.mem[i] = 0ull; P.status[i] = 2;
         } else {
           const DevCfg C = P.cfgs[e];
+          if (C.N > P.perm_stride) {   // the row cannot hold a mapping of [0, N): never read past it
+            P.latency[i] = qnan; P.mem[i] = C.mem; P.status[i] = 3;
+          } else {
           RowSrc row;
           row.sbuf = staged ? cur : nullptr;
           row.roff = (uint32_t)lane * rb;
@@ -492,6 +495,7 @@ __global__ void __launch_bounds__(kEvalThreads, 4) k_eval_stream(EvalParams P) {
             }
           } else {
             eval_general(P, S, C, row, i);
+          }
           }
         }
       }

@@ -127,8 +127,9 @@ __global__ void __launch_bounds__(kModelsThreads) k_models(ModelsParams P) {
   // bijection (Eq.2): a bitmap of N <= 1024 bits
   uint32_t seen[32];
   for (int j = 0; j < 32; ++j) seen[j] = 0u;
-  bool ok = true;
-  for (int w = 0; w < N; ++w) {
+  // a row shorter than N cannot hold a mapping of [0, N): status 3 without reading past it
+  bool ok = N <= P.perm_stride;
+  for (int w = 0; ok && w < N; ++w) {
     const uint32_t v = __ldg(row + w);
     if (v >= (uint32_t)N || (seen[v >> 5] >> (v & 31)) & 1u) ok = false;
     else seen[v >> 5] |= 1u << (v & 31);

@@ -125,6 +125,13 @@ struct S1Ctx {
   const double* tl_val;
   int nl_len, gl_len, tl_len;
   int n;
+  // MODE 1 (S1M): per node, its 2(n-1) ordered pairs in global-list order (entry = list
+  // index | (a | b << 8) << 16, rows of pt_stride entries padded with 0xffffffff), and the
+  // block's shared copy of the first plen entries of gl_ab
+  const uint32_t* pt;
+  int pt_stride;
+  const uint16_t* pl;
+  int plen;
 };
 
 // n <= 16 nodes and <= 15 stage-1 members per node.  T_in by ranks: for this config every
@@ -522,7 +529,7 @@ __device__ __forceinline__ void run_task(const SaParams& P, const SaTask T, cons
   double cur = L0, best = L0, best_tpp = tpp, best_tdp = __dadd_rn(s1.tin, s1.tex);
   int best_step = -1;
   uint32_t accepted = 0;
-  double beta = P.t0 > 0.0 ? __ddiv_rn(1.0, P.t0) : __ddiv_rn(1.0, __dmul_rn(P.tau, L0));
+  double beta = sa_beta0(P, T.f, L0);
   const double ia = P.alpha_inv;
   const int trow = (TRACE && active) ? P.trace_slot[slot] : -1;
 
@@ -847,7 +854,7 @@ __device__ __forceinline__ void run_task_hc(const SaParams& P, const SaTask T, c
   double cur = L0, best = L0, best_tpp = tpp, best_tdp = __dadd_rn(s1.tin, s1.tex);
   int best_step = -1;
   uint32_t accepted = 0;
-  double beta = P.t0 > 0.0 ? __ddiv_rn(1.0, P.t0) : __ddiv_rn(1.0, __dmul_rn(P.tau, L0));
+  double beta = sa_beta0(P, T.f, L0);
   const double ia = P.alpha_inv;
   const int trow = (TRACE && active) ? P.trace_slot[slot] : -1;
 
@@ -993,285 +1000,10 @@ __device__ __forceinline__ void run_task_hc(const SaParams& P, const SaTask T, c
   }
 }
 
-// ------------------------------------------------------------------ MODE 1: slot bytes
-// Chain state of MODE 1 (n <= 128 nodes, N <= 256 positions): the slot of every position
-// as a byte (same lane-interleaved layout as MODE 0); node(w) = slot(w) / spn.  The
-// block's table Tt[a * n + b] = fl(m2 * R[a][b]) of its configuration (one copy; a hop is
-// a byte extraction, the node, the pair index, one 64-bit shared load and one DADD).
-struct SbCtx {
-  const double* T;   // block table, n x n
-  int n;
-  uint32_t spn, spn_magic, spn_sh;   // spn_sh < 32: spn is a power of two
-  uint32_t m16;                      // ceil(2^16 / spn)
-  // node = floor(slot / spn) as (slot * m16) >> 16: exact for slot < 256 and spn < 256
-  // (the error slot * (m16 - 2^16/spn) / 2^16 < 1/256 never crosses an integer)
-  __device__ __forceinline__ uint32_t node(uint32_t slot) const { return (slot * m16) >> 16; }
-};
-
-template <int PP>
-__device__ __forceinline__ double sb_sum(const HcState& st, uint32_t z, int pp_rt, const SbCtx& K) {
-  double s = 0.0;
-  if constexpr (PP >= 4) {
-    constexpr int NW = PP / 4;
-    uint32_t wd[NW];
-#pragma unroll
-    for (int k = 0; k < NW; ++k) wd[k] = st.hw[(z * (uint32_t)NW + (uint32_t)k) * 32u];
-    uint32_t prev = K.node(wd[0] & 0xffu);
-#pragma unroll
-    for (int x = 1; x < PP; ++x) {
-      const uint32_t cur = K.node(__byte_perm(wd[x >> 2], 0u, 0x4440u | (uint32_t)(x & 3)));
-      s = __dadd_rn(s, K.T[prev * (uint32_t)K.n + cur]);
-      prev = cur;
-    }
-  } else {
-    const int pp = PP > 0 ? PP : pp_rt;
-    const uint32_t b = z * (uint32_t)pp;
-    uint32_t prev = K.node(st.hb[HcState::off(b)]);
-    for (int x = 1; x < pp; ++x) {
-      const uint32_t cur = K.node(st.hb[HcState::off(b + (uint32_t)x)]);
-      s = __dadd_rn(s, K.T[prev * (uint32_t)K.n + cur]);
-      prev = cur;
-    }
-  }
-  return s;
-}
-
-template <int PP>
-__device__ __forceinline__ void sb_sum2(const HcState& st, uint32_t za, uint32_t zb, int pp_rt, const SbCtx& K,
-                                        double& sa, double& sb) {
-  double a = 0.0, b = 0.0;
-  if constexpr (PP >= 4) {
-    constexpr int NW = PP / 4;
-    uint32_t wa[NW], wb[NW];
-#pragma unroll
-    for (int k = 0; k < NW; ++k) {
-      wa[k] = st.hw[(za * (uint32_t)NW + (uint32_t)k) * 32u];
-      wb[k] = st.hw[(zb * (uint32_t)NW + (uint32_t)k) * 32u];
-    }
-    uint32_t pa = K.node(wa[0] & 0xffu), pb = K.node(wb[0] & 0xffu);
-#pragma unroll
-    for (int x = 1; x < PP; ++x) {
-      const uint32_t ca = K.node(__byte_perm(wa[x >> 2], 0u, 0x4440u | (uint32_t)(x & 3)));
-      const uint32_t cb = K.node(__byte_perm(wb[x >> 2], 0u, 0x4440u | (uint32_t)(x & 3)));
-      a = __dadd_rn(a, K.T[pa * (uint32_t)K.n + ca]);
-      b = __dadd_rn(b, K.T[pb * (uint32_t)K.n + cb]);
-      pa = ca;
-      pb = cb;
-    }
-  } else {
-    const int pp = PP > 0 ? PP : pp_rt;
-    const uint32_t ba = za * (uint32_t)pp, bb = zb * (uint32_t)pp;
-    uint32_t pa = K.node(st.hb[HcState::off(ba)]), pb = K.node(st.hb[HcState::off(bb)]);
-    for (int x = 1; x < pp; ++x) {
-      const uint32_t ca = K.node(st.hb[HcState::off(ba + (uint32_t)x)]);
-      const uint32_t cb = K.node(st.hb[HcState::off(bb + (uint32_t)x)]);
-      a = __dadd_rn(a, K.T[pa * (uint32_t)K.n + ca]);
-      b = __dadd_rn(b, K.T[pb * (uint32_t)K.n + cb]);
-      pa = ca;
-      pb = cb;
-    }
-  }
-  sa = a;
-  sb = b;
-}
-
-template <int PP>
-__device__ __forceinline__ void sb_rescan(const HcState& st, int dp, int pp_rt, const SbCtx& K, double& mx, int& cnt) {
-  double m0 = 0.0, m1 = 0.0;
-  int c0 = 0, c1 = 0;
-  auto acc = [](double v, double& m, int& c) {
-    c = v > m ? 1 : c + (v == m ? 1 : 0);
-    m = fmax(m, v);
-  };
-  int z = 0;
-  for (; z + 2 <= dp; z += 2) {
-    double a, b;
-    sb_sum2<PP>(st, (uint32_t)z, (uint32_t)z + 1u, pp_rt, K, a, b);
-    acc(a, m0, c0);
-    acc(b, m1, c1);
-  }
-  if (z < dp) acc(sb_sum<PP>(st, (uint32_t)z, pp_rt, K), m0, c0);
-  mx = fmax(m0, m1);
-  cnt = (m0 == mx ? c0 : 0) + (m1 == mx ? c1 : 0);
-}
-
-// [slot plane][stage-1 counts: bytes, or nibbles when nib][psum]
-__host__ __device__ inline int sb_count_bytes(int n, bool nib) { return align16((nib ? (n + 7) / 8 : (n + 3) / 4) * 128); }
-__host__ __device__ inline int sb_warp_state_bytes(int N, int pp, int dp, int n, int dp_cap, bool nib) {
-  return align16(((N + 3) / 4) * 128) + sb_count_bytes(n, nib) + ((pp >= 4 && dp <= dp_cap) ? align16(dp * 256) : 0);
-}
-
-// One warp task of MODE 1 (same step structure as run_task_hc).
-template <bool TRACE, int PP, bool BIG>
-__device__ __forceinline__ void run_task_sb(const SaParams& P, const SaTask T, const DevCfg C, const double* Tt,
-                                            unsigned char* ws, int lane) {
-  const bool active = lane < T.count;
-  const int N = C.N, pp = PP > 0 ? PP : C.pp, dp = C.dp, n = P.n_nodes;
-  const uint32_t chain = (uint32_t)(T.c_first + (T.k0 + lane) * P.world);
-  const int slot = T.slot0 + lane;
-  S1Ctx X;
-  X.qi = P.qtab + C.qi_off; X.qe = P.qtab + C.qe_off;
-  X.nl_node = P.nl_node; X.nl_val = P.nl_val; X.gl_ab = P.gl_ab; X.gl_val = P.gl_val;
-  X.tl_ac = P.tl_ac + (size_t)T.f * P.tl_stride;
-  X.tl_val = P.tl_val + (size_t)T.f * P.tl_stride;
-  X.nl_len = 2 * (n - 1); X.gl_len = n * (n - 1); X.tl_len = P.tl_len[T.f];
-  X.n = n;
-  SbCtx K;
-  K.T = Tt; K.n = n; K.spn = (uint32_t)C.spn; K.spn_magic = C.spn_magic;
-  K.spn_sh = (C.spn & (C.spn - 1)) == 0 ? (uint32_t)(31 - __clz(C.spn)) : 32u;
-  K.m16 = (uint32_t)((65536u + (uint32_t)C.spn - 1u) / (uint32_t)C.spn);
-
-  const bool cache = pp >= 4 && dp <= P.psum_dp_cap;
-  const int plane = align16(((N + 3) / 4) * 128);
-  HcState st;
-  st.hb = ws + lane * 4;   // slot bytes (st.hb doubles as the slot plane)
-  st.sb = st.hb;
-  st.hw = reinterpret_cast<const uint32_t*>(ws) + lane;
-  // stage-1 state with warp-cooperative searches (S1Large; member counts as bytes, the
-  // same lane-interleaved layout as the slots).  (Per-lane searches were measured slower:
-  // a lane's long search stalls its whole warp.)
-  S1Large<RGlob> s1;
-  const RGlob Rg{P.R, n, lane};
-  s1.c = reinterpret_cast<uint32_t*>(ws + plane);
-  s1.lane = lane;
-  s1.set_nibbles(P.s1_nib != 0);
-  double* psum = reinterpret_cast<double*>(ws + plane + sb_count_bytes(n, P.s1_nib != 0));
-  uint16_t* bperm = P.best_perm + T.perm_off;
-  s1.clear(n);
-
-  for (int w = 0; w < N; ++w) {
-    st.hb[HcState::off((uint32_t)w)] = (uint8_t)w;
-    bperm[w * 32 + lane] = (uint16_t)w;
-  }
-  __syncwarp();
-  double tpp = 0.0;
-  int nmax = 0;
-  for (int z = 0; z < dp; ++z) {
-    s1.add_init(K.node((uint32_t)(z * pp)));
-    if (pp >= 2) {
-      const double s = sb_sum<PP>(st, (uint32_t)z, pp, K);
-      if (cache) psum[z * 32 + lane] = s;
-      if (s > tpp) { tpp = s; nmax = 1; } else if (s == tpp) { ++nmax; }
-    }
-  }
-  s1.finish_init(X, Rg);
-
-  const double L0 = compose(C.Sb, C.r, C.Ss, tpp, s1.tin, s1.tex);
-  double cur = L0, best = L0, best_tpp = tpp, best_tdp = __dadd_rn(s1.tin, s1.tex);
-  int best_step = -1;
-  uint32_t accepted = 0;
-  double beta = P.t0 > 0.0 ? __ddiv_rn(1.0, P.t0) : __ddiv_rn(1.0, __dmul_rn(P.tau, L0));
-  const double ia = P.alpha_inv;
-  const int trow = (TRACE && active) ? P.trace_slot[slot] : -1;
-
-  if (N >= 2) {
-    Draw dnext = draw_swap_rk(0u, chain, (uint32_t)C.e, P.rk, (uint32_t)N);
-    for (int i = 0; i < P.iterations; ++i) {
-      const Draw d = dnext;
-      dnext = draw_swap_rk((uint32_t)(i + 1), chain, (uint32_t)C.e, P.rk, (uint32_t)N);
-      const uint32_t p = d.p, q = d.q;
-      uint8_t* const bp = st.hb + HcState::off(p);
-      uint8_t* const bq = st.hb + HcState::off(q);
-      const uint32_t sp = *bp, sq = *bq;
-      bool dpchg = false;
-      const uint32_t np = K.node(sp), nq = K.node(sq);
-      double Lp = cur;
-      bool acc = true, improved = false;
-      if (pp >= 2) {
-        const uint32_t zp = PP > 0 ? p / (uint32_t)PP : div_small(p, C.pp_magic, (uint32_t)pp);
-        const uint32_t zq = PP > 0 ? q / (uint32_t)PP : div_small(q, C.pp_magic, (uint32_t)pp);
-        const uint32_t xp = p - zp * (uint32_t)pp, xq = q - zq * (uint32_t)pp;
-        const bool two = zq != zp;
-        const uint32_t zb = two ? zq : zp;
-        double oldA, oldB;
-        if (cache) {
-          oldA = psum[zp * 32 + lane];
-          oldB = psum[zb * 32 + lane];
-        } else {
-          sb_sum2<PP>(st, zp, zb, pp, K, oldA, oldB);
-        }
-        *bp = (uint8_t)sq;   // tentative swap
-        *bq = (uint8_t)sp;
-        double sA, sB;
-        sb_sum2<PP>(st, zp, zb, pp, K, sA, sB);
-        double tpp2 = tpp;
-        int nmax2 = nmax;
-        const double snew = fmax(sA, sB);
-        const int keep = nmax - (oldA == tpp ? 1 : 0) - ((two && oldB == tpp) ? 1 : 0);
-        if (keep > 0 || snew >= tpp) {
-          tpp2 = (keep > 0) ? fmax(tpp, snew) : snew;
-          nmax2 = (keep > 0 && tpp2 == tpp ? keep : 0) + (sA == tpp2 ? 1 : 0) + ((two && sB == tpp2) ? 1 : 0);
-        } else if (cache) {
-          double m0 = sA, m1 = two ? sB : 0.0;
-          int c0 = 1, c1 = two ? 1 : 0;
-          for (int z = 0; z < dp; ++z) {
-            const double v = ((uint32_t)z == zp || (uint32_t)z == zq) ? 0.0 : psum[z * 32 + lane];
-            if (z & 1) { c1 = v > m1 ? 1 : c1 + (v == m1 ? 1 : 0); m1 = fmax(m1, v); }
-            else { c0 = v > m0 ? 1 : c0 + (v == m0 ? 1 : 0); m0 = fmax(m0, v); }
-          }
-          tpp2 = fmax(m0, m1);
-          nmax2 = (m0 == tpp2 ? c0 : 0) + (m1 == tpp2 ? c1 : 0);
-        } else {
-          sb_rescan<PP>(st, dp, pp, K, tpp2, nmax2);
-        }
-        dpchg = ((xp == 0u) != (xq == 0u)) && np != nq;
-        if (dpchg) {
-          const uint32_t dn = xp == 0u ? np : nq;
-          const uint32_t up = xp == 0u ? nq : np;
-          s1.propose(dn, up, X, Rg);
-        }
-        s1.template coop<BIG>(X, Rg);   // converged: all lanes' flagged searches
-        double tin2 = s1.tin, tex2 = s1.tex;
-        if (dpchg) {
-          s1.finish(X);
-          tin2 = s1.tin2;
-          tex2 = s1.tex2;
-        }
-        Lp = compose(C.Sb, C.r, C.Ss, tpp2, tin2, tex2);
-        acc = metropolis_fast(__dadd_rn(Lp, -cur), beta, d.u);
-        if (acc) {
-          if (cache) {
-            psum[zp * 32 + lane] = sA;
-            psum[zb * 32 + lane] = sB;
-          }
-          tpp = tpp2;
-          nmax = nmax2;
-          if (dpchg) s1.commit();
-          cur = Lp;
-          if (Lp < best) {
-            best = Lp; best_step = i; best_tpp = tpp; best_tdp = __dadd_rn(s1.tin, s1.tex);
-            improved = true;
-          }
-        } else {
-          *bq = (uint8_t)sq;   // revert
-          *bp = (uint8_t)sp;
-        }
-      } else {
-        *bp = (uint8_t)sq;   // pp = 1: L' = cur (no hops, stage-1 multiset unchanged)
-        *bq = (uint8_t)sp;
-      }
-      if (acc) ++accepted;
-      for (uint32_t imp = __ballot_sync(0xffffffffu, improved); imp; imp &= imp - 1u) {   // (as in MODE 0)
-        const int L = __ffs(imp) - 1;
-        const uint8_t* sbL = ws + L * 4;
-        for (int w = lane; w < N; w += 32) bperm[w * 32 + L] = (uint16_t)sbL[HcState::off((uint32_t)w)];
-      }
-      if (TRACE && trow >= 0 && i < P.trace_cap) {
-        pipette_trace_record rec;
-        rec.i = (uint32_t)i; rec.p = (uint16_t)d.p; rec.q = (uint16_t)d.q;
-        rec.accept = acc ? 1u : 0u; rec.latency = Lp;
-        P.trace[(size_t)trow * P.trace_cap + i] = rec;
-      }
-      beta = __dmul_rn(beta, ia);
-    }
-  }
-  if (active) {
-    ChainOut o;
-    o.best = best; o.best_tpp = best_tpp; o.best_tdp = best_tdp; o.L0 = L0;
-    o.best_step = best_step; o.accepted = accepted; o.f = T.f; o.c = (int32_t)chain;
-    P.out[slot] = o;
-  }
-}
+// ------------------------------------------------------------------ MODE 1 (sa_mode1.cuh)
+// n <= 128 nodes, N <= 256 positions: slot-byte chain state, the block's shared R table,
+// stage-1 state S1M (canonical list witnesses), per-configuration warp regions.
+#include "sa_mode1.cuh"
 
 // ------------------------------------------------------------------ full move set (NEXT-1)
 // The paper's three movements (R21): swap, migration (remove the element at p,
@@ -1371,7 +1103,7 @@ __device__ __forceinline__ double full_eval(const uint8_t* sb, const uint32_t* s
     }
   };
   auto term = [&](uint32_t a, uint32_t b) -> double {
-    return MODE == 0 ? K.T[(a | (b << 4)) * 16u] : K.T[a * (uint32_t)n + b];
+    return MODE == 0 ? K.T[(a | (b << 4)) * 16u] : K.hop(a, b);
   };
   double tpp = 0.0;
   for (int z = 0; z < dp; ++z) {
@@ -1448,7 +1180,8 @@ __device__ __forceinline__ void run_task_full(const SaParams& P, const SaTask T,
   X.gl_ab = P.gl_ab; X.gl_val = P.gl_val; X.gl_len = n * (n - 1);
   X.n = n;
   SbCtx K;
-  K.T = MODE == 0 ? Tt + (lane & 15) : Tt; K.n = n; K.spn = (uint32_t)C.spn; K.spn_magic = C.spn_magic;
+  K.T = MODE == 0 ? Tt + (lane & 15) : Tt; K.m2 = C.m2; K.lg = (uint32_t)P.r_lg;
+  K.n = n; K.spn = (uint32_t)C.spn; K.spn_magic = C.spn_magic;
   K.spn_sh = (C.spn & (C.spn - 1)) == 0 ? (uint32_t)(31 - __clz(C.spn)) : 32u;
   K.m16 = (uint32_t)((65536u + (uint32_t)C.spn - 1u) / (uint32_t)C.spn);
   const int plane = align16(((N + 3) / 4) * 128);
@@ -1468,7 +1201,7 @@ __device__ __forceinline__ void run_task_full(const SaParams& P, const SaTask T,
   double cur = L0, best = L0, best_tpp = tpp, best_tdp = tdp;
   int best_step = -1;
   uint32_t accepted = 0;
-  double beta = P.t0 > 0.0 ? __ddiv_rn(1.0, P.t0) : __ddiv_rn(1.0, __dmul_rn(P.tau, L0));
+  double beta = sa_beta0(P, T.f, L0);
   const double ia = P.alpha_inv;
   const int trow = (TRACE && active) ? P.trace_slot[slot] : -1;
   const int th_swap = 2048 - P.w_migrate - P.w_reverse, th_mig = 2048 - P.w_reverse;
@@ -1525,8 +1258,8 @@ __device__ __forceinline__ void run_task_full(const SaParams& P, const SaTask T,
 // MODE 0 with n <= 8 (NW = 2): the m2*R table has 120 codes (15 KB), so 4 blocks fit.
 template <int MODE, bool BIG, int NW = 4>
 struct SaLB {
-  static constexpr int threads = (MODE == 1 && BIG) ? 256 : ((MODE == 0 && NW == 2) ? kSaThreadsN8 : 128);
-  static constexpr int blocks = MODE == 0 ? (NW == 2 ? kSaBlocksN8 : 3) : (MODE == 1 ? (BIG ? 1 : 3) : 2);
+  static constexpr int threads = MODE == 1 ? kSaM1Warps * 32 : ((MODE == 0 && NW == 2) ? kSaThreadsN8 : 128);
+  static constexpr int blocks = MODE == 0 ? (NW == 2 ? kSaBlocksN8 : 3) : (MODE == 1 ? 1 : 2);
 };
 
 // FULL: the full move set (run_task_full) -- a separate instantiation, so the swap kernel's
@@ -1538,7 +1271,7 @@ __global__ void __launch_bounds__(SaLB<MODE, BIG, NW>::threads, SaLB<MODE, BIG, 
   using S1 = S1Large<RT>;
   extern __shared__ __align__(16) unsigned char smem[];
   double* Rs = reinterpret_cast<double*>(smem);
-  const int n = P.n_nodes, nn = n * n;
+  const int n = P.n_nodes;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   RT R{P.R, n, lane};
   const double* Tl = Rs + (lane & 15);   // MODE 0: this lane's copy of the block's m2*R table
@@ -1550,6 +1283,18 @@ __global__ void __launch_bounds__(SaLB<MODE, BIG, NW>::threads, SaLB<MODE, BIG, 
   uint8_t* s1_rank = reinterpret_cast<uint8_t*>(s1_tab + 256);
   // (n <= 8 only: at n <= 16 the extra shared memory costs more than the loads save)
   const S1Shared SS{s1_rank, s1_vs, s1_qe, s1_tab};
+  // MODE 1: the cluster's R (row stride 2^r_lg) and the first plen entries of the global
+  // pair list, loaded once; every configuration shares them
+  const uint16_t* pl_s = reinterpret_cast<const uint16_t*>(smem + align16((8 << (2 * P.r_lg))));
+  if constexpr (MODE == 1) {
+    const int np = 1 << P.r_lg;
+    for (int i = threadIdx.x; i < np * np; i += blockDim.x) {
+      const int a = i >> P.r_lg, b = i & (np - 1);
+      Rs[i] = (a < n && b < n) ? P.R[a * n + b] : 0.0;
+    }
+    uint16_t* pw = const_cast<uint16_t*>(pl_s);
+    for (int i = threadIdx.x; i < P.plen; i += blockDim.x) pw[i] = P.gl_ab[i];
+  }
   unsigned char* ws = smem + P.r_smem_bytes + wid * P.warp_smem_bytes;
   __shared__ int s_chunk;
   int table_cfg = -1;
@@ -1587,7 +1332,7 @@ __global__ void __launch_bounds__(SaLB<MODE, BIG, NW>::threads, SaLB<MODE, BIG, 
     const int ch = s_chunk;
     if (ch >= P.n_chunks) break;
     const int2 chunk = P.chunks[ch];
-    if constexpr (MODE == 0 || MODE == 1) {
+    if constexpr (MODE == 0) {
       const int cfg0 = P.tasks[chunk.x].cfg;
       if (cfg0 != table_cfg) {   // block-uniform: rebuild the table for this configuration
         const double m2 = P.cfgs[cfg0].m2;
@@ -1610,8 +1355,6 @@ __global__ void __launch_bounds__(SaLB<MODE, BIG, NW>::threads, SaLB<MODE, BIG, 
             s1_tab[i] = (k >= 2 && k <= min(C0.dp, n)) ? __dmul_rn(P.qtab[C0.qe_off + k], P.subset_max[i]) : 0.0;
           }
           }
-        } else {
-          for (int i = threadIdx.x; i < nn; i += blockDim.x) Rs[i] = __dmul_rn(m2, P.R[i]);
         }
         table_cfg = cfg0;
       }
@@ -1621,6 +1364,8 @@ __global__ void __launch_bounds__(SaLB<MODE, BIG, NW>::threads, SaLB<MODE, BIG, 
     const int t = chunk.x + wid;
     const SaTask T = P.tasks[t];
     const DevCfg C = P.cfgs[T.cfg];
+    // MODE 1: the warp's region has its configuration's size (task flags, bits 0-15)
+    if constexpr (MODE == 1) ws = smem + P.r_smem_bytes + wid * (int)(((uint32_t)T.pad & 0xffffu) * 16u);
     unsigned long long t_start = 0;
     if (lane == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_start));
     if constexpr (FULL && (MODE == 0 || MODE == 1)) {   // the full move set
@@ -1642,13 +1387,13 @@ __global__ void __launch_bounds__(SaLB<MODE, BIG, NW>::threads, SaLB<MODE, BIG, 
       }
     } else if constexpr (MODE == 1) {
       switch (C.pp) {
-        case 1: run_task_sb<TRACE, 1, BIG>(P, T, C, Rs, ws, lane); break;
-        case 2: run_task_sb<TRACE, 2, BIG>(P, T, C, Rs, ws, lane); break;
-        case 4: run_task_sb<TRACE, 4, BIG>(P, T, C, Rs, ws, lane); break;
-        case 8: run_task_sb<TRACE, 8, BIG>(P, T, C, Rs, ws, lane); break;
-        case 16: run_task_sb<TRACE, 16, BIG>(P, T, C, Rs, ws, lane); break;
-        case 32: run_task_sb<TRACE, 32, BIG>(P, T, C, Rs, ws, lane); break;
-        default: run_task_sb<TRACE, 0, BIG>(P, T, C, Rs, ws, lane); break;
+        case 1: run_task_sb<TRACE, 1>(P, T, C, Rs, pl_s, ws, lane); break;
+        case 2: run_task_sb<TRACE, 2>(P, T, C, Rs, pl_s, ws, lane); break;
+        case 4: run_task_sb<TRACE, 4>(P, T, C, Rs, pl_s, ws, lane); break;
+        case 8: run_task_sb<TRACE, 8>(P, T, C, Rs, pl_s, ws, lane); break;
+        case 16: run_task_sb<TRACE, 16>(P, T, C, Rs, pl_s, ws, lane); break;
+        case 32: run_task_sb<TRACE, 32>(P, T, C, Rs, pl_s, ws, lane); break;
+        default: run_task_sb<TRACE, 0>(P, T, C, Rs, pl_s, ws, lane); break;
       }
     } else {
       switch (C.pp) {
@@ -1826,6 +1571,24 @@ __global__ void __launch_bounds__(256) k_argmin(const ChainOut* __restrict__ out
 }
 
 // Host-side handles of the K3 variants (MODE 0/1/2 as above; TRACE records).
+// Per-node pair rows for S1M (MODE 1): for node u (one warp per node), every ordered pair
+// with u as an endpoint, in global-list order (so by R descending, ties by index), entry =
+// list rank | (a | b << 8) << 16; rows of `stride` entries, padded with 0xffffffff.
+__global__ void k_partner_lists(const uint16_t* __restrict__ gl, int n, uint32_t* __restrict__ pt, int stride) {
+  const int u = blockIdx.x, lane = threadIdx.x & 31, L = n * (n - 1);
+  int base = 0;
+  for (int j0 = 0; j0 < L; j0 += 32) {
+    const int j = j0 + lane;
+    const uint32_t p = j < L ? (uint32_t)gl[j] : 0u;
+    const bool hit = j < L && ((int)(p & 0xffu) == u || (int)(p >> 8) == u);
+    const unsigned b = __ballot_sync(0xffffffffu, hit);
+    if (hit) pt[(size_t)u * stride + base + __popc(b & ((1u << lane) - 1u))] = (uint32_t)j | (p << 16);
+    base += __popc(b);
+  }
+  for (int i = base + lane; i < stride; i += 32) pt[(size_t)u * stride + i] = 0xffffffffu;
+}
+
+// Host-side handles of the K3 variants (MODE 0/1/2 as above; TRACE records).
 const void* sa_kernel(int mode, bool trace, int n_nodes, bool full) {
   if (full) {
     if (mode == 0 && n_nodes <= 8)
@@ -1834,21 +1597,23 @@ const void* sa_kernel(int mode, bool trace, int n_nodes, bool full) {
       return trace ? (const void*)k_sa_chains<0, true, 4, false, true> : (const void*)k_sa_chains<0, false, 4, false, true>;
     if (mode == 1)
       return trace ? (const void*)k_sa_chains<1, true, 4, false, true> : (const void*)k_sa_chains<1, false, 4, false, true>;
-    if (mode == 3)
-      return trace ? (const void*)k_sa_chains<1, true, 4, true, true> : (const void*)k_sa_chains<1, false, 4, true, true>;
     return nullptr;   // (MODE 2: rejected by the host)
   }
   if (mode == 0 && n_nodes <= 8) return trace ? (const void*)k_sa_chains<0, true, 2> : (const void*)k_sa_chains<0, false, 2>;
   if (mode == 0) return trace ? (const void*)k_sa_chains<0, true, 4> : (const void*)k_sa_chains<0, false, 4>;
   if (mode == 1) return trace ? (const void*)k_sa_chains<1, true> : (const void*)k_sa_chains<1, false>;
-  if (mode == 3) return trace ? (const void*)k_sa_chains<1, true, 4, true> : (const void*)k_sa_chains<1, false, 4, true>;
   return trace ? (const void*)k_sa_chains<2, true> : (const void*)k_sa_chains<2, false>;
 }
 
+// Per-warp chain-state bytes: MODE 0 and 2 (psum cached when dp <= dp_cap); MODE 1 with the
+// per-configuration flags of its tasks (counts, cache)
 int sa_warp_state_bytes(int mode, int N, int pp, int dp, int n, int dp_cap, bool nib) {
   if (mode == 0) return hc_warp_state_bytes(N, pp, dp, dp_cap);
-  if (mode == 1 || mode == 3) return sb_warp_state_bytes(N, pp, dp, n, dp_cap, nib);
   return warp_state_bytes<PosWide>(N, pp, dp, n, true, dp_cap);
 }
+int sa_m1_warp_state_bytes(int N, int dp, int n, bool counts, bool cache, bool nib) {
+  return m1_warp_state_bytes(N, dp, n, counts, cache, nib);
+}
+int sa_m1_count_bytes(int n, bool nib) { return sb_count_bytes(n, nib); }
 
 }  // namespace pip

@@ -10,6 +10,7 @@ namespace pip {
 
 constexpr int kMaxNodes = 128;      // v1 limit (R table and node ids)
 constexpr int kMaxGpus = 1024;      // v1 limit (G); N = G/tp <= 1024 slots
+constexpr int kMaxGpusPerNode = 255;   // v1 limit: stage-1 counts c_n <= gpus_per_node are bytes
 
 // One enumerated configuration (Alg.1 l.3-5) with its memory verdict (l.7) and the
 // per-config model constants of DESIGN.md section 3.  Built on the device by
@@ -27,6 +28,17 @@ constexpr int kSaCodesN8 = 120;
 #endif
 constexpr int kSaThreadsN8 = PIPETTE_N8_THREADS;
 constexpr int kSaBlocksN8 = PIPETTE_N8_BLOCKS;
+// K3 MODE 1: warps per block (one block per SM; a chunk runs as many of them as its
+// configuration's chain state fits); build-time knob for A/B runs.
+#ifndef PIPETTE_M1_WARPS
+#define PIPETTE_M1_WARPS 8
+#endif
+constexpr int kSaM1Warps = PIPETTE_M1_WARPS;
+constexpr int kSaM1PairPrefix = 2048;   // entries of the global pair list kept in shared memory
+// SaTask.pad of a MODE 1 task: warp-state stride / 16 in bits 0-15 and these flags
+constexpr uint32_t kTfCache = 1u << 16;    // Eq.5 pipeline sums cached in shared memory
+constexpr uint32_t kTfCounts = 1u << 17;   // stage-1 member counts kept (min(spn, dp) >= 2)
+constexpr uint32_t kTfDirect = 1u << 18;   // T_ex by member pairs (min(dp, n) <= 8)
 
 struct DevCfg {
   int32_t pp, tp, dp, mb;
@@ -112,7 +124,24 @@ struct SaParams {
   pipette_trace_record* trace;
   int32_t w_migrate, w_reverse;   // full move set (R21); both 0: swap only
   int32_t s1_nib;                 // MODE 1 swap kernels: stage-1 counts as nibbles (all <= 15)
+  // MODE 1: the block's R table has row stride 2^r_lg; pt = per-node pair rows in
+  // global-list order (k_partner_lists), pt_stride entries each; plen = pair-list prefix
+  // entries kept in shared memory
+  int32_t r_lg;
+  const uint32_t* pt;
+  int32_t pt_stride;
+  int32_t plen;
+  // per feasible config: beta0 = 1/T0 by self-calibration (R24, k_t0_calibrate), or null
+  const double* beta0;
 };
+
+// Inverse initial temperature of a chain (R13, R24): 1/t0 for an explicit t0 > 0, the
+// configuration's self-calibrated value when requested (t0 < 0), else 1/(tau * L(identity)).
+__device__ __forceinline__ double sa_beta0(const SaParams& P, int f, double L0) {
+  if (P.t0 > 0.0) return __ddiv_rn(1.0, P.t0);
+  if (P.beta0) return P.beta0[f];
+  return __ddiv_rn(1.0, __dmul_rn(P.tau, L0));
+}
 
 struct EvalParams {
   const DevCfg* cfgs;

@@ -560,3 +560,16 @@ def test_memory_mlp_filter_bit_exact(name):
     pip.set_memory_model(None)
     _, _, mem2, _ = pip.enumerate(model, w.bs_global)
     assert [int(x) for x in mem2] == [int(O.memory(mo, c.pp, c.tp, c.mb, c.n_mb)) for c in ref]
+
+
+@pytest.mark.parametrize("name,chains,iters,moves", [
+    ("C1", 2, 600, {}),
+    ("C2", 16, 1000, {"w_migrate": 683, "w_reverse": 682}),
+    ("C4", 32, 1000, {}),
+    ("C5", 8, 600, {}),
+])
+def test_search_self_calibrated_t0(name, chains, iters, moves):
+    # t0 < 0: SPEC S:448's self-calibrated initial temperature (R24, k_t0_calibrate) --
+    # sampled chains, traces and the plan bit-exact against the oracle's calibration
+    _sampled_chain_parity(W.WORKLOADS[name], chains=chains, iters=iters, n_sample=min(24, chains * 8), trace_n=2,
+                          t0=-1.0, **moves)
