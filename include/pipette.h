@@ -155,7 +155,11 @@ pipette_status pipette_init(pipette_ctx** out, const pipette_cluster* cluster,
                             const pipette_dist* dist);
 
 /* Replace the bandwidth matrix (host, same shape and rules as pipette_init); the
- * re-profiling step of Alg.1 l.1.  Synchronous. */
+ * re-profiling step of Alg.1 l.1.  The host computes R = 1/B and the copy and the derived
+ * tables are stream-ordered on the search stream: evals still in flight on any stream finish
+ * with the old tables (the update waits for them on the device), every later
+ * pipette_eval / pipette_search sees the new ones.  The caller's buffer may be reused on
+ * return.  No device-wide synchronisation. */
 pipette_status pipette_set_bandwidth(pipette_ctx* ctx, const double* bw_bytes_per_s);
 
 /* Stream used by pipette_search (cudaStream_t as void*; NULL = legacy default stream). */
@@ -268,6 +272,13 @@ pipette_status pipette_nccl_unique_id(void* id_out);
  * configuration) [start ns, end ns, SM id, config index e] from the device globaltimer,
  * written to out (cap tasks x 4 uint64, host).  Returns the task count (-1 on error). */
 int64_t pipette_last_task_profile(pipette_ctx* ctx, uint64_t* out, int64_t cap);
+
+/* Work plan of the last pipette_search on this rank (diagnostics and tests): out[0] K3
+ * variant (0: n <= 16 hop codes, 1: n <= 128 slot bytes, 2: wide positions), out[1] warp
+ * tasks (32 chains of one configuration each), out[2] block chunks, out[3] grid (resident
+ * blocks), out[4] warps per block, out[5] dynamic shared memory per block (bytes), out[6]
+ * of it the block's shared tables.  Writes min(cap, 7) values, returns that count. */
+int32_t pipette_last_search_stats(const pipette_ctx* ctx, int64_t* out, int32_t cap);
 
 /* Number of kernel launches the last pipette_search / pipette_eval issued. */
 int64_t pipette_last_launch_count(const pipette_ctx* ctx);

@@ -198,6 +198,13 @@ class Pipette:
     def last_launch_count(self) -> int:
         return int(self._L.pipette_last_launch_count(self._h))
 
+    def last_search_stats(self) -> dict:
+        """Work plan of the last search on this rank (pipette_last_search_stats)."""
+        out = (C.c_int64 * 7)()
+        k = int(self._L.pipette_last_search_stats(self._h, out, 7))
+        keys = ("mode", "tasks", "chunks", "grid", "warps_per_block", "smem_bytes", "table_bytes")
+        return {keys[i]: int(out[i]) for i in range(k)}
+
     def last_task_profile(self) -> np.ndarray:
         """(tasks, 4) uint64: [start ns, end ns, SM id, config e] of the last search's SA warp tasks."""
         n = int(self._L.pipette_last_task_profile(self._h, None, 0))

@@ -67,7 +67,7 @@ class Plan(C.Structure):
 
 
 EXPORTS = ("pipette_init", "pipette_enumerate", "pipette_set_bandwidth", "pipette_set_stream", "pipette_eval", "pipette_eval_models", "pipette_profile_bandwidth", "pipette_set_memory_model", "pipette_measure_peaks", "pipette_measure_smem_bw", "pipette_search",
-           "pipette_shard_items", "pipette_nccl_unique_id", "pipette_last_launch_count", "pipette_last_task_profile", "pipette_destroy",
+           "pipette_shard_items", "pipette_nccl_unique_id", "pipette_last_launch_count", "pipette_last_search_stats", "pipette_last_task_profile", "pipette_destroy",
            "pipette_last_error", "pipette_strerror")
 
 _lib = None
@@ -115,6 +115,8 @@ def lib() -> C.CDLL:
     L.pipette_nccl_unique_id.restype = C.c_int
     L.pipette_last_launch_count.argtypes = [vp]
     L.pipette_last_launch_count.restype = C.c_int64
+    L.pipette_last_search_stats.argtypes = [vp, C.POINTER(C.c_int64), C.c_int32]
+    L.pipette_last_search_stats.restype = C.c_int32
     L.pipette_last_task_profile.argtypes = [vp, P(C.c_uint64), C.c_int64]
     L.pipette_last_task_profile.restype = C.c_int64
     L.pipette_destroy.argtypes = [vp]

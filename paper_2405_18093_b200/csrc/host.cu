@@ -1,6 +1,7 @@
 // host.cu -- the C ABI of include/pipette.h: validation, context, device tables,
 // launch orchestration of K1-K6 and the NCCL combine across ranks.
 #include <nccl.h>
+#include <nvtx3/nvToolsExt.h>
 
 #include <algorithm>
 #include <cmath>
@@ -167,6 +168,15 @@ struct pipette_ctx {
   // host copies of the last uploaded SA work lists (skip identical re-uploads)
   std::vector<unsigned char> up_tasks, up_chunks, up_cfg_slot, up_slot_perm_off, up_slot_lane;
   cudaEvent_t ev[6] = {};
+  // stream ordering of the device tables (R, subset-max, sorted lists, K2's vin): a rewrite
+  // on ctx->stream waits for the evals still in flight on their streams (one event per
+  // stream an eval ran on), and every later eval/search waits for ev_tables
+  cudaEvent_t ev_tables = nullptr;
+  std::vector<std::pair<cudaStream_t, cudaEvent_t>> eval_streams;
+  double* hR = nullptr;   // pinned staging of R for the stream-ordered upload
+  struct FnAttr { const void* fn; size_t smem; int threads; int occ; };
+  std::vector<FnAttr> fn_cache;   // dynamic shared-memory limit set and occupancy, per kernel/shape
+  int64_t stats[8] = {};          // last search: mode, tasks, chunks, grid, warps/block, smem, r_bytes, launches
 };
 
 namespace {
@@ -222,6 +232,49 @@ cudaError_t ensure_up(DevBuf& b, size_t bytes, std::vector<unsigned char>& up) {
   return e;
 }
 
+// Blocks per SM of kern at (threads, smem); the kernel's dynamic shared-memory limit is
+// raised once per size (cached: no attribute call or occupancy query per launch).
+pipette_status kernel_occupancy(pipette_ctx* ctx, const void* kern, int threads, size_t smem, int* occ) {
+  for (const auto& a : ctx->fn_cache)
+    if (a.fn == kern && a.smem == smem && a.threads == threads) { *occ = a.occ; return PIPETTE_OK; }
+  CU(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  int o = 0;
+  CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, kern, threads, smem));
+  o = std::max(o, 1);
+  ctx->fn_cache.push_back({kern, smem, threads, o});
+  *occ = o;
+  return PIPETTE_OK;
+}
+
+// Table updates happen on ctx->stream between tables_begin (wait for every eval in flight)
+// and tables_end (record ev_tables); a launch on stream s first waits for ev_tables.
+cudaError_t tables_begin(pipette_ctx* ctx) {
+  for (const auto& se : ctx->eval_streams)
+    if (se.first != ctx->stream) {
+      cudaError_t e = cudaStreamWaitEvent(ctx->stream, se.second, 0);
+      if (e != cudaSuccess) return e;
+    }
+  return cudaSuccess;
+}
+cudaError_t tables_end(pipette_ctx* ctx) { return cudaEventRecord(ctx->ev_tables, ctx->stream); }
+cudaError_t wait_tables(pipette_ctx* ctx, cudaStream_t s) { return cudaStreamWaitEvent(s, ctx->ev_tables, 0); }
+// an eval was launched on s: the next table rewrite waits for it
+cudaError_t note_eval(pipette_ctx* ctx, cudaStream_t s) {
+  for (auto& se : ctx->eval_streams)
+    if (se.first == s) return cudaEventRecord(se.second, s);
+  if (ctx->eval_streams.size() >= 16) {   // many streams: keep the table rewrites safe by a device sync
+    for (auto& se : ctx->eval_streams) cudaEventDestroy(se.second);
+    ctx->eval_streams.clear();
+    cudaError_t e = cudaDeviceSynchronize();
+    if (e != cudaSuccess) return e;
+  }
+  cudaEvent_t ev;
+  cudaError_t e = cudaEventCreateWithFlags(&ev, cudaEventDisableTiming);
+  if (e != cudaSuccess) return e;
+  ctx->eval_streams.push_back({s, ev});
+  return cudaEventRecord(ev, s);
+}
+
 int n_div(long long n) {
   int c = 0;
   for (long long d = 1; d * d <= n; ++d)
@@ -237,33 +290,36 @@ pipette_status check_bw(pipette_ctx* ctx, const double* bw, int n) {
   return PIPETTE_OK;
 }
 
+// R = 1/B (R5, IEEE division on the host) and the tables derived from it, uploaded in
+// stream order on ctx->stream (pinned staging, no device-wide synchronisation): evals in
+// flight finish with the old tables, every later call sees the new ones.
 pipette_status upload_bw(pipette_ctx* ctx, const double* bw) {
   const int n = ctx->n_nodes;
-  std::vector<double> R((size_t)n * n);
-  for (int i = 0; i < n * n; ++i) R[i] = 1.0 / bw[i];  // R5: IEEE division, never symmetrised
-  CU(cudaMemcpy(ctx->dR, R.data(), sizeof(double) * n * n, cudaMemcpyHostToDevice));
-  if (n <= 16) {
-    if (!ctx->dTab) CU(cudaMalloc(&ctx->dTab, sizeof(double) << n));
-    k_subset_max<<<((1 << n) + 255) / 256, 256>>>(ctx->dR, n, ctx->dTab);
-    CU(cudaGetLastError());
-    CU(cudaDeviceSynchronize());
-  }
-  if (n >= 2) {   // sorted partner / pair lists (MODE 1 and 2 stage-1 searches)
-    const size_t L1 = (size_t)n * 2 * (n - 1), L2 = (size_t)n * (n - 1);
-    if (!ctx->dNlNode) {
-      CU(cudaMalloc(&ctx->dNlNode, L1));
-      CU(cudaMalloc(&ctx->dNlVal, sizeof(double) * L1));
-      CU(cudaMalloc(&ctx->dGlAb, sizeof(uint16_t) * L2));
-      CU(cudaMalloc(&ctx->dGlVal, sizeof(double) * L2));
-    }
+  if (!ctx->hR) CU(cudaMallocHost(&ctx->hR, sizeof(double) * n * n));
+  CU(cudaEventSynchronize(ctx->ev_tables));   // the previous upload has left the staging buffer
+  for (int i = 0; i < n * n; ++i) ctx->hR[i] = 1.0 / bw[i];  // R5: IEEE division, never symmetrised
+  if (n <= 16 && !ctx->dTab) CU(cudaMalloc(&ctx->dTab, sizeof(double) << n));
+  const size_t L1 = (size_t)n * 2 * (n - 1), L2 = (size_t)n * (n - 1);
+  if (n >= 2 && !ctx->dNlNode) {   // sorted partner / pair lists (MODE 1 and 2 stage-1 searches)
+    CU(cudaMalloc(&ctx->dNlNode, L1));
+    CU(cudaMalloc(&ctx->dNlVal, sizeof(double) * L1));
+    CU(cudaMalloc(&ctx->dGlAb, sizeof(uint16_t) * L2));
+    CU(cudaMalloc(&ctx->dGlVal, sizeof(double) * L2));
     ctx->pt_stride = ((2 * (n - 1)) + 3) & ~3;
-    if (!ctx->dPt) CU(cudaMalloc(&ctx->dPt, sizeof(uint32_t) * (size_t)n * ctx->pt_stride));
-    k_node_lists<<<n, 256>>>(ctx->dR, n, ctx->dNlNode, ctx->dNlVal);
-    k_pair_list<<<(unsigned)((L2 + 255) / 256), 256>>>(ctx->dR, n, ctx->dGlAb, ctx->dGlVal);
-    k_partner_lists<<<n, 32>>>(ctx->dGlAb, n, ctx->dPt, ctx->pt_stride);
-    CU(cudaGetLastError());
-    CU(cudaDeviceSynchronize());
+    CU(cudaMalloc(&ctx->dPt, sizeof(uint32_t) * (size_t)n * ctx->pt_stride));
   }
+  cudaStream_t s = ctx->stream;
+  CU(tables_begin(ctx));
+  CU(cudaMemcpyAsync(ctx->dR, ctx->hR, sizeof(double) * n * n, cudaMemcpyHostToDevice, s));
+  if (n <= 16) k_subset_max<<<((1 << n) + 255) / 256, 256, 0, s>>>(ctx->dR, n, ctx->dTab);
+  if (n >= 2) {
+    k_node_lists<<<n, 256, 0, s>>>(ctx->dR, n, ctx->dNlNode, ctx->dNlVal);
+    k_pair_list<<<(unsigned)((L2 + 255) / 256), 256, 0, s>>>(ctx->dR, n, ctx->dGlAb, ctx->dGlVal);
+    k_partner_lists<<<n, 32, 0, s>>>(ctx->dGlAb, n, ctx->dPt, ctx->pt_stride);
+  }
+  CU(cudaGetLastError());
+  CU(tables_end(ctx));
+  ctx->vin_valid = false;
   return PIPETTE_OK;
 }
 
@@ -341,6 +397,13 @@ pipette_status build_plan(pipette_ctx* ctx, int chains, int W, int r, const char
   std::vector<SaTask>& sorted = hp.sorted;
   sorted.resize(tasks.size());
   for (size_t i = 0; i < order.size(); ++i) sorted[i] = tasks[order[i]];
+  if (const char* only = getenv("PIPETTE_DIAG_ONLY_CFG")) {   // diagnostics (per-config profiles):
+    const int e = atoi(only);                                // run only configuration e's tasks;
+    std::vector<SaTask> keep;                                // the plan is then meaningless
+    for (const SaTask& t : sorted)
+      if (t.cfg == e) keep.push_back(t);
+    sorted.swap(keep);
+  }
 
   const int n = ctx->n_nodes;
   // MODE 0 (n <= 16): packed positions, register stage-1 state, lane-replicated R,
@@ -354,8 +417,10 @@ pipette_status build_plan(pipette_ctx* ctx, int chains, int W, int r, const char
     // the pair-list prefix; a chunk of a configuration runs as many warps as that
     // configuration's chain state fits in the rest of shared memory.  Per configuration:
     // stage-1 counts when some node can hold >= 2 members, T_ex by member pairs when N1
-    // never exceeds 8 nodes, and the pipeline-sum cache unless it costs more than a few
-    // resident warps (PIPETTE_M1_CACHE_MIN).
+    // never exceeds 8 nodes, and the pipeline-sum cache when it saves re-summing long
+    // pipelines (pp >= PIPETTE_M1_CACHE_PP, default 2; the old sums of the two touched
+    // pipelines are otherwise re-summed) and costs at most a few resident warps
+    // (PIPETTE_M1_CACHE_MIN).
     int lg = 0;
     while ((1 << lg) < n) ++lg;
     const int plen = std::min(n * (n - 1), kSaM1PairPrefix);
@@ -368,6 +433,8 @@ pipette_status build_plan(pipette_ctx* ctx, int chains, int W, int r, const char
     }
     const char* cm_env = getenv("PIPETTE_M1_CACHE_MIN");
     const int cache_min = cm_env ? atoi(cm_env) : 6;
+    const char* cp_env = getenv("PIPETTE_M1_CACHE_PP");
+    const int cache_pp = cp_env ? atoi(cp_env) : 2;
     std::vector<int> fbytes(F), fwarps(F);
     std::vector<uint32_t> fflags(F);
     for (int f = 0; f < F; ++f) {
@@ -378,7 +445,7 @@ pipette_status build_plan(pipette_ctx* ctx, int chains, int W, int r, const char
                                   : sa_m1_warp_state_bytes(c.N, c.dp, n, counts, false, nib);
       const int with = sa_m1_warp_state_bytes(c.N, c.dp, n, counts, true, nib);
       const int w_nc = std::min(kSaM1Warps, avail / base), w_c = std::min(kSaM1Warps, avail / with);
-      const bool cache = !full_moves && c.pp >= 2 && w_c >= 1 && w_c >= std::min(w_nc, cache_min);
+      const bool cache = !full_moves && c.pp >= std::max(2, cache_pp) && w_c >= 1 && w_c >= std::min(w_nc, cache_min);
       fbytes[f] = cache ? with : base;
       fwarps[f] = cache ? w_c : w_nc;
       if (fwarps[f] < 1)
@@ -533,6 +600,13 @@ const char* pipette_last_error(const pipette_ctx* ctx) { return ctx ? ctx->err.c
 
 int64_t pipette_last_launch_count(const pipette_ctx* ctx) { return ctx ? ctx->launches : 0; }
 
+int32_t pipette_last_search_stats(const pipette_ctx* ctx, int64_t* out, int32_t cap) {
+  if (!ctx || !out) return 0;
+  const int32_t k = std::min<int32_t>(cap, 7);
+  for (int32_t i = 0; i < k; ++i) out[i] = ctx->stats[i];
+  return k;
+}
+
 int64_t pipette_last_task_profile(pipette_ctx* ctx, uint64_t* out, int64_t cap) {
   if (!ctx || ctx->n_tasks_last <= 0 || !ctx->task_prof.p) return 0;
   const int64_t n = ctx->n_tasks_last;
@@ -660,9 +734,13 @@ pipette_status pipette_init(pipette_ctx** out, const pipette_cluster* cl, const 
       fail(ctx, PIPETTE_E_CUDA, "profile upload failed");
       return bail(PIPETTE_E_CUDA);
     }
-    if ((st = upload_bw(ctx, bw)) != PIPETTE_OK) return bail(st);
     for (auto& e : ctx->ev)
       if (cudaEventCreate(&e) != cudaSuccess) { fail(ctx, PIPETTE_E_CUDA, "event create failed"); return bail(PIPETTE_E_CUDA); }
+    if (cudaEventCreateWithFlags(&ctx->ev_tables, cudaEventDisableTiming) != cudaSuccess) {
+      fail(ctx, PIPETTE_E_CUDA, "event create failed");
+      return bail(PIPETTE_E_CUDA);
+    }
+    if ((st = upload_bw(ctx, bw)) != PIPETTE_OK) return bail(st);
   }
   if (ctx->world > 1) {
     ncclUniqueId id;
@@ -679,9 +757,7 @@ pipette_status pipette_set_bandwidth(pipette_ctx* ctx, const double* bw) {
   pipette_status st = check_bw(ctx, bw, ctx->n_nodes);
   if (st != PIPETTE_OK) return st;
   CU(cudaSetDevice(ctx->device));
-  CU(cudaStreamSynchronize(ctx->stream));
-  ctx->vin_valid = false;
-  return upload_bw(ctx, bw);
+  return upload_bw(ctx, bw);   // stream-ordered (tables_begin / tables_end)
 }
 
 pipette_status pipette_set_stream(pipette_ctx* ctx, void* stream) {
@@ -710,6 +786,9 @@ void pipette_destroy(pipette_ctx* ctx) {
   if (ctx->dProf) cudaFree(ctx->dProf);
   for (auto& e : ctx->ev)
     if (e) cudaEventDestroy(e);
+  if (ctx->ev_tables) cudaEventDestroy(ctx->ev_tables);
+  for (auto& se : ctx->eval_streams) cudaEventDestroy(se.second);
+  if (ctx->hR) cudaFreeHost(ctx->hR);
   delete ctx;
 }
 
@@ -758,12 +837,14 @@ pipette_status pipette_eval(pipette_ctx* ctx, const pipette_model* model, int64_
   P.qtab = (const double*)ctx->qtab.p;
   P.R = ctx->dR;
   P.subset_max = ctx->dTab;
-  if (mode == 0 && !ctx->vin_valid) {
+  if (mode == 0 && !ctx->vin_valid) {   // a table rewrite: ordered on ctx->stream after evals in flight
     CU(ensure(ctx->vin, sizeof(double) * 256 * (size_t)std::max(1, ctx->E)));
-    k_tin_values<<<std::max(1, ctx->E), 256, 0, s>>>((const DevCfg*)ctx->cfgs.p, (const double*)ctx->qtab.p, ctx->dR,
-                                                    ctx->n_nodes, (double*)ctx->vin.p);
+    CU(tables_begin(ctx));
+    k_tin_values<<<std::max(1, ctx->E), 256, 0, ctx->stream>>>((const DevCfg*)ctx->cfgs.p, (const double*)ctx->qtab.p,
+                                                              ctx->dR, ctx->n_nodes, (double*)ctx->vin.p);
     ctx->launches++;
     CU(cudaGetLastError());
+    CU(tables_end(ctx));
     ctx->vin_valid = true;
   }
   P.vin = (const double*)ctx->vin.p;
@@ -787,16 +868,18 @@ pipette_status pipette_eval(pipette_ctx* ctx, const pipette_model* model, int64_
   if (smem > 227 * 1024) return fail(ctx, PIPETTE_E_UNSUPPORTED, "eval shared memory %zu B too large", smem);
   if (ctx->E >= 32767) return fail(ctx, PIPETTE_E_UNSUPPORTED, "eval supports < 32767 enumerated configurations");
   const void* kern = eval_kernel(mode);
-  CU(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   int occ = 0;
-  CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, 256, smem));
-  occ = std::max(occ, 1);
+  if ((st = kernel_occupancy(ctx, kern, 256, smem, &occ)) != PIPETTE_OK) return st;
   const long long need = (n + eval_tile_size() - 1) / eval_tile_size();   // candidate tiles
   const int grid = (int)std::min<long long>(need, (long long)occ * ctx->n_sms);
   void* args[] = {&P};
+  nvtxRangePushA("pipette_eval K2");
+  CU(wait_tables(ctx, s));
   CU(cudaLaunchKernel(kern, dim3(grid), dim3(256), args, smem, s));
   ctx->launches++;
   CU(cudaGetLastError());
+  CU(note_eval(ctx, s));
+  nvtxRangePop();
   return PIPETTE_OK;
 }
 
@@ -814,11 +897,13 @@ pipette_status pipette_eval_models(pipette_ctx* ctx, const pipette_model* model,
     return fail(ctx, PIPETTE_E_INVALID, "null device pointer");
   CU(cudaSetDevice(ctx->device));
   if ((st = enumerate(ctx, model, bs_global, false)) != PIPETTE_OK) return st;
+  CU(wait_tables(ctx, (cudaStream_t)stream));
   st = models_launch((const DevCfg*)ctx->cfgs.p, (const unsigned long long*)ctx->keys.p, ctx->E,
                      (const double*)ctx->qtab.p, ctx->dR, ctx->n_nodes, n, d_cfg, d_perm, perm_stride, d_t_pipette,
                      d_t_prev, d_t_des, d_status, stream);
   ctx->launches++;
   if (st != PIPETTE_OK) return fail(ctx, st, "k_models launch failed: %s", cudaGetErrorString(cudaGetLastError()));
+  CU(note_eval(ctx, (cudaStream_t)stream));
   return PIPETTE_OK;
 }
 
@@ -841,8 +926,13 @@ pipette_status pipette_search(pipette_ctx* ctx, const pipette_model* model, int6
     return fail(ctx, PIPETTE_E_INVALID, "move weights must satisfy 0 <= w_migrate, w_reverse and sum <= 2048");
   CU(cudaSetDevice(ctx->device));
   cudaStream_t s = ctx->stream;
+  nvtxRangePushA("pipette_search");
+  struct NvtxPop { ~NvtxPop() { nvtxRangePop(); } } nvtx_pop_;   // (every return path)
 
+  CU(wait_tables(ctx, s));   // (the stream may have changed since the last table update)
+  nvtxRangeId_t nv = nvtxRangeStartA("K1 enumerate + memory filter");
   if ((st = enumerate(ctx, model, bs_global, true)) != PIPETTE_OK) return st;
+  nvtxRangeEnd(nv);
   const int E = ctx->E, F = ctx->F;
   out->configs_enumerated = E;
   out->configs_rejected_oom = E - F;
@@ -998,11 +1088,12 @@ pipette_status pipette_search(pipette_ctx* ctx, const pipette_model* model, int6
   P.plen = pl.plen;
 
   const void* kern = sa_kernel(mode, tracing, n, o.w_migrate || o.w_reverse);
-  CU(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   int occ = 0;
-  CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, wpb * 32, smem));
-  occ = std::max(occ, 1);
+  if ((st = kernel_occupancy(ctx, kern, wpb * 32, smem, &occ)) != PIPETTE_OK) return st;
   const int grid = (int)std::max<long long>(1, std::min<long long>((long long)chunks.size(), (long long)occ * ctx->n_sms));
+  ctx->stats[0] = mode; ctx->stats[1] = (int64_t)sorted.size(); ctx->stats[2] = (int64_t)chunks.size();
+  ctx->stats[3] = grid; ctx->stats[4] = wpb; ctx->stats[5] = (int64_t)smem; ctx->stats[6] = r_bytes;
+  nv = nvtxRangeStartA("K3 sa_chains (+ T_in lists, T0 calibration)");
   CU(cudaEventRecord(ctx->ev[2], s));
   if (mode == 0) {
     k_tin_rank<<<F, 256, 0, s>>>((const DevCfg*)ctx->cfgs.p, (const int*)ctx->feas.p, (const double*)ctx->qtab.p,
@@ -1029,11 +1120,15 @@ pipette_status pipette_search(pipette_ctx* ctx, const pipette_model* model, int6
     CU(cudaGetLastError());
   }
   CU(cudaEventRecord(ctx->ev[3], s));
+  nvtxRangeEnd(nv);
+  nv = nvtxRangeStartA("K4 argmin");
   k_argmin<<<F, 256, 0, s>>>((const ChainOut*)ctx->chain_out.p, (const int*)ctx->cfg_slot.p, F,
                               (CfgBest*)ctx->cfg_best.p);
   ctx->launches++;
   CU(cudaGetLastError());
   CU(cudaEventRecord(ctx->ev[4], s));
+  nvtxRangeEnd(nv);
+  nv = nvtxRangeStartA("combine (NCCL allreduce min, min, sum)");
 
   // ---- combine (R18): min latency bits, then min item among ranks attaining it, then
   //      the owners' plans (one fused allreduce(sum) of owner-only rows)
@@ -1059,6 +1154,7 @@ pipette_status pipette_search(pipette_ctx* ctx, const pipette_model* model, int6
   CU(cudaGetLastError());
   if (W > 1) NC(ncclAllReduce(pack, pack, (size_t)F * row_words + 1, ncclUint64, ncclSum, ctx->comm, s));
   CU(cudaEventRecord(ctx->ev[5], s));
+  nvtxRangeEnd(nv);
 
   std::vector<unsigned long long> hb(F), hi(F), hp((size_t)F * row_words + 1);
   CU(cudaMemcpyAsync(hb.data(), gbits, sizeof(unsigned long long) * F, cudaMemcpyDeviceToHost, s));

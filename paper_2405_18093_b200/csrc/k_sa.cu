@@ -1386,15 +1386,7 @@ __global__ void __launch_bounds__(SaLB<MODE, BIG, NW>::threads, SaLB<MODE, BIG, 
         default: run_task_hc<TRACE, 0, NW>(P, T, C, Tl, SS, ws, lane); break;
       }
     } else if constexpr (MODE == 1) {
-      switch (C.pp) {
-        case 1: run_task_sb<TRACE, 1>(P, T, C, Rs, pl_s, ws, lane); break;
-        case 2: run_task_sb<TRACE, 2>(P, T, C, Rs, pl_s, ws, lane); break;
-        case 4: run_task_sb<TRACE, 4>(P, T, C, Rs, pl_s, ws, lane); break;
-        case 8: run_task_sb<TRACE, 8>(P, T, C, Rs, pl_s, ws, lane); break;
-        case 16: run_task_sb<TRACE, 16>(P, T, C, Rs, pl_s, ws, lane); break;
-        case 32: run_task_sb<TRACE, 32>(P, T, C, Rs, pl_s, ws, lane); break;
-        default: run_task_sb<TRACE, 0>(P, T, C, Rs, pl_s, ws, lane); break;
-      }
+      run_task_sb_pp<TRACE, false>(P, T, C, Rs, pl_s, ws, lane);
     } else {
       switch (C.pp) {
         case 1: run_task<POS, S1, RT, TRACE, 1>(P, T, C, R, ws, lane); break;

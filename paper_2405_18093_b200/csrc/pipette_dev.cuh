@@ -34,7 +34,9 @@ constexpr int kSaBlocksN8 = PIPETTE_N8_BLOCKS;
 #define PIPETTE_M1_WARPS 8
 #endif
 constexpr int kSaM1Warps = PIPETTE_M1_WARPS;
-constexpr int kSaM1PairPrefix = 2048;   // entries of the global pair list kept in shared memory
+// entries of the global pair list kept in shared memory (list-mode witness scans start at
+// the old witness's rank, expected (n/k)^2 <= 64 probes for |N1| >= 16 at n = 128)
+constexpr int kSaM1PairPrefix = 1024;
 // SaTask.pad of a MODE 1 task: warp-state stride / 16 in bits 0-15 and these flags
 constexpr uint32_t kTfCache = 1u << 16;    // Eq.5 pipeline sums cached in shared memory
 constexpr uint32_t kTfCounts = 1u << 17;   // stage-1 member counts kept (min(spn, dp) >= 2)

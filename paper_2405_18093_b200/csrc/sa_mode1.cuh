@@ -27,7 +27,9 @@
 constexpr int kNoWit = 0x7fffffff;         // no T_ex witness (|N1| < 2)
 
 // Block context of MODE 1 (also used by the full move set of MODE 0 with its hop-code table).
-struct SbCtx {
+// ID: every node holds one slot (spn = 1), so node(slot) = slot.
+template <bool ID = false>
+struct SbCtxT {
   const double* T;   // MODE 1: R = 1/B, row stride 2^lg; MODE 0: the 16-copy m2*R hop-code table
   double m2;
   uint32_t lg;
@@ -36,14 +38,15 @@ struct SbCtx {
   uint32_t m16;      // ceil(2^16 / spn)
   // node = floor(slot / spn) as (slot * m16) >> 16: exact for slot < 256 and spn < 256
   // (the error slot * (m16 - 2^16/spn) / 2^16 < 1/256 never crosses an integer)
-  __device__ __forceinline__ uint32_t node(uint32_t slot) const { return (slot * m16) >> 16; }
+  __device__ __forceinline__ uint32_t node(uint32_t slot) const { return ID ? slot : (slot * m16) >> 16; }
   __device__ __forceinline__ double r(uint32_t a, uint32_t b) const { return T[(a << lg) + b]; }
   // the Eq.5 hop term fl(m2 * R[a][b]) (MODE 1)
   __device__ __forceinline__ double hop(uint32_t a, uint32_t b) const { return __dmul_rn(m2, r(a, b)); }
 };
+using SbCtx = SbCtxT<false>;
 
-template <int PP>
-__device__ __forceinline__ double sb_sum(const HcState& st, uint32_t z, int pp_rt, const SbCtx& K) {
+template <int PP, class KT>
+__device__ __forceinline__ double sb_sum(const HcState& st, uint32_t z, int pp_rt, const KT& K) {
   double s = 0.0;
   if constexpr (PP >= 4) {
     constexpr int NW = PP / 4;
@@ -71,8 +74,8 @@ __device__ __forceinline__ double sb_sum(const HcState& st, uint32_t z, int pp_r
 }
 
 // Two pipelines in one interleaved loop (two independent DMUL/DADD chains); za == zb allowed.
-template <int PP>
-__device__ __forceinline__ void sb_sum2(const HcState& st, uint32_t za, uint32_t zb, int pp_rt, const SbCtx& K,
+template <int PP, class KT>
+__device__ __forceinline__ void sb_sum2(const HcState& st, uint32_t za, uint32_t zb, int pp_rt, const KT& K,
                                         double& sa, double& sb) {
   double a = 0.0, b = 0.0;
   if constexpr (PP >= 4) {
@@ -110,25 +113,43 @@ __device__ __forceinline__ void sb_sum2(const HcState& st, uint32_t za, uint32_t
   sb = b;
 }
 
-// max over all dp pipelines of the Eq.5 sums and its multiplicity, from the slot plane
-template <int PP>
-__device__ __forceinline__ void sb_rescan(const HcState& st, int dp, int pp_rt, const SbCtx& K, double& mx, int& cnt) {
-  double m0 = 0.0, m1 = 0.0;
-  int c0 = 0, c1 = 0;
-  auto acc = [](double v, double& m, int& c) {
-    c = v > m ? 1 : c + (v == m ? 1 : 0);
-    m = fmax(m, v);
-  };
-  int z = 0;
-  for (; z + 2 <= dp; z += 2) {
-    double a, b;
-    sb_sum2<PP>(st, (uint32_t)z, (uint32_t)z + 1u, pp_rt, K, a, b);
-    acc(a, m0, c0);
-    acc(b, m1, c1);
+// T_PP of a lane's tentative mapping when its unique max pipeline decreased: the max over
+// all dp Eq.5 sums and its multiplicity, computed by the whole warp (called converged).
+// For each flagged lane L, lane j takes pipelines j, j + 32, ... -- lane L's cached sums
+// with the two touched pipelines substituted (cache), or re-summed in stage order from lane
+// L's slot plane, which already holds the tentative swap.  The reads hit one bank (lane L's
+// column), so they cost shared-memory wavefronts, not the divergent per-lane loop over all
+// dp pipelines that one lane's rescan would make its warp execute.
+template <int PP, class KT>
+__device__ __forceinline__ void coop_tpp(bool need, unsigned char* ws, const double* psum, bool cache, int dp, int pp,
+                                         uint32_t zp, uint32_t zb, double sA, double sB, const KT& K, int lane,
+                                         double& tpp2, int& nmax2) {
+  const unsigned full = 0xffffffffu;
+  for (unsigned todo = __ballot_sync(full, need); todo; todo &= todo - 1u) {
+    const int L = __ffs(todo) - 1;
+    const uint32_t zpL = __shfl_sync(full, zp, L), zbL = __shfl_sync(full, zb, L);
+    const double sAL = __shfl_sync(full, sA, L), sBL = __shfl_sync(full, sB, L);
+    HcState stL;
+    stL.hb = ws + L * 4;
+    stL.sb = stL.hb;
+    stL.hw = reinterpret_cast<const uint32_t*>(ws) + L;
+    double m = 0.0;
+    int c = 0;
+    for (int z = lane; z < dp; z += 32) {
+      const double v = cache ? ((uint32_t)z == zpL ? sAL : ((uint32_t)z == zbL ? sBL : psum[z * 32 + L]))
+                             : sb_sum<PP, KT>(stL, (uint32_t)z, pp, K);
+      c = v > m ? 1 : c + (v == m ? 1 : 0);
+      m = fmax(m, v);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {   // (max, count at max) over the lanes
+      const double m2 = __shfl_xor_sync(full, m, o);
+      const int c2 = __shfl_xor_sync(full, c, o);
+      c = m2 > m ? c2 : (m2 == m ? c + c2 : c);
+      m = fmax(m, m2);
+    }
+    if (lane == L) { tpp2 = m; nmax2 = c; }
   }
-  if (z < dp) acc(sb_sum<PP>(st, (uint32_t)z, pp_rt, K), m0, c0);
-  mx = fmax(m0, m1);
-  cnt = (m0 == mx ? c0 : 0) + (m1 == mx ? c1 : 0);
 }
 
 // [slot plane][stage-1 counts: bytes, or nibbles when nib][psum]
@@ -167,7 +188,8 @@ struct S1M {
   }
 
   // max over ordered member pairs a != b of m of R[a][b], with a witness pair
-  static __device__ __forceinline__ double pairs_max(const Mask4& m, const SbCtx& K, uint32_t& wab_o) {
+  template <class KT>
+  static __device__ __forceinline__ double pairs_max(const Mask4& m, const KT& K, uint32_t& wab_o) {
     double mx = 0.0;
     uint32_t w = 0xffffu;
 #pragma unroll
@@ -193,7 +215,8 @@ struct S1M {
     return mx;
   }
   // max over members b != u of m of R[u][b] and R[b][u]
-  static __device__ __forceinline__ double join_max(const Mask4& m, uint32_t u, const SbCtx& K, uint32_t& wab_o) {
+  template <class KT>
+  static __device__ __forceinline__ double join_max(const Mask4& m, uint32_t u, const KT& K, uint32_t& wab_o) {
     double mx = 0.0;
     uint32_t w = 0xffffu;
 #pragma unroll
@@ -240,7 +263,8 @@ struct S1M {
     if (counts) add(a, +1);
     mask.set(a);
   }
-  __device__ __forceinline__ void finish_init(const S1Ctx& X, const SbCtx& K) {
+  template <class KT>
+  __device__ __forceinline__ void finish_init(const S1Ctx& X, const KT& K) {
     k = mask.count();
     tin = 0.0;
     win = -1;
@@ -268,7 +292,8 @@ struct S1M {
   }
 
   // a stage-1 member moves from node dn to node up (tentative); long searches are flagged
-  __device__ __forceinline__ void propose(uint32_t dn, uint32_t up, const S1Ctx& X, const SbCtx& K) {
+  template <class KT>
+  __device__ __forceinline__ void propose(uint32_t dn, uint32_t up, const S1Ctx& X, const KT& K) {
     dn_ = dn; up_ = up;
     const uint32_t cd = counts ? get_of(dn, lane) : 1u, cu = counts ? get_of(up, lane) : 0u;
     c_dn_ = cd - 1u; c_up_ = cu + 1u;
@@ -317,7 +342,8 @@ struct S1M {
   }
 
   // warp-cooperative searches (called by all 32 lanes, converged)
-  __device__ __forceinline__ void coop(const S1Ctx& X, const SbCtx& K) {
+  template <class KT>
+  __device__ __forceinline__ void coop(const S1Ctx& X, const KT& K) {
     const unsigned full = 0xffffffffu;
     if (counts) {   // T_in: first (a, c) entry (by value) whose node has c members after the move
       unsigned todo = __ballot_sync(full, need_tin);
@@ -432,7 +458,7 @@ struct S1M {
 // ------------------------------------------------------------------ one warp task of MODE 1
 // Same step structure as run_task_hc: the swap is applied tentatively, the touched
 // pipelines are re-summed in stage order, T_PP keeps the count of pipelines at its max.
-template <bool TRACE, int PP>
+template <bool TRACE, int PP, bool ID>
 __device__ __forceinline__ void run_task_sb(const SaParams& P, const SaTask T, const DevCfg C, const double* Rt,
                                             const uint16_t* pl, unsigned char* ws, int lane) {
   const bool active = lane < T.count;
@@ -449,7 +475,7 @@ __device__ __forceinline__ void run_task_sb(const SaParams& P, const SaTask T, c
   X.nl_len = 2 * (n - 1);
   X.n = n;
   X.pt = P.pt; X.pt_stride = P.pt_stride; X.pl = pl; X.plen = P.plen;
-  SbCtx K;
+  SbCtxT<ID> K;
   K.T = Rt; K.m2 = C.m2; K.lg = (uint32_t)P.r_lg; K.n = n;
   K.spn = (uint32_t)C.spn; K.spn_magic = C.spn_magic;
   K.spn_sh = (C.spn & (C.spn - 1)) == 0 ? (uint32_t)(31 - __clz(C.spn)) : 32u;
@@ -481,7 +507,7 @@ __device__ __forceinline__ void run_task_sb(const SaParams& P, const SaTask T, c
   for (int z = 0; z < dp; ++z) {
     s1.add_init(K.node((uint32_t)(z * pp)));
     if (pp >= 2) {
-      const double s = sb_sum<PP>(st, (uint32_t)z, pp, K);
+      const double s = sb_sum<PP, SbCtxT<ID>>(st, (uint32_t)z, pp, K);
       if (cache) psum[z * 32 + lane] = s;
       if (s > tpp) { tpp = s; nmax = 1; } else if (s == tpp) { ++nmax; }
     }
@@ -520,40 +546,37 @@ __device__ __forceinline__ void run_task_sb(const SaParams& P, const SaTask T, c
           oldA = psum[zp * 32 + lane];
           oldB = psum[zb * 32 + lane];
         } else {
-          sb_sum2<PP>(st, zp, zb, pp, K, oldA, oldB);
+          sb_sum2<PP, SbCtxT<ID>>(st, zp, zb, pp, K, oldA, oldB);
         }
         *bp = (uint8_t)sq;   // tentative swap
         *bq = (uint8_t)sp;
         double sA, sB;
-        sb_sum2<PP>(st, zp, zb, pp, K, sA, sB);
+        sb_sum2<PP, SbCtxT<ID>>(st, zp, zb, pp, K, sA, sB);
         double tpp2 = tpp;
         int nmax2 = nmax;
         const double snew = fmax(sA, sB);
         const int keep = nmax - (oldA == tpp ? 1 : 0) - ((two && oldB == tpp) ? 1 : 0);
-        if (keep > 0 || snew >= tpp) {
+        const bool fast = keep > 0 || snew >= tpp;
+        if (fast) {
           tpp2 = (keep > 0) ? fmax(tpp, snew) : snew;
           nmax2 = (keep > 0 && tpp2 == tpp ? keep : 0) + (sA == tpp2 ? 1 : 0) + ((two && sB == tpp2) ? 1 : 0);
-        } else if (cache) {
-          double m0 = sA, m1 = two ? sB : 0.0;
-          int c0 = 1, c1 = two ? 1 : 0;
-          int z = 0;
-          for (; z + 2 <= dp; z += 2) {
-            const double v0 = ((uint32_t)z == zp || (uint32_t)z == zq) ? 0.0 : psum[z * 32 + lane];
-            const double v1 = ((uint32_t)z + 1u == zp || (uint32_t)z + 1u == zq) ? 0.0 : psum[(z + 1) * 32 + lane];
-            c0 = v0 > m0 ? 1 : c0 + (v0 == m0 ? 1 : 0);
-            m0 = fmax(m0, v0);
-            c1 = v1 > m1 ? 1 : c1 + (v1 == m1 ? 1 : 0);
-            m1 = fmax(m1, v1);
+        }
+        // the unique max pipeline decreased: rescan over all pipelines -- a few cached sums
+        // per lane, else warp-cooperatively
+        if (cache && dp <= 16) {
+          if (!fast) {
+            double m = 0.0;
+            int c = 0;
+            for (int z = 0; z < dp; ++z) {
+              const double v = (uint32_t)z == zp ? sA : ((uint32_t)z == zb ? sB : psum[z * 32 + lane]);
+              c = v > m ? 1 : c + (v == m ? 1 : 0);
+              m = fmax(m, v);
+            }
+            tpp2 = m;
+            nmax2 = c;
           }
-          if (z < dp) {
-            const double v0 = ((uint32_t)z == zp || (uint32_t)z == zq) ? 0.0 : psum[z * 32 + lane];
-            c0 = v0 > m0 ? 1 : c0 + (v0 == m0 ? 1 : 0);
-            m0 = fmax(m0, v0);
-          }
-          tpp2 = fmax(m0, m1);
-          nmax2 = (m0 == tpp2 ? c0 : 0) + (m1 == tpp2 ? c1 : 0);
         } else {
-          sb_rescan<PP>(st, dp, pp, K, tpp2, nmax2);
+          coop_tpp<PP, SbCtxT<ID>>(!fast, ws, psum, cache, dp, pp, zp, zb, sA, sB, K, lane, tpp2, nmax2);
         }
         dpchg = ((xp == 0u) != (xq == 0u)) && np != nq;
         if (dpchg) {
@@ -611,5 +634,23 @@ __device__ __forceinline__ void run_task_sb(const SaParams& P, const SaTask T, c
     o.best = best; o.best_tpp = best_tpp; o.best_tdp = best_tdp; o.L0 = L0;
     o.best_step = best_step; o.accepted = accepted; o.f = T.f; o.c = (int32_t)chain;
     P.out[slot] = o;
+  }
+}
+
+// Compile-time pipeline depth for the common power-of-two depths (the Eq.5 sums unroll).
+// (ID = true, node(slot) = slot for spn = 1, saves two instructions per node read, but
+// with both variants in one kernel ptxas spills in the hot loop at 255 registers, and as
+// separate non-inlined functions too; only the general variant is instantiated.)
+template <bool TRACE, bool ID>
+__device__ __forceinline__ void run_task_sb_pp(const SaParams& P, const SaTask T, const DevCfg C, const double* Rt,
+                                               const uint16_t* pl, unsigned char* ws, int lane) {
+  switch (C.pp) {
+    case 1: run_task_sb<TRACE, 1, ID>(P, T, C, Rt, pl, ws, lane); break;
+    case 2: run_task_sb<TRACE, 2, ID>(P, T, C, Rt, pl, ws, lane); break;
+    case 4: run_task_sb<TRACE, 4, ID>(P, T, C, Rt, pl, ws, lane); break;
+    case 8: run_task_sb<TRACE, 8, ID>(P, T, C, Rt, pl, ws, lane); break;
+    case 16: run_task_sb<TRACE, 16, ID>(P, T, C, Rt, pl, ws, lane); break;
+    case 32: run_task_sb<TRACE, 32, ID>(P, T, C, Rt, pl, ws, lane); break;
+    default: run_task_sb<TRACE, 0, ID>(P, T, C, Rt, pl, ws, lane); break;
   }
 }

@@ -311,7 +311,7 @@ def test_search_is_deterministic_and_bandwidth_update_matters():
     assert c.latency_s > a.latency_s
 
 
-def _sampled_chain_parity(w, chains, iters, n_sample, seed=2, trace_n=3, **moves):
+def _sampled_chain_parity(w, chains, iters, n_sample, seed=2, trace_n=3, stats=None, **moves):
     pip, B, prof = _ctx(w)
     model, mo, cl = _models(w)
     P = O.make_profile(prof)
@@ -321,6 +321,8 @@ def _sampled_chain_parity(w, chains, iters, n_sample, seed=2, trace_n=3, **moves
     items = rng.choice(len(feas) * chains, size=trace_n, replace=False).tolist()
     res = pip.search(model, w.bs_global, chains, iters, w.seed, chain_results=True, per_config=True,
                      trace_items=items, trace_cap=iters, **moves)
+    if stats is not None:
+        stats.update(pip.last_search_stats())
     rows = res["chains"]
     assert len(rows) == len(feas) * chains
     by_e = {c.e: c for c in feas}
@@ -573,3 +575,33 @@ def test_search_self_calibrated_t0(name, chains, iters, moves):
     # sampled chains, traces and the plan bit-exact against the oracle's calibration
     _sampled_chain_parity(W.WORKLOADS[name], chains=chains, iters=iters, n_sample=min(24, chains * 8), trace_n=2,
                           t0=-1.0, **moves)
+
+
+# ---- full-size launch paths: more block chunks than resident blocks, so blocks take a
+# second (and later) chunk of another configuration -- table rebuilds (MODE 0), per-warp
+# region re-layout (MODE 1) and warp-state reuse are exercised -- in every kernel variant
+
+@pytest.mark.parametrize("name,chains,iters,mode", [("C3", 2048, 2000, 0), ("C4", 2048, 2000, 1), ("C5", 2560, 1000, 1)])
+def test_search_more_chunks_than_resident_blocks(name, chains, iters, mode):
+    st = {}
+    res = _sampled_chain_parity(W.WORKLOADS[name], chains=chains, iters=iters, n_sample=32, trace_n=2, stats=st)
+    assert st["mode"] == mode
+    assert st["chunks"] > st["grid"], st          # blocks run >= 2 chunks
+    assert res["plan"].sa_steps == sum(chains * iters for p in res["per_config"] if len(p.perm) >= 2)
+
+
+def test_search_mode2_more_chunks_than_resident_blocks():
+    # N > 256 (tp = 1 on 40 nodes x 8 GPUs): 32-bit positions, with enough chains that blocks
+    # take several chunks
+    w = W.Workload("C0", 40, 8, W.GPT_345M, 320, 80_000_000_000, 100, 8, 600, 0.2, 0.2, 11)
+    st = {}
+    res = _sampled_chain_parity(w, chains=1024, iters=300, n_sample=16, trace_n=2, stats=st)
+    assert st["mode"] == 2 and st["chunks"] > st["grid"], st
+    assert any(p.cfg[0] * p.cfg[2] > 256 for p in res["per_config"])
+
+
+def test_search_mode1_c4_ten_thousand_iterations():
+    # the cold end of the 10k-step schedule (beta x e^10) in MODE 1
+    st = {}
+    _sampled_chain_parity(W.WORKLOADS["C4"], chains=64, iters=10000, n_sample=24, trace_n=2, stats=st)
+    assert st["mode"] == 1
