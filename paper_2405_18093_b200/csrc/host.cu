@@ -21,6 +21,9 @@ __global__ void k_enumerate_filter(int, int, unsigned long long, int, pipette_mo
                                    const pipette_profile_entry*, int, DevCfg*, unsigned long long*, int, int*,
                                    double*, int, EnumOut*);
 const void* eval_kernel(int mode);
+const void* eval_warp_kernel();
+size_t eval_warp_smem_bytes(int n_nodes, int E);
+int eval_warp_threads();
 void launch_mlp_filter(const double* P, int G, int n_nodes, const pipette_model& m, long long bs, unsigned long long cap,
                        int margin, DevCfg* cfgs, int* feas, EnumOut* out, cudaStream_t s);
 int eval_tile_size();
@@ -409,7 +412,10 @@ pipette_status build_plan(pipette_ctx* ctx, int chains, int W, int r, const char
   // MODE 0 (n <= 16): packed positions, register stage-1 state, lane-replicated R,
   // subset-max table.  MODE 1 (N <= 256): slot bytes, the block's shared R table, S1M
   // stage-1 state.  MODE 2: 32-bit positions (N > 256).
-  const int mode = (n <= 16 && maxN <= 256 && ctx->g <= 15 && ctx->dTab) ? 0 : (maxN <= 256 ? 1 : 2);
+  // (the MODE 1 swap kernel maps slots to nodes by shifts: gpus_per_node a power of two)
+  const bool g_pow2 = (ctx->g & (ctx->g - 1)) == 0;
+  const int mode = (n <= 16 && maxN <= 256 && ctx->g <= 15 && ctx->dTab) ? 0
+                 : ((maxN <= 256 && (g_pow2 || full_moves)) ? 1 : 2);
   if (mode == 2 && full_moves)
     return fail(ctx, PIPETTE_E_UNSUPPORTED, "the full move set needs N = pp*dp <= 256 (max N here %d)", maxN);
   if (mode == 1) {
@@ -860,22 +866,37 @@ pipette_status pipette_eval(pipette_ctx* ctx, const pipette_model* model, int64_
   P.latency = d_latency;
   P.mem = (unsigned long long*)d_mem;
   P.status = d_status;
-  // rows gathered into per-warp shared staging buffers when they are 16-byte aligned and
-  // the buffers fit beside the tables (else read straight from global memory)
-  size_t smem = eval_smem_bytes(mode, perm_stride, P.vec16 != 0, ctx->n_nodes, ctx->E, P.bm_words);
-  P.staged = P.vec16 && perm_stride <= 64 && smem <= 96 * 1024;   // long rows: direct 16-byte loads measured faster
-  if (!P.staged) smem = eval_smem_bytes(mode, perm_stride, false, ctx->n_nodes, ctx->E, P.bm_words);
-  if (smem > 227 * 1024) return fail(ctx, PIPETTE_E_UNSUPPORTED, "eval shared memory %zu B too large", smem);
   if (ctx->E >= 32767) return fail(ctx, PIPETTE_E_UNSUPPORTED, "eval supports < 32767 enumerated configurations");
-  const void* kern = eval_kernel(mode);
-  int occ = 0;
-  if ((st = kernel_occupancy(ctx, kern, 256, smem, &occ)) != PIPETTE_OK) return st;
-  const long long need = (n + eval_tile_size() - 1) / eval_tile_size();   // candidate tiles
-  const int grid = (int)std::min<long long>(need, (long long)occ * ctx->n_sms);
+  const void* kern;
+  size_t smem;
+  int threads, grid, occ = 0;
+  const char* thr_env = getenv("PIPETTE_EVAL_THREAD");   // A/B knob: the thread-per-candidate MODE 1 path
+  if (mode == 1 && !(thr_env && atoi(thr_env) == 1)) {
+    // large clusters: one warp per candidate (k_eval_warp)
+    kern = eval_warp_kernel();
+    threads = eval_warp_threads();
+    smem = eval_warp_smem_bytes(ctx->n_nodes, ctx->E);
+    if (smem > 227 * 1024) return fail(ctx, PIPETTE_E_UNSUPPORTED, "eval shared memory %zu B too large", smem);
+    if ((st = kernel_occupancy(ctx, kern, threads, smem, &occ)) != PIPETTE_OK) return st;
+    const long long need = (n + threads / 32 - 1) / (threads / 32);
+    grid = (int)std::min<long long>(need, (long long)occ * ctx->n_sms);
+  } else {
+    // rows gathered into per-warp shared staging buffers when they are 16-byte aligned and
+    // the buffers fit beside the tables (else read straight from global memory)
+    smem = eval_smem_bytes(mode, perm_stride, P.vec16 != 0, ctx->n_nodes, ctx->E, P.bm_words);
+    P.staged = P.vec16 && perm_stride <= 64 && smem <= 96 * 1024;   // long rows: direct 16-byte loads measured faster
+    if (!P.staged) smem = eval_smem_bytes(mode, perm_stride, false, ctx->n_nodes, ctx->E, P.bm_words);
+    if (smem > 227 * 1024) return fail(ctx, PIPETTE_E_UNSUPPORTED, "eval shared memory %zu B too large", smem);
+    kern = eval_kernel(mode);
+    threads = 256;
+    if ((st = kernel_occupancy(ctx, kern, 256, smem, &occ)) != PIPETTE_OK) return st;
+    const long long need = (n + eval_tile_size() - 1) / eval_tile_size();   // candidate tiles
+    grid = (int)std::min<long long>(need, (long long)occ * ctx->n_sms);
+  }
   void* args[] = {&P};
   nvtxRangePushA("pipette_eval K2");
   CU(wait_tables(ctx, s));
-  CU(cudaLaunchKernel(kern, dim3(grid), dim3(256), args, smem, s));
+  CU(cudaLaunchKernel(kern, dim3(grid), dim3(threads), args, smem, s));
   ctx->launches++;
   CU(cudaGetLastError());
   CU(note_eval(ctx, s));

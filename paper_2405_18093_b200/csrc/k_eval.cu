@@ -536,3 +536,221 @@ const void* eval_kernel(int mode) {
 }
 
 }  // namespace pip
+
+namespace pip {
+
+// ------------------------------------------------------------------ K2 MODE 1: warp per candidate
+// Large clusters (n > 16 nodes or more than 15 slots per node), where a candidate's mapping is
+// long (N up to 1024) and Eq.6's stage-1 set has many nodes: one WARP per candidate
+// (north_star: "one warp per candidate ... lane-parallel reductions over links and stages
+// via warp shuffles").  The row is read coalesced across the lanes (slot p by lane p mod 32),
+// the bijection is tested with a per-warp bitmap (atomicOr: a duplicate finds its bit set),
+// node ids go to a per-warp byte array; lane z sums pipeline z of Eq.5 in stage order (the
+// normative order), T_PP is a shuffle max; stage-1 counts are per-warp byte counters, N1 a
+// 128-bit mask OR-reduced over the lanes; T_ex takes the k(k-1) member pairs split over the
+// lanes (k <= 16) or the first pair inside N1 of the R-descending pair list, 32 probes per
+// round.  R (n x n) lives in shared memory; one block of 16 warps per SM.
+constexpr int kEvalWarpThreads = 512;
+constexpr int kEvalWarpMaxN = 1024;   // (G <= 1024)
+
+struct WarpScratch {
+  uint32_t bm[kEvalWarpMaxN / 32];   // bijection bitmap
+  uint32_t cnt[kMaxNodes / 4];       // stage-1 member counts, bytes (c_n <= gpus_per_node <= 255)
+  uint8_t nd[kEvalWarpMaxN];         // node of every position
+};
+
+__device__ __forceinline__ double warp_max(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+
+// One candidate, processed by the whole warp (raw = its 8-byte configuration record, ch =
+// this lane's 16-byte chunk of the row when the row is read as one uint4 per lane).
+__device__ __forceinline__ void eval_warp_one(const EvalParams& P, const double* Rs, const unsigned long long* keys,
+                                              WarpScratch* ws, long long i, unsigned long long raw, const uint4& ch,
+                                              bool vec, unsigned long long& last_raw, int& e, int lane) {
+  const unsigned full = 0xffffffffu;
+  const double qnan = __longlong_as_double(0x7ff8000000000000ll);
+  const int n = P.n_nodes;
+  // configuration lookup (Alg.1 l.3-5 membership), warp-uniform; repeated records skip it
+  if (raw != last_raw) {
+    const pipette_config cf = *reinterpret_cast<const pipette_config*>(&raw);
+    const unsigned long long key = ((unsigned long long)cf.pp << 48) | ((unsigned long long)cf.tp << 32) |
+                                   ((unsigned long long)cf.dp << 16) | (unsigned long long)cf.mb;
+    int lo = 0, hi = P.E;
+    while (lo < hi) {
+      const int mid = (lo + hi) >> 1;
+      if (keys[mid] < key) lo = mid + 1; else hi = mid;
+    }
+    e = (lo >= P.E || keys[lo] != key) ? -1 : lo;
+    last_raw = raw;
+  }
+  if (e < 0) {
+    if (lane == 0) { P.latency[i] = qnan; P.mem[i] = 0ull; P.status[i] = 2; }
+    return;
+  }
+  const DevCfg C = P.cfgs[e];
+  const int N = C.N, pp = C.pp, dp = C.dp;
+  if (N > P.perm_stride || N > kEvalWarpMaxN) {   // the row cannot hold a mapping of [0, N)
+    if (lane == 0) { P.latency[i] = qnan; P.mem[i] = C.mem; P.status[i] = 3; }
+    return;
+  }
+  // ---- the row: bijection (Eq.2) and the node of every position
+  for (int w = lane; w < (N + 31) / 32; w += 32) ws->bm[w] = 0u;
+  for (int w = lane; w < (n + 3) / 4; w += 32) ws->cnt[w] = 0u;
+  __syncwarp();
+  bool bad = false;
+  auto visit = [&](int p, uint32_t v) {
+    if (v >= (uint32_t)N) {
+      bad = true;
+    } else {
+      const uint32_t bit = 1u << (v & 31);
+      bad |= (atomicOr(&ws->bm[v >> 5], bit) & bit) != 0u;
+      ws->nd[p] = (uint8_t)div_small(v, C.spn_magic, (uint32_t)C.spn);
+    }
+  };
+  if (vec) {   // slots 8 lane .. 8 lane + 7 from this lane's prefetched chunk
+    const uint32_t wv[4] = {ch.x, ch.y, ch.z, ch.w};
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const int p = lane * 8 + j;
+      if (p < N) visit(p, (wv[j >> 1] >> ((j & 1) * 16)) & 0xffffu);
+    }
+  } else {
+    const uint16_t* row = P.perm + i * (long long)P.perm_stride;
+    for (int p = lane; p < N; p += 32) visit(p, __ldg(row + p));
+  }
+  if (__any_sync(full, bad) || !C.has_profile) {
+    if (lane == 0) { P.latency[i] = qnan; P.mem[i] = C.mem; P.status[i] = C.has_profile ? 3 : 4; }
+    __syncwarp();
+    return;
+  }
+  __syncwarp();
+  // ---- Eq.5: lane z sums pipeline z in stage order; T_PP = max over pipelines
+  double tpp = 0.0;
+  uint32_t m0 = 0u, m1 = 0u, m2w = 0u, m3 = 0u;   // N1 bits held by this lane
+  for (int z = lane; z < dp; z += 32) {
+    const int b = z * pp;
+    uint32_t prev = ws->nd[b];
+    double s = 0.0;
+    for (int x = 1; x < pp; ++x) {
+      const uint32_t cur = ws->nd[b + x];
+      s = __dadd_rn(s, __dmul_rn(C.m2, Rs[prev * (uint32_t)n + cur]));
+      prev = cur;
+    }
+    tpp = fmax(tpp, s);
+    const uint32_t a = ws->nd[b];           // stage-1 worker of pipeline z (Eq.6)
+    atomicAdd(&ws->cnt[a >> 2], 1u << ((a & 3) * 8));
+    const uint32_t bit = 1u << (a & 31), q = a >> 5;
+    m0 |= q == 0u ? bit : 0u; m1 |= q == 1u ? bit : 0u; m2w |= q == 2u ? bit : 0u; m3 |= q == 3u ? bit : 0u;
+  }
+  tpp = warp_max(tpp);
+  Mask4 m;
+  m.w0 = __reduce_or_sync(full, m0); m.w1 = __reduce_or_sync(full, m1);
+  m.w2 = __reduce_or_sync(full, m2w); m.w3 = __reduce_or_sync(full, m3);
+  __syncwarp();
+  // ---- Eq.6, intra: nodes with c >= 2 stage-1 members (each counted by its pipelines' lanes)
+  double tin = 0.0;
+  for (int z = lane; z < dp; z += 32) {
+    const uint32_t a = ws->nd[z * pp];
+    const uint32_t c = (ws->cnt[a >> 2] >> ((a & 3) * 8)) & 0xffu;
+    if (c >= 2u) tin = fmax(tin, __dmul_rn(__ldg(P.qtab + C.qi_off + c), Rs[a * (uint32_t)n + a]));
+  }
+  tin = warp_max(tin);
+  // ---- Eq.6, inter: the slowest link among the k stage-1 nodes
+  const int k = m.count();
+  double mx = 0.0;
+  if (k >= 2) {
+    if (k <= 16) {   // the k(k-1) member pairs over the lanes; lane t holds member t
+      uint32_t memv = 0u;
+      {
+        const uint32_t c0 = __popc(m.w0), c1 = c0 + __popc(m.w1), c2 = c1 + __popc(m.w2);
+        const uint32_t t = (uint32_t)lane;
+        const uint32_t wd = t < c0 ? 0u : (t < c1 ? 1u : (t < c2 ? 2u : 3u));
+        const uint32_t r = t - (wd == 0u ? 0u : (wd == 1u ? c0 : (wd == 2u ? c1 : c2)));
+        if (t < (uint32_t)k) memv = wd * 32u + (uint32_t)__fns(m.word((int)wd), 0u, (int)r + 1);
+      }
+      const uint32_t kk = (uint32_t)k, npair = kk * kk;
+      const uint32_t mg = (uint32_t)((0x100000000ull + kk - 1u) / kk);
+      for (uint32_t base = 0; base < npair; base += 32u) {
+        const uint32_t j = base + (uint32_t)lane;
+        const uint32_t ia = __umulhi(j, mg), ib = j - ia * kk;
+        const uint32_t a = __shfl_sync(full, memv, (int)(ia & 31u)), b = __shfl_sync(full, memv, (int)(ib & 31u));
+        if (j < npair && ia != ib) mx = fmax(mx, Rs[a * (uint32_t)n + b]);
+      }
+      mx = warp_max(mx);
+    } else {         // first pair of the R-descending list inside N1 (expected (n/k)^2 probes)
+      const int len = n * (n - 1);
+      for (int base = 0; base < len; base += 32) {
+        const int j = base + lane;
+        uint32_t ab = 0u;
+        bool h = false;
+        if (j < len) {
+          ab = __ldg(P.gl_ab + j);
+          h = m.test(ab & 0xffu) && m.test(ab >> 8);
+        }
+        const unsigned bal = __ballot_sync(full, h);
+        if (bal) {
+          ab = __shfl_sync(full, ab, __ffs(bal) - 1);
+          mx = Rs[(ab & 0xffu) * (uint32_t)n + (ab >> 8)];
+          break;
+        }
+      }
+    }
+  }
+  if (lane == 0) {
+    const double tex = k >= 2 ? __dmul_rn(__ldg(P.qtab + C.qe_off + k), mx) : 0.0;
+    P.latency[i] = compose(C.Sb, C.r, C.Ss, tpp, tin, tex);
+    P.mem[i] = C.mem;
+    P.status[i] = C.feasible ? 0 : 1;
+  }
+  __syncwarp();
+}
+
+__global__ void __launch_bounds__(kEvalWarpThreads, 1) k_eval_warp(EvalParams P) {
+  extern __shared__ __align__(128) unsigned char smem[];
+  const int n = P.n_nodes, nn = n * n;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nwarps = kEvalWarpThreads / 32;
+  double* Rs = reinterpret_cast<double*>(smem);
+  unsigned long long* keys = reinterpret_cast<unsigned long long*>(smem + (size_t)nn * 8);
+  WarpScratch* ws = reinterpret_cast<WarpScratch*>(smem + (size_t)nn * 8 + (((size_t)P.E * 8 + 15) & ~(size_t)15)) + wid;
+  for (int i = threadIdx.x; i < nn; i += blockDim.x) Rs[i] = P.R[i];
+  for (int i = threadIdx.x; i < P.E; i += blockDim.x) keys[i] = P.keys[i];
+  __syncthreads();
+  // rows of up to 256 slots in 16-byte aligned rows: one uint4 per lane, prefetched two
+  // candidates ahead (the loads of the next rows are in flight while this one is evaluated)
+  const bool vec = P.vec16 != 0 && P.perm_stride <= 256;
+  const long long step = (long long)gridDim.x * nwarps;
+  const unsigned long long* cand = reinterpret_cast<const unsigned long long*>(P.cand);
+  auto fetch = [&](long long j, unsigned long long& raw, uint4& ch) {
+    raw = ~0ull;
+    ch = make_uint4(0u, 0u, 0u, 0u);
+    if (j < P.n) {
+      raw = __ldg(cand + j);
+      if (vec && lane * 8 < P.perm_stride)
+        ch = __ldg(reinterpret_cast<const uint4*>(P.perm + j * (long long)P.perm_stride) + lane);
+    }
+  };
+  unsigned long long last_raw = ~0ull;
+  int e = -1;
+  long long i = (long long)blockIdx.x * nwarps + wid;
+  unsigned long long r0, r1, r2;
+  uint4 c0, c1, c2;
+  fetch(i, r0, c0);
+  fetch(i + step, r1, c1);
+  for (; i < P.n; i += step) {
+    fetch(i + 2 * step, r2, c2);
+    eval_warp_one(P, Rs, keys, ws, i, r0, c0, vec, last_raw, e, lane);
+    r0 = r1; c0 = c1; r1 = r2; c1 = c2;
+  }
+}
+
+const void* eval_warp_kernel() { return (const void*)k_eval_warp; }
+size_t eval_warp_smem_bytes(int n_nodes, int E) {
+  return (size_t)n_nodes * n_nodes * 8 + (((size_t)E * 8 + 15) & ~(size_t)15) +
+         (size_t)(kEvalWarpThreads / 32) * sizeof(WarpScratch);
+}
+int eval_warp_threads() { return kEvalWarpThreads; }
+
+}  // namespace pip

@@ -1386,7 +1386,7 @@ __global__ void __launch_bounds__(SaLB<MODE, BIG, NW>::threads, SaLB<MODE, BIG, 
         default: run_task_hc<TRACE, 0, NW>(P, T, C, Tl, SS, ws, lane); break;
       }
     } else if constexpr (MODE == 1) {
-      run_task_sb_pp<TRACE, false>(P, T, C, Rs, pl_s, ws, lane);
+      run_task_sb_pp<TRACE, true>(P, T, C, Rs, pl_s, ws, lane);   // (power-of-two spn: the host's MODE 1 rule)
     } else {
       switch (C.pp) {
         case 1: run_task<POS, S1, RT, TRACE, 1>(P, T, C, R, ws, lane); break;

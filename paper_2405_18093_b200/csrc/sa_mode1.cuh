@@ -27,28 +27,50 @@
 constexpr int kNoWit = 0x7fffffff;         // no T_ex witness (|N1| < 2)
 
 // Block context of MODE 1 (also used by the full move set of MODE 0 with its hop-code table).
-// ID: every node holds one slot (spn = 1), so node(slot) = slot.
-template <bool ID = false>
+// P2 (the swap kernel; the host routes clusters whose gpus_per_node is not a power of two to
+// MODE 2): spn is a power of two, node(slot) = slot >> sh, and the four nodes of a slot word
+// are (word >> sh) & bmask in one shift and one AND.
+template <bool P2 = false>
 struct SbCtxT {
+  static constexpr bool kP2 = P2;
   const double* T;   // MODE 1: R = 1/B, row stride 2^lg; MODE 0: the 16-copy m2*R hop-code table
   double m2;
   uint32_t lg;
   int n;
   uint32_t spn, spn_magic, spn_sh;
   uint32_t m16;      // ceil(2^16 / spn)
-  // node = floor(slot / spn) as (slot * m16) >> 16: exact for slot < 256 and spn < 256
-  // (the error slot * (m16 - 2^16/spn) / 2^16 < 1/256 never crosses an integer)
-  __device__ __forceinline__ uint32_t node(uint32_t slot) const { return ID ? slot : (slot * m16) >> 16; }
+  uint32_t sh, bmask, rowmul, tbase;   // P2: log2(spn), per-byte node mask, 8 << lg, shared address of T
+  // node = floor(slot / spn): a shift (P2), else (slot * m16) >> 16, exact for slot < 256 and
+  // spn < 256 (the error slot * (m16 - 2^16/spn) / 2^16 < 1/256 never crosses an integer)
+  __device__ __forceinline__ uint32_t node(uint32_t slot) const { return P2 ? slot >> sh : (slot * m16) >> 16; }
   __device__ __forceinline__ double r(uint32_t a, uint32_t b) const { return T[(a << lg) + b]; }
   // the Eq.5 hop term fl(m2 * R[a][b]) (MODE 1)
   __device__ __forceinline__ double hop(uint32_t a, uint32_t b) const { return __dmul_rn(m2, r(a, b)); }
+  // R at a shared-memory byte address (P2 sums: row address + 8 * column, one LEA)
+  __device__ __forceinline__ double ld(uint32_t addr) const {
+    double v;
+    asm("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(addr));   // (the table is read-only here)
+    return v;
+  }
 };
 using SbCtx = SbCtxT<false>;
 
 template <int PP, class KT>
 __device__ __forceinline__ double sb_sum(const HcState& st, uint32_t z, int pp_rt, const KT& K) {
   double s = 0.0;
-  if constexpr (PP >= 4) {
+  if constexpr (PP >= 4 && KT::kP2) {   // node words, row addresses: ~6 instructions per hop
+    constexpr int NW = PP / 4;
+    uint32_t wd[NW];
+#pragma unroll
+    for (int k = 0; k < NW; ++k) wd[k] = (st.hw[(z * (uint32_t)NW + (uint32_t)k) * 32u] >> K.sh) & K.bmask;
+    uint32_t row = K.tbase + (wd[0] & 0xffu) * K.rowmul;
+#pragma unroll
+    for (int x = 1; x < PP; ++x) {
+      const uint32_t cur = __byte_perm(wd[x >> 2], 0u, 0x4440u | (uint32_t)(x & 3));
+      s = __dadd_rn(s, __dmul_rn(K.m2, K.ld(row + cur * 8u)));
+      row = K.tbase + cur * K.rowmul;
+    }
+  } else if constexpr (PP >= 4) {
     constexpr int NW = PP / 4;
     uint32_t wd[NW];
 #pragma unroll
@@ -78,7 +100,25 @@ template <int PP, class KT>
 __device__ __forceinline__ void sb_sum2(const HcState& st, uint32_t za, uint32_t zb, int pp_rt, const KT& K,
                                         double& sa, double& sb) {
   double a = 0.0, b = 0.0;
-  if constexpr (PP >= 4) {
+  if constexpr (PP >= 4 && KT::kP2) {   // node words, row addresses: ~6 instructions per hop
+    constexpr int NW = PP / 4;
+    uint32_t wa[NW], wb[NW];
+#pragma unroll
+    for (int k = 0; k < NW; ++k) {
+      wa[k] = (st.hw[(za * (uint32_t)NW + (uint32_t)k) * 32u] >> K.sh) & K.bmask;
+      wb[k] = (st.hw[(zb * (uint32_t)NW + (uint32_t)k) * 32u] >> K.sh) & K.bmask;
+    }
+    uint32_t ra = K.tbase + (wa[0] & 0xffu) * K.rowmul, rb = K.tbase + (wb[0] & 0xffu) * K.rowmul;
+#pragma unroll
+    for (int x = 1; x < PP; ++x) {
+      const uint32_t ca = __byte_perm(wa[x >> 2], 0u, 0x4440u | (uint32_t)(x & 3));
+      const uint32_t cb = __byte_perm(wb[x >> 2], 0u, 0x4440u | (uint32_t)(x & 3));
+      a = __dadd_rn(a, __dmul_rn(K.m2, K.ld(ra + ca * 8u)));
+      b = __dadd_rn(b, __dmul_rn(K.m2, K.ld(rb + cb * 8u)));
+      ra = K.tbase + ca * K.rowmul;
+      rb = K.tbase + cb * K.rowmul;
+    }
+  } else if constexpr (PP >= 4) {
     constexpr int NW = PP / 4;
     uint32_t wa[NW], wb[NW];
 #pragma unroll
@@ -115,9 +155,9 @@ __device__ __forceinline__ void sb_sum2(const HcState& st, uint32_t za, uint32_t
 
 // T_PP of a lane's tentative mapping when its unique max pipeline decreased: the max over
 // all dp Eq.5 sums and its multiplicity, computed by the whole warp (called converged).
-// For each flagged lane L, lane j takes pipelines j, j + 32, ... -- lane L's cached sums
-// with the two touched pipelines substituted (cache), or re-summed in stage order from lane
-// L's slot plane, which already holds the tentative swap.  The reads hit one bank (lane L's
+// For each flagged lane L, lane j takes pipelines j, j + 32, ... -- lane L's cached sums,
+// which already hold the two touched pipelines' new sums (cache), or re-summed in stage order
+// from lane L's slot plane, which already holds the tentative swap.  The reads hit one bank (lane L's
 // column), so they cost shared-memory wavefronts, not the divergent per-lane loop over all
 // dp pipelines that one lane's rescan would make its warp execute.
 template <int PP, class KT>
@@ -125,6 +165,7 @@ __device__ __forceinline__ void coop_tpp(bool need, unsigned char* ws, const dou
                                          uint32_t zp, uint32_t zb, double sA, double sB, const KT& K, int lane,
                                          double& tpp2, int& nmax2) {
   const unsigned full = 0xffffffffu;
+  __syncwarp();   // (flagged lanes' tentative cache writes are visible to the warp)
   for (unsigned todo = __ballot_sync(full, need); todo; todo &= todo - 1u) {
     const int L = __ffs(todo) - 1;
     const uint32_t zpL = __shfl_sync(full, zp, L), zbL = __shfl_sync(full, zb, L);
@@ -136,7 +177,7 @@ __device__ __forceinline__ void coop_tpp(bool need, unsigned char* ws, const dou
     double m = 0.0;
     int c = 0;
     for (int z = lane; z < dp; z += 32) {
-      const double v = cache ? ((uint32_t)z == zpL ? sAL : ((uint32_t)z == zbL ? sBL : psum[z * 32 + L]))
+      const double v = cache ? psum[z * 32 + L]
                              : sb_sum<PP, KT>(stL, (uint32_t)z, pp, K);
       c = v > m ? 1 : c + (v == m ? 1 : 0);
       m = fmax(m, v);
@@ -480,6 +521,10 @@ __device__ __forceinline__ void run_task_sb(const SaParams& P, const SaTask T, c
   K.spn = (uint32_t)C.spn; K.spn_magic = C.spn_magic;
   K.spn_sh = (C.spn & (C.spn - 1)) == 0 ? (uint32_t)(31 - __clz(C.spn)) : 32u;
   K.m16 = (uint32_t)((65536u + (uint32_t)C.spn - 1u) / (uint32_t)C.spn);
+  K.sh = (uint32_t)(31 - __clz(C.spn));   // (P2: spn is a power of two)
+  K.bmask = (0xffu >> K.sh) * 0x01010101u;
+  K.rowmul = 8u << K.lg;
+  K.tbase = (uint32_t)__cvta_generic_to_shared(Rt);
 
   const bool cache = (flags & kTfCache) != 0;
   const int plane = align16(((N + 3) / 4) * 128);
@@ -561,14 +606,19 @@ __device__ __forceinline__ void run_task_sb(const SaParams& P, const SaTask T, c
           tpp2 = (keep > 0) ? fmax(tpp, snew) : snew;
           nmax2 = (keep > 0 && tpp2 == tpp ? keep : 0) + (sA == tpp2 ? 1 : 0) + ((two && sB == tpp2) ? 1 : 0);
         }
-        // the unique max pipeline decreased: rescan over all pipelines -- a few cached sums
-        // per lane, else warp-cooperatively
-        if (cache && dp <= 16) {
+        // the unique max pipeline decreased: rescan over all pipelines -- up to 4 cached sums
+        // per lane, else warp-cooperatively (measured per configuration: a dp = 16 per-lane
+        // rescan ran at 3 active lanes and cost 400 warp instructions per step)
+        if (!fast && cache) {   // the new sums enter the cache tentatively (restored if rejected)
+          psum[zp * 32 + lane] = sA;
+          psum[zb * 32 + lane] = sB;
+        }
+        if (cache && dp <= 8) {
           if (!fast) {
             double m = 0.0;
             int c = 0;
             for (int z = 0; z < dp; ++z) {
-              const double v = (uint32_t)z == zp ? sA : ((uint32_t)z == zb ? sB : psum[z * 32 + lane]);
+              const double v = psum[z * 32 + lane];
               c = v > m ? 1 : c + (v == m ? 1 : 0);
               m = fmax(m, v);
             }
@@ -607,6 +657,10 @@ __device__ __forceinline__ void run_task_sb(const SaParams& P, const SaTask T, c
             improved = true;
           }
         } else {
+          if (!fast && cache) {   // restore the cached sums of the rejected proposal
+            psum[zb * 32 + lane] = oldB;
+            psum[zp * 32 + lane] = oldA;
+          }
           *bq = (uint8_t)sq;   // revert
           *bp = (uint8_t)sp;
         }
@@ -638,9 +692,8 @@ __device__ __forceinline__ void run_task_sb(const SaParams& P, const SaTask T, c
 }
 
 // Compile-time pipeline depth for the common power-of-two depths (the Eq.5 sums unroll).
-// (ID = true, node(slot) = slot for spn = 1, saves two instructions per node read, but
-// with both variants in one kernel ptxas spills in the hot loop at 255 registers, and as
-// separate non-inlined functions too; only the general variant is instantiated.)
+// ID: the context's node map (true: power-of-two spn, the only variant the swap kernel
+// instantiates -- two variants in one kernel made ptxas spill in the hot loop).
 template <bool TRACE, bool ID>
 __device__ __forceinline__ void run_task_sb_pp(const SaParams& P, const SaTask T, const DevCfg C, const double* Rt,
                                                const uint16_t* pl, unsigned char* ws, int lane) {

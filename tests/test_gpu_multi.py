@@ -20,12 +20,14 @@ def _ngpu():
     return torch.cuda.device_count()
 
 
-@pytest.mark.parametrize("world,chains,moves", [(2, 8, (0, 0)), (2, 7, (0, 0)), (4, 8, (0, 0)), (4, 5, (0, 0)),
-                                               (8, 8, (0, 0)), (2, 6, (683, 682)), (4, 5, (683, 682))])
-def test_multi_gpu_plan_bit_identical(world, chains, moves, tmp_path):
+@pytest.mark.parametrize("world,chains,moves,name,iters", [
+    (2, 8, (0, 0), "C1", 1000), (2, 7, (0, 0), "C1", 1000), (4, 8, (0, 0), "C1", 1000), (4, 5, (0, 0), "C1", 1000),
+    (8, 8, (0, 0), "C1", 1000), (2, 6, (683, 682), "C1", 1000), (4, 5, (683, 682), "C1", 1000),
+    # the headline shape: 128 nodes, MODE 1 (shared R table, S1M witnesses), NCCL combine
+    (2, 8, (0, 0), "C5", 150), (4, 9, (0, 0), "C5", 150), (8, 8, (0, 0), "C5", 150)])
+def test_multi_gpu_plan_bit_identical(world, chains, moves, name, iters, tmp_path):
     if _ngpu() < world:
         pytest.skip(f"needs {world} GPUs")
-    name, iters = "C1", 1000
     out = tmp_path / "plan.json"
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={world}",
            "--master-addr=127.0.0.1", "--master-port=29533", os.path.join(HERE, "helpers", "mp_search.py"),

@@ -501,7 +501,9 @@ def test_eval_models_bit_exact(name):
 
 # ------------------------------------------------------------------ non-power-of-two shapes
 # pp in {3, 6, 9, 18, ...} takes the runtime pipeline-depth paths, spn in {6, 3} the
-# divide-by-magic node ids (MODE 0: 3 nodes x 6 GPUs; MODE 1: 20 nodes x 6 GPUs)
+# divide-by-magic node ids (MODE 0: 3 nodes x 6 GPUs; 20 nodes x 6 GPUs: the swap search
+# takes MODE 2 -- the MODE 1 swap kernel maps slots to nodes by shifts, so it needs a
+# power-of-two gpus_per_node -- and the full move set MODE 1's general node map)
 ODD0 = W.Workload("C0", 3, 6, W.GPT_345M, 72, 80_000_000_000, 100, 8, 600, 0.3, 0.3, 21)
 ODD1 = W.Workload("C0", 20, 6, W.GPT_345M, 120, 80_000_000_000, 100, 4, 400, 0.3, 0.3, 22)
 
