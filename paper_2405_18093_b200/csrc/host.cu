@@ -42,6 +42,7 @@ int sa_m1_count_bytes(int n, bool nib);
 void launch_t0_calibrate(const DevCfg*, const int*, int, const double*, const double*, int, const RoundKeys&, int, int,
                          double, double*, cudaStream_t);
 __global__ void k_partner_lists(const uint16_t*, int, uint32_t*, int);
+__global__ void k_cfg_cost(const unsigned long long*, const SaTask*, int, unsigned long long*);
 __global__ void k_node_lists(const double*, int, uint8_t*, double*);
 __global__ void k_pair_list(const double*, int, uint16_t*, double*);
 __global__ void k_tin_list(const DevCfg*, const int*, const double*, const double*, int, int, uint16_t*, double*, int*);
@@ -125,6 +126,7 @@ struct HostPlan {
   int slots = 0, perm_words = 0, maxN = 1, mode = 0, r_bytes = 0, dp_cap = 0, warp_bytes = 16, tl_stride = 1, wpb = 1;
   int r_lg = 0, plen = 0;   // MODE 1: R row stride 2^r_lg, pair-list prefix entries
   bool big = false, nib = false;
+  bool measured = false;    // tasks ordered by measured per-configuration durations
   size_t smem = 0;
 };
 
@@ -163,7 +165,10 @@ struct pipette_ctx {
   DevBuf mlp;   // Eq.7 MLP parameters (NEXT-4), empty = analytic memory (R11)
   DevBuf claimed;   // SA chunk claim flags + per-SM first-fetch slots
   DevBuf tasks, chunks, counter, chain_out, best_perm, cfg_slot, cfg_best, gbits, items, gitems, pack, accepted,
-      slot_perm_off, slot_lane, trace_slot, trace, task_prof, tin_rank, tin_vs, tl_ac, tl_val, tl_len, beta0;
+      slot_perm_off, slot_lane, trace_slot, trace, task_prof, tin_rank, tin_vs, tl_ac, tl_val, tl_len, beta0, cfg_cost;
+  // measured mean task duration (ms) of each enumerated configuration from the last search's
+  // task profile (k_cfg_cost), for the longest-first order of the next work plan; empty = none
+  std::vector<double> cfg_cost_ms;
   int64_t n_tasks_last = 0;
   HostPlanKey plan_key{};
   HostPlan plan;
@@ -382,6 +387,16 @@ pipette_status build_plan(pipette_ctx* ctx, int chains, int W, int r, const char
   std::vector<double> cost(tasks.size());
   const char* cf_env = getenv("PIPETTE_COST_FIT");
   const bool cost_fit = !(cf_env && atoi(cf_env) == 0);
+  // measured durations of the previous search on this enumeration, when every configuration
+  // has one (the plan is then rebuilt once: ordering never changes results, chains are
+  // independent and their Philox streams are indexed by (step, chain, e))
+  // (MODE 0 keeps its fitted model: ordering by measured means interleaves pipeline depths
+  // on an SM and measured C3 165 vs 150 ms, C2 up to 17.9 vs 16.0 ms -- I-cache)
+  const bool mode0_plan = ctx->n_nodes <= 16 && maxN <= 256 && ctx->g <= 15 && ctx->dTab;
+  bool measured = cost_fit && !mode0_plan && !ctx->cfg_cost_ms.empty();
+  for (size_t i = 0; measured && i < tasks.size(); ++i)
+    measured = tasks[i].cfg < (int)ctx->cfg_cost_ms.size() && ctx->cfg_cost_ms[tasks[i].cfg] > 0.0;
+  hp.measured = measured;
   const int n_nodes = ctx->n_nodes;
   const bool mode0 = n_nodes <= 16 && maxN <= 256 && ctx->g <= 15 && ctx->dTab;
   for (size_t i = 0; i < tasks.size(); ++i) {
@@ -390,8 +405,9 @@ pipette_status build_plan(pipette_ctx* ctx, int chains, int W, int r, const char
     double v = c.pp >= 2 ? 60.0 + 12.0 * (c.pp - 1) + pchg * (40.0 + 4.0 * n_nodes) : 10.0;
     if (cost_fit && mode0 && n_nodes <= 8)
       v = c.pp >= 2 ? 10.3 + 0.079 * c.pp + 0.037 * c.N + 0.067 * c.dp + 3.06 * pchg : 1.8;
-    else if (cost_fit && !mode0)
-      v = c.pp >= 2 ? 1.0 - 0.0135 * c.pp + 0.0026 * c.N - 0.02 * c.dp + pchg * (0.9 + 0.028 * n_nodes) : 0.05;
+    else if (cost_fit && !mode0)   // (fit to C5 task durations after the round-2 MODE 1 redesign)
+      v = c.pp >= 2 ? 48.4 - 0.26 * (c.pp - 1) - 72.4 * pchg + 0.17 * c.dp - 5.3 * (c.spn > 1 ? 1.0 : 0.0) : 1.0;
+    if (measured) v = ctx->cfg_cost_ms[tasks[i].cfg];
     cost[i] = c.N < 2 ? 0.0 : v;
   }
   std::vector<int> order(tasks.size());
@@ -451,7 +467,10 @@ pipette_status build_plan(pipette_ctx* ctx, int chains, int W, int r, const char
                                   : sa_m1_warp_state_bytes(c.N, c.dp, n, counts, false, nib);
       const int with = sa_m1_warp_state_bytes(c.N, c.dp, n, counts, true, nib);
       const int w_nc = std::min(kSaM1Warps, avail / base), w_c = std::min(kSaM1Warps, avail / with);
-      const bool cache = !full_moves && c.pp >= std::max(2, cache_pp) && w_c >= 1 && w_c >= std::min(w_nc, cache_min);
+      // (measured on C5: the cache pays for a lost resident warp only when it saves re-summing
+      // long pipelines -- (4,8,32) 8 uncached warps beat 7 cached, (8,4,32) 8 beat 5)
+      const int need = cm_env ? std::min(w_nc, cache_min) : (c.pp >= 16 ? std::min(w_nc, 6) : w_nc);
+      const bool cache = !full_moves && c.pp >= std::max(2, cache_pp) && w_c >= 1 && w_c >= need;
       fbytes[f] = cache ? with : base;
       fwarps[f] = cache ? w_c : w_nc;
       if (fwarps[f] < 1)
@@ -581,6 +600,7 @@ pipette_status enumerate(pipette_ctx* ctx, const pipette_model* m, long long bs,
   if (eo.F) CU(cudaMemcpy(ctx->hfeas.data(), ctx->feas.p, sizeof(int) * eo.F, cudaMemcpyDeviceToHost));
   ctx->enum_valid = true;
   ctx->vin_valid = false;
+  ctx->cfg_cost_ms.clear();   // (measured task durations belong to the previous enumeration)
   ctx->plan_valid = false;   // the SA work plan is built from this enumeration
   ctx->enum_model = *m;
   ctx->enum_bs = bs;
@@ -779,7 +799,7 @@ void pipette_destroy(pipette_ctx* ctx) {
                     &ctx->chain_out, &ctx->best_perm, &ctx->cfg_slot, &ctx->cfg_best, &ctx->gbits, &ctx->items,
                     &ctx->gitems, &ctx->pack, &ctx->accepted, &ctx->slot_perm_off, &ctx->slot_lane,
                     &ctx->trace_slot, &ctx->trace, &ctx->task_prof, &ctx->tin_rank, &ctx->tin_vs, &ctx->tl_ac,
-                    &ctx->tl_val, &ctx->tl_len, &ctx->beta0};
+                    &ctx->tl_val, &ctx->tl_len, &ctx->beta0, &ctx->cfg_cost};
   for (DevBuf* b : bufs)
     if (b->p) cudaFree(b->p);
   if (ctx->dR) cudaFree(ctx->dR);
@@ -1140,6 +1160,16 @@ pipette_status pipette_search(pipette_ctx* ctx, const pipette_model* model, int6
     ctx->launches++;
     CU(cudaGetLastError());
   }
+  const bool learn_costs = !pl.measured && !sorted.empty() && mode != 0;   // (once per work plan)
+  if (learn_costs) {
+    CU(ensure(ctx->cfg_cost, sizeof(unsigned long long) * 2 * (size_t)E));
+    CU(cudaMemsetAsync(ctx->cfg_cost.p, 0, sizeof(unsigned long long) * 2 * (size_t)E, s));
+    k_cfg_cost<<<(unsigned)((sorted.size() + 255) / 256), 256, 0, s>>>(
+        (const unsigned long long*)ctx->task_prof.p, (const SaTask*)ctx->tasks.p, (int)sorted.size(),
+        (unsigned long long*)ctx->cfg_cost.p);
+    ctx->launches++;
+    CU(cudaGetLastError());
+  }
   CU(cudaEventRecord(ctx->ev[3], s));
   nvtxRangeEnd(nv);
   nv = nvtxRangeStartA("K4 argmin");
@@ -1191,12 +1221,23 @@ pipette_status pipette_search(pipette_ctx* ctx, const pipette_model* model, int6
       CU(cudaMemcpyAsync(hperm.data(), ctx->best_perm.p, sizeof(uint16_t) * perm_words, cudaMemcpyDeviceToHost, s));
     }
   }
+  std::vector<unsigned long long> hcost;
+  if (learn_costs) {
+    hcost.resize(2 * (size_t)E);
+    CU(cudaMemcpyAsync(hcost.data(), ctx->cfg_cost.p, sizeof(unsigned long long) * hcost.size(), cudaMemcpyDeviceToHost, s));
+  }
   std::vector<pipette_trace_record> htr;
   if (tracing) {
     htr.resize((size_t)o.n_trace * o.trace_cap);
     CU(cudaMemcpyAsync(htr.data(), ctx->trace.p, sizeof(pipette_trace_record) * htr.size(), cudaMemcpyDeviceToHost, s));
   }
   CU(cudaStreamSynchronize(s));
+  if (learn_costs) {   // the next call orders its tasks by these measured durations
+    ctx->cfg_cost_ms.assign(E, 0.0);
+    for (int e = 0; e < E; ++e)
+      if (hcost[2 * e + 1]) ctx->cfg_cost_ms[e] = (double)hcost[2 * e] / (double)hcost[2 * e + 1] * 1e-6;
+    ctx->plan_valid = false;
+  }
   out->enumerate_ms = elapsed(ctx->ev[0], ctx->ev[1]);
   out->sa_ms = elapsed(ctx->ev[2], ctx->ev[3]);
   out->argmin_ms = elapsed(ctx->ev[3], ctx->ev[4]);

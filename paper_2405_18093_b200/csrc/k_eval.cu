@@ -600,26 +600,41 @@ __device__ __forceinline__ void eval_warp_one(const EvalParams& P, const double*
   for (int w = lane; w < (N + 31) / 32; w += 32) ws->bm[w] = 0u;
   for (int w = lane; w < (n + 3) / 4; w += 32) ws->cnt[w] = 0u;
   __syncwarp();
+  // bijection: every id < N, and the union of the ids' bits (fire-and-forget atomicOr into
+  // the warp's bitmap) has N bits -- a duplicate leaves one of them unset
   bool bad = false;
-  auto visit = [&](int p, uint32_t v) {
-    if (v >= (uint32_t)N) {
-      bad = true;
-    } else {
-      const uint32_t bit = 1u << (v & 31);
-      bad |= (atomicOr(&ws->bm[v >> 5], bit) & bit) != 0u;
-      ws->nd[p] = (uint8_t)div_small(v, C.spn_magic, (uint32_t)C.spn);
-    }
-  };
-  if (vec) {   // slots 8 lane .. 8 lane + 7 from this lane's prefetched chunk
+  if (vec) {   // slots 8 lane .. 8 lane + 7 from this lane's prefetched chunk; nodes stored as 8 bytes
     const uint32_t wv[4] = {ch.x, ch.y, ch.z, ch.w};
+    uint32_t nw0 = 0u, nw1 = 0u;
 #pragma unroll
     for (int j = 0; j < 8; ++j) {
       const int p = lane * 8 + j;
-      if (p < N) visit(p, (wv[j >> 1] >> ((j & 1) * 16)) & 0xffffu);
+      const uint32_t v = (wv[j >> 1] >> ((j & 1) * 16)) & 0xffffu;
+      if (p < N) {
+        if (v >= (uint32_t)N) bad = true;
+        else atomicOr(&ws->bm[v >> 5], 1u << (v & 31));
+        const uint32_t nd = div_small(min(v, (uint32_t)N - 1u), C.spn_magic, (uint32_t)C.spn);
+        if (j < 4) nw0 |= nd << (8 * j); else nw1 |= nd << (8 * (j - 4));
+      }
     }
+    if (lane * 8 < N) *reinterpret_cast<uint2*>(ws->nd + lane * 8) = make_uint2(nw0, nw1);
   } else {
     const uint16_t* row = P.perm + i * (long long)P.perm_stride;
-    for (int p = lane; p < N; p += 32) visit(p, __ldg(row + p));
+    for (int p = lane; p < N; p += 32) {
+      const uint32_t v = __ldg(row + p);
+      if (v >= (uint32_t)N) {
+        bad = true;
+      } else {
+        atomicOr(&ws->bm[v >> 5], 1u << (v & 31));
+        ws->nd[p] = (uint8_t)div_small(v, C.spn_magic, (uint32_t)C.spn);
+      }
+    }
+  }
+  __syncwarp();
+  {
+    int c = 0;
+    for (int w = lane; w < (N + 31) / 32; w += 32) c += __popc(ws->bm[w]);
+    bad |= (int)__reduce_add_sync(full, (uint32_t)c) != N;
   }
   if (__any_sync(full, bad) || !C.has_profile) {
     if (lane == 0) { P.latency[i] = qnan; P.mem[i] = C.mem; P.status[i] = C.has_profile ? 3 : 4; }
@@ -634,10 +649,21 @@ __device__ __forceinline__ void eval_warp_one(const EvalParams& P, const double*
     const int b = z * pp;
     uint32_t prev = ws->nd[b];
     double s = 0.0;
-    for (int x = 1; x < pp; ++x) {
-      const uint32_t cur = ws->nd[b + x];
-      s = __dadd_rn(s, __dmul_rn(C.m2, Rs[prev * (uint32_t)n + cur]));
-      prev = cur;
+    if ((pp & 3) == 0) {   // the pipeline's node bytes as whole words
+      const uint32_t* nw = reinterpret_cast<const uint32_t*>(ws->nd + b);
+      uint32_t wd = nw[0];
+      for (int x = 1; x < pp; ++x) {
+        if ((x & 3) == 0) wd = nw[x >> 2];
+        const uint32_t cur = __byte_perm(wd, 0u, 0x4440u | (uint32_t)(x & 3));
+        s = __dadd_rn(s, __dmul_rn(C.m2, Rs[prev * (uint32_t)n + cur]));
+        prev = cur;
+      }
+    } else {
+      for (int x = 1; x < pp; ++x) {
+        const uint32_t cur = ws->nd[b + x];
+        s = __dadd_rn(s, __dmul_rn(C.m2, Rs[prev * (uint32_t)n + cur]));
+        prev = cur;
+      }
     }
     tpp = fmax(tpp, s);
     const uint32_t a = ws->nd[b];           // stage-1 worker of pipeline z (Eq.6)

@@ -1609,3 +1609,18 @@ int sa_m1_warp_state_bytes(int N, int dp, int n, bool counts, bool cache, bool n
 int sa_m1_count_bytes(int n, bool nib) { return sb_count_bytes(n, nib); }
 
 }  // namespace pip
+
+namespace pip {
+// Per enumerated configuration e: the sum of its warp tasks' durations (ns, globaltimer
+// stamps of the task profile) and their count -- the longest-first order of the next
+// search's work plan uses the means (host.cu, build_plan).
+__global__ void k_cfg_cost(const unsigned long long* __restrict__ prof, const SaTask* __restrict__ tasks, int n_tasks,
+                           unsigned long long* __restrict__ acc) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= n_tasks) return;
+  const ulonglong4 p = reinterpret_cast<const ulonglong4*>(prof)[t];
+  const int e = tasks[t].cfg;
+  atomicAdd(acc + 2 * e, p.y > p.x ? p.y - p.x : 0ull);
+  atomicAdd(acc + 2 * e + 1, 1ull);
+}
+}  // namespace pip

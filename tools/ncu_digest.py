@@ -2,7 +2,7 @@
 digest travels back): headline metrics, stall reasons per issue, and the top source lines
 by executed warp instructions and by stall samples.
 
-    python tools/ncu_digest.py REPORT.ncu-rep [units] > digest.txt
+    python tools/ncu_digest.py REPORT.ncu-rep [units [lines.tsv]] > digest.txt
 
 `units` (optional) divides the instruction counts (e.g. SA warp-steps = chains*iters/32).
 """
@@ -63,6 +63,10 @@ def main():
         except ValueError:
             continue
         out.append((ins, samp, thr, f"{fname}:{r[0]}", r[1][:80]))
+    if len(sys.argv) > 3:   # the whole per-line table (file:line, warp inst, samples, thread inst)
+        with open(sys.argv[3], "w") as f:
+            for ins, samp, thr, loc, s in out:
+                f.write(f"{loc}\t{ins}\t{samp}\t{thr}\n")
     ti = sum(o[0] for o in out) or 1
     ts = sum(o[1] for o in out) or 1
     for key, name in ((0, "instructions"), (1, "stall samples")):
