@@ -559,10 +559,14 @@ struct WarpScratch {
   uint8_t nd[kEvalWarpMaxN];         // node of every position
 };
 
+// Warp max of non-negative doubles: their bit patterns order like the values, so two 32-bit
+// redux.sync on the halves (instead of a five-level shuffle butterfly of doubles).
 __device__ __forceinline__ double warp_max(double v) {
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
-  return v;
+  const unsigned long long b = (unsigned long long)__double_as_longlong(v);
+  const uint32_t hi = (uint32_t)(b >> 32);
+  const uint32_t H = __reduce_max_sync(0xffffffffu, hi);
+  const uint32_t L = __reduce_max_sync(0xffffffffu, hi == H ? (uint32_t)b : 0u);
+  return __longlong_as_double((long long)(((unsigned long long)H << 32) | L));
 }
 
 // One candidate, processed by the whole warp (raw = its 8-byte configuration record, ch =

@@ -153,6 +153,20 @@ __device__ __forceinline__ void sb_sum2(const HcState& st, uint32_t za, uint32_t
   sb = b;
 }
 
+// Warp max of non-negative doubles (their bit patterns order like the values) by two 32-bit
+// redux.sync, and the sum of c over the lanes holding it: three REDUX instead of a five-level
+// shuffle butterfly on (double, int) pairs.
+__device__ __forceinline__ double warp_max_nonneg(double m, uint32_t c, uint32_t& count) {
+  const unsigned full = 0xffffffffu;
+  const unsigned long long b = (unsigned long long)__double_as_longlong(m);
+  const uint32_t hi = (uint32_t)(b >> 32), lo = (uint32_t)b;
+  const uint32_t H = __reduce_max_sync(full, hi);
+  const uint32_t Lo = __reduce_max_sync(full, hi == H ? lo : 0u);
+  const unsigned long long B = ((unsigned long long)H << 32) | Lo;
+  count = __reduce_add_sync(full, b == B ? c : 0u);
+  return __longlong_as_double((long long)B);
+}
+
 // T_PP of a lane's tentative mapping when its unique max pipeline decreased: the max over
 // all dp Eq.5 sums and its multiplicity, computed by the whole warp (called converged).
 // For each flagged lane L, lane j takes pipelines j, j + 32, ... -- lane L's cached sums,
@@ -182,14 +196,9 @@ __device__ __forceinline__ void coop_tpp(bool need, unsigned char* ws, const dou
       c = v > m ? 1 : c + (v == m ? 1 : 0);
       m = fmax(m, v);
     }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {   // (max, count at max) over the lanes
-      const double m2 = __shfl_xor_sync(full, m, o);
-      const int c2 = __shfl_xor_sync(full, c, o);
-      c = m2 > m ? c2 : (m2 == m ? c + c2 : c);
-      m = fmax(m, m2);
-    }
-    if (lane == L) { tpp2 = m; nmax2 = c; }
+    uint32_t cnt;
+    m = warp_max_nonneg(m, (uint32_t)c, cnt);   // (max, count at max) over the lanes
+    if (lane == L) { tpp2 = m; nmax2 = (int)cnt; }
   }
 }
 
@@ -454,13 +463,11 @@ struct S1M {
             if (v > mx) { mx = v; wbest = a | (b << 8); }
           }
         }
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) {   // max-reduce (any witness of an equal max is fine)
-          const double v2 = __shfl_xor_sync(full, mx, o);
-          const uint32_t w2 = __shfl_xor_sync(full, wbest, o);
-          if (v2 > mx) { mx = v2; wbest = w2; }
-        }
-        if (lane == L) { need_scan = false; maxR2 = mx; wab2 = wbest; }
+        uint32_t cnt;   // max-reduce; the witness of the lowest lane holding it (any equal max is fine)
+        const double gmx = warp_max_nonneg(mx, 1u, cnt);
+        const unsigned holders = __ballot_sync(full, mx == gmx);
+        wbest = __shfl_sync(full, wbest, __ffs(holders) - 1);
+        if (lane == L) { need_scan = false; maxR2 = gmx; wab2 = wbest; }
         continue;
       }
       const int start = __shfl_sync(full, jw, L) + 1;
