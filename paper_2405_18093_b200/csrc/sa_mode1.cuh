@@ -395,6 +395,7 @@ struct S1M {
   template <class KT>
   __device__ __forceinline__ void coop(const S1Ctx& X, const KT& K) {
     const unsigned full = 0xffffffffu;
+    if (!__any_sync(full, need_tin | need_scan)) return;   // (the common case: one vote)
     if (counts) {   // T_in: first (a, c) entry (by value) whose node has c members after the move
       unsigned todo = __ballot_sync(full, need_tin);
       while (todo) {
@@ -567,11 +568,13 @@ __device__ __forceinline__ void run_task_sb(const SaParams& P, const SaTask T, c
   s1.finish_init(X, K);
 
   const double L0 = compose(C.Sb, C.r, C.Ss, tpp, s1.tin, s1.tex);
-  double cur = L0, best = L0, best_tpp = tpp, best_tdp = __dadd_rn(s1.tin, s1.tex);
-  int best_step = -1;
+  // the best point's breakdown and step go straight to the chain's output record (rarely
+  // written; kept out of the registers of the step loop)
+  ChainOut* const out = P.out + slot;
+  if (active) { out->best_tpp = tpp; out->best_tdp = __dadd_rn(s1.tin, s1.tex); out->best_step = -1; out->L0 = L0; }
+  double cur = L0, best = L0;
   uint32_t accepted = 0;
   double beta = sa_beta0(P, T.f, L0);
-  const double ia = P.alpha_inv;
   const int trow = (TRACE && active) ? P.trace_slot[slot] : -1;
 
   if (N >= 2) {
@@ -660,7 +663,8 @@ __device__ __forceinline__ void run_task_sb(const SaParams& P, const SaTask T, c
           if (dpchg) s1.commit();
           cur = Lp;
           if (Lp < best) {
-            best = Lp; best_step = i; best_tpp = tpp; best_tdp = __dadd_rn(s1.tin, s1.tex);
+            best = Lp;
+            if (active) { out->best_tpp = tpp; out->best_tdp = __dadd_rn(s1.tin, s1.tex); out->best_step = i; }
             improved = true;
           }
         } else {
@@ -687,15 +691,10 @@ __device__ __forceinline__ void run_task_sb(const SaParams& P, const SaTask T, c
         rec.accept = acc ? 1u : 0u; rec.latency = Lp;
         P.trace[(size_t)trow * P.trace_cap + i] = rec;
       }
-      beta = __dmul_rn(beta, ia);
+      beta = __dmul_rn(beta, P.alpha_inv);
     }
   }
-  if (active) {
-    ChainOut o;
-    o.best = best; o.best_tpp = best_tpp; o.best_tdp = best_tdp; o.L0 = L0;
-    o.best_step = best_step; o.accepted = accepted; o.f = T.f; o.c = (int32_t)chain;
-    P.out[slot] = o;
-  }
+  if (active) { out->best = best; out->accepted = accepted; out->f = T.f; out->c = (int32_t)chain; }
 }
 
 // Compile-time pipeline depth for the common power-of-two depths (the Eq.5 sums unroll).
