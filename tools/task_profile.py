@@ -42,6 +42,15 @@ def main(name="C2", chains=None, iters=None):
     ts = np.linspace(0, (tp[:, 1].max() - t0), 20)
     act = [int(np.sum((tp[:, 0] - t0 <= t) & (tp[:, 1] - t0 > t))) for t in ts]
     print("active warps over time:", act)
+    # chunk barrier waste: the warps of one block chunk start together on one SM; the early
+    # finishers idle until the chunk's last warp ends (the block's next fetch is collective)
+    groups = collections.defaultdict(list)
+    for s, e, sm, c in tp:
+        groups[(int(sm), int(s) // 20000)].append(int(e))   # same SM, starts within 20 us
+    idle = sum(max(es) - e for es in groups.values() for e in es)
+    busy = float(np.sum(tp[:, 1] - tp[:, 0]))
+    print(f"chunk barrier idle: {idle / 1e6:.1f} warp-ms = {100 * idle / busy:.1f}% of busy warp time "
+          f"({len(groups)} chunks)")
 
 
 if __name__ == "__main__":
