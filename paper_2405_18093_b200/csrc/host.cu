@@ -1,5 +1,7 @@
 // host.cu -- the C ABI of include/pipette.h: validation, context, device tables,
 // launch orchestration of K1-K6 and the NCCL combine across ranks.
+#include <cuda.h>
+#include <cudaTypedefs.h>
 #include <nccl.h>
 #include <nvtx3/nvToolsExt.h>
 
@@ -238,6 +240,22 @@ cudaError_t ensure_up(DevBuf& b, size_t bytes, std::vector<unsigned char>& up) {
   cudaError_t e = ensure(b, bytes);
   if (b.p != before) up.clear();
   return e;
+}
+
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no libcuda link); null if
+// the driver does not provide it
+PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static bool tried = false;
+  if (!tried) {
+    tried = true;
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = (PFN_cuTensorMapEncodeTiled_v12000)p;
+  }
+  return fn;
 }
 
 // Blocks per SM of kern at (threads, smem); the kernel's dynamic shared-memory limit is
@@ -890,8 +908,15 @@ pipette_status pipette_eval(pipette_ctx* ctx, const pipette_model* model, int64_
   const void* kern;
   size_t smem;
   int threads, grid, occ = 0;
-  const char* thr_env = getenv("PIPETTE_EVAL_THREAD");   // A/B knob: the thread-per-candidate MODE 1 path
-  if (mode == 1 && !(thr_env && atoi(thr_env) == 1)) {
+  CUtensorMap tmap;
+  std::memset(&tmap, 0, sizeof tmap);
+  P.tma = 0;
+  // one warp per candidate for large clusters (n >= 64: the R table is >= 32 KB and leaves
+  // the thread path one block per SM; measured C5 8.1e8 vs 5.2e8 candidates/s), else one
+  // thread per candidate (C4, n = 32: 2.5e9 vs 8.9e8).  PIPETTE_EVAL_THREAD=1/0 forces a path.
+  const char* thr_env = getenv("PIPETTE_EVAL_THREAD");
+  const bool warp_path = mode == 1 && (thr_env ? atoi(thr_env) == 0 : ctx->n_nodes >= 64);
+  if (warp_path) {
     // large clusters: one warp per candidate (k_eval_warp)
     kern = eval_warp_kernel();
     threads = eval_warp_threads();
@@ -906,6 +931,22 @@ pipette_status pipette_eval(pipette_ctx* ctx, const pipette_model* model, int64_
     smem = eval_smem_bytes(mode, perm_stride, P.vec16 != 0, ctx->n_nodes, ctx->E, P.bm_words);
     P.staged = P.vec16 && perm_stride <= 64 && smem <= 96 * 1024;   // long rows: direct 16-byte loads measured faster
     if (!P.staged) smem = eval_smem_bytes(mode, perm_stride, false, ctx->n_nodes, ctx->E, P.bm_words);
+    // single-configuration tiles of 128-byte rows: TMA tensor copies (SWIZZLE_128B) instead of
+    // per-lane cp.async (PIPETTE_EVAL_TMA=0 disables)
+    const char* tma_env = getenv("PIPETTE_EVAL_TMA");
+    if (P.staged && perm_stride == 64 && !(tma_env && atoi(tma_env) == 0)) {
+      if (PFN_cuTensorMapEncodeTiled_v12000 enc = tensor_map_encoder()) {
+        cuuint64_t dims[2] = {64, (cuuint64_t)n};
+        cuuint64_t strides[1] = {128};
+        cuuint32_t box[2] = {64, 32}, estr[2] = {1, 1};
+        if (enc(&tmap, CU_TENSOR_MAP_DATA_TYPE_UINT16, 2, (void*)d_perm, dims, strides, box, estr,
+                CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS) {
+          P.tma = 1;
+          smem += 1024;   // (1024-byte alignment of the staging buffers)
+        }
+      }
+    }
     if (smem > 227 * 1024) return fail(ctx, PIPETTE_E_UNSUPPORTED, "eval shared memory %zu B too large", smem);
     kern = eval_kernel(mode);
     threads = 256;
@@ -913,7 +954,9 @@ pipette_status pipette_eval(pipette_ctx* ctx, const pipette_model* model, int64_
     const long long need = (n + eval_tile_size() - 1) / eval_tile_size();   // candidate tiles
     grid = (int)std::min<long long>(need, (long long)occ * ctx->n_sms);
   }
-  void* args[] = {&P};
+  void* args_thread[] = {&P, &tmap};
+  void* args_warp[] = {&P};
+  void** args = warp_path ? args_warp : args_thread;
   nvtxRangePushA("pipette_eval K2");
   CU(wait_tables(ctx, s));
   CU(cudaLaunchKernel(kern, dim3(grid), dim3(threads), args, smem, s));

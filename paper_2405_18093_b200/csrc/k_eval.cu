@@ -19,6 +19,8 @@
 //          link of Eq.6 is one load from the subset-max table.
 //   MODE 1 (general): bitmap and counts in thread-interleaved shared memory (bank-
 //          conflict free), pairwise scan of the stage-1 node set.
+#include <cuda.h>
+
 #include "devmath.cuh"
 #include "pipette_dev.cuh"
 
@@ -364,10 +366,35 @@ __device__ __forceinline__ void gather_contig(const EvalParams& P, unsigned char
   asm volatile("cp.async.commit_group;\n" ::: "memory");
 }
 
+// TMA (cp.async.bulk.tensor) staging of a single-configuration tile's rows when a row is
+// exactly 128 bytes (perm_stride = 64): the tensor map describes the candidate rows as a 2-D
+// u16 tensor (64 x n) with SWIZZLE_128B, whose smem layout -- 16-byte chunk c of row r at
+// chunk c ^ (r & 7) -- is the XOR swizzle the per-thread row reads use (swz), so one elected
+// lane's copy replaces the warp's per-lane cp.async address and swizzle arithmetic.  The
+// copy completes on a per-warp mbarrier (transaction bytes); rows past n are zero-filled.
+__device__ __forceinline__ void tma_rows(const CUtensorMap* tmap, unsigned char* dst, uint32_t mbar, long long row0) {
+  const uint32_t d = (uint32_t)__cvta_generic_to_shared(dst);
+  asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");   // (after the generic reads of the buffer)
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(mbar), "r"(32u * 128u) : "memory");
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];\n" ::
+          "r"(d), "l"(reinterpret_cast<unsigned long long>(tmap)), "r"(0), "r"((int)row0), "r"(mbar)
+      : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint32_t mbar, uint32_t phase) {
+  uint32_t done = 0;
+  while (!done)
+    asm volatile("{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }\n"
+                 : "=r"(done) : "r"(mbar), "r"(phase) : "memory");
+}
+
 template <int MODE>
-__global__ void __launch_bounds__(kEvalThreads, 4) k_eval_stream(EvalParams P) {
+__global__ void __launch_bounds__(kEvalThreads, 4) k_eval_stream(EvalParams P, const __grid_constant__ CUtensorMap tmap) {
   constexpr bool REP = MODE == 0;
-  extern __shared__ __align__(128) unsigned char smem[];
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  // (TMA's 128-byte swizzle needs 1024-byte aligned destinations: the host adds 1 KB)
+  unsigned char* smem = P.tma ? smem_raw + ((1024u - ((uint32_t)__cvta_generic_to_shared(smem_raw) & 1023u)) & 1023u)
+                              : smem_raw;
   const int n = P.n_nodes, nn = n * n;
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5, nwarps = kEvalThreads / 32;
   // layout: [warp staging buffers nwarps x 32 x rb][R][keys][per-thread scratch]
@@ -376,6 +403,13 @@ __global__ void __launch_bounds__(kEvalThreads, 4) k_eval_stream(EvalParams P) {
   const bool staged = P.staged != 0;
   const uint32_t wb_bytes = staged ? 32u * rb : 0u;   // one buffer
   unsigned char* wbuf = smem + (size_t)wid * wb_bytes;
+  __shared__ __align__(8) unsigned long long s_mbar[kEvalThreads / 32];
+  const uint32_t mbar = (uint32_t)__cvta_generic_to_shared(&s_mbar[wid]);
+  uint32_t mbar_phase = 0;
+  if (P.tma && lane == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(mbar) : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
   size_t off = (size_t)nwarps * wb_bytes;
   double* Rs = reinterpret_cast<double*>(smem + off);
   const uint32_t lgn = n <= 1 ? 0u : 32u - __clz(n - 1);   // MODE 0 padded side 2^lgn >= n
@@ -463,9 +497,15 @@ __global__ void __launch_bounds__(kEvalThreads, 4) k_eval_stream(EvalParams P) {
     for (int g = wid; g < groups; g += nwarps) {
       unsigned char* cur = wbuf;
       if (staged) {   // (one buffer per warp: the other resident warps hide the gather)
-        if (mixed) gather_rows(P, wbuf, order + g * 32, base, rb, lane);
-        else gather_contig(P, wbuf, base + (long long)g * 32, min(32, cnt_valid - g * 32), rb, lane);
-        asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+        if (!mixed && P.tma) {   // one elected lane, the tensor engine does the copy
+          if (lane == 0) tma_rows(&tmap, wbuf, mbar, base + (long long)g * 32);
+          mbar_wait(mbar, mbar_phase);
+          mbar_phase ^= 1u;
+        } else {
+          if (mixed) gather_rows(P, wbuf, order + g * 32, base, rb, lane);
+          else gather_contig(P, wbuf, base + (long long)g * 32, min(32, cnt_valid - g * 32), rb, lane);
+          asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+        }
         __syncwarp();
       }
       const int sidx = g * 32 + lane;

@@ -164,6 +164,7 @@ struct EvalParams {
   int32_t staged;            // rows gathered into per-warp shared staging buffers (vec16, fits)
   int32_t bm_words;          // bitmap words per thread (ceil(maxN/32))
   int32_t rep;
+  int32_t tma;               // single-configuration tiles staged by TMA (128-byte rows, tensor map)
   double* latency;
   unsigned long long* mem;
   uint8_t* status;

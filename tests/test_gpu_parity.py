@@ -607,3 +607,37 @@ def test_search_mode1_c4_ten_thousand_iterations():
     st = {}
     _sampled_chain_parity(W.WORKLOADS["C4"], chains=64, iters=10000, n_sample=24, trace_n=2, stats=st)
     assert st["mode"] == 1
+
+
+@pytest.mark.parametrize("name,stride_pad,force", [("C4", 0, "0"), ("C4", 3, "0"), ("C5", 5, "0"), ("C5", 0, "1")])
+def test_eval_both_k2_paths_any_stride(name, stride_pad, force, monkeypatch):
+    # PIPETTE_EVAL_THREAD forces K2's path: the warp-per-candidate kernel on C4 (k <= 16 member
+    # pairs and the sorted-list T_ex), the thread path on C5; an odd stride takes the unaligned
+    # row reads (no uint4 prefetch); plus invalid rows (duplicate, id >= N) and unknown configs
+    monkeypatch.setenv("PIPETTE_EVAL_THREAD", force)
+    w = W.WORKLOADS[name]
+    pip, B, prof = _ctx(w)
+    model, mo, cl = _models(w)
+    P = O.make_profile(prof)
+    R = O.inverse_bandwidth(B)
+    feas = [c for c in O.enumerate_configs(cl, mo, w.bs_global, P) if c.feasible]
+    rng = np.random.default_rng(17)
+    stride = max(c.pp * c.dp for c in feas) + stride_pad
+    rows, perms, want, st_want = [], [], [], []
+    for c in feas:
+        K = O.constants(cl, mo, c, P)
+        for p in W.random_perms(K.N, 10, int(rng.integers(1 << 30))):
+            row = np.zeros(stride, dtype=np.uint16)
+            row[:K.N] = p
+            rows.append((c.pp, c.tp, c.dp, c.mb)); perms.append(row); want.append(O.latency(K, R, p).T); st_want.append(0)
+    c = feas[0]
+    bad = np.zeros(stride, dtype=np.uint16); bad[:c.pp * c.dp] = np.arange(c.pp * c.dp); bad[1] = bad[0]
+    big = np.zeros(stride, dtype=np.uint16); big[:c.pp * c.dp] = np.arange(c.pp * c.dp); big[2] = c.pp * c.dp
+    for r_ in (bad, big):
+        rows.append((c.pp, c.tp, c.dp, c.mb)); perms.append(r_); want.append(np.nan); st_want.append(3)
+    rows.append((c.pp + 1000, c.tp, c.dp, c.mb)); perms.append(bad); want.append(np.nan); st_want.append(2)
+    lat, mem, st = _eval_batch(pip, model, w.bs_global, rows, np.stack(perms))
+    assert st.tolist() == st_want
+    ok = np.array(st_want) == 0
+    assert _assert_close(lat[ok], np.array(want)[ok]) == 0
+    assert np.all(np.isnan(lat[~ok]))
