@@ -303,7 +303,7 @@ def sa_roofline(cfgs, feas, chains, iterations, world, sa_avg_s, measured, pk, w
             "pp1_share_of_proposals": props1 / max(props, 1),
             "traffic": ncu_traffic("k_sa_chains", workload),
             "traffic_note": "DRAM bytes per launch (ncu): chain state lives in shared memory, R and lists in L2",
-            "pipes": ncu_pipes(f"r02_sa_{workload.lower()}_ncu_summary.txt"),
+            "pipes": ncu_pipes(f"r02_sa_{workload.lower()}_fullsize_ncu_digest.txt"),
             "note": "counts and ceilings in DESIGN.md 8; pipes = ncu pipe utilisation of the committed capture"}
 
 

@@ -148,6 +148,20 @@ __device__ __forceinline__ bool metropolis_fast(double d, double beta, double u)
   return metropolis_exact(x, u);
 }
 
+// Warp max of non-negative doubles (their bit patterns order like the values) by two 32-bit
+// redux.sync, and the sum of c over the lanes holding it: three REDUX instead of a five-level
+// shuffle butterfly on (double, int) pairs.
+__device__ __forceinline__ double warp_max_nonneg(double m, uint32_t c, uint32_t& count) {
+  const unsigned full = 0xffffffffu;
+  const unsigned long long b = (unsigned long long)__double_as_longlong(m);
+  const uint32_t hi = (uint32_t)(b >> 32), lo = (uint32_t)b;
+  const uint32_t H = __reduce_max_sync(full, hi);
+  const uint32_t Lo = __reduce_max_sync(full, hi == H ? lo : 0u);
+  const unsigned long long B = ((unsigned long long)H << 32) | Lo;
+  count = __reduce_add_sync(full, b == B ? c : 0u);
+  return __longlong_as_double((long long)B);
+}
+
 // Eq.3-4 composition with the Eq.5 value inside T_bubble (R6):
 // T = (((Sb + T_PP) * r) + Ss) + (T_in + T_ex).
 __device__ __forceinline__ double compose(double Sb, double r, double Ss, double tpp, double tin, double tex) {

@@ -22,7 +22,7 @@ namespace pip {
 __global__ void k_enumerate_filter(int, int, unsigned long long, int, pipette_model, long long,
                                    const pipette_profile_entry*, int, DevCfg*, unsigned long long*, int, int*,
                                    double*, int, EnumOut*);
-const void* eval_kernel(int mode);
+const void* eval_kernel(int mode, int threads);
 const void* eval_warp_kernel();
 size_t eval_warp_smem_bytes(int n_nodes, int E);
 int eval_warp_threads();
@@ -35,7 +35,8 @@ pipette_status models_launch(const DevCfg* cfgs, const unsigned long long* keys,
                              const double* R, int n_nodes, long long n, const pipette_config* cand,
                              const uint16_t* perm, int stride, double* tp, double* tprev, double* tdes,
                              uint8_t* status, void* stream);
-size_t eval_smem_bytes(int mode, int perm_stride, bool staged, int n_nodes, int E, int bm_words);
+size_t eval_smem_bytes(int mode, int perm_stride, bool staged, int n_nodes, int E, int bm_words, int threads,
+                       bool cnt_nib, int plen);
 __global__ void k_tin_values(const DevCfg*, const double*, const double*, int, double*);
 const void* sa_kernel(int mode, bool trace, int n_nodes, bool full);
 int sa_warp_state_bytes(int mode, int N, int pp, int dp, int n, int dp_cap, bool nib);
@@ -900,7 +901,7 @@ pipette_status pipette_eval(pipette_ctx* ctx, const pipette_model* model, int64_
   P.perm = d_perm;
   P.perm_stride = perm_stride;
   P.vec16 = ((uintptr_t)d_perm % 16 == 0) && (perm_stride % 8 == 0);
-  P.bm_words = (maxN + 31) / 32;
+  P.bm_words = (std::min(maxN, (int)perm_stride) + 31) / 32;   // (a row longer than perm_stride gets status 3)
   P.latency = d_latency;
   P.mem = (unsigned long long*)d_mem;
   P.status = d_status;
@@ -911,11 +912,18 @@ pipette_status pipette_eval(pipette_ctx* ctx, const pipette_model* model, int64_
   CUtensorMap tmap;
   std::memset(&tmap, 0, sizeof tmap);
   P.tma = 0;
-  // one warp per candidate for large clusters (n >= 64: the R table is >= 32 KB and leaves
-  // the thread path one block per SM; measured C5 8.1e8 vs 5.2e8 candidates/s), else one
-  // thread per candidate (C4, n = 32: 2.5e9 vs 8.9e8).  PIPETTE_EVAL_THREAD=1/0 forces a path.
+  // K2 path: one thread per candidate, in blocks of 768 for n >= 64 (the R table of up to
+  // 128 KB leaves one block per SM; nibble counts, a bitmap sized by perm_stride and the
+  // pair-list prefix in shared memory keep 24 warps resident) -- measured on C5 1.2e9 vs
+  // 8.1e8 candidates/s for one warp per candidate (k_eval_warp) and 5.6e8 with 8 warps.
+  // Knobs: PIPETTE_EVAL_THREAD=0 (warp path) / 1 (thread), PIPETTE_EVAL_THREADS=256/768.
   const char* thr_env = getenv("PIPETTE_EVAL_THREAD");
-  const bool warp_path = mode == 1 && (thr_env ? atoi(thr_env) == 0 : ctx->n_nodes >= 64);
+  const char* thn_env = getenv("PIPETTE_EVAL_THREADS");
+  const bool warp_path = mode == 1 && thr_env && atoi(thr_env) == 0;
+  P.cnt_nib = ctx->g <= 15 ? 1 : 0;   // (a stage-1 count never exceeds gpus_per_node)
+  P.plen = mode == 1 ? std::min(ctx->n_nodes * (ctx->n_nodes - 1), kSaM1PairPrefix) : 0;
+  int eval_threads = (mode == 1 && ctx->n_nodes >= 64) ? 768 : 256;
+  if (thn_env && (atoi(thn_env) == 256 || (atoi(thn_env) == 768 && mode == 1))) eval_threads = atoi(thn_env);
   if (warp_path) {
     // large clusters: one warp per candidate (k_eval_warp)
     kern = eval_warp_kernel();
@@ -928,9 +936,17 @@ pipette_status pipette_eval(pipette_ctx* ctx, const pipette_model* model, int64_
   } else {
     // rows gathered into per-warp shared staging buffers when they are 16-byte aligned and
     // the buffers fit beside the tables (else read straight from global memory)
-    smem = eval_smem_bytes(mode, perm_stride, P.vec16 != 0, ctx->n_nodes, ctx->E, P.bm_words);
+    smem = eval_smem_bytes(mode, perm_stride, P.vec16 != 0, ctx->n_nodes, ctx->E, P.bm_words, eval_threads,
+                           P.cnt_nib != 0, P.plen);
     P.staged = P.vec16 && perm_stride <= 64 && smem <= 96 * 1024;   // long rows: direct 16-byte loads measured faster
-    if (!P.staged) smem = eval_smem_bytes(mode, perm_stride, false, ctx->n_nodes, ctx->E, P.bm_words);
+    if (!P.staged)
+      smem = eval_smem_bytes(mode, perm_stride, false, ctx->n_nodes, ctx->E, P.bm_words, eval_threads,
+                             P.cnt_nib != 0, P.plen);
+    if (eval_threads == 768 && smem > 227 * 1024) {   // (does not fit: the 256-thread block)
+      eval_threads = 256;
+      smem = eval_smem_bytes(mode, perm_stride, false, ctx->n_nodes, ctx->E, P.bm_words, eval_threads,
+                             P.cnt_nib != 0, P.plen);
+    }
     // single-configuration tiles of 128-byte rows: TMA tensor copies (SWIZZLE_128B) instead of
     // per-lane cp.async (PIPETTE_EVAL_TMA=0 disables)
     const char* tma_env = getenv("PIPETTE_EVAL_TMA");
@@ -948,9 +964,9 @@ pipette_status pipette_eval(pipette_ctx* ctx, const pipette_model* model, int64_
       }
     }
     if (smem > 227 * 1024) return fail(ctx, PIPETTE_E_UNSUPPORTED, "eval shared memory %zu B too large", smem);
-    kern = eval_kernel(mode);
-    threads = 256;
-    if ((st = kernel_occupancy(ctx, kern, 256, smem, &occ)) != PIPETTE_OK) return st;
+    kern = eval_kernel(mode, eval_threads);
+    threads = eval_threads;
+    if ((st = kernel_occupancy(ctx, kern, threads, smem, &occ)) != PIPETTE_OK) return st;
     const long long need = (n + eval_tile_size() - 1) / eval_tile_size();   // candidate tiles
     grid = (int)std::min<long long>(need, (long long)occ * ctx->n_sms);
   }

@@ -89,8 +89,11 @@ struct RowSrc {
 struct EvalShared {
   const double* Rs;
   uint32_t* bm;     // [bm_words][T]
-  uint32_t* cnt;    // [ceil(n/4)][T]
+  uint32_t* cnt;    // [ceil(n/4)][T] byte counts, or [ceil(n/8)][T] nibbles (cnt_nib)
+  const uint16_t* pl;   // MODE 1: shared prefix of the R-sorted pair list (plen entries)
   int n, tid, lane, T;
+  int plen;
+  uint32_t cnt_nib;     // 1: stage-1 counts as nibbles (every count <= 15)
   uint32_t lgn;     // MODE 0: log2 of the padded table side
   const unsigned char* Rl;   // MODE 0: this lane's copy, &Rs[lane & 15]
   uint32_t row_bytes;        // MODE 0: 2^lgn * 16 copies * 8 B
@@ -244,7 +247,8 @@ __device__ __forceinline__ void eval_general(const EvalParams& P, const EvalShar
   const int N = C.N, pp = C.pp;
   const uint32_t spn = (uint32_t)C.spn;
   for (int w = 0; w < (N + 31) / 32; ++w) S.bm[w * S.T + S.tid] = 0u;
-  for (int w = 0; w < (S.n + 3) / 4; ++w) S.cnt[w * S.T + S.tid] = 0u;
+  const uint32_t clg = 2u + S.cnt_nib, cbits = 8u >> S.cnt_nib, cmask = (1u << cbits) - 1u;   // count plane
+  for (int w = 0; w < ((S.n - 1) >> clg) + 1; ++w) S.cnt[w * S.T + S.tid] = 0u;
   Mask<4> mask;
   mask.clear();
   bool ok = true;
@@ -263,7 +267,7 @@ __device__ __forceinline__ void eval_general(const EvalParams& P, const EvalShar
       nd = div_small(v, C.spn_magic, spn);
     }
     if (x == 0) {
-      S.cnt[(nd >> 2) * S.T + S.tid] += 1u << ((nd & 3) * 8);
+      S.cnt[(nd >> clg) * S.T + S.tid] += 1u << ((nd & ((1u << clg) - 1u)) * cbits);
       mask.set(nd);
       s = 0.0;
     } else {
@@ -303,7 +307,7 @@ __device__ __forceinline__ void eval_general(const EvalParams& P, const EvalShar
     while (bits) {
       const uint32_t a = wd * 32 + __ffs(bits) - 1;
       bits &= bits - 1;
-      const uint32_t c = (S.cnt[(a >> 2) * S.T + S.tid] >> ((a & 3) * 8)) & 0xffu;
+      const uint32_t c = (S.cnt[(a >> clg) * S.T + S.tid] >> ((a & ((1u << clg) - 1u)) * cbits)) & cmask;
       if (c >= 2) t_in = fmax(t_in, __dmul_rn(__ldg(qi + c), r_at<false>(S, a, a)));
       if (pairs) {
 #pragma unroll
@@ -318,11 +322,11 @@ __device__ __forceinline__ void eval_general(const EvalParams& P, const EvalShar
       }
     }
   }
-  if (!pairs && k >= 2) {
+  if (!pairs && k >= 2) {   // first pair of the R-sorted list inside N1; the value from the R table
     const int len = S.n * (S.n - 1);
     for (int j = 0; j < len; ++j) {
-      const uint32_t ab = __ldg(P.gl_ab + j);
-      if (mask.test(ab & 0xffu) && mask.test(ab >> 8)) { mx = __ldg(P.gl_val + j); break; }
+      const uint32_t ab = j < S.plen ? (uint32_t)S.pl[j] : (uint32_t)__ldg(P.gl_ab + j);
+      if (mask.test(ab & 0xffu) && mask.test(ab >> 8)) { mx = r_at<false>(S, ab & 0xffu, ab >> 8); break; }
     }
   }
   const double t_ex = k >= 2 ? __dmul_rn(__ldg(P.qtab + C.qe_off + k), mx) : 0.0;
@@ -388,8 +392,10 @@ __device__ __forceinline__ void mbar_wait(uint32_t mbar, uint32_t phase) {
                  : "=r"(done) : "r"(mbar), "r"(phase) : "memory");
 }
 
-template <int MODE>
-__global__ void __launch_bounds__(kEvalThreads, 4) k_eval_stream(EvalParams P, const __grid_constant__ CUtensorMap tmap) {
+template <int MODE, int THREADS>
+__global__ void __launch_bounds__(THREADS, THREADS <= 256 ? 4 : 1)
+    k_eval_stream(EvalParams P, const __grid_constant__ CUtensorMap tmap) {
+  constexpr int kEvalThreads = THREADS;   // (block size: 256, or 768 for large clusters)
   constexpr bool REP = MODE == 0;
   extern __shared__ __align__(128) unsigned char smem_raw[];
   // (TMA's 128-byte swizzle needs 1024-byte aligned destinations: the host adds 1 KB)
@@ -418,7 +424,10 @@ __global__ void __launch_bounds__(kEvalThreads, 4) k_eval_stream(EvalParams P, c
   unsigned long long* keys = reinterpret_cast<unsigned long long*>(smem + off);
   off += ((size_t)P.E * 8 + 15) & ~(size_t)15;
   uint32_t* bm = reinterpret_cast<uint32_t*>(smem + off);
-  off += (size_t)(P.bm_words + (n + 3) / 4) * kEvalThreads * 4;
+  const int cnt_words = P.cnt_nib ? (n + 7) / 8 : (n + 3) / 4;
+  off += (size_t)(P.bm_words + cnt_words) * kEvalThreads * 4;
+  uint16_t* pl = reinterpret_cast<uint16_t*>(smem + off);   // MODE 1: pair-list prefix
+  off += ((size_t)P.plen * 2 + 15) & ~(size_t)15;
   short* tile_e = reinterpret_cast<short*>(smem + off);   // config index per candidate (E < 32767)
   int* hist = reinterpret_cast<int*>(tile_e + kEvalTile);
   short* order = reinterpret_cast<short*>(hist + ((P.E + 2 + 3) & ~3));
@@ -433,9 +442,11 @@ __global__ void __launch_bounds__(kEvalThreads, 4) k_eval_stream(EvalParams P, c
     for (int i = tid; i < nn; i += kEvalThreads) Rs[i] = P.R[i];
   }
   for (int i = tid; i < P.E; i += kEvalThreads) keys[i] = P.keys[i];
+  for (int i = tid; i < P.plen; i += kEvalThreads) pl[i] = P.gl_ab[i];
   __syncthreads();
-  const EvalShared S{Rs, bm, bm + P.bm_words * kEvalThreads, n, tid, lane, kEvalThreads, lgn,
-                     reinterpret_cast<const unsigned char*>(Rs + (lane & 15)), (uint32_t)np * 128u};
+  const EvalShared S{Rs, bm, bm + P.bm_words * kEvalThreads, pl, n, tid, lane, kEvalThreads, P.plen,
+                     (uint32_t)P.cnt_nib, lgn, reinterpret_cast<const unsigned char*>(Rs + (lane & 15)),
+                     (uint32_t)np * 128u};
   const double qnan = __longlong_as_double(0x7ff8000000000000ll);
   const bool bucket_ok = true;   // (E < 32767 is checked by the host)
   unsigned long long last_raw = ~0ull;   // (pp = 0xffff is never a valid record)
@@ -547,15 +558,18 @@ __global__ void __launch_bounds__(kEvalThreads, 4) k_eval_stream(EvalParams P, c
 
 int eval_tile_size() { return kEvalTile; }
 
-// Dynamic shared memory of k_eval_stream (staged: per-warp double-buffered row staging).
-size_t eval_smem_bytes(int mode, int perm_stride, bool staged, int n_nodes, int E, int bm_words) {
+// Dynamic shared memory of k_eval_stream (staged: per-warp row staging; cnt_nib: nibble
+// counts; plen: pair-list prefix entries; threads: block size).
+size_t eval_smem_bytes(int mode, int perm_stride, bool staged, int n_nodes, int E, int bm_words, int threads,
+                       bool cnt_nib, int plen) {
   const size_t nn = (size_t)n_nodes * n_nodes;
   const size_t wb = staged ? (size_t)32 * perm_stride * 2 : 0;
   size_t np = 1;
   while (np < (size_t)n_nodes) np <<= 1;
-  return (size_t)(kEvalThreads / 32) * wb + (mode == 0 ? np * np * 16 : nn) * 8 + (((size_t)E * 8 + 15) & ~(size_t)15) +
-         (size_t)(bm_words + (n_nodes + 3) / 4) * kEvalThreads * 4 + (size_t)kEvalTile * sizeof(short) +
-         (size_t)((E + 2 + 3) & ~3) * sizeof(int) + (size_t)kEvalTile * sizeof(short);
+  const size_t cnt_words = cnt_nib ? (n_nodes + 7) / 8 : (n_nodes + 3) / 4;
+  return (size_t)(threads / 32) * wb + (mode == 0 ? np * np * 16 : nn) * 8 + (((size_t)E * 8 + 15) & ~(size_t)15) +
+         (size_t)(bm_words + cnt_words) * threads * 4 + (((size_t)plen * 2 + 15) & ~(size_t)15) +
+         (size_t)kEvalTile * sizeof(short) + (size_t)((E + 2 + 3) & ~3) * sizeof(int) + (size_t)kEvalTile * sizeof(short);
 }
 
 // qi(c) R[a][a] for every enumerated config, node a < n <= 16 and c < 16 (0 for c < 2):
@@ -571,8 +585,9 @@ __global__ void k_tin_values(const DevCfg* __restrict__ cfgs, const double* __re
 }
 
 // Host-side handle of the K2 variant (MODE 0 small clusters, 1 general).
-const void* eval_kernel(int mode) {
-  return mode == 0 ? (const void*)k_eval_stream<0> : (const void*)k_eval_stream<1>;
+const void* eval_kernel(int mode, int threads) {
+  if (mode == 0) return (const void*)k_eval_stream<0, 256>;
+  return threads == 768 ? (const void*)k_eval_stream<1, 768> : (const void*)k_eval_stream<1, 256>;
 }
 
 }  // namespace pip

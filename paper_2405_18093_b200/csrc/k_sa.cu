@@ -777,6 +777,33 @@ __device__ __forceinline__ void hc_rescan(const HcState& st, int dp, int pp_rt, 
   cnt = (m0 == mx ? c0 : 0) + (m1 == mx ? c1 : 0);
 }
 
+// MODE 0 counterpart of sa_mode1.cuh's coop_tpp: for each flagged lane L (its unique max
+// pipeline decreased), lane j takes pipelines j, j + 32, ... -- L's cached sums (which hold
+// the tentative new sums) or re-summed from L's hop codes (which hold the tentative swap) --
+// and the (max, count) pair is reduced by redux.sync.  Called by all lanes, converged.
+template <int PP>
+__device__ __forceinline__ void hc_coop_tpp(bool need, unsigned char* ws, const double* psum, bool cache, int dp, int pp,
+                                            const double* Tl, int lane, double& tpp2, int& nmax2) {
+  __syncwarp();
+  for (unsigned todo = __ballot_sync(0xffffffffu, need); todo; todo &= todo - 1u) {
+    const int L = __ffs(todo) - 1;
+    HcState stL;
+    stL.hb = ws + L * 4;
+    stL.sb = nullptr;
+    stL.hw = reinterpret_cast<const uint32_t*>(ws) + L;
+    double m = 0.0;
+    int c = 0;
+    for (int z = lane; z < dp; z += 32) {
+      const double v = cache ? psum[z * 32 + L] : hc_sum<PP>(stL, (uint32_t)z, pp, Tl);
+      c = v > m ? 1 : c + (v == m ? 1 : 0);
+      m = fmax(m, v);
+    }
+    uint32_t cnt;
+    m = warp_max_nonneg(m, (uint32_t)c, cnt);
+    if (lane == L) { tpp2 = m; nmax2 = (int)cnt; }
+  }
+}
+
 __host__ __device__ inline int hc_warp_state_bytes(int N, int pp, int dp, int dp_cap) {
   const int plane = align16(((N + 3) / 4) * 128);
   return 2 * plane + ((pp >= 4 && dp <= dp_cap) ? align16(dp * 256) : 0);
@@ -906,32 +933,36 @@ __device__ __forceinline__ void run_task_hc(const SaParams& P, const SaTask T, c
         int nmax2 = nmax;
         const double snew = fmax(sA, sB);
         const int keep = nmax - (oldA == tpp ? 1 : 0) - ((two && oldB == tpp) ? 1 : 0);  // untouched at max
-        if (keep > 0 || snew >= tpp) {
+        const bool fast = keep > 0 || snew >= tpp;
+        if (fast) {
           tpp2 = (keep > 0) ? fmax(tpp, snew) : snew;
           nmax2 = (keep > 0 && tpp2 == tpp ? keep : 0) + (sA == tpp2 ? 1 : 0) + ((two && sB == tpp2) ? 1 : 0);
-        } else if (cache) {
-          // the unique max pipeline decreased: rescan the cached sums
-          double m0 = sA, m1 = two ? sB : 0.0;
-          int c0 = 1, c1 = two ? 1 : 0;
-          int z = 0;
-          for (; z + 2 <= dp; z += 2) {
-            const double v0 = ((uint32_t)z == zp || (uint32_t)z == zq) ? 0.0 : psum[z * 32 + lane];
-            const double v1 = ((uint32_t)z + 1u == zp || (uint32_t)z + 1u == zq) ? 0.0 : psum[(z + 1) * 32 + lane];
-            c0 = v0 > m0 ? 1 : c0 + (v0 == m0 ? 1 : 0);
-            m0 = fmax(m0, v0);
-            c1 = v1 > m1 ? 1 : c1 + (v1 == m1 ? 1 : 0);
-            m1 = fmax(m1, v1);
+        }
+        // the unique max pipeline decreased: rescan over all pipelines (the new sums enter the
+        // cache tentatively, restored if rejected) -- up to 8 cached sums per lane, else the
+        // whole warp (as MODE 1's coop_tpp: a per-lane rescan runs at a few active lanes)
+        if (!fast && cache) {
+          psum[zp * 32 + lane] = sA;
+          psum[zb * 32 + lane] = sB;
+        }
+        if (dp <= 8) {   // (few pipelines: per lane; uncached pp = 2 C2 configs measured 19 vs 16 ms coop)
+          if (!fast) {
+            if (cache) {
+              double m = 0.0;
+              int c = 0;
+              for (int z = 0; z < dp; ++z) {
+                const double v = psum[z * 32 + lane];
+                c = v > m ? 1 : c + (v == m ? 1 : 0);
+                m = fmax(m, v);
+              }
+              tpp2 = m;
+              nmax2 = c;
+            } else {
+              hc_rescan<PP>(st, dp, pp, Tl, tpp2, nmax2);   // (H already holds the tentative swap)
+            }
           }
-          if (z < dp) {
-            const double v0 = ((uint32_t)z == zp || (uint32_t)z == zq) ? 0.0 : psum[z * 32 + lane];
-            c0 = v0 > m0 ? 1 : c0 + (v0 == m0 ? 1 : 0);
-            m0 = fmax(m0, v0);
-          }
-          tpp2 = fmax(m0, m1);
-          nmax2 = (m0 == tpp2 ? c0 : 0) + (m1 == tpp2 ? c1 : 0);
         } else {
-          // no cache: re-sum every pipeline of the tentative mapping (H already holds it)
-          hc_rescan<PP>(st, dp, pp, Tl, tpp2, nmax2);
+          hc_coop_tpp<PP>(!fast, ws, psum, cache, dp, pp, Tl, lane, tpp2, nmax2);
         }
         // ---- Eq.6: the stage-1 node multiset changes only if exactly one of p, q is a
         //      stage-1 position and the two nodes differ
@@ -960,6 +991,10 @@ __device__ __forceinline__ void run_task_hc(const SaParams& P, const SaTask T, c
             improved = true;
           }
         } else {   // revert the tentative hop codes (reverse order: adjacent bytes end right)
+          if (!fast && cache) {
+            psum[zb * 32 + lane] = oldB;
+            psum[zp * 32 + lane] = oldA;
+          }
           if (qn) *bq1 = (uint8_t)hq1;
           *bq = (uint8_t)hq;
           if (pn) *bp1 = (uint8_t)hp1;

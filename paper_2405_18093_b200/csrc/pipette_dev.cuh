@@ -165,6 +165,8 @@ struct EvalParams {
   int32_t bm_words;          // bitmap words per thread (ceil(maxN/32))
   int32_t rep;
   int32_t tma;               // single-configuration tiles staged by TMA (128-byte rows, tensor map)
+  int32_t cnt_nib;           // per-thread stage-1 counts as nibbles (every count <= 15)
+  int32_t plen;              // MODE 1: entries of the R-sorted pair list copied to shared memory
   double* latency;
   unsigned long long* mem;
   uint8_t* status;

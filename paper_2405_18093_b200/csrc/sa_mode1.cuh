@@ -153,20 +153,6 @@ __device__ __forceinline__ void sb_sum2(const HcState& st, uint32_t za, uint32_t
   sb = b;
 }
 
-// Warp max of non-negative doubles (their bit patterns order like the values) by two 32-bit
-// redux.sync, and the sum of c over the lanes holding it: three REDUX instead of a five-level
-// shuffle butterfly on (double, int) pairs.
-__device__ __forceinline__ double warp_max_nonneg(double m, uint32_t c, uint32_t& count) {
-  const unsigned full = 0xffffffffu;
-  const unsigned long long b = (unsigned long long)__double_as_longlong(m);
-  const uint32_t hi = (uint32_t)(b >> 32), lo = (uint32_t)b;
-  const uint32_t H = __reduce_max_sync(full, hi);
-  const uint32_t Lo = __reduce_max_sync(full, hi == H ? lo : 0u);
-  const unsigned long long B = ((unsigned long long)H << 32) | Lo;
-  count = __reduce_add_sync(full, b == B ? c : 0u);
-  return __longlong_as_double((long long)B);
-}
-
 // T_PP of a lane's tentative mapping when its unique max pipeline decreased: the max over
 // all dp Eq.5 sums and its multiplicity, computed by the whole warp (called converged).
 // For each flagged lane L, lane j takes pipelines j, j + 32, ... -- lane L's cached sums,

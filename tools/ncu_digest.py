@@ -34,10 +34,11 @@ def main():
     units = float(sys.argv[2]) if len(sys.argv) > 2 else None
     rows = list(csv.reader(io.StringIO(run(rep, "--page", "raw", "--csv"))))
     d = dict(zip(rows[0], rows[2])) if len(rows) > 2 else {}
+    u = dict(zip(rows[0], rows[1])) if len(rows) > 2 else {}
     print(f"# ncu digest of {rep}")
     for k in METRICS:
         if k in d:
-            print(f"{k} {d[k].replace(',', '')}")
+            print(f"{k} {d[k].replace(',', '')} {u.get(k, '')}".rstrip())
     for k, v in d.items():
         if "issue_stalled" in k and k.endswith("per_issue_active.ratio"):
             try:
