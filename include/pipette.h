@@ -50,12 +50,26 @@ typedef struct {
   double c_layer_s, tp_layer_s;
 } pipette_profile_entry;
 
+/* Host transport of the combine (optional, see pipette_dist): allreduce of `count` uint64
+ * words in place on a HOST buffer, op 0 = element-wise min, 1 = element-wise sum (mod 2^64);
+ * returns 0 on success, anything else fails the search with E_NCCL.  Called on the thread
+ * that called pipette_search, three times per search, in the same order on every rank. */
+typedef int (*pipette_host_allreduce_fn)(void* user, uint64_t* buf, int64_t count, int32_t op);
+
 /* Multi-GPU description (one process per GPU).  world == 1 needs no NCCL id. For
- * world > 1, nccl_unique_id points to the 128-byte ncclUniqueId produced on rank 0 by
- * pipette_nccl_unique_id() and broadcast by the caller (e.g. torch.distributed). */
+ * world > 1 either
+ *   - nccl_unique_id points to the 128-byte ncclUniqueId produced on rank 0 by
+ *     pipette_nccl_unique_id() and broadcast by the caller (e.g. torch.distributed): the
+ *     combine's reductions run as ncclAllReduce on the context's stream; or
+ *   - nccl_unique_id == NULL and host_allreduce != NULL: the same three reductions (R18)
+ *     run through the caller's host collective on D2H-staged buffers (e.g. a gloo process
+ *     group, or several ranks sharing one GPU, which NCCL refuses).  Identical results.
+ * host_allreduce / host_user may be NULL/unused otherwise. */
 typedef struct {
   int32_t rank, world, device;
   const void* nccl_unique_id;
+  pipette_host_allreduce_fn host_allreduce;
+  void* host_user;
 } pipette_dist;
 
 /* GPT-style model shape (Eq.7 inputs; message sizes R4; memory R11).

@@ -19,7 +19,7 @@ import numpy as np
 
 from . import _abi
 
-__all__ = ["Pipette", "Model", "PipetteError", "shard_items", "nccl_unique_id", "STATUS"]
+__all__ = ["Pipette", "Model", "PipetteError", "shard_items", "nccl_unique_id", "torch_host_allreduce", "STATUS"]
 
 STATUS = {0: "ok", 1: "oom", 2: "invalid_config", 3: "invalid_mapping", 4: "no_profile"}
 
@@ -135,13 +135,39 @@ def load_memory_mlp(path=None) -> dict:
         return json.load(f)
 
 
+_SIGN = np.uint64(1 << 63)
+
+
+def torch_host_allreduce(group=None):
+    """A pipette_dist.host_allreduce over a torch.distributed process group (e.g. gloo):
+    the library hands over a host uint64 buffer and the op (0 min, 1 sum); this only moves
+    it through dist.all_reduce (plumbing; uint64 order kept by flipping the sign bit)."""
+    import torch
+    import torch.distributed as dist
+
+    def fn(user, buf, count, op):
+        try:
+            a = np.ctypeslib.as_array(buf, shape=(int(count),))
+            if op == 0:
+                a ^= _SIGN
+            t = torch.from_numpy(a.view(np.int64))
+            dist.all_reduce(t, op=dist.ReduceOp.MIN if op == 0 else dist.ReduceOp.SUM, group=group)
+            if op == 0:
+                a ^= _SIGN
+            return 0
+        except Exception:   # noqa: BLE001 -- reported to the library as a failed transport
+            return 1
+    return fn
+
+
 class Pipette:
-    """A pipette_ctx on one GPU.  For world > 1 pass rank/world/device and the 128-byte
-    NCCL id from rank 0 (see `from_torch_distributed`)."""
+    """A pipette_ctx on one GPU.  For world > 1 pass rank/world/device and either the
+    128-byte NCCL id from rank 0 (see `from_torch_distributed`) or `host_allreduce`, a
+    callable (user, buf, count, op) -> int run on host buffers (`torch_host_allreduce`)."""
 
     def __init__(self, n_nodes: int, gpus_per_node: int, bandwidth, profile, mem_capacity_bytes: int = 80_000_000_000,
                  mem_margin_permille: int = 100, rank: int = 0, world: int = 1, device: int | None = None,
-                 nccl_id: bytes | None = None):
+                 nccl_id: bytes | None = None, host_allreduce=None):
         import torch
         self._L = _abi.lib()
         self.n_nodes, self.gpus_per_node = int(n_nodes), int(gpus_per_node)
@@ -156,8 +182,9 @@ class Pipette:
             arr[i] = _abi.ProfileEntry(int(tp), int(mb), float(c), float(t))
         cl = _abi.Cluster(self.n_nodes, self.gpus_per_node, int(mem_capacity_bytes), int(mem_margin_permille))
         self._idbuf = C.create_string_buffer(nccl_id, 128) if nccl_id is not None else None
+        self._host_ar = _abi.HOST_ALLREDUCE(host_allreduce) if host_allreduce is not None else _abi.HOST_ALLREDUCE()
         dist = _abi.Dist(self.rank, self.world, self.device,
-                         C.cast(self._idbuf, C.c_void_p) if self._idbuf is not None else None)
+                         C.cast(self._idbuf, C.c_void_p) if self._idbuf is not None else None, self._host_ar, None)
         h = C.c_void_p()
         st = self._L.pipette_init(C.byref(h), C.byref(cl), B.ctypes.data_as(C.POINTER(C.c_double)), arr,
                                   len(prof), C.byref(dist))
@@ -166,12 +193,20 @@ class Pipette:
         self._h = h
 
     @classmethod
-    def from_torch_distributed(cls, n_nodes, gpus_per_node, bandwidth, profile, **kw):
+    def from_torch_distributed(cls, n_nodes, gpus_per_node, bandwidth, profile, transport: str = "nccl", **kw):
         """Build a context on every rank of the default torch.distributed process group:
-        rank 0 creates the NCCL id, torch.distributed broadcasts it (plumbing only)."""
+        transport "nccl": rank 0 creates the NCCL id, torch.distributed broadcasts it (plumbing
+        only); "host": the combine's reductions go through the process group itself
+        (`torch_host_allreduce`; e.g. gloo, or ranks sharing one GPU)."""
         import torch
         import torch.distributed as dist
         rank, world = dist.get_rank(), dist.get_world_size()
+        if transport == "host":
+            dev = kw.pop("device", torch.cuda.current_device())
+            return cls(n_nodes, gpus_per_node, bandwidth, profile, rank=rank, world=world, device=dev,
+                       host_allreduce=torch_host_allreduce() if world > 1 else None, **kw)
+        if transport != "nccl":
+            raise ValueError(f"transport must be 'nccl' or 'host', not {transport!r}")
         obj = [nccl_unique_id() if rank == 0 else None]
         if world > 1:
             dist.broadcast_object_list(obj, src=0)

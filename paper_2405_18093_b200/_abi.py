@@ -23,8 +23,12 @@ class ProfileEntry(C.Structure):
     _fields_ = [("tp", C.c_int32), ("mb", C.c_int32), ("c_layer_s", C.c_double), ("tp_layer_s", C.c_double)]
 
 
+HOST_ALLREDUCE = C.CFUNCTYPE(C.c_int, C.c_void_p, C.POINTER(C.c_uint64), C.c_int64, C.c_int32)
+
+
 class Dist(C.Structure):
-    _fields_ = [("rank", C.c_int32), ("world", C.c_int32), ("device", C.c_int32), ("nccl_unique_id", C.c_void_p)]
+    _fields_ = [("rank", C.c_int32), ("world", C.c_int32), ("device", C.c_int32), ("nccl_unique_id", C.c_void_p),
+                ("host_allreduce", HOST_ALLREDUCE), ("host_user", C.c_void_p)]
 
 
 class Model(C.Structure):

@@ -140,6 +140,10 @@ struct pipette_ctx {
   int n_sms = 148;
   cudaStream_t stream = nullptr;
   ncclComm_t comm = nullptr;
+  pipette_host_allreduce_fn host_ar = nullptr;   // host transport of the combine (no NCCL)
+  void* host_user = nullptr;
+  unsigned long long* h_ar = nullptr;            // its pinned staging buffer
+  size_t h_ar_words = 0;
   std::string err;
   int64_t launches = 0;
   // device tables
@@ -223,6 +227,31 @@ pipette_status fail(pipette_ctx* c, pipette_status s, const char* fmt, ...) {
     ncclResult_t r_ = (call);                                                                            \
     if (r_ != ncclSuccess) return fail(ctx, PIPETTE_E_NCCL, "%s: %s", #call, ncclGetErrorString(r_)); \
   } while (0)
+
+// One reduction of the combine (R18) over `count` uint64 words, op 0 = min, 1 = sum: NCCL
+// on the stream, or the caller's host collective (pipette_dist.host_allreduce) on a pinned
+// copy -- the stream is drained around the host call, the result copied back in order.
+pipette_status allreduce_u64(pipette_ctx* ctx, const unsigned long long* src, unsigned long long* dst, size_t count,
+                             int op, cudaStream_t s) {
+  if (ctx->comm) {
+    NC(ncclAllReduce(src, dst, count, ncclUint64, op == 0 ? ncclMin : ncclSum, ctx->comm, s));
+    return PIPETTE_OK;
+  }
+  if (!ctx->host_ar) return fail(ctx, PIPETTE_E_NCCL, "world > 1 without a transport");
+  if (ctx->h_ar_words < count) {
+    if (ctx->h_ar) cudaFreeHost(ctx->h_ar);
+    ctx->h_ar = nullptr;
+    ctx->h_ar_words = 0;
+    CU(cudaMallocHost(&ctx->h_ar, sizeof(unsigned long long) * count));
+    ctx->h_ar_words = count;
+  }
+  CU(cudaMemcpyAsync(ctx->h_ar, src, sizeof(unsigned long long) * count, cudaMemcpyDeviceToHost, s));
+  CU(cudaStreamSynchronize(s));
+  if (ctx->host_ar(ctx->host_user, reinterpret_cast<uint64_t*>(ctx->h_ar), (int64_t)count, op) != 0)
+    return fail(ctx, PIPETTE_E_NCCL, "host allreduce (op %d, %zu words) failed", op, count);
+  CU(cudaMemcpyAsync(dst, ctx->h_ar, sizeof(unsigned long long) * count, cudaMemcpyHostToDevice, s));
+  return PIPETTE_OK;
+}
 
 cudaError_t ensure(DevBuf& b, size_t bytes) {
   if (b.bytes >= bytes && b.p) return cudaSuccess;
@@ -746,7 +775,7 @@ pipette_status pipette_init(pipette_ctx** out, const pipette_cluster* cl, const 
       return bail(PIPETTE_E_INVALID);
     }
   }
-  if (dist && (dist->world < 1 || dist->rank < 0 || dist->rank >= dist->world || (dist->world > 1 && !dist->nccl_unique_id))) {
+  if (dist && (dist->world < 1 || dist->rank < 0 || dist->rank >= dist->world || (dist->world > 1 && !dist->nccl_unique_id && !dist->host_allreduce))) {
     fail(ctx, PIPETTE_E_INVALID, "bad dist description");
     return bail(PIPETTE_E_INVALID);
   }
@@ -787,7 +816,10 @@ pipette_status pipette_init(pipette_ctx** out, const pipette_cluster* cl, const 
     }
     if ((st = upload_bw(ctx, bw)) != PIPETTE_OK) return bail(st);
   }
-  if (ctx->world > 1) {
+  if (ctx->world > 1 && !dist->nccl_unique_id) {
+    ctx->host_ar = dist->host_allreduce;
+    ctx->host_user = dist->host_user;
+  } else if (ctx->world > 1) {
     ncclUniqueId id;
     std::memcpy(&id, dist->nccl_unique_id, sizeof id);
     ncclResult_t r = ncclCommInitRank(&ctx->comm, ctx->world, id, ctx->rank);
@@ -814,6 +846,7 @@ pipette_status pipette_set_stream(pipette_ctx* ctx, void* stream) {
 void pipette_destroy(pipette_ctx* ctx) {
   if (!ctx) return;
   if (ctx->comm) ncclCommDestroy(ctx->comm);
+  if (ctx->h_ar) cudaFreeHost(ctx->h_ar);
   DevBuf* bufs[] = {&ctx->cfgs, &ctx->keys, &ctx->feas, &ctx->qtab, &ctx->eout, &ctx->vin, &ctx->mlp, &ctx->claimed, &ctx->tasks, &ctx->chunks, &ctx->counter,
                     &ctx->chain_out, &ctx->best_perm, &ctx->cfg_slot, &ctx->cfg_best, &ctx->gbits, &ctx->items,
                     &ctx->gitems, &ctx->pack, &ctx->accepted, &ctx->slot_perm_off, &ctx->slot_lane,
@@ -1249,11 +1282,12 @@ pipette_status pipette_search(pipette_ctx* ctx, const pipette_model* model, int6
   // local latency bits of each config (ChainOut.best is the first field of CfgBest)
   CU(cudaMemcpy2DAsync(gbits, sizeof(unsigned long long), ctx->cfg_best.p, sizeof(CfgBest),
                        sizeof(unsigned long long), F, cudaMemcpyDeviceToDevice, s));
-  if (W > 1) NC(ncclAllReduce(gbits, gbits, F, ncclUint64, ncclMin, ctx->comm, s));
+  if (W > 1 && (st = allreduce_u64(ctx, gbits, gbits, F, 0, s)) != PIPETTE_OK) return st;
   k_combine_items<<<(F + 127) / 128, 128, 0, s>>>((const CfgBest*)ctx->cfg_best.p, gbits, F, chains, items);
   ctx->launches++;
-  if (W > 1) NC(ncclAllReduce(items, gitems, F, ncclUint64, ncclMin, ctx->comm, s));
-  else CU(cudaMemcpyAsync(gitems, items, sizeof(unsigned long long) * F, cudaMemcpyDeviceToDevice, s));
+  if (W > 1) {
+    if ((st = allreduce_u64(ctx, items, gitems, F, 0, s)) != PIPETTE_OK) return st;
+  } else CU(cudaMemcpyAsync(gitems, items, sizeof(unsigned long long) * F, cudaMemcpyDeviceToDevice, s));
   k_combine_pack<<<F, 128, 0, s>>>((const CfgBest*)ctx->cfg_best.p, gitems, (const DevCfg*)ctx->cfgs.p,
                                     (const int*)ctx->feas.p, (const int*)ctx->slot_perm_off.p,
                                     (const int*)ctx->slot_lane.p, (const uint16_t*)ctx->best_perm.p, F, chains,
@@ -1262,7 +1296,7 @@ pipette_status pipette_search(pipette_ctx* ctx, const pipette_model* model, int6
   k_sum_accepted<<<1, 32, 0, s>>>((const CfgBest*)ctx->cfg_best.p, F, pack + (size_t)F * row_words);
   ctx->launches++;
   CU(cudaGetLastError());
-  if (W > 1) NC(ncclAllReduce(pack, pack, (size_t)F * row_words + 1, ncclUint64, ncclSum, ctx->comm, s));
+  if (W > 1 && (st = allreduce_u64(ctx, pack, pack, (size_t)F * row_words + 1, 1, s)) != PIPETTE_OK) return st;
   CU(cudaEventRecord(ctx->ev[5], s));
   nvtxRangeEnd(nv);
 

@@ -10,9 +10,15 @@
 // 1F1B order; op k of stage s is F(k) for k < w = min(pp-s-1, n_mb), F(w + j/2) or B(j/2)
 // for j = k - w < 2(n_mb - w) (even / odd j), else B(k - n_mb).  The dependency of op
 // (s, k) -- F(s-1, m) for a forward, B(s+1, m) for a backward -- sits at op index k or
-// k-1 of the neighbour stage (checked for pp < 40, n_mb < 70 in the survey of this kernel
-// and by the parity tests), so the ops are computed by increasing k with two rows of end
-// times, forwards in ascending s and backwards in descending s within a k.  Every op is
+// k-1 of the neighbour stage, for every pp and n_mb: with w_s = min(pp-s-1, n_mb),
+//   F: w_{s-1} is w_s + 1 or (both = n_mb) w_s; m < w_s gives index m = k; m = w_s < w_{s-1}
+//      gives index w_s = k; otherwise 2m - w_{s-1} = k - 1 (m >= w_s = n_mb cannot occur);
+//   B: w_{s+1} is w_s - 1 or (both = n_mb) w_s; m < n_mb - w_s gives w_{s+1} + 2m + 1 =
+//      k - 1; m = n_mb - w_s with w_{s+1} = w_s - 1 gives w_s + 2m = n_mb + m = k; otherwise
+//      n_mb + m = k
+// (tests/test_oracle_models.py checks it against the explicit op lists), so the
+// ops are computed by increasing k with two rows of end times, forwards in ascending s
+// and backwards in descending s within a k.  Every op is
 // start = max(stage free, dependency end + hop), end = start + f (or b): the oracle's
 // event loop computes the same IEEE values in another order, so the results are identical.
 #include "devmath.cuh"

@@ -28,11 +28,23 @@ def _ngpu():
 def test_multi_gpu_plan_bit_identical(world, chains, moves, name, iters, tmp_path):
     if _ngpu() < world:
         pytest.skip(f"needs {world} GPUs")
+    _run_and_check(world, chains, moves, name, iters, tmp_path, "nccl")
+
+
+# the same protocol through the library's host transport (pipette_dist.host_allreduce over a
+# gloo group): runs on a 1-GPU box too, the W ranks sharing the device
+@pytest.mark.parametrize("world,chains,moves,name,iters", [
+    (2, 8, (0, 0), "C1", 1000), (3, 7, (683, 682), "C1", 1000), (2, 6, (0, 0), "C3", 300), (3, 8, (0, 0), "C5", 150)])
+def test_host_transport_plan_bit_identical(world, chains, moves, name, iters, tmp_path):
+    _run_and_check(world, chains, moves, name, iters, tmp_path, "host")
+
+
+def _run_and_check(world, chains, moves, name, iters, tmp_path, transport):
     out = tmp_path / "plan.json"
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={world}",
            "--master-addr=127.0.0.1", "--master-port=29533", os.path.join(HERE, "helpers", "mp_search.py"),
            str(out), name, str(chains), str(iters), str(moves[0]), str(moves[1])]
-    subprocess.run(cmd, check=True, timeout=600)
+    subprocess.run(cmd, check=True, timeout=600, env={**os.environ, "PIPETTE_TRANSPORT": transport})
     recs = json.load(open(out))
     w = W.WORKLOADS[name]
     B, prof = W.workload_inputs(w)
@@ -44,6 +56,7 @@ def test_multi_gpu_plan_bit_identical(world, chains, moves, name, iters, tmp_pat
     assert len(recs) == world
     for r in recs:
         assert r == {**recs[0], "rank": r["rank"]}                      # identical on every rank
+        assert r["transport"] == transport and r["world"] == world
         assert float.fromhex(r["latency"]) == ref.latency
         assert (r["cfg_index"], r["chain"], r["best_step"]) == (ref.cfg_index, ref.chain, ref.best_step)
         assert r["perm"] == ref.perm.tolist()

@@ -462,7 +462,7 @@ def test_full_moves_unsupported_above_256_positions_and_bad_weights():
 
 
 # ------------------------------------------------------------------ NEXT-2: Eq.1 and the 1F1B DES (R22)
-@pytest.mark.parametrize("name", ["C1", "C2", "C3", "C4"])
+@pytest.mark.parametrize("name", ["C1", "C2", "C3", "C4", "C5"])
 def test_eval_models_bit_exact(name):
     import torch
     w = W.WORKLOADS[name]
@@ -472,7 +472,7 @@ def test_eval_models_bit_exact(name):
     R = O.inverse_bandwidth(B)
     feas = [c for c in O.enumerate_configs(cl, mo, w.bs_global, P) if c.feasible]
     rng = np.random.default_rng(11)
-    per = 6 if name != "C4" else 3
+    per = {"C4": 3, "C5": 4}.get(name, 6)     # (C5: pp up to 32, n_mb up to 384)
     Nmax = max(c.pp * c.dp for c in feas)
     stride = ((Nmax + 7) // 8) * 8
     rows, perms, want = [], [], []

@@ -108,3 +108,47 @@ def test_pipette_closer_to_des_than_eq1_when_microbatches_outnumber_stages():
             ep.append(abs(tp - tdes) / tdes)
             eprev.append(abs(tprev - tdes) / tdes)
     assert len(ep) > 20 and np.mean(ep) < np.mean(eprev)
+
+
+def _op_positions(pp, n_mb):
+    """Megatron 1F1B op order per stage s: w = min(pp-s-1, n_mb) warm-up
+    forwards, then F/B pairs, then the cool-down backwards; positions of F(m) and B(m)."""
+    pos = []
+    for s in range(pp):
+        w = min(pp - s - 1, n_mb)
+        ops = [("F", m) for m in range(w)]
+        for j in range(n_mb - w):
+            ops += [("F", w + j), ("B", j)]
+        ops += [("B", m) for m in range(n_mb - w, n_mb)]
+        assert len(ops) == 2 * n_mb
+        pos.append({op: k for k, op in enumerate(ops)})
+    return pos
+
+
+def _closed_positions(pp, n_mb):
+    s = np.arange(pp)[:, None]
+    m = np.arange(n_mb)[None, :]
+    w = np.minimum(pp - s - 1, n_mb)
+    f = np.where(m < w, m, 2 * m - w)
+    b = np.where(m < n_mb - w, w + 2 * m + 1, n_mb + m)
+    return f, b
+
+
+def test_des_dependency_sits_at_index_k_or_k_minus_1():
+    # k_models.cu computes the 1F1B ops by increasing op index k with two rows of end times:
+    # valid iff F(s-1, m) sits at index k or k-1 of stage s-1 when F(s, m) is op k of stage s,
+    # and B(s+1, m) at k or k-1 of stage s+1 when B(s, m) is op k (any pp, n_mb).
+    for pp in range(1, 41):
+        for n_mb in range(1, 80, 3):
+            pos = _op_positions(pp, n_mb)
+            f, b = _closed_positions(pp, n_mb)
+            for s in range(pp):
+                assert [pos[s][("F", m)] for m in range(n_mb)] == f[s].tolist()
+                assert [pos[s][("B", m)] for m in range(n_mb)] == b[s].tolist()
+    for pp in range(2, 129):
+        for n_mb in list(range(1, 140)) + [255, 256, 257, 500, 511, 512, 1000, 1024]:
+            f, b = _closed_positions(pp, n_mb)
+            df = f[1:] - f[:-1]          # k(s) - index of F(s-1) in stage s-1
+            db = b[:-1] - b[1:]          # k(s) - index of B(s+1) in stage s+1
+            assert df.min() >= 0 and df.max() <= 1, (pp, n_mb)
+            assert db.min() >= 0 and db.max() <= 1, (pp, n_mb)

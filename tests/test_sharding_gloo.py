@@ -3,8 +3,9 @@ covers every SA item exactly once, and the two-step combine -- allreduce(min) of
 per-config best latency bits, then allreduce(min) of the item ids attaining it, then
 the owners' plans by an allreduce(sum) of owner-only rows -- reproduces the single-rank
 search of the oracle bit for bit.  The per-rank SA work is done by the oracle here (no
-GPU); on the GPU the same protocol runs in pipette_search over NCCL
-(tests/test_gpu_multi.py)."""
+GPU); on the GPU the same protocol runs in pipette_search over NCCL or over the library's
+host transport, which the last test here drives through the binding's gloo callback
+(tests/test_gpu_multi.py runs both end to end)."""
 import os
 import socket
 
@@ -105,3 +106,39 @@ def test_gloo_two_step_combine_matches_single_rank(world):
         assert perm == ref.perm.tolist()
         assert owners == F                                             # exactly one owner per config
         assert acc == ref.sa_accepted
+
+
+def _ar_worker(rank, world, port, out_q):
+    import ctypes as C
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_2405_18093_b200 import _abi, torch_host_allreduce
+    fn = _abi.HOST_ALLREDUCE(torch_host_allreduce())     # exactly what pipette_init receives
+    vals = [[~0 & (2**64 - 1), 5, 2**63 + 7, 2**63 - 1], [3, 2**64 - 2, 2**63 + 1, 2**63]]
+    outs = []
+    for op in (0, 1):
+        buf = (C.c_uint64 * 4)(*vals[rank % 2])
+        assert fn(None, buf, 4, op) == 0
+        outs.append(list(buf))
+    out_q.put((rank, outs))
+    dist.destroy_process_group()
+
+
+def test_torch_host_allreduce_is_uint64_min_and_wrapping_sum():
+    # the host transport of the combine (pipette_dist.host_allreduce): uint64 order for min
+    # (no-owner items are ~0), sum modulo 2^64, on every rank
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_ar_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = dict(q.get(timeout=300) for _ in range(2))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    a, b = [2**64 - 1, 5, 2**63 + 7, 2**63 - 1], [3, 2**64 - 2, 2**63 + 1, 2**63]
+    for r in (0, 1):
+        assert res[r][0] == [min(x, y) for x, y in zip(a, b)]
+        assert res[r][1] == [(x + y) % 2**64 for x, y in zip(a, b)]
