@@ -241,10 +241,13 @@ __device__ __forceinline__ void dispatch_n(const EvalParams& P, const EvalShared
   else eval_small<PP, false>(P, S, C, row, i, e);
 }
 
-// MODE 1 (general) evaluation of one candidate.
+// MODE 1 (general) evaluation of one candidate.  PP > 0: compile-time pipeline depth for
+// 16-byte rows with N % 8 == 0 (a power of two up to 32): the stage of a slot follows from
+// its place in the 8-slot chunk, so the slot loop carries no stage counter or branches.
+template <int PP>
 __device__ __forceinline__ void eval_general(const EvalParams& P, const EvalShared& S, const DevCfg& C,
                                              const RowSrc& row, long long i) {
-  const int N = C.N, pp = C.pp;
+  const int N = C.N, pp = PP > 0 ? PP : C.pp;
   const uint32_t spn = (uint32_t)C.spn;
   for (int w = 0; w < (N + 31) / 32; ++w) S.bm[w * S.T + S.tid] = 0u;
   const uint32_t clg = 2u + S.cnt_nib, cbits = 8u >> S.cnt_nib, cmask = (1u << cbits) - 1u;   // count plane
@@ -255,6 +258,40 @@ __device__ __forceinline__ void eval_general(const EvalParams& P, const EvalShar
   double tpp = 0.0, s = 0.0;
   uint32_t prev = 0;
   int x = 0;
+  if constexpr (PP > 0) {
+    const double m2 = C.m2;
+    for (int w0 = 0; w0 < N; w0 += 8) {
+      const uint4 v4 = row.chunk(w0 >> 3);
+      const uint32_t pk[4] = {v4.x, v4.y, v4.z, v4.w};
+      const bool head = PP >= 8 ? (w0 & (PP - 1)) == 0 : true;            // chunk starts a pipeline
+      const bool tail = PP >= 8 ? ((w0 + 8) & (PP - 1)) == 0 : true;      // chunk ends one
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const uint32_t v = (pk[j >> 1] >> ((j & 1) * 16)) & 0xffffu;
+        uint32_t nd = 0;
+        if (v >= (uint32_t)N) {
+          ok = false;
+        } else {
+          uint32_t& bw = S.bm[(v >> 5) * S.T + S.tid];
+          const uint32_t bit = 1u << (v & 31);
+          ok = ok && (bw & bit) == 0u;
+          bw |= bit;
+          nd = div_small(v, C.spn_magic, spn);
+        }
+        const bool st0 = PP >= 8 ? (j == 0 && head) : (j % PP) == 0;
+        if (st0) {
+          S.cnt[(nd >> clg) * S.T + S.tid] += 1u << ((nd & ((1u << clg) - 1u)) * cbits);
+          mask.set(nd);
+          s = 0.0;
+        } else {
+          s = __dadd_rn(s, __dmul_rn(m2, r_at<false>(S, prev, nd)));
+        }
+        prev = nd;
+        const bool last = PP >= 8 ? (j == 7 && tail) : (j % PP) == PP - 1;
+        if (PP >= 2 && last) tpp = fmax(tpp, s);
+      }
+    }
+  } else {
   auto visit = [&](uint32_t v) {
     uint32_t nd = 0;
     if (v >= (uint32_t)N) {
@@ -289,6 +326,7 @@ __device__ __forceinline__ void eval_general(const EvalParams& P, const EvalShar
     }
   } else {
     for (int w = 0; w < N; ++w) visit(row.slot(w));
+  }
   }
   P.mem[i] = C.mem;
   const double qnan = __longlong_as_double(0x7ff8000000000000ll);
@@ -544,8 +582,21 @@ __global__ void __launch_bounds__(THREADS, THREADS <= 256 ? 4 : 1)
               case 8: dispatch_n<8>(P, S, C, row, i, e); break;
               default: dispatch_n<0>(P, S, C, row, i, e); break;
             }
+          } else if (!mixed && row.vec && (C.N & 7) == 0) {
+            // single-configuration tile: compile-time depth (mixed tiles take the generic pass:
+            // warps of several depths on one SM thrash the instruction cache -- measured C4
+            // mixed 3.8e9 -> 2.2e9 candidates/s with per-depth code there)
+            switch (C.pp) {
+              case 1: eval_general<1>(P, S, C, row, i); break;
+              case 2: eval_general<2>(P, S, C, row, i); break;
+              case 4: eval_general<4>(P, S, C, row, i); break;
+              case 8: eval_general<8>(P, S, C, row, i); break;
+              case 16: eval_general<16>(P, S, C, row, i); break;
+              case 32: eval_general<32>(P, S, C, row, i); break;
+              default: eval_general<0>(P, S, C, row, i); break;
+            }
           } else {
-            eval_general(P, S, C, row, i);
+            eval_general<0>(P, S, C, row, i);
           }
           }
         }

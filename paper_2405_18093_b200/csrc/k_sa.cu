@@ -1421,7 +1421,7 @@ __global__ void __launch_bounds__(SaLB<MODE, BIG, NW>::threads, SaLB<MODE, BIG, 
         default: run_task_hc<TRACE, 0, NW>(P, T, C, Tl, SS, ws, lane); break;
       }
     } else if constexpr (MODE == 1) {
-      run_task_sb_pp<TRACE, true>(P, T, C, Rs, pl_s, ws, lane);   // (power-of-two spn: the host's MODE 1 rule)
+      run_task_sb_pp<TRACE, true, BIG>(P, T, C, Rs, pl_s, ws, lane);   // (power-of-two spn: the host's MODE 1 rule)
     } else {
       switch (C.pp) {
         case 1: run_task<POS, S1, RT, TRACE, 1>(P, T, C, R, ws, lane); break;
@@ -1628,6 +1628,8 @@ const void* sa_kernel(int mode, bool trace, int n_nodes, bool full) {
   }
   if (mode == 0 && n_nodes <= 8) return trace ? (const void*)k_sa_chains<0, true, 2> : (const void*)k_sa_chains<0, false, 2>;
   if (mode == 0) return trace ? (const void*)k_sa_chains<0, true, 4> : (const void*)k_sa_chains<0, false, 4>;
+  if (mode == 1 && n_nodes >= 64)   // (BIG: large clusters, direct-mode joins always cooperative)
+    return trace ? (const void*)k_sa_chains<1, true, 4, true> : (const void*)k_sa_chains<1, false, 4, true>;
   if (mode == 1) return trace ? (const void*)k_sa_chains<1, true> : (const void*)k_sa_chains<1, false>;
   return trace ? (const void*)k_sa_chains<2, true> : (const void*)k_sa_chains<2, false>;
 }

@@ -195,6 +195,17 @@ __host__ __device__ inline int m1_warp_state_bytes(int N, int dp, int n, bool co
 }
 
 // ------------------------------------------------------------------ stage-1 state (Eq.6)
+// Direct-mode joins of one step go through the warp when at most this many lanes have one,
+// else per lane: measured on B200, always cooperative on C5 (128 nodes, N <= 256: 847 vs
+// 871 ms per search at 0), at most 2 on C4 (32 nodes, N = 32: a stage-1 move in ~3x more
+// proposals; 40.2 ms vs 63.7 always cooperative).  Build-time override for A/B runs.
+#ifndef PIPETTE_JOIN_COOP_MAX
+#define PIPETTE_JOIN_COOP_MAX -1
+#endif
+__device__ __forceinline__ int join_coop_max(int n) {
+  return PIPETTE_JOIN_COOP_MAX >= 0 ? PIPETTE_JOIN_COOP_MAX : (n >= 64 ? 32 : 2);
+}
+
 struct S1M {
   uint32_t* c;   // count plane [ceil(n / per-word)][32] (counts configurations only)
   int lane;
@@ -204,7 +215,7 @@ struct S1M {
   int k, k2, win, win2, jw, jw2;             // |N1|; T_in witness node; T_ex witness rank
   uint32_t wab, wab2;                        // T_ex witness pair a | b << 8 (0xffff: none)
   uint32_t dn_, up_, c_dn_, c_up_;
-  bool need_tin, need_scan;
+  bool need_tin, need_scan, need_join;
   double tin, tin2, tex, tex2, maxR, maxR2;
 
   __device__ __forceinline__ void set_nibbles(bool nib) {   // (nibbles: every count <= 15)
@@ -221,6 +232,23 @@ struct S1M {
   }
   static __device__ __forceinline__ uint32_t pair_at(const S1Ctx& X, int j) {
     return j < X.plen ? (uint32_t)X.pl[j] : (uint32_t)__ldg(X.gl_ab + j);
+  }
+  // node id of the t-th (0-based) member of m, t < |m| (else meaningless): the word by
+  // popcount prefixes, then a five-step popcount bisection inside it
+  static __device__ __forceinline__ uint32_t nth_member(const Mask4& m, uint32_t t) {
+    const uint32_t c0 = __popc(m.w0), c1 = c0 + __popc(m.w1), c2 = c1 + __popc(m.w2);
+    uint32_t x = t < c0 ? m.w0 : (t < c1 ? m.w1 : (t < c2 ? m.w2 : m.w3));
+    uint32_t r = t - (t < c0 ? 0u : (t < c1 ? c0 : (t < c2 ? c1 : c2)));
+    uint32_t pos = t < c0 ? 0u : (t < c1 ? 32u : (t < c2 ? 64u : 96u));
+#pragma unroll
+    for (uint32_t h = 16u; h >= 1u; h >>= 1) {
+      const uint32_t c = __popc(x & ((1u << h) - 1u));
+      const bool up = r >= c;
+      r = up ? r - c : r;
+      x = up ? x >> h : x;
+      pos = up ? pos + h : pos;
+    }
+    return pos;
   }
 
   // max over ordered member pairs a != b of m of R[a][b], with a witness pair
@@ -250,7 +278,7 @@ struct S1M {
     wab_o = w;
     return mx;
   }
-  // max over members b != u of m of R[u][b] and R[b][u]
+  // max over members b != u of m of R[u][b] and R[b][u] (per lane)
   template <class KT>
   static __device__ __forceinline__ double join_max(const Mask4& m, uint32_t u, const KT& K, uint32_t& wab_o) {
     double mx = 0.0;
@@ -324,7 +352,7 @@ struct S1M {
       }
     }
     tex = k >= 2 ? __dmul_rn(__ldg(X.qe + k), maxR) : 0.0;
-    need_tin = need_scan = false;
+    need_tin = need_scan = need_join = false;
   }
 
   // a stage-1 member moves from node dn to node up (tentative); long searches are flagged
@@ -357,9 +385,7 @@ struct S1M {
       if (wit_left || k < 2) {
         need_scan = true;   // recompute over the member pairs, split over the warp (coop)
       } else if (join) {
-        uint32_t w;
-        const double v = join_max(mask2, up, K, w);
-        if (v > maxR2) { maxR2 = v; wab2 = w; }
+        need_join = true;   // the new pairs (up, b), (b, up): one cooperative round
       }
     } else {
       bool found = false;
@@ -377,11 +403,12 @@ struct S1M {
     }
   }
 
-  // warp-cooperative searches (called by all 32 lanes, converged)
-  template <class KT>
+  // warp-cooperative searches (called by all 32 lanes, converged).  JC: direct-mode joins
+  // always through the warp (no per-lane join code in the kernel: large clusters)
+  template <bool JC = false, class KT>
   __device__ __forceinline__ void coop(const S1Ctx& X, const KT& K) {
     const unsigned full = 0xffffffffu;
-    if (!__any_sync(full, need_tin | need_scan)) return;   // (the common case: one vote)
+    if (!__any_sync(full, need_tin | need_scan | need_join)) return;   // (the common case: one vote)
     if (counts) {   // T_in: first (a, c) entry (by value) whose node has c members after the move
       unsigned todo = __ballot_sync(full, need_tin);
       while (todo) {
@@ -417,9 +444,19 @@ struct S1M {
         }
       }
     }
+    // T_ex, direct mode: many joins in one step go per lane (in parallel, each over the k'
+    // members), a few through the warp (one round each, below)
+    if (!JC && direct && __popc(__ballot_sync(full, need_join && !need_scan)) > join_coop_max(X.n)) {
+      if (need_join && !need_scan) {
+        uint32_t w;
+        const double v = join_max(mask2, up_, K, w);
+        if (v > maxR2) { maxR2 = v; wab2 = w; }
+      }
+      need_join = false;
+    }
     // T_ex: the witness pair left N1 -- first pair inside N1' after the old witness's rank
     // (list mode), or the max over N1's member pairs split over the lanes (direct mode)
-    unsigned todo = __ballot_sync(full, need_scan);
+    unsigned todo = __ballot_sync(full, need_scan | need_join);
     while (todo) {
       const int L = __ffs(todo) - 1;
       todo &= todo - 1;
@@ -427,34 +464,40 @@ struct S1M {
       m.w0 = __shfl_sync(full, mask2.w0, L); m.w1 = __shfl_sync(full, mask2.w1, L);
       m.w2 = __shfl_sync(full, mask2.w2, L); m.w3 = __shfl_sync(full, mask2.w3, L);
       if (direct) {
-        // lane i holds the i-th member node; pair j = (j / k, j % k) comes by shuffles
+        // lane t (mod 8) holds the t-th member node of N1' (k' <= 8); a join pairs the new
+        // node with every member (lanes 0-15, one round), a recompute takes the k' x k'
+        // ordered pairs (lane j of round r: pair (8r + j / 8, j % 8))
         const uint32_t kk = (uint32_t)__shfl_sync(full, k2, L);
-        uint32_t memv = 0u;
-        {
-          const uint32_t c0 = __popc(m.w0), c1 = c0 + __popc(m.w1), c2 = c1 + __popc(m.w2);
-          const uint32_t i = (uint32_t)lane;
-          const uint32_t wd = i < c0 ? 0u : (i < c1 ? 1u : (i < c2 ? 2u : 3u));
-          const uint32_t r = i - (wd == 0u ? 0u : (wd == 1u ? c0 : (wd == 2u ? c1 : c2)));
-          if (i < kk) memv = wd * 32u + (uint32_t)__fns(m.word((int)wd), 0u, (int)r + 1);
-        }
-        const uint32_t npair = kk * kk;
-        const uint32_t mg = (uint32_t)((0x100000000ull + kk - 1u) / kk);   // j / k = umulhi(j, mg), j < 2^16
+        const bool jo = __shfl_sync(full, (int)(need_join && !need_scan), L) != 0;
+        const uint32_t t = (uint32_t)lane & 7u;
+        const uint32_t memv = nth_member(m, t);
         double mx = 0.0;
         uint32_t wbest = 0xffffu;
-        for (uint32_t base = 0; base < npair; base += 32u) {
-          const uint32_t j = base + (uint32_t)lane;
-          const uint32_t ia = __umulhi(j, mg), ib = j - ia * kk;
-          const uint32_t a = __shfl_sync(full, memv, (int)(ia & 31u)), b = __shfl_sync(full, memv, (int)(ib & 31u));
-          if (j < npair && ia != ib) {
-            const double v = K.r(a, b);
-            if (v > mx) { mx = v; wbest = a | (b << 8); }
+        if (jo) {
+          const uint32_t upL = (uint32_t)__shfl_sync(full, up_, L);
+          if (lane < 16 && t < kk && memv != upL) {
+            const uint32_t a = lane < 8 ? upL : memv, b = lane < 8 ? memv : upL;
+            mx = K.r(a, b);
+            wbest = a | (b << 8);
+          }
+        } else {
+          for (uint32_t base = 0; base < kk * 8u; base += 32u) {
+            const uint32_t ia = (base + (uint32_t)lane) >> 3, ib = t;
+            const uint32_t a = __shfl_sync(full, memv, (int)(ia & 7u)), b = __shfl_sync(full, memv, (int)ib);
+            if (ia < kk && ib < kk && ia != ib) {
+              const double v = K.r(a, b);
+              if (v > mx) { mx = v; wbest = a | (b << 8); }
+            }
           }
         }
         uint32_t cnt;   // max-reduce; the witness of the lowest lane holding it (any equal max is fine)
         const double gmx = warp_max_nonneg(mx, 1u, cnt);
         const unsigned holders = __ballot_sync(full, mx == gmx);
         wbest = __shfl_sync(full, wbest, __ffs(holders) - 1);
-        if (lane == L) { need_scan = false; maxR2 = gmx; wab2 = wbest; }
+        if (lane == L) {
+          if (!jo || gmx > maxR2) { maxR2 = gmx; wab2 = wbest; }
+          need_scan = need_join = false;
+        }
         continue;
       }
       const int start = __shfl_sync(full, jw, L) + 1;
@@ -493,7 +536,7 @@ struct S1M {
 // ------------------------------------------------------------------ one warp task of MODE 1
 // Same step structure as run_task_hc: the swap is applied tentatively, the touched
 // pipelines are re-summed in stage order, T_PP keeps the count of pipelines at its max.
-template <bool TRACE, int PP, bool ID>
+template <bool TRACE, int PP, bool ID, bool JC>
 __device__ __forceinline__ void run_task_sb(const SaParams& P, const SaTask T, const DevCfg C, const double* Rt,
                                             const uint16_t* pl, unsigned char* ws, int lane) {
   const bool active = lane < T.count;
@@ -610,14 +653,14 @@ __device__ __forceinline__ void run_task_sb(const SaParams& P, const SaTask T, c
           psum[zb * 32 + lane] = sB;
         }
         if (cache && dp <= 8) {
-          if (!fast) {
-            double m = 0.0;
+          if (!fast) {   // (unrolled: independent loads and a max tree, then the tie count)
+            double v[8];
+#pragma unroll
+            for (int z = 0; z < 8; ++z) v[z] = z < dp ? psum[z * 32 + lane] : 0.0;
+            const double m = fmax(fmax(fmax(v[0], v[1]), fmax(v[2], v[3])), fmax(fmax(v[4], v[5]), fmax(v[6], v[7])));
             int c = 0;
-            for (int z = 0; z < dp; ++z) {
-              const double v = psum[z * 32 + lane];
-              c = v > m ? 1 : c + (v == m ? 1 : 0);
-              m = fmax(m, v);
-            }
+#pragma unroll
+            for (int z = 0; z < 8; ++z) c += (z < dp && v[z] == m) ? 1 : 0;
             tpp2 = m;
             nmax2 = c;
           }
@@ -630,7 +673,7 @@ __device__ __forceinline__ void run_task_sb(const SaParams& P, const SaTask T, c
           const uint32_t up = xp == 0u ? nq : np;
           s1.propose(dn, up, X, K);
         }
-        s1.coop(X, K);   // converged: all lanes' flagged searches
+        s1.coop<JC>(X, K);   // converged: all lanes' flagged searches
         double tin2 = s1.tin, tex2 = s1.tex;
         if (dpchg) {
           s1.finish(X);
@@ -686,16 +729,16 @@ __device__ __forceinline__ void run_task_sb(const SaParams& P, const SaTask T, c
 // Compile-time pipeline depth for the common power-of-two depths (the Eq.5 sums unroll).
 // ID: the context's node map (true: power-of-two spn, the only variant the swap kernel
 // instantiates -- two variants in one kernel made ptxas spill in the hot loop).
-template <bool TRACE, bool ID>
+template <bool TRACE, bool ID, bool JC>
 __device__ __forceinline__ void run_task_sb_pp(const SaParams& P, const SaTask T, const DevCfg C, const double* Rt,
                                                const uint16_t* pl, unsigned char* ws, int lane) {
   switch (C.pp) {
-    case 1: run_task_sb<TRACE, 1, ID>(P, T, C, Rt, pl, ws, lane); break;
-    case 2: run_task_sb<TRACE, 2, ID>(P, T, C, Rt, pl, ws, lane); break;
-    case 4: run_task_sb<TRACE, 4, ID>(P, T, C, Rt, pl, ws, lane); break;
-    case 8: run_task_sb<TRACE, 8, ID>(P, T, C, Rt, pl, ws, lane); break;
-    case 16: run_task_sb<TRACE, 16, ID>(P, T, C, Rt, pl, ws, lane); break;
-    case 32: run_task_sb<TRACE, 32, ID>(P, T, C, Rt, pl, ws, lane); break;
-    default: run_task_sb<TRACE, 0, ID>(P, T, C, Rt, pl, ws, lane); break;
+    case 1: run_task_sb<TRACE, 1, ID, JC>(P, T, C, Rt, pl, ws, lane); break;
+    case 2: run_task_sb<TRACE, 2, ID, JC>(P, T, C, Rt, pl, ws, lane); break;
+    case 4: run_task_sb<TRACE, 4, ID, JC>(P, T, C, Rt, pl, ws, lane); break;
+    case 8: run_task_sb<TRACE, 8, ID, JC>(P, T, C, Rt, pl, ws, lane); break;
+    case 16: run_task_sb<TRACE, 16, ID, JC>(P, T, C, Rt, pl, ws, lane); break;
+    case 32: run_task_sb<TRACE, 32, ID, JC>(P, T, C, Rt, pl, ws, lane); break;
+    default: run_task_sb<TRACE, 0, ID, JC>(P, T, C, Rt, pl, ws, lane); break;
   }
 }

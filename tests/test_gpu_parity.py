@@ -171,6 +171,41 @@ def test_eval_stream_homogeneous_tiles(name, n_cand):
         assert _assert_close(lat[ok], want) == 0
 
 
+@pytest.mark.parametrize("name", ["C4", "C5"])
+def test_eval_stream_homogeneous_tiles_every_depth(name):
+    """Single-configuration tiles of one configuration per pipeline depth present (K2 MODE 1
+    takes a compile-time-depth path there, pp = 1..32): a full tile plus a ragged tail,
+    duplicates and out-of-range ids inside, every latency compared bit for bit."""
+    w = W.WORKLOADS[name]
+    pip, B, prof = _ctx(w)
+    model, mo, cl = _models(w)
+    P = O.make_profile(prof)
+    R = O.inverse_bandwidth(B)
+    feas = [c for c in O.enumerate_configs(cl, mo, w.bs_global, P) if c.feasible]
+    by_pp = {}
+    for c in feas:
+        by_pp.setdefault(c.pp, c)
+    assert len(by_pp) >= 5
+    n_cand = 2048 + 301
+    for pp, c in sorted(by_pp.items()):
+        K = O.constants(cl, mo, c, P)
+        stride = ((K.N + 7) // 8) * 8
+        rng = np.random.default_rng(K.N * 31 + pp)
+        rows = np.zeros((n_cand, stride), dtype=np.uint16)
+        rows[:, :K.N] = W.random_perms(K.N, n_cand, int(rng.integers(1 << 30)))
+        bad = rng.choice(n_cand, size=40, replace=False)
+        for j, i in enumerate(bad):
+            a, b = rng.choice(K.N, size=2, replace=False)
+            rows[i, a] = [rows[i, b], K.N, 0xFFFF][j % 3]
+        lat, mem, st = _eval_batch(pip, model, w.bs_global, [(c.pp, c.tp, c.dp, c.mb)] * n_cand, rows)
+        want_st = np.zeros(n_cand, dtype=np.int64)
+        want_st[bad] = 3
+        assert st.tolist() == want_st.tolist(), pp
+        ok = want_st == 0
+        want = [O.latency(K, R, rows[i, :K.N]).T for i in np.flatnonzero(ok)]
+        assert _assert_close(lat[ok], want) == 0, pp
+
+
 def test_eval_single_gpu_cluster_and_empty_batch():
     import torch
     from paper_2405_18093_b200 import Model, Pipette
