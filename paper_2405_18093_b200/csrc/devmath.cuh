@@ -217,10 +217,10 @@ struct Mask4 {
     const uint32_t b = ~(1u << (a & 31)), q = a >> 5;
     w0 &= q == 0u ? b : ~0u; w1 &= q == 1u ? b : ~0u; w2 &= q == 2u ? b : ~0u; w3 &= q == 3u ? b : ~0u;
   }
-  __device__ __forceinline__ bool test(uint32_t a) const {
-    const uint32_t q = a >> 5;
-    const uint32_t x = q == 0u ? w0 : (q == 1u ? w1 : (q == 2u ? w2 : w3));
-    return (x >> (a & 31)) & 1u;
+  __device__ __forceinline__ bool test(uint32_t a) const {   // a < 128: two select levels, a wrapping funnel shift
+    const uint32_t lo = (a & 32u) ? w1 : w0, hi = (a & 32u) ? w3 : w2;
+    const uint32_t x = (a & 64u) ? hi : lo;
+    return (__funnelshift_r(x, x, a) & 1u) != 0u;
   }
   __device__ __forceinline__ int count() const { return __popc(w0) + __popc(w1) + __popc(w2) + __popc(w3); }
 };

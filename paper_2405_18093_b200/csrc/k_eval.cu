@@ -259,7 +259,12 @@ __device__ __forceinline__ void eval_general(const EvalParams& P, const EvalShar
   uint32_t prev = 0;
   int x = 0;
   if constexpr (PP > 0) {
+    // branch-free slots: an id >= N flags the row and is clamped to N - 1 for the (then
+    // meaningless) bitmap and node updates
     const double m2 = C.m2;
+    uint32_t* const bmt = S.bm + S.tid;   // this thread's bitmap column (word stride T)
+    const uint32_t nm1 = (uint32_t)N - 1u;
+    uint32_t bad = 0u;
     for (int w0 = 0; w0 < N; w0 += 8) {
       const uint4 v4 = row.chunk(w0 >> 3);
       const uint32_t pk[4] = {v4.x, v4.y, v4.z, v4.w};
@@ -268,20 +273,16 @@ __device__ __forceinline__ void eval_general(const EvalParams& P, const EvalShar
 #pragma unroll
       for (int j = 0; j < 8; ++j) {
         const uint32_t v = (pk[j >> 1] >> ((j & 1) * 16)) & 0xffffu;
-        uint32_t nd = 0;
-        if (v >= (uint32_t)N) {
-          ok = false;
-        } else {
-          uint32_t& bw = S.bm[(v >> 5) * S.T + S.tid];
-          const uint32_t bit = 1u << (v & 31);
-          ok = ok && (bw & bit) == 0u;
-          bw |= bit;
-          nd = div_small(v, C.spn_magic, spn);
-        }
+        bad |= (uint32_t)(v > nm1);
+        const uint32_t vc = min(v, nm1);
+        uint32_t* const bw = bmt + (vc >> 5) * (uint32_t)S.T;
+        const uint32_t bit = 1u << (vc & 31), old = *bw;
+        bad |= old & bit;
+        *bw = old | bit;
+        const uint32_t nd = div_small(vc, C.spn_magic, spn);
         const bool st0 = PP >= 8 ? (j == 0 && head) : (j % PP) == 0;
         if (st0) {
           S.cnt[(nd >> clg) * S.T + S.tid] += 1u << ((nd & ((1u << clg) - 1u)) * cbits);
-          mask.set(nd);
           s = 0.0;
         } else {
           s = __dadd_rn(s, __dmul_rn(m2, r_at<false>(S, prev, nd)));
@@ -291,6 +292,7 @@ __device__ __forceinline__ void eval_general(const EvalParams& P, const EvalShar
         if (PP >= 2 && last) tpp = fmax(tpp, s);
       }
     }
+    ok = bad == 0u;
   } else {
   auto visit = [&](uint32_t v) {
     uint32_t nd = 0;
@@ -305,7 +307,6 @@ __device__ __forceinline__ void eval_general(const EvalParams& P, const EvalShar
     }
     if (x == 0) {
       S.cnt[(nd >> clg) * S.T + S.tid] += 1u << ((nd & ((1u << clg) - 1u)) * cbits);
-      mask.set(nd);
       s = 0.0;
     } else {
       s = __dadd_rn(s, __dmul_rn(C.m2, r_at<false>(S, prev, nd)));
@@ -334,20 +335,48 @@ __device__ __forceinline__ void eval_general(const EvalParams& P, const EvalShar
   if (!C.has_profile) { P.latency[i] = qnan; P.status[i] = 4; return; }
   const double* qi = P.qtab + C.qi_off;
   double t_in = 0.0, mx = 0.0;
+  // N1 (nodes with a stage-1 member) and T_in (Eq.6 intra term over nodes with >= 2) from
+  // the count plane, one word of 8 nibbles (or 4 bytes) at a time: the non-zero fields
+  // compressed to a byte of N1, the fields >= 2 visited for T_in (fmax: any order)
+  for (int w = 0; w < ((S.n - 1) >> clg) + 1; ++w) {
+    const uint32_t cw = S.cnt[w * S.T + S.tid];
+    if (cw == 0u) continue;
+    uint32_t nz, ge2, x = cw | (cw >> 1);
+    if (S.cnt_nib) {
+      x = (x | (x >> 2)) & 0x11111111u;
+      x = (x | (x >> 3)) & 0x03030303u;
+      x = (x | (x >> 6)) & 0x000f000fu;
+      nz = ((x | (x >> 12)) & 0xffu) << ((w & 3) * 8);
+      ge2 = cw & 0xeeeeeeeeu;
+    } else {
+      x |= x >> 2;
+      x = (x | (x >> 4)) & 0x01010101u;
+      x = (x | (x >> 7)) & 0x00030003u;
+      nz = ((x | (x >> 14)) & 0xfu) << ((w & 7) * 4);
+      ge2 = cw & 0xfefefefeu;
+    }
+    const uint32_t q = (uint32_t)w >> (S.cnt_nib ? 2 : 3);   // mask word
+#pragma unroll
+    for (int m = 0; m < 4; ++m) mask.w[m] |= q == (uint32_t)m ? nz : 0u;
+    while (ge2) {
+      const uint32_t sh = (uint32_t)(__ffs(ge2) - 1) & ~(cbits - 1u);
+      ge2 &= ~(cmask << sh);
+      const uint32_t a = ((uint32_t)w << clg) + sh / cbits, c = (cw >> sh) & cmask;
+      t_in = fmax(t_in, __dmul_rn(__ldg(qi + c), r_at<false>(S, a, a)));
+    }
+  }
   const int k = mask.count();
   // slowest link of N1: the k(k-1) member pairs when k^2 <= n, else the first pair inside N1
   // of the R-descending pair list (expected ~(n/k)^2 probes; every thread scans the same
   // prefix, so it stays in L1).  Both give the exact max.
   const bool pairs = k * k <= S.n;
+  if (pairs) {
 #pragma unroll
-  for (int wd = 0; wd < 4; ++wd) {
-    uint32_t bits = mask.w[wd];
-    while (bits) {
-      const uint32_t a = wd * 32 + __ffs(bits) - 1;
-      bits &= bits - 1;
-      const uint32_t c = (S.cnt[(a >> clg) * S.T + S.tid] >> ((a & ((1u << clg) - 1u)) * cbits)) & cmask;
-      if (c >= 2) t_in = fmax(t_in, __dmul_rn(__ldg(qi + c), r_at<false>(S, a, a)));
-      if (pairs) {
+    for (int wd = 0; wd < 4; ++wd) {
+      uint32_t bits = mask.w[wd];
+      while (bits) {
+        const uint32_t a = wd * 32 + __ffs(bits) - 1;
+        bits &= bits - 1;
 #pragma unroll
         for (int wd2 = 0; wd2 < 4; ++wd2) {
           uint32_t bits2 = mask.w[wd2];
