@@ -148,6 +148,11 @@ __device__ __forceinline__ bool metropolis_fast(double d, double beta, double u)
   return metropolis_exact(x, u);
 }
 
+// max of two non-NaN doubles: DSETP + two selects (fmax adds NaN handling, ~5 SASS
+// instructions).  Every latency term, sum and table value here is finite and >= +0, where it
+// returns the same value as fmax.
+__device__ __forceinline__ double dmax(double a, double b) { return a > b ? a : b; }
+
 // Warp max of non-negative doubles (their bit patterns order like the values) by two 32-bit
 // redux.sync, and the sum of c over the lanes holding it: three REDUX instead of a five-level
 // shuffle butterfly on (double, int) pairs.

@@ -40,7 +40,7 @@ size_t eval_smem_bytes(int mode, int perm_stride, bool staged, int n_nodes, int 
 __global__ void k_tin_values(const DevCfg*, const double*, const double*, int, double*);
 const void* sa_kernel(int mode, bool trace, int n_nodes, bool full);
 int sa_warp_state_bytes(int mode, int N, int pp, int dp, int n, int dp_cap, bool nib);
-int sa_m1_warp_state_bytes(int N, int dp, int n, bool counts, bool cache, bool nib);
+int sa_m1_warp_state_bytes(int N, int dp, int n, bool counts, bool cache, bool nib, bool direct);
 int sa_m1_count_bytes(int n, bool nib);
 void launch_t0_calibrate(const DevCfg*, const int*, int, const double*, const double*, int, const RoundKeys&, int, int,
                          double, double*, cudaStream_t);
@@ -512,8 +512,8 @@ pipette_status build_plan(pipette_ctx* ctx, int chains, int W, int r, const char
       const bool counts = full_moves || std::min(c.spn, c.dp) >= 2;
       const bool direct = std::min(c.dp, n) <= 8;
       const int base = full_moves ? align16(((c.N + 3) / 4) * 128) + sa_m1_count_bytes(n, false)
-                                  : sa_m1_warp_state_bytes(c.N, c.dp, n, counts, false, nib);
-      const int with = sa_m1_warp_state_bytes(c.N, c.dp, n, counts, true, nib);
+                                  : sa_m1_warp_state_bytes(c.N, c.dp, n, counts, false, nib, direct);
+      const int with = sa_m1_warp_state_bytes(c.N, c.dp, n, counts, true, nib, direct);
       const int w_nc = std::min(kSaM1Warps, avail / base), w_c = std::min(kSaM1Warps, avail / with);
       // (measured on C5: the cache pays for a lost resident warp only when it saves re-summing
       // long pipelines -- (4,8,32) 8 uncached warps beat 7 cached, (8,4,32) 8 beat 5)

@@ -149,7 +149,7 @@ __device__ __forceinline__ void eval_small(const EvalParams& P, const EvalShared
       s = __dadd_rn(s, __dmul_rn(C.m2, r_at<true>(S, prev, nd)));
     }
     prev = nd;
-    if (last && pp >= 2) tpp = fmax(tpp, s);
+    if (last && pp >= 2) tpp = dmax(tpp, s);
   };
   auto flags = [&](int w0, int j, bool& st, bool& la) {
     if constexpr (PP == 1) {
@@ -225,7 +225,7 @@ __device__ __forceinline__ void eval_small(const EvalParams& P, const EvalShared
     while (b) {
       const uint32_t sh = (uint32_t)(__ffs(b) - 1) & ~3u;
       b &= ~(15u << sh);
-      t_in = fmax(t_in, __ldg(vin + (hw * 8 + (sh >> 2)) * 16 + ((h >> sh) & 15u)));
+      t_in = dmax(t_in, __ldg(vin + (hw * 8 + (sh >> 2)) * 16 + ((h >> sh) & 15u)));
     }
   }
   const int k = __popc(mask);
@@ -289,7 +289,7 @@ __device__ __forceinline__ void eval_general(const EvalParams& P, const EvalShar
         }
         prev = nd;
         const bool last = PP >= 8 ? (j == 7 && tail) : (j % PP) == PP - 1;
-        if (PP >= 2 && last) tpp = fmax(tpp, s);
+        if (PP >= 2 && last) tpp = dmax(tpp, s);
       }
     }
     ok = bad == 0u;
@@ -314,7 +314,7 @@ __device__ __forceinline__ void eval_general(const EvalParams& P, const EvalShar
     prev = nd;
     if (++x == pp) {
       x = 0;
-      if (pp >= 2) tpp = fmax(tpp, s);
+      if (pp >= 2) tpp = dmax(tpp, s);
     }
   };
   if (row.vec) {
@@ -362,7 +362,7 @@ __device__ __forceinline__ void eval_general(const EvalParams& P, const EvalShar
       const uint32_t sh = (uint32_t)(__ffs(ge2) - 1) & ~(cbits - 1u);
       ge2 &= ~(cmask << sh);
       const uint32_t a = ((uint32_t)w << clg) + sh / cbits, c = (cw >> sh) & cmask;
-      t_in = fmax(t_in, __dmul_rn(__ldg(qi + c), r_at<false>(S, a, a)));
+      t_in = dmax(t_in, __dmul_rn(__ldg(qi + c), r_at<false>(S, a, a)));
     }
   }
   const int k = mask.count();
@@ -383,7 +383,7 @@ __device__ __forceinline__ void eval_general(const EvalParams& P, const EvalShar
           while (bits2) {
             const uint32_t b = wd2 * 32 + __ffs(bits2) - 1;
             bits2 &= bits2 - 1;
-            if (a != b) mx = fmax(mx, r_at<false>(S, a, b));
+            if (a != b) mx = dmax(mx, r_at<false>(S, a, b));
           }
         }
       }
@@ -804,7 +804,7 @@ __device__ __forceinline__ void eval_warp_one(const EvalParams& P, const double*
         prev = cur;
       }
     }
-    tpp = fmax(tpp, s);
+    tpp = dmax(tpp, s);
     const uint32_t a = ws->nd[b];           // stage-1 worker of pipeline z (Eq.6)
     atomicAdd(&ws->cnt[a >> 2], 1u << ((a & 3) * 8));
     const uint32_t bit = 1u << (a & 31), q = a >> 5;
@@ -820,7 +820,7 @@ __device__ __forceinline__ void eval_warp_one(const EvalParams& P, const double*
   for (int z = lane; z < dp; z += 32) {
     const uint32_t a = ws->nd[z * pp];
     const uint32_t c = (ws->cnt[a >> 2] >> ((a & 3) * 8)) & 0xffu;
-    if (c >= 2u) tin = fmax(tin, __dmul_rn(__ldg(P.qtab + C.qi_off + c), Rs[a * (uint32_t)n + a]));
+    if (c >= 2u) tin = dmax(tin, __dmul_rn(__ldg(P.qtab + C.qi_off + c), Rs[a * (uint32_t)n + a]));
   }
   tin = warp_max(tin);
   // ---- Eq.6, inter: the slowest link among the k stage-1 nodes
@@ -842,7 +842,7 @@ __device__ __forceinline__ void eval_warp_one(const EvalParams& P, const double*
         const uint32_t j = base + (uint32_t)lane;
         const uint32_t ia = __umulhi(j, mg), ib = j - ia * kk;
         const uint32_t a = __shfl_sync(full, memv, (int)(ia & 31u)), b = __shfl_sync(full, memv, (int)(ib & 31u));
-        if (j < npair && ia != ib) mx = fmax(mx, Rs[a * (uint32_t)n + b]);
+        if (j < npair && ia != ib) mx = dmax(mx, Rs[a * (uint32_t)n + b]);
       }
       mx = warp_max(mx);
     } else {         // first pair of the R-descending list inside N1 (expected (n/k)^2 probes)

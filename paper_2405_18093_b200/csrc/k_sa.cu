@@ -571,11 +571,11 @@ __device__ __forceinline__ void run_task(const SaParams& P, const SaTask T, cons
           pos.swap(d.p, d.q, rp, rq);
           if (two) pipe_sum2<RT, PP>(zp, zq, pp, pos, kNone, kNone, 0u, 0u, C.m2, R, sA, sB);
           else sA = pipe_sum<RT, PP>(zp, pp, pos, kNone, kNone, 0u, 0u, C.m2, R);
-          const double snew = two ? fmax(sA, sB) : sA;
+          const double snew = two ? dmax(sA, sB) : sA;
           const int keep = nmax - (oldA == tpp ? 1 : 0) - ((two && oldB == tpp) ? 1 : 0);  // untouched at max
           if (keep > 0 || snew >= tpp) {
             // the max is max(tpp if an untouched pipeline still holds it, new sums)
-            tpp2 = (keep > 0) ? fmax(tpp, snew) : snew;
+            tpp2 = (keep > 0) ? dmax(tpp, snew) : snew;
             nmax2 = (keep > 0 && tpp2 == tpp ? keep : 0) + (sA == tpp2 ? 1 : 0) + ((two && sB == tpp2) ? 1 : 0);
           } else if (cache) {
             // the unique max pipeline decreased: rescan for the max and its multiplicity in
@@ -587,16 +587,16 @@ __device__ __forceinline__ void run_task(const SaParams& P, const SaTask T, cons
               const double v0 = (z == zp || z == zq) ? 0.0 : psum[z * 32 + lane];
               const double v1 = (z + 1 == zp || z + 1 == zq) ? 0.0 : psum[(z + 1) * 32 + lane];
               c0 = v0 > m0 ? 1 : c0 + (v0 == m0 ? 1 : 0);
-              m0 = fmax(m0, v0);
+              m0 = dmax(m0, v0);
               c1 = v1 > m1 ? 1 : c1 + (v1 == m1 ? 1 : 0);
-              m1 = fmax(m1, v1);
+              m1 = dmax(m1, v1);
             }
             if (z < dp) {
               const double v0 = (z == zp || z == zq) ? 0.0 : psum[z * 32 + lane];
               c0 = v0 > m0 ? 1 : c0 + (v0 == m0 ? 1 : 0);
-              m0 = fmax(m0, v0);
+              m0 = dmax(m0, v0);
             }
-            tpp2 = fmax(m0, m1);
+            tpp2 = dmax(m0, m1);
             nmax2 = (m0 == tpp2 ? c0 : 0) + (m1 == tpp2 ? c1 : 0);
           } else {
             // no cache: re-sum every pipeline of the tentative mapping
@@ -753,7 +753,7 @@ __device__ __forceinline__ void hc_rescan(const HcState& st, int dp, int pp_rt, 
   int c0 = 0, c1 = 0;
   auto acc = [](double v, double& m, int& c) {
     c = v > m ? 1 : c + (v == m ? 1 : 0);
-    m = fmax(m, v);
+    m = dmax(m, v);
   };
   if constexpr (PP == 2) {
     const int full = dp >> 1;
@@ -773,7 +773,7 @@ __device__ __forceinline__ void hc_rescan(const HcState& st, int dp, int pp_rt, 
     }
     if (z < dp) acc(hc_sum<PP>(st, (uint32_t)z, pp_rt, Tl), m0, c0);
   }
-  mx = fmax(m0, m1);
+  mx = dmax(m0, m1);
   cnt = (m0 == mx ? c0 : 0) + (m1 == mx ? c1 : 0);
 }
 
@@ -796,7 +796,7 @@ __device__ __forceinline__ void hc_coop_tpp(bool need, unsigned char* ws, const 
     for (int z = lane; z < dp; z += 32) {
       const double v = cache ? psum[z * 32 + L] : hc_sum<PP>(stL, (uint32_t)z, pp, Tl);
       c = v > m ? 1 : c + (v == m ? 1 : 0);
-      m = fmax(m, v);
+      m = dmax(m, v);
     }
     uint32_t cnt;
     m = warp_max_nonneg(m, (uint32_t)c, cnt);
@@ -931,11 +931,11 @@ __device__ __forceinline__ void run_task_hc(const SaParams& P, const SaTask T, c
         // ---- T_PP (Eq.5): max over pipelines with its multiplicity
         double tpp2 = tpp;
         int nmax2 = nmax;
-        const double snew = fmax(sA, sB);
+        const double snew = dmax(sA, sB);
         const int keep = nmax - (oldA == tpp ? 1 : 0) - ((two && oldB == tpp) ? 1 : 0);  // untouched at max
         const bool fast = keep > 0 || snew >= tpp;
         if (fast) {
-          tpp2 = (keep > 0) ? fmax(tpp, snew) : snew;
+          tpp2 = (keep > 0) ? dmax(tpp, snew) : snew;
           nmax2 = (keep > 0 && tpp2 == tpp ? keep : 0) + (sA == tpp2 ? 1 : 0) + ((two && sB == tpp2) ? 1 : 0);
         }
         // the unique max pipeline decreased: rescan over all pipelines (the new sums enter the
@@ -953,7 +953,7 @@ __device__ __forceinline__ void run_task_hc(const SaParams& P, const SaTask T, c
               for (int z = 0; z < dp; ++z) {
                 const double v = psum[z * 32 + lane];
                 c = v > m ? 1 : c + (v == m ? 1 : 0);
-                m = fmax(m, v);
+                m = dmax(m, v);
               }
               tpp2 = m;
               nmax2 = c;
@@ -1091,7 +1091,7 @@ __device__ __forceinline__ double pair_max_lane(const Mask4& m, int kk, const S1
           while (bb) {
             const int b = wd2 * 32 + __ffs(bb) - 1;
             bb &= bb - 1;
-            if (b != a) mx = fmax(mx, __ldg(R + a * n + b));
+            if (b != a) mx = dmax(mx, __ldg(R + a * n + b));
           }
         }
       }
@@ -1166,7 +1166,7 @@ __device__ __forceinline__ double full_eval(const uint8_t* sb, const uint32_t* s
         prev = cur;
       }
     }
-    tpp = fmax(tpp, s);
+    tpp = dmax(tpp, s);
   }
   double tin = 0.0, tex = 0.0;
   if constexpr (MODE == 0) {
@@ -1189,7 +1189,7 @@ __device__ __forceinline__ double full_eval(const uint8_t* sb, const uint32_t* s
         const uint32_t a = (uint32_t)(wd * 32 + __ffs(bits) - 1);
         bits &= bits - 1;
         const uint32_t c = cb[HcState::off(a)];
-        if (c >= 2u) tin = fmax(tin, __dmul_rn(__ldg(X.qi + c), __ldg(R + a * (uint32_t)n + a)));
+        if (c >= 2u) tin = dmax(tin, __dmul_rn(__ldg(X.qi + c), __ldg(R + a * (uint32_t)n + a)));
       }
     }
     const int k = mask.count();
@@ -1517,7 +1517,7 @@ __global__ void k_subset_max(const double* __restrict__ R, int n, double* __rest
   for (int a = 0; a < n; ++a) {
     if (!((m >> a) & 1u)) continue;
     for (int b = 0; b < n; ++b)
-      if (b != a && ((m >> b) & 1u)) mx = fmax(mx, R[a * n + b]);
+      if (b != a && ((m >> b) & 1u)) mx = dmax(mx, R[a * n + b]);
   }
   tab[m] = mx;
 }
@@ -1640,8 +1640,8 @@ int sa_warp_state_bytes(int mode, int N, int pp, int dp, int n, int dp_cap, bool
   if (mode == 0) return hc_warp_state_bytes(N, pp, dp, dp_cap);
   return warp_state_bytes<PosWide>(N, pp, dp, n, true, dp_cap);
 }
-int sa_m1_warp_state_bytes(int N, int dp, int n, bool counts, bool cache, bool nib) {
-  return m1_warp_state_bytes(N, dp, n, counts, cache, nib);
+int sa_m1_warp_state_bytes(int N, int dp, int n, bool counts, bool cache, bool nib, bool direct) {
+  return m1_warp_state_bytes(N, dp, n, counts, cache, nib, direct);
 }
 int sa_m1_count_bytes(int n, bool nib) { return sb_count_bytes(n, nib); }
 

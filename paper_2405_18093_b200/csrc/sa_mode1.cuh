@@ -168,8 +168,6 @@ __device__ __forceinline__ void coop_tpp(bool need, unsigned char* ws, const dou
   __syncwarp();   // (flagged lanes' tentative cache writes are visible to the warp)
   for (unsigned todo = __ballot_sync(full, need); todo; todo &= todo - 1u) {
     const int L = __ffs(todo) - 1;
-    const uint32_t zpL = __shfl_sync(full, zp, L), zbL = __shfl_sync(full, zb, L);
-    const double sAL = __shfl_sync(full, sA, L), sBL = __shfl_sync(full, sB, L);
     HcState stL;
     stL.hb = ws + L * 4;
     stL.sb = stL.hb;
@@ -180,7 +178,7 @@ __device__ __forceinline__ void coop_tpp(bool need, unsigned char* ws, const dou
       const double v = cache ? psum[z * 32 + L]
                              : sb_sum<PP, KT>(stL, (uint32_t)z, pp, K);
       c = v > m ? 1 : c + (v == m ? 1 : 0);
-      m = fmax(m, v);
+      m = dmax(m, v);
     }
     uint32_t cnt;
     m = warp_max_nonneg(m, (uint32_t)c, cnt);   // (max, count at max) over the lanes
@@ -190,8 +188,11 @@ __device__ __forceinline__ void coop_tpp(bool need, unsigned char* ws, const dou
 
 // [slot plane][stage-1 counts: bytes, or nibbles when nib][psum]
 __host__ __device__ inline int sb_count_bytes(int n, bool nib) { return align16((nib ? (n + 7) / 8 : (n + 3) / 4) * 128); }
-__host__ __device__ inline int m1_warp_state_bytes(int N, int dp, int n, bool counts, bool cache, bool nib) {
-  return align16(((N + 3) / 4) * 128) + (counts ? sb_count_bytes(n, nib) : 0) + (cache ? align16(dp * 256) : 0);
+// [slot plane][stage-1 counts][psum cache][direct mode: N1 member bytes, 2 words per lane]
+__host__ __device__ inline int m1_warp_state_bytes(int N, int dp, int n, bool counts, bool cache, bool nib,
+                                                   bool direct) {
+  return align16(((N + 3) / 4) * 128) + (counts ? sb_count_bytes(n, nib) : 0) + (cache ? align16(dp * 256) : 0) +
+         (direct ? 256 : 0);
 }
 
 // ------------------------------------------------------------------ stage-1 state (Eq.6)
@@ -208,6 +209,7 @@ __device__ __forceinline__ int join_coop_max(int n) {
 
 struct S1M {
   uint32_t* c;   // count plane [ceil(n / per-word)][32] (counts configurations only)
+  uint32_t* ml;  // direct mode: N1's member nodes as bytes, any order, [2][32] (k bytes valid)
   int lane;
   uint32_t lgw = 2u, bw = 8u, cm = 0xffu;   // log2 counts per word, bits per count, count mask
   bool counts, direct;
@@ -232,23 +234,6 @@ struct S1M {
   }
   static __device__ __forceinline__ uint32_t pair_at(const S1Ctx& X, int j) {
     return j < X.plen ? (uint32_t)X.pl[j] : (uint32_t)__ldg(X.gl_ab + j);
-  }
-  // node id of the t-th (0-based) member of m, t < |m| (else meaningless): the word by
-  // popcount prefixes, then a five-step popcount bisection inside it
-  static __device__ __forceinline__ uint32_t nth_member(const Mask4& m, uint32_t t) {
-    const uint32_t c0 = __popc(m.w0), c1 = c0 + __popc(m.w1), c2 = c1 + __popc(m.w2);
-    uint32_t x = t < c0 ? m.w0 : (t < c1 ? m.w1 : (t < c2 ? m.w2 : m.w3));
-    uint32_t r = t - (t < c0 ? 0u : (t < c1 ? c0 : (t < c2 ? c1 : c2)));
-    uint32_t pos = t < c0 ? 0u : (t < c1 ? 32u : (t < c2 ? 64u : 96u));
-#pragma unroll
-    for (uint32_t h = 16u; h >= 1u; h >>= 1) {
-      const uint32_t c = __popc(x & ((1u << h) - 1u));
-      const bool up = r >= c;
-      r = up ? r - c : r;
-      x = up ? x >> h : x;
-      pos = up ? pos + h : pos;
-    }
-    return pos;
   }
 
   // max over ordered member pairs a != b of m of R[a][b], with a witness pair
@@ -353,6 +338,16 @@ struct S1M {
     }
     tex = k >= 2 ? __dmul_rn(__ldg(X.qe + k), maxR) : 0.0;
     need_tin = need_scan = need_join = false;
+    if (direct) {   // member bytes in ascending node order (k <= 8)
+      unsigned long long l = 0ull;
+      int t = 0;
+#pragma unroll
+      for (int wd = 0; wd < 4; ++wd)
+        for (uint32_t bb = mask.word(wd); bb; bb &= bb - 1u, ++t)
+          l |= (unsigned long long)(wd * 32 + __ffs(bb) - 1) << (8 * t);
+      ml[lane] = (uint32_t)l;
+      ml[32 + lane] = (uint32_t)(l >> 32);
+    }
   }
 
   // a stage-1 member moves from node dn to node up (tentative); long searches are flagged
@@ -460,31 +455,37 @@ struct S1M {
     while (todo) {
       const int L = __ffs(todo) - 1;
       todo &= todo - 1;
-      Mask4 m;
-      m.w0 = __shfl_sync(full, mask2.w0, L); m.w1 = __shfl_sync(full, mask2.w1, L);
-      m.w2 = __shfl_sync(full, mask2.w2, L); m.w3 = __shfl_sync(full, mask2.w3, L);
       if (direct) {
-        // lane t (mod 8) holds the t-th member node of N1' (k' <= 8); a join pairs the new
-        // node with every member (lanes 0-15, one round), a recompute takes the k' x k'
-        // ordered pairs (lane j of round r: pair (8r + j / 8, j % 8))
-        const uint32_t kk = (uint32_t)__shfl_sync(full, k2, L);
-        const bool jo = __shfl_sync(full, (int)(need_join && !need_scan), L) != 0;
+        // lane t (mod 8) holds member slot t of lane L's N1' = N1 - dn (+ up): slots 0..k-1
+        // are N1's member bytes (dn's slot taken by up, or empty, when dn leaves), slot k is
+        // up when it joins without a leave.  A join pairs up with every member (lanes 0-15,
+        // one round); a recompute takes the ordered slot pairs (lane j of round r: slots
+        // (4r + j / 8, j % 8)).
+        const uint32_t info = __shfl_sync(full, dn_ | (up_ << 8) | ((uint32_t)k << 16) | ((c_dn_ == 0u) ? 1u << 20 : 0u) |
+                                                    ((c_up_ == 1u) ? 1u << 21 : 0u) |
+                                                    ((need_join && !need_scan) ? 1u << 22 : 0u), L);
+        const uint32_t dnL = info & 0xffu, upL = (info >> 8) & 0xffu, kL = (info >> 16) & 0xfu;
+        const bool lv = (info >> 20) & 1u, jn = (info >> 21) & 1u, jo = (info >> 22) & 1u;
         const uint32_t t = (uint32_t)lane & 7u;
-        const uint32_t memv = nth_member(m, t);
+        uint32_t memv = __byte_perm(t < 4u ? ml[L] : ml[32 + L], 0u, 0x4440u | (t & 3u));
+        bool val = t < kL;
+        if (val && lv && memv == dnL) { memv = upL; val = jn; }
+        if (!lv && jn && t == kL) { memv = upL; val = true; }
+        memv = val ? memv : 0xffffffffu;
+        const uint32_t slots = kL + ((!lv && jn) ? 1u : 0u);
         double mx = 0.0;
         uint32_t wbest = 0xffffu;
         if (jo) {
-          const uint32_t upL = (uint32_t)__shfl_sync(full, up_, L);
-          if (lane < 16 && t < kk && memv != upL) {
+          if (lane < 16 && memv != 0xffffffffu && memv != upL) {
             const uint32_t a = lane < 8 ? upL : memv, b = lane < 8 ? memv : upL;
             mx = K.r(a, b);
             wbest = a | (b << 8);
           }
         } else {
-          for (uint32_t base = 0; base < kk * 8u; base += 32u) {
-            const uint32_t ia = (base + (uint32_t)lane) >> 3, ib = t;
-            const uint32_t a = __shfl_sync(full, memv, (int)(ia & 7u)), b = __shfl_sync(full, memv, (int)ib);
-            if (ia < kk && ib < kk && ia != ib) {
+          for (uint32_t base = 0; base < slots * 8u; base += 32u) {
+            const uint32_t ia = (base + (uint32_t)lane) >> 3;
+            const uint32_t a = __shfl_sync(full, memv, (int)(ia & 7u)), b = __shfl_sync(full, memv, (int)t);
+            if (ia != t && a != 0xffffffffu && b != 0xffffffffu) {
               const double v = K.r(a, b);
               if (v > mx) { mx = v; wbest = a | (b << 8); }
             }
@@ -500,6 +501,9 @@ struct S1M {
         }
         continue;
       }
+      Mask4 m;
+      m.w0 = __shfl_sync(full, mask2.w0, L); m.w1 = __shfl_sync(full, mask2.w1, L);
+      m.w2 = __shfl_sync(full, mask2.w2, L); m.w3 = __shfl_sync(full, mask2.w3, L);
       const int start = __shfl_sync(full, jw, L) + 1;
       int hit = -1;
       uint32_t pab = 0u;
@@ -529,6 +533,24 @@ struct S1M {
   __device__ __forceinline__ void finish(const S1Ctx& X) { tex2 = k2 >= 2 ? __dmul_rn(__ldg(X.qe + k2), maxR2) : 0.0; }
   __device__ __forceinline__ void commit() {
     if (counts) { add(dn_, -1); add(up_, +1); }
+    if (direct && (c_dn_ == 0u || c_up_ == 1u)) {   // member bytes: dn's byte <- the last one; up appended
+      unsigned long long l = (unsigned long long)ml[lane] | ((unsigned long long)ml[32 + lane] << 32);
+      int kk = k;
+      if (c_dn_ == 0u) {
+        const uint32_t d4 = dn_ * 0x01010101u;
+        unsigned long long e = (unsigned long long)__vcmpeq4(ml[lane], d4) |
+                               ((unsigned long long)__vcmpeq4(ml[32 + lane], d4) << 32);
+        e &= kk >= 8 ? ~0ull : (1ull << (8 * kk)) - 1ull;
+        const int pos = (__ffsll((long long)e) - 1) >> 3;
+        const unsigned long long last = (l >> (8 * (kk - 1))) & 0xffull;
+        l = (l & ~(0xffull << (8 * pos))) | (last << (8 * pos));
+        l &= ~(0xffull << (8 * (kk - 1)));
+        --kk;
+      }
+      if (c_up_ == 1u) l |= (unsigned long long)up_ << (8 * kk);
+      ml[lane] = (uint32_t)l;
+      ml[32 + lane] = (uint32_t)(l >> 32);
+    }
     mask = mask2; k = k2; tin = tin2; win = win2; tex = tex2; maxR = maxR2; wab = wab2; jw = jw2;
   }
 };
@@ -576,6 +598,7 @@ __device__ __forceinline__ void run_task_sb(const SaParams& P, const SaTask T, c
   s1.c = reinterpret_cast<uint32_t*>(ws + plane);
   s1.set_nibbles(P.s1_nib != 0);
   double* psum = reinterpret_cast<double*>(ws + plane + (s1.counts ? sb_count_bytes(n, P.s1_nib != 0) : 0));
+  s1.ml = reinterpret_cast<uint32_t*>(reinterpret_cast<unsigned char*>(psum) + (cache ? align16(dp * 256) : 0));
   uint16_t* bperm = P.best_perm + T.perm_off;
   s1.clear(n);
 
@@ -638,11 +661,11 @@ __device__ __forceinline__ void run_task_sb(const SaParams& P, const SaTask T, c
         sb_sum2<PP, SbCtxT<ID>>(st, zp, zb, pp, K, sA, sB);
         double tpp2 = tpp;
         int nmax2 = nmax;
-        const double snew = fmax(sA, sB);
+        const double snew = dmax(sA, sB);
         const int keep = nmax - (oldA == tpp ? 1 : 0) - ((two && oldB == tpp) ? 1 : 0);
         const bool fast = keep > 0 || snew >= tpp;
         if (fast) {
-          tpp2 = (keep > 0) ? fmax(tpp, snew) : snew;
+          tpp2 = (keep > 0) ? dmax(tpp, snew) : snew;
           nmax2 = (keep > 0 && tpp2 == tpp ? keep : 0) + (sA == tpp2 ? 1 : 0) + ((two && sB == tpp2) ? 1 : 0);
         }
         // the unique max pipeline decreased: rescan over all pipelines -- up to 4 cached sums
@@ -657,7 +680,7 @@ __device__ __forceinline__ void run_task_sb(const SaParams& P, const SaTask T, c
             double v[8];
 #pragma unroll
             for (int z = 0; z < 8; ++z) v[z] = z < dp ? psum[z * 32 + lane] : 0.0;
-            const double m = fmax(fmax(fmax(v[0], v[1]), fmax(v[2], v[3])), fmax(fmax(v[4], v[5]), fmax(v[6], v[7])));
+            const double m = dmax(dmax(dmax(v[0], v[1]), dmax(v[2], v[3])), dmax(dmax(v[4], v[5]), dmax(v[6], v[7])));
             int c = 0;
 #pragma unroll
             for (int z = 0; z < 8; ++z) c += (z < dp && v[z] == m) ? 1 : 0;
