@@ -369,7 +369,10 @@ __device__ __forceinline__ void eval_general(const EvalParams& P, const EvalShar
   // slowest link of N1: the k(k-1) member pairs when k^2 <= n, else the first pair inside N1
   // of the R-descending pair list (expected ~(n/k)^2 probes; every thread scans the same
   // prefix, so it stays in L1).  Both give the exact max.
-  const bool pairs = k * k <= S.n;
+  // (a converged warp scans the list cooperatively, below: there the list beats the pairs
+  // from k = 6 on; a lone lane probes ~(n/k)^2 pairs, so it takes the pairs while k^2 <= n)
+  const bool coop = __activemask() == 0xffffffffu;
+  const bool pairs = coop ? k <= 5 : k * k <= S.n;
   if (pairs) {
 #pragma unroll
     for (int wd = 0; wd < 4; ++wd) {
@@ -389,7 +392,60 @@ __device__ __forceinline__ void eval_general(const EvalParams& P, const EvalShar
       }
     }
   }
-  if (!pairs && k >= 2) {   // first pair of the R-sorted list inside N1; the value from the R table
+  // first pair of the R-sorted list inside N1; the value from the R table
+  const bool want = !pairs && k >= 2;
+  if (coop && __activemask() == 0xffffffffu) {
+    // whole warp converged: one cooperative scan for all its lanes.  Every lane probes the
+    // same list prefix, so the warp takes 32 consecutive pairs per round, one per lane, and
+    // tests them against all 32 lanes' N1 at once through the transposed membership (lane t
+    // holds, for node 32q + t, the bit set of the lanes whose N1 has it): a lane's witness
+    // is its first hit in list order.  (A lane alone would probe ~(n/k)^2 pairs, the warp in
+    // lockstep the max of 32 such runs.)
+    const unsigned full = 0xffffffffu;
+    unsigned pending = __ballot_sync(full, want);
+    if (pending) {
+      const int nq = (S.n + 31) >> 5;
+      uint32_t mt[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {   // 32 x 32 bit transpose by five shuffle stages
+        uint32_t x = mask.w[q];
+        if (q < nq) {
+#pragma unroll
+          for (int jj = 16; jj >= 1; jj >>= 1) {
+            const uint32_t m = jj == 16 ? 0x0000ffffu : (jj == 8 ? 0x00ff00ffu : (jj == 4 ? 0x0f0f0f0fu
+                             : (jj == 2 ? 0x33333333u : 0x55555555u)));
+            const uint32_t y = __shfl_xor_sync(full, x, jj);
+            x = (S.lane & jj) ? ((x & ~m) | ((y & ~m) >> jj)) : ((x & m) | ((y & m) << jj));
+          }
+        }
+        mt[q] = x;
+      }
+      const int len = S.n * (S.n - 1);
+      for (int base = 0; pending != 0u && base < len; base += 32) {
+        const int j = base + S.lane;
+        const uint32_t ab = j < len ? (j < S.plen ? (uint32_t)S.pl[j] : (uint32_t)__ldg(P.gl_ab + j)) : 0u;
+        const uint32_t a = ab & 0xffu, b = ab >> 8;
+        uint32_t ma = 0u, mb = 0u;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          if (q < nq) {
+            const uint32_t xa = __shfl_sync(full, mt[q], (int)(a & 31u)), xb = __shfl_sync(full, mt[q], (int)(b & 31u));
+            ma = (a >> 5) == (uint32_t)q ? xa : ma;
+            mb = (b >> 5) == (uint32_t)q ? xb : mb;
+          }
+        }
+        const uint32_t hit = j < len ? (ma & mb & pending) : 0u;
+        const unsigned got = __reduce_or_sync(full, hit);   // lanes with a witness in this round
+        for (unsigned todo = got; todo; todo &= todo - 1u) {
+          const int l = __ffs(todo) - 1;
+          const int t = __ffs(__ballot_sync(full, (hit >> l) & 1u)) - 1;
+          const uint32_t abt = __shfl_sync(full, ab, t);
+          if (S.lane == l) mx = r_at<false>(S, abt & 0xffu, abt >> 8);
+        }
+        pending &= ~got;
+      }
+    }
+  } else if (want) {
     const int len = S.n * (S.n - 1);
     for (int j = 0; j < len; ++j) {
       const uint32_t ab = j < S.plen ? (uint32_t)S.pl[j] : (uint32_t)__ldg(P.gl_ab + j);
