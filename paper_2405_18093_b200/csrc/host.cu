@@ -489,8 +489,8 @@ pipette_status build_plan(pipette_ctx* ctx, int chains, int W, int r, const char
     // stage-1 counts when some node can hold >= 2 members, T_ex by member pairs when N1
     // never exceeds 8 nodes, and the pipeline-sum cache when it saves re-summing long
     // pipelines (pp >= PIPETTE_M1_CACHE_PP, default 2; the old sums of the two touched
-    // pipelines are otherwise re-summed) and costs at most a few resident warps
-    // (PIPETTE_M1_CACHE_MIN).
+    // pipelines are otherwise re-summed) and costs at most one resident warp
+    // (PIPETTE_M1_CACHE_MIN: the fewest warps the cache may leave).
     int lg = 0;
     while ((1 << lg) < n) ++lg;
     const int plen = std::min(n * (n - 1), kSaM1PairPrefix);
@@ -502,7 +502,7 @@ pipette_status build_plan(pipette_ctx* ctx, int chains, int W, int r, const char
       nib = nib && std::min(c.spn, c.dp) <= 15;
     }
     const char* cm_env = getenv("PIPETTE_M1_CACHE_MIN");
-    const int cache_min = cm_env ? atoi(cm_env) : 6;
+    const int cache_min = cm_env ? atoi(cm_env) : kSaM1Warps - 1;
     const char* cp_env = getenv("PIPETTE_M1_CACHE_PP");
     const int cache_pp = cp_env ? atoi(cp_env) : 2;
     std::vector<int> fbytes(F), fwarps(F);
@@ -515,9 +515,10 @@ pipette_status build_plan(pipette_ctx* ctx, int chains, int W, int r, const char
                                   : sa_m1_warp_state_bytes(c.N, c.dp, n, counts, false, nib, direct);
       const int with = sa_m1_warp_state_bytes(c.N, c.dp, n, counts, true, nib, direct);
       const int w_nc = std::min(kSaM1Warps, avail / base), w_c = std::min(kSaM1Warps, avail / with);
-      // (measured on C5: the cache pays for a lost resident warp only when it saves re-summing
-      // long pipelines -- (4,8,32) 8 uncached warps beat 7 cached, (8,4,32) 8 beat 5)
-      const int need = cm_env ? std::min(w_nc, cache_min) : (c.pp >= 16 ? std::min(w_nc, 6) : w_nc);
+      // (measured on C5, 3 alternating reps: keeping the cache at the cost of at most one
+      // resident warp, 770-775 ms per search, beats both no lost warp (822-826) and the earlier
+      // pp >= 16 rule that let (16,4,16) drop to 6 warps (779-782))
+      const int need = std::min(w_nc, cm_env ? cache_min : kSaM1Warps - 1);
       const bool cache = !full_moves && c.pp >= std::max(2, cache_pp) && w_c >= 1 && w_c >= need;
       fbytes[f] = cache ? with : base;
       fwarps[f] = cache ? w_c : w_nc;
