@@ -88,3 +88,49 @@ def test_profile_bandwidth_feeds_the_search():
     ref = O.search(cl, B, O.make_profile(prof), mo, 8 * n, 4, 300, 5)
     p = res["plan"]
     assert (p.latency_s, p.cfg_index, p.chain) == (ref.latency, ref.cfg_index, ref.chain)
+
+
+def test_host_transport_rank0_of_two_in_one_process():
+    """Product combine path at W = 2 in ONE process: rank 0's context with a host transport
+    that stands in for an absent peer (min/sum of one contribution = identity).  The plan is
+    then rank 0's shard (items j = f*chains + c with j even, R18), which the oracle computes
+    chain by chain; a failing transport surfaces as E_NCCL."""
+    from paper_2405_18093_b200 import Model, Pipette, PipetteError
+    w = W.WORKLOADS["C1"]
+    B, prof = W.workload_inputs(w)
+    m = w.model
+    calls = []
+
+    def identity(user, buf, count, op):
+        calls.append((int(count), int(op)))
+        return 0
+
+    pip = Pipette(w.n_nodes, w.gpus_per_node, B, prof, w.cap_bytes, w.margin_permille, rank=0, world=2,
+                  host_allreduce=identity)
+    chains, iters = 5, 400
+    model = Model(m.n_layers, m.hidden, m.heads, m.seq_len, m.vocab)
+    res = pip.search(model, w.bs_global, chains, iters, w.seed)
+    assert [op for _, op in calls] == [0, 0, 1]          # min bits, min items, sum of plan rows
+    cl = O.make_cluster(w.n_nodes, w.gpus_per_node, w.cap_bytes, w.margin_permille)
+    mo = O.make_model(m.n_layers, m.hidden, m.heads, m.seq_len, m.vocab)
+    P = O.make_profile(prof)
+    R = O.inverse_bandwidth(B)
+    feas = [c for c in O.enumerate_configs(cl, mo, w.bs_global, P) if c.feasible]
+    best = None
+    for j in range(0, len(feas) * chains, 2):
+        f, c = divmod(j, chains)
+        K = O.constants(cl, mo, feas[f], P)
+        r = O.sa_chain(K, R, iters, w.seed, c, feas[f].e)
+        if best is None or r.best < best[0]:
+            best = (r.best, f, c, r.best_perm)
+    p = res["plan"]
+    assert p.latency_s == best[0] and p.chain == best[2] and p.perm.tolist() == best[3].tolist()
+
+    def failing(user, buf, count, op):
+        return 7
+
+    bad = Pipette(w.n_nodes, w.gpus_per_node, B, prof, w.cap_bytes, w.margin_permille, rank=1, world=2,
+                  host_allreduce=failing)
+    with pytest.raises(PipetteError) as ei:
+        bad.search(model, w.bs_global, chains, iters, w.seed)
+    assert ei.value.status == 5 and "host allreduce" in str(ei.value)
