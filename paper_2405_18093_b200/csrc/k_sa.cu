@@ -126,7 +126,8 @@ struct S1Ctx {
   int nl_len, gl_len, tl_len;
   int n;
   // MODE 1 (S1M): per node, its 2(n-1) ordered pairs in global-list order (entry = list
-  // index | (a | b << 8) << 16, rows of pt_stride entries padded with 0xffffffff), and the
+  // index | other node << 16 | node first << 24, rows of pt_stride entries padded with
+  // 0xffffffff; k_partner_lists), and the
   // block's shared copy of the first plen entries of gl_ab
   const uint32_t* pt;
   int pt_stride;
@@ -1600,7 +1601,8 @@ __global__ void __launch_bounds__(256) k_argmin(const ChainOut* __restrict__ out
 // Host-side handles of the K3 variants (MODE 0/1/2 as above; TRACE records).
 // Per-node pair rows for S1M (MODE 1): for node u (one warp per node), every ordered pair
 // with u as an endpoint, in global-list order (so by R descending, ties by index), entry =
-// list rank | (a | b << 8) << 16; rows of `stride` entries, padded with 0xffffffff.
+// list rank | other endpoint << 16 | (u is the first endpoint) << 24; rows of `stride`
+// entries (a multiple of 4), padded with 0xffffffff (rank 0xffff: beyond any witness).
 __global__ void k_partner_lists(const uint16_t* __restrict__ gl, int n, uint32_t* __restrict__ pt, int stride) {
   const int u = blockIdx.x, lane = threadIdx.x & 31, L = n * (n - 1);
   int base = 0;
@@ -1609,7 +1611,8 @@ __global__ void k_partner_lists(const uint16_t* __restrict__ gl, int n, uint32_t
     const uint32_t p = j < L ? (uint32_t)gl[j] : 0u;
     const bool hit = j < L && ((int)(p & 0xffu) == u || (int)(p >> 8) == u);
     const unsigned b = __ballot_sync(0xffffffffu, hit);
-    if (hit) pt[(size_t)u * stride + base + __popc(b & ((1u << lane) - 1u))] = (uint32_t)j | (p << 16);
+    const uint32_t first = (p & 0xffu) == (uint32_t)u ? 1u : 0u, other = first ? (p >> 8) : (p & 0xffu);
+    if (hit) pt[(size_t)u * stride + base + __popc(b & ((1u << lane) - 1u))] = (uint32_t)j | (other << 16) | (first << 24);
     base += __popc(b);
   }
   for (int i = base + lane; i < stride; i += 32) pt[(size_t)u * stride + i] = 0xffffffffu;

@@ -288,16 +288,15 @@ struct S1M {
   static __device__ __forceinline__ bool partner_scan(uint32_t u, const Mask4& m, int lim, const S1Ctx& X, int& j_o,
                                                       uint32_t& ab_o) {
     const uint4* row = reinterpret_cast<const uint4*>(X.pt + (size_t)u * (size_t)X.pt_stride);
-    for (int i = 0; i < X.nl_len; i += 4) {
+    for (int i = 0; i < X.nl_len; i += 4) {   // (the padding's rank 0xffff ends a partial last chunk)
       const uint4 e4 = __ldg(row + (i >> 2));
       const uint32_t e[4] = {e4.x, e4.y, e4.z, e4.w};
 #pragma unroll
       for (int t = 0; t < 4; ++t) {
-        if (i + t >= X.nl_len) return false;
         const int g = (int)(e[t] & 0xffffu);
         if (g >= lim) return false;
-        const uint32_t p = e[t] >> 16, a = p & 0xffu, b = p >> 8;
-        if (m.test(a == u ? b : a)) { j_o = g; ab_o = p; return true; }
+        const uint32_t o = (e[t] >> 16) & 0xffu;
+        if (m.test(o)) { j_o = g; ab_o = (e[t] >> 24) ? (u | (o << 8)) : (o | (u << 8)); return true; }
       }
     }
     return false;
