@@ -512,7 +512,7 @@ struct S1M {
         bool h = false;
         if (j < X.gl_len) {
           p = pair_at(X, j);
-          h = m.test(p & 0xffu) && m.test(p >> 8);
+          h = m.test(p & 0xffu) & m.test(p >> 8);   // (both tests, no branch: 747 vs 750.5 ms on C5)
         }
         const unsigned b = __ballot_sync(full, h);
         if (b) {
