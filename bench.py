@@ -235,6 +235,12 @@ def run_reference(args):
         return
     w, B, prof = setup(args.workload)
     cores = host_cores()
+    import oracle as O
+    m = w.model
+    cl = O.make_cluster(w.n_nodes, w.gpus_per_node, w.cap_bytes, w.margin_permille)
+    mo = O.make_model(m.n_layers, m.hidden, m.heads, m.seq_len, m.vocab)
+    cfgs = O.enumerate_configs(cl, mo, w.bs_global, O.make_profile(prof))
+    ref_config = run_config(w, args.weak, args.gpus, [c.pp * c.dp for c in cfgs if c.feasible], len(cfgs))
     for _ in range(args.warmup):
         oracle_sample(w, B, prof, min(0.5, args.ref_seconds), threads=cores)
     vals, secs, nch = [], 0.0, 0
@@ -247,13 +253,23 @@ def run_reference(args):
             "ms_per_step": 1000.0 * secs / args.steps, "higher_is_better": True,
             "scaling": "weak" if args.weak else "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (workloads/)",
-            "config": {"workload": workload_text(w, args.weak), "l2": "n/a (host)"},
+            "config": ref_config,
+            "timing": {"l2": "n/a (host)", "parallelism": f"host threads ({cores}), rank 0 only"},
             "cpu_baseline": {"value": value, "unit": "evals/s", "cores": cores, "kind": "oracle",
                              "cpu_model": cpu_model(),
                              "sample": f"{nch} full-length SA chains in total on {cores} host threads, round-robin "
                                        f"over the feasible configs, {args.ref_seconds:.0f} s per step x {args.steps} steps"},
             "e2e": {"value": value, "unit": "evals/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line))
+
+
+def run_config(w, weak: bool, world: int, n_per_feasible, n_enumerated: int) -> dict:
+    """`config` of both arms (identical for the same workload): the workload and its size.
+    n_per_feasible: N = pp*dp of every feasible configuration (a chain with N < 2 proposes nothing)."""
+    chains = w.chains * world if weak else w.chains
+    return {"workload": workload_text(w, weak), "chains_per_config": chains,
+            "feasible_configs": len(n_per_feasible), "enumerated_configs": int(n_enumerated),
+            "sa_proposals_per_step": int(sum(chains * w.iterations for N in n_per_feasible if N >= 2))}
 
 
 def workload_text(w, weak: bool) -> str:
@@ -448,10 +464,9 @@ def run_ours(args):
                                                  "(enumeration read-back, work plan, tables, search)"},
                 "higher_is_better": True, "scaling": "weak" if args.weak else "strong", "vs_baseline": None,
                 "dtype": "f64", "data": "synthetic (workloads/: B with per-link variance, Megatron-flop profile)",
-                "config": {"workload": workload_text(w, args.weak),
-                           "chains_per_config": chains, "feasible_configs": int(feas.sum()),
-                           "enumerated_configs": int(len(feas)), "sa_proposals_per_step": evals_per_step,
-                           "l2": "flushed between timed steps (256 MiB write)",
+                "config": run_config(w, args.weak, world, [int(c[0]) * int(c[2]) for c, f in zip(cfgs, feas) if f],
+                                     len(feas)),
+                "timing": {"l2": "flushed between timed steps (256 MiB write)",
                            "parallelism": f"chains striped j mod {world} (R18), NCCL combine"},
                 "plan": {"cfg": list(plan.cfg), "latency_s": plan.latency_s, "cfg_index": plan.cfg_index,
                          "chain": plan.chain, "best_step": plan.best_step},

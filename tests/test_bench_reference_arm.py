@@ -30,6 +30,13 @@ def test_reference_arm_prints_one_json_line():
     assert d["value"] > 0 and d["cpu_baseline"]["value"] == d["value"]
     assert d["cpu_baseline"]["kind"] == "oracle" and d["cpu_baseline"]["cores"] >= 1
     assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["e2e"]["d2h_bytes_per_step"] == 0
+    # the same `config` our arm writes (bench.run_config): the workload and its size only
+    import workloads as W
+    c, w = d["config"], W.WORKLOADS["C1"]
+    assert set(c) == {"workload", "chains_per_config", "feasible_configs", "enumerated_configs",
+                      "sa_proposals_per_step"}
+    assert c["chains_per_config"] == w.chains and c["workload"].startswith("C1:")
+    assert c["sa_proposals_per_step"] <= c["chains_per_config"] * c["feasible_configs"] * w.iterations
 
 
 def test_reference_arm_nonzero_rank_is_silent():
