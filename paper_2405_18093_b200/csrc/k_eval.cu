@@ -457,7 +457,6 @@ __device__ __forceinline__ void eval_general(const EvalParams& P, const EvalShar
   P.status[i] = C.feasible ? 0 : 1;
 }
 
-constexpr int kEvalThreads = 256;
 constexpr int kEvalTile = 2048;   // candidates per block tile (bucketed by configuration)
 
 // Gather the mapping rows of 32 candidates (tile positions ks[0..31], -1 = none) into a
