@@ -147,6 +147,7 @@ struct S1Reg {
   CT cnt, cnt2;
   uint32_t mask, mask2;
   uint32_t rk0, rk1, rk2_, rk3, nk0, nk1, nk2, nk3;   // current / tentative rank bytes
+  uint32_t pend;   // NW = 4: the tentative move instead, dn | up << 8 | dn's new rank << 16 | up's << 24
   int k, k2;
   double tin, tex, tin2, tex2;
 
@@ -185,22 +186,40 @@ struct S1Reg {
     tex = tex_of(mask, k, X);
   }
   // a stage-1 member moves from node dn to node up (tentative state)
+  // NW = 4 keeps only the move and the two new ranks live until commit (C3 145.7 -> 121.3 ms:
+  // the 16-node state spilled); NW = 2 keeps the whole tentative state (C2 14.9 vs 17.2 ms)
   __device__ __forceinline__ void propose(uint32_t dn, uint32_t up, const S1Ctx& X, const RT& R) {
     const uint32_t c_dn = get(cnt, dn) - 1u, c_up = get(cnt, up) + 1u;
-    cnt2 = cnt - ((CT)1 << (4u * dn)) + ((CT)1 << (4u * up));
-    mask2 = (mask & (c_dn == 0u ? ~(1u << dn) : 0xffffffffu)) | (1u << up);
-    k2 = __popc(mask2);
-    nk0 = rk0; nk1 = rk1; nk2 = rk2_; nk3 = rk3;
-    set_byte(nk0, nk1, nk2, nk3, dn, X.rank[dn * 16 + c_dn]);
-    set_byte(nk0, nk1, nk2, nk3, up, X.rank[up * 16 + c_up]);
-    tin2 = tin_of(nk0, nk1, nk2, nk3, X);
-    tex2 = (mask2 == mask) ? tex : tex_of(mask2, k2, X);
+    const uint32_t m2 = (mask & (c_dn == 0u ? ~(1u << dn) : 0xffffffffu)) | (1u << up);
+    const uint32_t r_dn = X.rank[dn * 16 + c_dn], r_up = X.rank[up * 16 + c_up];
+    uint32_t t0 = rk0, t1 = rk1, t2 = rk2_, t3 = rk3;
+    set_byte(t0, t1, t2, t3, dn, r_dn);
+    set_byte(t0, t1, t2, t3, up, r_up);
+    tin2 = tin_of(t0, t1, t2, t3, X);
+    tex2 = (m2 == mask) ? tex : tex_of(m2, __popc(m2), X);
+    if constexpr (NW == 4) {
+      pend = dn | (up << 8) | (r_dn << 16) | (r_up << 24);
+    } else {
+      cnt2 = cnt - ((CT)1 << (4u * dn)) + ((CT)1 << (4u * up));
+      mask2 = m2; k2 = __popc(m2);
+      nk0 = t0; nk1 = t1; nk2 = t2; nk3 = t3;
+    }
   }
   __device__ __forceinline__ void coop(const S1Ctx&, const RT&) {}
   __device__ __forceinline__ void finish(const S1Ctx&) {}
   __device__ __forceinline__ void commit() {
-    cnt = cnt2; mask = mask2; k = k2; tin = tin2; tex = tex2;
-    rk0 = nk0; rk1 = nk1; rk2_ = nk2; rk3 = nk3;
+    if constexpr (NW == 4) {
+      const uint32_t dn = pend & 0xffu, up = (pend >> 8) & 0xffu;
+      mask = (mask & (get(cnt, dn) == 1u ? ~(1u << dn) : 0xffffffffu)) | (1u << up);
+      cnt = cnt - ((CT)1 << (4u * dn)) + ((CT)1 << (4u * up));
+      k = __popc(mask);
+      set_byte(rk0, rk1, rk2_, rk3, dn, (pend >> 16) & 0xffu);
+      set_byte(rk0, rk1, rk2_, rk3, up, pend >> 24);
+    } else {
+      cnt = cnt2; mask = mask2; k = k2;
+      rk0 = nk0; rk1 = nk1; rk2_ = nk2; rk3 = nk3;
+    }
+    tin = tin2; tex = tex2;
   }
 };
 
